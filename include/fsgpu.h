@@ -1,0 +1,199 @@
+/*
+ * fsgpu.h — C-ABI of the B200 (sm_100a) sorted-interval lookup library.
+ *
+ * The reference (`fastsearch` 0.1.0, /root/reference/pkg) is pure Python +
+ * numpy; its "FFI" for the hot path is the operator boundary in
+ * pkg/src/fastsearch/batch.py (prepare / PreparedKernel.lanes / batch_search)
+ * and the index builder in pkg/src/fastsearch/direct.py.  Every entry point
+ * below replaces one of those functions; the reference interface it stands
+ * in for is cited beside it.  A Python (ctypes) binding of exactly these
+ * symbols lives in paper_1506_08620_b200/_lib.py; INTEGRATION.md shows the
+ * stub a fastsearch maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device memory;
+ *    "host" pointers are host memory (pinned or pageable).
+ *  - Every call is stream-ordered on the cudaStream_t passed as `void*`
+ *    (NULL = legacy default stream).  Calls marked SYNC synchronise that
+ *    stream before returning; all others are asynchronous.
+ *  - No global mutable state; calls are thread-safe.
+ *  - Return value: an fs_status code.  Positions (first offending element)
+ *    are written through `pos_out` where the reference exception carries a
+ *    `position` attribute (errors.py:28-62).
+ *  - Floating point semantics are the reference's numpy semantics: IEEE-754
+ *    round-to-nearest-even in the partition's own precision, subnormals kept
+ *    (no FTZ), no contraction, truncation toward zero for the bucket index.
+ */
+#ifndef FSGPU_H
+#define FSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map 1:1 onto fastsearch.errors, errors.py:1-82) ---- */
+typedef enum fs_status {
+  FS_OK = 0,
+  FS_NOT_DISTINGUISHABLE = 1, /* errors.NotDistinguishable(position)          */
+  FS_OVERFLOW = 2,            /* errors.Overflow                              */
+  FS_OUT_OF_DOMAIN = 3,       /* errors.OutOfDomain(position)                 */
+  FS_INVALID_ARG = 4,         /* ValueError (qbits, q, sizes, dtype, ...)     */
+  FS_CUDA_ERROR = 5,          /* CUDA runtime failure; see fs_last_error()    */
+  FS_INCONSISTENT = 6,        /* build_index: "(h, r) pair is inconsistent"  */
+  FS_TOO_LARGE = 7            /* table/workspace does not fit the device path */
+} fs_status;
+
+/* ---- element types ---- */
+enum { FS_F32 = 0, FS_F64 = 1 };
+
+/* ---- algorithms: the names of batch.ALGORITHMS (batch.py:35-45) ---- */
+enum {
+  FS_ALGO_CLASSIC = 0,      /* binsearch.classic_seq      binsearch.py:48-57   */
+  FS_ALGO_BITSET1 = 1,      /* binsearch.bitset1_seq      binsearch.py:60-69   */
+  FS_ALGO_BITSET2 = 2,      /* binsearch.bitset2_seq      binsearch.py:72-86   */
+  FS_ALGO_BITSET3 = 3,      /* binsearch.bitset3_seq      binsearch.py:89-99   */
+  FS_ALGO_OFFSET = 4,       /* binsearch.offset_seq       binsearch.py:102-114 */
+  FS_ALGO_EYTZINGER = 5,    /* eytzinger.eytzinger_seq    eytzinger.py:84-89   */
+  FS_ALGO_DIRECT = 6,       /* batch lanes, gap 1         batch.py:315-317     */
+  FS_ALGO_DIRECT_GAP2 = 7,  /* batch lanes, gap 2         batch.py:341-343     */
+  FS_ALGO_DIRECT_CACHE = 8, /* batch lanes, fused records batch.py:368-371     */
+  FS_ALGO_DIRECT_GENERIC = 9 /* direct.direct_search_generic direct.py:294-300 */
+};
+
+/* ---- table placement (reported by fs_plan_placement) ---- */
+enum {
+  FS_PLACE_GLOBAL = 0,  /* tables gathered through L2 (ld.global.nc)               */
+  FS_PLACE_SMEM_X = 1,  /* knots (or padded/tree array) staged in shared memory   */
+  FS_PLACE_SMEM_K = 2,  /* bucket table / fused records staged in shared memory   */
+  FS_PLACE_SMEM_TOP = 4 /* bitset2: top levels in smem, bottom levels via L2      */
+};
+
+/*
+ * A prepared search structure resident in device memory — the device image
+ * of batch.PreparedKernel.structure (batch.py:132-140).  All pointers are
+ * device pointers owned by the caller.
+ */
+typedef struct fs_plan {
+  int32_t algorithm;  /* FS_ALGO_*                                               */
+  int32_t dtype;      /* FS_F32 / FS_F64                                         */
+  uint64_t n1;        /* number of knots N+1 (>= 2)                              */
+  const void* x;      /* knots X[0..N], n1 elements of dtype                     */
+  const void* table;  /* direct/gap2/generic: K (uint32, r+1 entries);
+                         direct-cache: fused records ((r+1) x 8 B f32 / 16 B f64);
+                         bitset2: padded knots (2^pbits elements);
+                         eytzinger: heap-order tree (2^pbits - 1 elements);
+                         others: unused (NULL)                                     */
+  uint64_t r;         /* direct family: bucket count R (table has R+1 entries)   */
+  double h;           /* direct family: scale factor H (exact in dtype)          */
+  double x0, xn;      /* domain [X0, XN) (exact in dtype)                        */
+  int32_t q;          /* direct family: gap (1, 2, >2 generic)                   */
+  int32_t pbits;      /* bitset family: bit_length(N); eytzinger: depth L   */
+  int32_t smem_policy;/* 0 auto, 1 force global (L2) gathers                      */
+  int32_t reserved;
+} fs_plan;
+
+/* Library identification. */
+const char* fs_version(void);
+/* Message for the last FS_CUDA_ERROR / FS_INVALID_ARG on this thread. */
+const char* fs_last_error(void);
+/* Bytes of device workspace the build entry points need (status block). */
+size_t fs_workspace_bytes(void);
+
+/* ---------------------------------------------------------------------------
+ * Index construction (direct.py:433-561)
+ * ------------------------------------------------------------------------ */
+
+/*
+ * Certified scale factor.  Replaces direct.compute_h_r (direct.py:433-489):
+ * D = RN(X - X0); collision of D[i+q] == D[i] -> FS_NOT_DISTINGUISHABLE with
+ * *pos_out = first i+q; h = RN(1 / min RN(D[i+b] - D[i])), b = min(q, N);
+ * FS_OVERFLOW unless RN(h * D_N) < 2^qbits; growth loop with doubling ulp
+ * increments re-certifying every pair; r = floor(RN(h * D_N)).
+ * h_out / h_start_out receive the values in the partition's dtype (float* or
+ * double*).  SYNC (one device->host read per growth iteration).
+ */
+int fs_certify(int32_t dtype, const void* x_dev, uint64_t n1, int32_t qbits, int32_t q,
+               void* ws_dev, void* h_out, void* h_start_out, uint64_t* r_out,
+               uint32_t* increments_out, int64_t* pos_out, void* stream);
+
+/*
+ * Knot buckets f_i = floor(RN(h * RN(X_i - X0))) as uint64.  Replaces
+ * direct.knot_buckets (direct.py:492-495).
+ */
+int fs_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t* f_dev,
+                    void* stream);
+
+/*
+ * Bucket table K.  Replaces direct.build_index (direct.py:498-541) and
+ * knot_buckets (direct.py:492-495): f_i = floor(RN(h * RN(X_i - X0)));
+ * FS_INCONSISTENT unless f_N == r; q == 1: K[j] = i for f_{i-1} < j <= f_i,
+ * K[0] = 0; q > 1: K[j] = max{i : f_i <= j}.  k_dev holds r+1 uint32.
+ * f_scratch_dev holds n1 uint64.  SYNC (reads back the consistency flag).
+ */
+int fs_build_table(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
+                   int32_t q, uint32_t* k_dev, uint64_t* f_scratch_dev, void* ws_dev,
+                   void* stream);
+
+/*
+ * Cache-fused (idx, val) records.  Replaces direct.with_fused
+ * (direct.py:553-561): rec[j] = {K[j], X[K[j]]}; 8 B records for f32,
+ * 16 B {u32 idx, u32 pad = 0, f64 val} for f64.
+ */
+int fs_build_fused(int32_t dtype, const void* x_dev, uint64_t n1, const uint32_t* k_dev,
+                   uint64_t r, void* rec_dev, void* stream);
+
+/* Right padding to 2^pbits with X_N.  Replaces partition.pad_right_pow2
+ * (partition.py:163-171). */
+int fs_build_padded(int32_t dtype, const void* x_dev, uint64_t n1, int32_t pbits,
+                    void* xpad_dev, void* stream);
+
+/* Heap-order (Eytzinger) tree of depth L.  Replaces eytzinger.build_layout
+ * (eytzinger.py:45-63). tree_dev holds 2^L - 1 elements. */
+int fs_build_eytzinger(int32_t dtype, const void* x_dev, uint64_t n1, int32_t depth,
+                       void* tree_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Batch search (batch.py:399-441)
+ * ------------------------------------------------------------------------ */
+
+/*
+ * Resolve m device-resident queries into device `out` (out_bytes = 4 for
+ * int32, 8 for int64).  Replaces PreparedKernel.lanes + the domain check of
+ * batch_search (batch.py:411-413): the first query with !(X0 <= z < XN)
+ * (NaN included) is atomically min-reduced into *first_bad_dev, which this
+ * call initialises to UINT64_MAX.  `out` is unspecified where a query is
+ * out of domain.  ASYNC: one kernel launch (plus a 8-byte memset).
+ */
+int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* out_dev,
+                     int32_t out_bytes, unsigned long long* first_bad_dev, void* stream);
+
+/*
+ * End-to-end host-buffer search: the whole batch_search contract
+ * (batch.py:399-441) on host arrays.  Copies z_host -> z_dev in chunks on
+ * `copy_stream` overlapped with the search kernel per chunk on `stream`;
+ * then reads the first-bad word and, only if every query is in domain,
+ * copies the results to out_host (nothing is written on error, as
+ * batch.py:404 promises).  z_dev/out_dev are device scratch of m elements.
+ * SYNC.  On FS_OUT_OF_DOMAIN *pos_out is the first offending position.
+ */
+int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host,
+                   int32_t out_bytes, void* z_dev, void* out_dev,
+                   unsigned long long* first_bad_dev, uint64_t chunk_elems,
+                   int64_t* pos_out, void* stream, void* copy_stream);
+
+/* Placement the search kernel will use for this plan (FS_PLACE_* bit set),
+ * plus the dynamic shared memory bytes per CTA it stages. */
+int fs_plan_placement(const fs_plan* plan, int32_t* placement_out, uint64_t* smem_bytes_out);
+
+/* Number of kernel launches fs_search_device issues for this plan (for the
+ * bench's gpu_launches accounting). */
+int fs_search_launches(const fs_plan* plan, uint64_t m);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSGPU_H */

@@ -1,0 +1,79 @@
+"""Device plumbing: torch supplies device memory and the current stream.
+
+Nothing here computes anything on the search path; it allocates, uploads
+and hands raw pointers to the C-ABI (``_lib``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_TORCH = {
+    np.dtype(np.float32): torch.float32,
+    np.dtype(np.float64): torch.float64,
+    np.dtype(np.int32): torch.int32,
+    np.dtype(np.int64): torch.int64,
+    np.dtype(np.uint32): torch.uint32,
+    np.dtype(np.uint64): torch.uint64,
+    np.dtype(np.uint8): torch.uint8,
+}
+
+
+def require_cuda() -> torch.device:
+    """Current CUDA device; raises when there is none (no CPU fallback)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1506_08620_b200 runs on a CUDA device (sm_100a); none is available "
+            "and there is deliberately no CPU fallback"
+        )
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def torch_dtype(dtype) -> torch.dtype:
+    return _TORCH[np.dtype(dtype)]
+
+
+def empty(n: int, dtype, device=None) -> torch.Tensor:
+    dev = device if device is not None else require_cuda()
+    return torch.empty(int(n), dtype=torch_dtype(dtype), device=dev)
+
+
+def upload(arr: np.ndarray, device=None) -> torch.Tensor:
+    dev = device if device is not None else require_cuda()
+    a = np.ascontiguousarray(arr)
+    t = torch.empty(a.shape, dtype=torch_dtype(a.dtype), device=dev)
+    t.copy_(torch.from_numpy(a.copy() if not a.flags.writeable else a))
+    return t
+
+
+def download(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else int(t.data_ptr())
+
+
+class Workspace:
+    """Small per-device status block of the build entry points."""
+
+    _cache: dict[int, torch.Tensor] = {}
+
+    @classmethod
+    def get(cls) -> torch.Tensor:
+        dev = require_cuda()
+        ws = cls._cache.get(dev.index)
+        if ws is None:
+            nbytes = int(_lib.load().fs_workspace_bytes())
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            cls._cache[dev.index] = ws
+        return ws

@@ -1,0 +1,329 @@
+"""The operator boundary: prepare / PreparedKernel / batch_search on the GPU.
+
+Drop-in for ``fastsearch/batch.py`` (batch.py:1-451).  ``prepare`` builds the
+search structure of any of the nine ``ALGORITHMS`` on the device and returns
+a ``PreparedKernel`` whose ``lanes``/``scalar`` callables and whose use in
+``batch_search``/``run_batch`` dispatch one CUDA kernel over the whole batch
+(csrc/search.cuh).  What the reference guarantees, this keeps:
+
+  * ``out[j]`` is query j's answer, independent of the lane width ``d`` and
+    the thread count (batch.py:402-403) -- the GPU has no lane/tail split,
+    so invariance holds by construction;
+  * OutOfDomain(position = first bad j) for any !(X0 <= z < XN), NaN
+    included, with nothing written to a host ``out`` (batch.py:404, 411-413):
+    the check is fused into the search kernel and results are copied back
+    only when the batch is clean;
+  * infeasible direct layouts raise from ``prepare`` (batch.py:159-160).
+    ``prepare_with_fallback`` is the explicit policy the paper implies
+    (PAPER.md:877): direct when feasible, else the padded bit-set search.
+
+Inputs: numpy arrays / QueryBatch (host; copied in chunks overlapped with
+the kernel) or CUDA torch tensors (device-resident; no copies).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+from . import _device, _lib
+from .binsearch import offset_constants, probe_constant
+from .direct import DirectIndex, build
+from .errors import InfeasibleError, OutOfDomain
+from .eytzinger import EytzingerLayout, build_layout
+from .partition import PaddedPartition, QueryBatch, SortedPartition, coerce_queries, fs_dtype, pad_right_pow2
+
+ALGORITHMS = (
+    "classic",
+    "bitset1",
+    "bitset2",
+    "bitset3",
+    "offset",
+    "eytzinger",
+    "direct",
+    "direct-gap2",
+    "direct-cache",
+)
+
+THREADS_ENV = "FASTSEARCH_THREADS"
+
+#: host->device chunk for the end-to-end path (elements); ~64 MB of queries
+HOST_CHUNK_BYTES = 64 << 20
+
+_copy_streams: dict = {}
+
+
+def _copy_stream():
+    import torch
+
+    dev = torch.cuda.current_device()
+    s = _copy_streams.get(dev)
+    if s is None:
+        s = torch.cuda.Stream(device=dev)
+        _copy_streams[dev] = s
+    return s
+
+
+def _plan_for(algorithm: str, structure, p: SortedPartition):
+    """fs_plan for ``algorithm`` over ``structure``; returns (plan, keepalive)."""
+    plan = _lib.FsPlan()
+    plan.algorithm = _lib.ALGO_CODES[algorithm]
+    plan.dtype = fs_dtype(p.precision)
+    plan.n1 = len(p.values)
+    x = p.device_values()
+    plan.x = x.data_ptr()
+    plan.x0 = float(p.values[0])
+    plan.xn = float(p.values[-1])
+    plan.q = 1
+    plan.pbits = max(1, p.n_intervals.bit_length())
+    keep = [x]
+    if algorithm.startswith("direct"):
+        idx: DirectIndex = structure
+        plan.r = idx.r
+        plan.h = float(idx.h)
+        plan.q = idx.q
+        if algorithm == "direct-cache":
+            plan.table = idx.fused_dev.data_ptr()
+            keep.append(idx.fused_dev)
+        else:
+            plan.table = idx.k_dev.data_ptr()
+            keep.append(idx.k_dev)
+    elif algorithm == "bitset2":
+        pp: PaddedPartition = structure
+        plan.table = pp.padded_dev.data_ptr()
+        plan.pbits = pp.p
+        keep.append(pp.padded_dev)
+    elif algorithm == "eytzinger":
+        lay: EytzingerLayout = structure
+        plan.table = lay.tree_dev.data_ptr()
+        plan.pbits = lay.L
+        keep.append(lay.tree_dev)
+    return plan, keep
+
+
+def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = HOST_CHUNK_BYTES) -> None:
+    """End-to-end search of host queries into host ``out[:m]`` (fs_search_host)."""
+    m = len(z)
+    if m == 0:
+        return
+    _device.require_cuda()
+    z = np.ascontiguousarray(z)
+    direct_out = out.dtype in (np.int32, np.int64) and out.flags.c_contiguous and out.flags.writeable
+    target = out[:m] if direct_out else np.empty(m, dtype=np.int64)
+    ob = target.dtype.itemsize
+    z_dev = _device.empty(m, z.dtype)
+    o_dev = _device.empty(m, target.dtype)
+    fb = _device.empty(1, np.uint64)
+    pos = ctypes.c_int64(-1)
+    rc = _lib.load().fs_search_host(
+        ctypes.byref(plan), z.ctypes.data, m, target.ctypes.data, ob, z_dev.data_ptr(), o_dev.data_ptr(),
+        fb.data_ptr(), max(4, chunk_bytes // z.dtype.itemsize), ctypes.byref(pos), _device.stream_ptr(),
+        _device.stream_ptr(_copy_stream()),
+    )
+    _lib.check(rc, pos=pos.value, what="fs_search_host")
+    if not direct_out:
+        out[:m] = target
+
+
+def _launch_device(plan, z, out, first_bad) -> None:
+    """Asynchronous device search (fs_search_device); first_bad is a 1-element
+    uint64 CUDA tensor that receives the first out-of-domain position."""
+    rc = _lib.load().fs_search_device(ctypes.byref(plan), z.data_ptr(), z.numel(), out.data_ptr(),
+                                      out.element_size(), first_bad.data_ptr(), _device.stream_ptr())
+    _lib.check(rc, what="fs_search_device")
+
+
+def _search_device_tensor(plan, z, out) -> None:
+    import torch
+
+    fb = torch.empty(1, dtype=torch.uint64, device=z.device)
+    _launch_device(plan, z, out, fb)
+    bad = int(fb.view(torch.int64).item())
+    if bad != -1:
+        raise OutOfDomain(position=bad)
+
+
+def _is_torch(a) -> bool:
+    mod = type(a).__module__
+    return mod.startswith("torch")
+
+
+@dataclass(frozen=True)
+class PreparedKernel:
+    """A device search structure plus its scalar and batch entry points
+    (batch.py:132-140).  ``plan`` is the C-ABI descriptor; ``buffers`` keeps
+    its device tables alive."""
+
+    algorithm: str
+    partition: SortedPartition
+    structure: object
+    scalar: Callable
+    lanes: Callable | None
+    plan: object = field(default=None, repr=False, compare=False)
+    buffers: tuple = field(default=(), repr=False, compare=False)
+
+    # -- device-level API (no host copies, no synchronisation) -------------
+    def launch(self, z, out, first_bad) -> None:
+        """Enqueue one search kernel on the current stream.  ``z``: CUDA tensor
+        of the partition's dtype; ``out``: int32/int64 CUDA tensor; ``first_bad``:
+        1-element uint64 CUDA tensor (UINT64_MAX when every query is in
+        domain).  ``out`` is unspecified for out-of-domain queries."""
+        _launch_device(self.plan, z, out, first_bad)
+
+    def placement(self) -> dict:
+        """Where the kernel keeps its tables: {'smem_x', 'smem_table',
+        'smem_top', 'smem_bytes'}."""
+        flags = ctypes.c_int32(0)
+        smem = ctypes.c_uint64(0)
+        _lib.check(_lib.load().fs_plan_placement(ctypes.byref(self.plan), ctypes.byref(flags), ctypes.byref(smem)))
+        f = flags.value
+        return {
+            "smem_x": bool(f & _lib.PLACE_SMEM_X),
+            "smem_table": bool(f & _lib.PLACE_SMEM_K),
+            "smem_top": bool(f & _lib.PLACE_SMEM_TOP),
+            "smem_bytes": int(smem.value),
+        }
+
+    def launches_per_batch(self, m: int) -> int:
+        return int(_lib.load().fs_search_launches(ctypes.byref(self.plan), m))
+
+
+@dataclass(frozen=True)
+class LaneConfig:
+    """Lane width, kernel name, prepared structure (batch.py:143-153).  ``d``
+    is validated and otherwise has no effect on the GPU."""
+
+    d: int
+    kernel: str
+    structure: PreparedKernel
+
+    def __post_init__(self):
+        if self.d < 1:
+            raise ValueError("lane width must be >= 1")
+
+
+def _make_callables(plan, p: SortedPartition):
+    dtype = p.values.dtype
+
+    def lanes(z):
+        if _is_torch(z):
+            import torch
+
+            out = torch.empty(z.numel(), dtype=torch.int64, device=z.device)
+            _search_device_tensor(plan, z.contiguous(), out)
+            return out
+        zz = coerce_queries(z, dtype)
+        out = np.empty(len(zz), dtype=np.int64)
+        _search_host_array(plan, zz, out)
+        return out
+
+    def scalar(z):
+        out = np.empty(1, dtype=np.int64)
+        _search_host_array(plan, coerce_queries(np.asarray([z]), dtype), out)
+        return int(out[0])
+
+    return scalar, lanes
+
+
+def prepare(algorithm: str, p: SortedPartition, qbits: int = 32) -> PreparedKernel:
+    """Build the device search structure for ``algorithm`` (batch.py:156-255).
+
+    Direct-family preparation propagates NotDistinguishable/Overflow from
+    index construction, as the reference does.
+    """
+    n = p.n_intervals
+    if algorithm == "classic":
+        structure = p
+    elif algorithm in ("bitset1", "bitset3"):
+        structure = probe_constant(n)
+    elif algorithm == "bitset2":
+        structure = pad_right_pow2(p)
+    elif algorithm == "offset":
+        structure = offset_constants(n)
+    elif algorithm == "eytzinger":
+        structure = build_layout(p)
+    elif algorithm in ("direct", "direct-gap2", "direct-cache"):
+        q = 2 if algorithm == "direct-gap2" else 1
+        structure, _ = build(p, qbits=qbits, q=q, fused=(algorithm == "direct-cache"))
+    else:
+        raise ValueError(f"unknown algorithm {algorithm!r}; pick one of {ALGORITHMS}")
+    plan, keep = _plan_for(algorithm, structure, p)
+    scalar, lanes = _make_callables(plan, p)
+    return PreparedKernel(algorithm, p, structure, scalar, lanes, plan=plan, buffers=tuple(keep))
+
+
+def prepare_with_fallback(p: SortedPartition, qbits: int = 32, algorithm: str = "direct",
+                          fallback: str = "bitset2") -> PreparedKernel:
+    """Direct search when its index is feasible, else the padded bit-set
+    binary search -- the fall-back the paper describes and
+    the reference leaves to its harness (bench/harness.py:153-159)."""
+    try:
+        return prepare(algorithm, p, qbits)
+    except InfeasibleError:
+        return prepare(fallback, p, qbits)
+
+
+def resolve_threads(threads: int | None) -> int:
+    """batch.py:376-382 (validated; the GPU path does not use host threads)."""
+    if threads is not None:
+        if threads < 1:
+            raise ValueError("thread count must be >= 1")
+        return threads
+    env = os.environ.get(THREADS_ENV)
+    return max(1, int(env)) if env else 1
+
+
+def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None) -> int:
+    """Resolve every query into ``out``; returns the number resolved
+    (batch.py:399-441).
+
+    Raises OutOfDomain(position) for the first query outside [X_0, X_N);
+    a host ``out`` is left untouched in that case.
+    """
+    kern = cfg.structure
+    resolve_threads(threads)
+    if isinstance(queries, QueryBatch):
+        z = queries.values
+    elif _is_torch(queries):
+        z = queries
+    else:
+        z = np.asarray(queries)
+    m = len(z)
+    if len(out) < m:
+        raise ValueError("output array is smaller than the query batch")
+    p = kern.partition
+    if _is_torch(z) or _is_torch(out):
+        import torch
+
+        if not (_is_torch(z) and _is_torch(out) and z.is_cuda and out.is_cuda):
+            raise ValueError("device-resident batches need CUDA tensors for both queries and out")
+        if z.dtype != _device.torch_dtype(p.values.dtype):
+            raise ValueError(f"query dtype {z.dtype} does not match the partition's {p.values.dtype}")
+        if out.dtype not in (torch.int32, torch.int64):
+            raise ValueError("out must be int32 or int64")
+        _search_device_tensor(kern.plan, z.contiguous(), out[:m])
+        return m
+    zz = coerce_queries(z, p.values.dtype)
+    _search_host_array(kern.plan, zz, out)
+    return m
+
+
+def run_batch(prepared: PreparedKernel, queries, d: int = 1, threads: int | None = None):
+    """Allocate an int64 output and run batch_search (batch.py:444-451)."""
+    if isinstance(queries, QueryBatch):
+        z = queries.values
+    elif _is_torch(queries):
+        import torch
+
+        out = torch.empty(len(queries), dtype=torch.int64, device=queries.device)
+        batch_search(LaneConfig(d=d, kernel=prepared.algorithm, structure=prepared), queries, out, threads)
+        return out
+    else:
+        z = np.asarray(queries)
+    out = np.empty(len(z), dtype=np.int64)
+    batch_search(LaneConfig(d=d, kernel=prepared.algorithm, structure=prepared), z, out, threads)
+    return out

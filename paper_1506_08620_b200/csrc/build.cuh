@@ -1,0 +1,233 @@
+// build.cuh — index construction kernels.
+//
+//   certify_prep / certify_finalize / certify_check / certify_grow
+//       restate direct.compute_h_r (direct.py:433-489) op for op
+//   knot_buckets_kernel  direct.knot_buckets + the f[-1] == r check
+//                        (direct.py:492-495, 513-515)
+//   fill_table_kernel    the np.repeat of build_index (direct.py:516-524),
+//                        restated as K[j] = lower_bound(f, j) (gap 1) or
+//                        upper_bound(f, j) - 1 (gap > 1): bucket-parallel,
+//                        coalesced writes, O(R log(range)) instead of a
+//                        per-knot scatter whose run lengths vary by 10^4x
+//   fill_fused_kernel    direct.with_fused (direct.py:553-561)
+//   pad_right_kernel     partition.pad_right_pow2 (partition.py:163-171)
+//   eytzinger_kernel     eytzinger.build_layout (eytzinger.py:45-63)
+#pragma once
+
+#include "common.cuh"
+
+namespace fsg {
+
+// Device status block of the certification (lives in caller workspace).
+struct CertStatus {
+  unsigned long long collide_pos;  // min i+q with D[i+q] == D[i]
+  unsigned long long min_key;      // order key of min RN(D[i+b] - D[i])
+  unsigned long long fail;         // any pair with floor(hD[i+q]) <= floor(hD[i])
+  unsigned long long inconsistent; // build_index: f[N] != r
+  double h;                        // current H (exact in dtype)
+  double h_start;                  // initial guess
+  double growth;                   // current increment
+  double r_float;                  // floor(RN(h * D_N))
+  int32_t status;                  // 0 ok, 1 not distinguishable, 2 overflow
+  uint32_t increments;
+};
+
+__global__ void cert_init_kernel(CertStatus* st) {
+  st->collide_pos = ~0ull;
+  st->min_key = ~0ull;
+  st->fail = 0;
+  st->inconsistent = 0;
+  st->h = st->h_start = st->growth = st->r_float = 0.0;
+  st->status = 0;
+  st->increments = 0;
+}
+
+template <int NT>
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v) {
+  __shared__ unsigned long long red[NT / 32];
+  v = warp_min_u64(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < NT / 32 ? red[threadIdx.x] : ~0ull;
+    v = warp_min_u64(v);
+  }
+  __syncthreads();
+  return v;  // valid in thread 0
+}
+
+// K1: collisions of the rounded offsets and the smallest gap-b difference.
+// direct.py:454-464.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) certify_prep(const T* __restrict__ x, uint64_t n1, uint64_t q,
+                                                   uint64_t basis, CertStatus* st) {
+  const T x0 = x[0];
+  unsigned long long coll = ~0ull, mk = ~0ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * NT + threadIdx.x; i < n1; i += (uint64_t)gridDim.x * NT) {
+    const T di = sub_rn(__ldg(x + i), x0);
+    if (i + q < n1) {
+      const T dq = sub_rn(__ldg(x + i + q), x0);
+      if (dq == di && i + q < coll) coll = i + q;
+    }
+    if (i + basis < n1) {
+      const T db = sub_rn(__ldg(x + i + basis), x0);
+      const unsigned long long k = order_key(sub_rn(db, di));
+      mk = k < mk ? k : mk;
+    }
+  }
+  coll = block_min_u64<NT>(coll);
+  mk = block_min_u64<NT>(mk);
+  if (threadIdx.x == 0) {
+    if (coll != ~0ull) atomicMin(&st->collide_pos, coll);
+    if (mk != ~0ull) atomicMin(&st->min_key, mk);
+  }
+}
+
+// Initial guess, overflow test and first increment.  direct.py:456-471.
+template <typename T>
+__global__ void certify_finalize(const T* __restrict__ x, uint64_t n1, int qbits, CertStatus* st) {
+  if (st->collide_pos != ~0ull) {
+    st->status = 1;
+    return;
+  }
+  const T mn = from_key<T>(st->min_key);
+  const T h = div_rn(T(1), mn);
+  const T span = sub_rn(x[n1 - 1], x[0]);
+  const T limit = qbits == 64 ? T(18446744073709551616.0) : T(4294967296.0);
+  st->h = (double)h;
+  st->h_start = (double)h;
+  if (!(mul_rn(h, span) < limit)) {
+    st->status = 2;
+    return;
+  }
+  st->growth = (double)sub_rn(next_up(h), h);
+}
+
+// K2: certify every gap-q pair at the current H.  direct.py:474-476, 483.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) certify_check(const T* __restrict__ x, uint64_t n1, uint64_t q,
+                                                    CertStatus* st) {
+  if (st->status != 0) return;
+  const T x0 = x[0];
+  const T h = (T)st->h;
+  bool bad = false;
+  for (uint64_t i = (uint64_t)blockIdx.x * NT + threadIdx.x; i + q < n1; i += (uint64_t)gridDim.x * NT) {
+    const T fi = floor(mul_rn(h, sub_rn(__ldg(x + i), x0)));
+    const T fq = floor(mul_rn(h, sub_rn(__ldg(x + i + q), x0)));
+    bad |= !(fq > fi);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) st->fail = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->r_float = (double)floor(mul_rn(h, sub_rn(x[n1 - 1], x0)));
+}
+
+// One growth step: h += growth; overflow test; growth doubles.
+// direct.py:477-481.
+template <typename T>
+__global__ void certify_grow(const T* __restrict__ x, uint64_t n1, int qbits, CertStatus* st) {
+  const T span = sub_rn(x[n1 - 1], x[0]);
+  const T limit = qbits == 64 ? T(18446744073709551616.0) : T(4294967296.0);
+  T h = (T)st->h;
+  T g = (T)st->growth;
+  h = add_rn(h, g);
+  st->h = (double)h;
+  st->increments += 1;
+  st->fail = 0;
+  if (!(mul_rn(h, span) < limit)) {
+    st->status = 2;
+    return;
+  }
+  st->growth = (double)add_rn(g, g);
+}
+
+// f_i = floor(RN(h * RN(X_i - X0))) as an integer.  direct.py:492-495.
+template <typename T>
+__global__ void knot_buckets_kernel(const T* __restrict__ x, uint64_t n1, T h, uint64_t r,
+                                    uint64_t* __restrict__ f, CertStatus* st) {
+  const T x0 = x[0];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += (uint64_t)gridDim.x * blockDim.x) {
+    const T v = floor(mul_rn(h, sub_rn(__ldg(x + i), x0)));
+    const uint64_t fi = trunc_to<uint64_t>(v);
+    f[i] = fi;
+    if (st && i == n1 - 1 && fi != r) st->inconsistent = 1;
+  }
+}
+
+// First index in [lo, hi) with f[i] >= key (UPPER=false) or f[i] > key (UPPER=true).
+template <bool UPPER>
+__device__ __forceinline__ uint64_t bound_search(const uint64_t* __restrict__ f, uint64_t lo, uint64_t hi,
+                                                 uint64_t key) {
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    const uint64_t v = __ldg(f + mid);
+    const bool go_right = UPPER ? (v <= key) : (v < key);
+    if (go_right) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// K[j] for j in [0, r]: gap 1 -> lower_bound(f, j); gap > 1 -> upper_bound(f, j) - 1.
+// Each CTA owns a tile of TILE consecutive buckets; thread 0 brackets the
+// knot range of the tile once, then every thread searches only inside it.
+template <int NT, int ITEMS, bool UPPER>
+__global__ void __launch_bounds__(NT) fill_table_kernel(const uint64_t* __restrict__ f, uint64_t n1, uint64_t r,
+                                                        uint32_t* __restrict__ K) {
+  constexpr uint64_t TILE = (uint64_t)NT * ITEMS;
+  __shared__ uint64_t rng[2];
+  const uint64_t total = r + 1;
+  for (uint64_t t0 = (uint64_t)blockIdx.x * TILE; t0 < total; t0 += (uint64_t)gridDim.x * TILE) {
+    const uint64_t t1 = (t0 + TILE < total ? t0 + TILE : total) - 1;  // inclusive
+    if (threadIdx.x == 0) {
+      rng[0] = bound_search<UPPER>(f, 0, n1, t0);
+      rng[1] = bound_search<UPPER>(f, 0, n1, t1);
+    }
+    __syncthreads();
+    // lower_bound answers lie in [rng0, rng1]; upper_bound answers too.
+    const uint64_t lo = rng[0], hi = rng[1] + 1 < n1 ? rng[1] + 1 : n1;
+    for (uint64_t j = t0 + threadIdx.x; j <= t1; j += NT) {
+      const uint64_t b = bound_search<UPPER>(f, lo, hi, j);
+      K[j] = (uint32_t)(UPPER ? b - 1 : b);
+    }
+    __syncthreads();
+  }
+}
+
+// Fused (idx, val) records.  direct.py:553-561.
+__global__ void fill_fused_f32(const float* __restrict__ x, const uint32_t* __restrict__ K, uint64_t r,
+                               uint2* __restrict__ rec) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= r; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = K[j];
+    rec[j] = make_uint2(t, __float_as_uint(__ldg(x + t)));
+  }
+}
+__global__ void fill_fused_f64(const double* __restrict__ x, const uint32_t* __restrict__ K, uint64_t r,
+                               double2* __restrict__ rec) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= r; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = K[j];
+    rec[j] = make_double2(__longlong_as_double((long long)(unsigned long long)t), __ldg(x + t));
+  }
+}
+
+// xpad[i] = X[min(i, N)], i < 2^pbits.  partition.py:163-171.
+template <typename T>
+__global__ void pad_right_kernel(const T* __restrict__ x, uint64_t n1, uint64_t len, T* __restrict__ xpad) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x)
+    xpad[i] = __ldg(x + (i < n1 ? i : n1 - 1));
+}
+
+// Heap-order tree: slot s (1-based q = s + 1) at level l = floor(log2 q)
+// holds the padded knot of in-order rank (q - 2^l) * 2^(L-l) + 2^(L-l-1) - 1.
+// eytzinger.py:45-63.
+template <typename T>
+__global__ void eytzinger_kernel(const T* __restrict__ x, uint64_t n1, int depth, T* __restrict__ tree) {
+  const uint64_t size = (1ull << depth) - 1;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < size; s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t qs = s + 1;
+    const int lvl = 63 - __clzll((long long)qs);
+    const uint64_t stride = 1ull << (depth - lvl);
+    const uint64_t rank = (qs - (1ull << lvl)) * stride + (stride >> 1) - 1;
+    tree[s] = __ldg(x + (rank < n1 ? rank : n1 - 1));
+  }
+}
+
+}  // namespace fsg

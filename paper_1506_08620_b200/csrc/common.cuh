@@ -1,0 +1,195 @@
+// common.cuh — sm_100a device helpers shared by the search and build kernels.
+//
+// Numeric helpers pin the reference's numpy semantics exactly
+// (SURVEY.md Appendix A): every float op is an explicit _rn intrinsic so
+// nvcc can neither contract nor reassociate, and the bucket index is a
+// round-toward-zero conversion (numpy .astype(np.int64) on a non-negative
+// value, batch.py:316).  The library is compiled without --use_fast_math and
+// with -ftz=false -prec-div=true so subnormals survive, as in numpy.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fsg {
+
+// ---------------------------------------------------------------------------
+// Exact arithmetic in the partition's precision
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// Truncation toward zero (values here are >= 0 or NaN; saturating cvt keeps
+// out-of-domain lanes in range before the clamp).
+template <typename J> __device__ __forceinline__ J trunc_to(float v);
+template <typename J> __device__ __forceinline__ J trunc_to(double v);
+template <> __device__ __forceinline__ uint32_t trunc_to<uint32_t>(float v) { return __float2uint_rz(v); }
+template <> __device__ __forceinline__ uint32_t trunc_to<uint32_t>(double v) { return __double2uint_rz(v); }
+template <> __device__ __forceinline__ uint64_t trunc_to<uint64_t>(float v) { return __float2ull_rz(v); }
+template <> __device__ __forceinline__ uint64_t trunc_to<uint64_t>(double v) { return __double2ull_rz(v); }
+
+// nextafter(h, +inf) for a positive finite (or +inf) value: one ulp up.
+__device__ __forceinline__ float next_up(float v) {
+  return __int_as_float(__float_as_int(v) + (v < INFINITY ? 1 : 0));
+}
+__device__ __forceinline__ double next_up(double v) {
+  return __longlong_as_double(__double_as_longlong(v) + (v < (double)INFINITY ? 1ll : 0ll));
+}
+
+// Order-preserving key of a non-negative float (positive floats sort like
+// their bit patterns), for exact atomic min reductions.
+__device__ __forceinline__ unsigned long long order_key(float v) { return (unsigned long long)__float_as_uint(v); }
+__device__ __forceinline__ unsigned long long order_key(double v) { return (unsigned long long)__double_as_longlong(v); }
+template <typename T> __device__ __forceinline__ T from_key(unsigned long long k);
+template <> __device__ __forceinline__ float from_key<float>(unsigned long long k) { return __uint_as_float((unsigned)k); }
+template <> __device__ __forceinline__ double from_key<double>(unsigned long long k) { return __longlong_as_double((long long)k); }
+
+// ---------------------------------------------------------------------------
+// Streaming global memory access (the query stream is touched exactly once)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];"
+               : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+
+__device__ __forceinline__ void st_stream(int4* p, int4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(longlong2* p, longlong2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(int32_t* p, int32_t v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(int64_t* p, int64_t v) {
+  __stcs(reinterpret_cast<long long*>(p), (long long)v);
+}
+
+// Read-only table gathers through L2 (tables are re-read by every query).
+template <typename T> __device__ __forceinline__ T ld_table(const T* p) { return __ldg(p); }
+
+// ---------------------------------------------------------------------------
+// Shared-memory staging with the bulk-copy engine (cp.async.bulk + mbarrier)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// One bulk copy global -> shared (dst/src 16 B aligned, bytes % 16 == 0,
+// bytes < 2^20 per mbarrier phase).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// A table to stage: `bytes` from global `src` into shared `dst`.
+struct StageSeg {
+  void* dst;
+  const void* src;
+  uint32_t bytes;
+};
+
+// Stage up to 3 tables into shared memory.  The 16-B aligned body of each
+// table goes through the bulk-copy engine (one elected thread issues, the
+// mbarrier's transaction count tracks completion); any misaligned head/tail
+// bytes are copied by the remaining threads.  On return all tables are
+// visible to every thread of the CTA.
+__device__ __forceinline__ void stage_tables(const StageSeg* segs, int nseg, uint64_t* bar) {
+  const int tid = threadIdx.x;
+  if (tid == 0) mbar_init(bar, 1);
+  __syncthreads();
+  uint32_t bulk_total = 0;
+  uint32_t body_lo[3], body_hi[3];
+  for (int s = 0; s < nseg; ++s) {
+    uintptr_t src = reinterpret_cast<uintptr_t>(segs[s].src);
+    uintptr_t dst = reinterpret_cast<uintptr_t>(segs[s].dst);
+    uint32_t lo = 0, hi = 0;
+    // bulk copy needs src and dst with the same alignment mod 16
+    if (((src ^ dst) & 15u) == 0) {
+      lo = (uint32_t)((16u - (src & 15u)) & 15u);
+      if (lo > segs[s].bytes) lo = segs[s].bytes;
+      hi = lo + ((segs[s].bytes - lo) & ~15u);
+    }
+    body_lo[s] = lo;
+    body_hi[s] = hi;
+    bulk_total += hi - lo;
+  }
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar, bulk_total);
+    for (int s = 0; s < nseg; ++s) {
+      uint32_t off = body_lo[s];
+      while (off < body_hi[s]) {
+        uint32_t n = body_hi[s] - off;
+        if (n > (1u << 16)) n = 1u << 16;  // keep individual copies moderate
+        bulk_g2s(static_cast<char*>(segs[s].dst) + off, static_cast<const char*>(segs[s].src) + off, n,
+                 bar);
+        off += n;
+      }
+    }
+  }
+  // head/tail (and whole misaligned tables) byte copies
+  for (int s = 0; s < nseg; ++s) {
+    const unsigned char* src = static_cast<const unsigned char*>(segs[s].src);
+    unsigned char* dst = static_cast<unsigned char*>(segs[s].dst);
+    for (uint32_t b = tid; b < body_lo[s]; b += blockDim.x) dst[b] = src[b];
+    for (uint32_t b = body_hi[s] + tid; b < segs[s].bytes; b += blockDim.x) dst[b] = src[b];
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+}
+
+// ---------------------------------------------------------------------------
+// Warp reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// Fold a lane's first-bad candidate into the global word (one atomic per
+// warp that saw a bad query; nothing on the clean path but a vote).
+__device__ __forceinline__ void flush_first_bad(unsigned long long mine, unsigned long long* first_bad) {
+  if (__any_sync(0xffffffffu, mine != ~0ull)) {
+    unsigned long long w = warp_min_u64(mine);
+    if ((threadIdx.x & 31) == 0) atomicMin(first_bad, w);
+  }
+}
+
+}  // namespace fsg

@@ -1,0 +1,583 @@
+// fsgpu.cu — C-ABI implementation (include/fsgpu.h).
+//
+// Host-side runtime of the library: argument validation, table placement
+// (shared memory vs L2), launch geometry (persistent grid sized from the
+// occupancy calculator x SM count), the certification loop of
+// direct.compute_h_r, and the chunked host<->device pipeline of the
+// end-to-end batch_search path.  No torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/fsgpu.h"
+#include "build.cuh"
+#include "common.cuh"
+#include "search.cuh"
+
+using namespace fsg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define FS_CUDA(expr)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(FS_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+size_t smem_budget() {
+  int dev = 0, optin = 227 * 1024;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return (size_t)optin - 1024;  // static smem (mbarrier, reductions) + slack
+}
+
+int bit_length(uint64_t v) { return v ? 64 - __builtin_clzll(v) : 0; }
+
+inline uint64_t align128(uint64_t b) { return (b + 127) & ~127ull; }
+
+int grid_1d(uint64_t work, int threads) {
+  uint64_t b = (work + threads - 1) / threads;
+  uint64_t cap = (uint64_t)sm_count() * 8;
+  if (b > cap) b = cap;
+  return (int)std::max<uint64_t>(b, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Placement
+// ---------------------------------------------------------------------------
+struct Placement {
+  uint32_t x_bytes = 0;      // bytes staged at smem offset 0 (X / padded / tree / top)
+  uint32_t table_bytes = 0;  // bytes staged after align128(x_bytes) (K / records)
+  int top_bits = 0;          // bitset2
+  bool xs = false, ks = false, top = false;
+  int flags = FS_PLACE_GLOBAL;
+  size_t smem = 0;
+  const void* seg0_src = nullptr;  // bulk-copied segments
+  const void* seg1_src = nullptr;
+  uint32_t seg0_bytes = 0, seg1_bytes = 0;
+  int nseg = 0;
+};
+
+int validate_plan(const fs_plan* p) {
+  if (!p) return fail(FS_INVALID_ARG, "plan is NULL");
+  if (p->dtype != FS_F32 && p->dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  if (p->n1 < 2) return fail(FS_INVALID_ARG, "a partition needs at least two knots");
+  if (p->n1 - 1 >= (1ull << 32)) return fail(FS_INVALID_ARG, "table entries are 32-bit; partition is too large");
+  if (!p->x) return fail(FS_INVALID_ARG, "plan.x is NULL");
+  switch (p->algorithm) {
+    case FS_ALGO_DIRECT:
+    case FS_ALGO_DIRECT_GAP2:
+    case FS_ALGO_DIRECT_GENERIC:
+    case FS_ALGO_DIRECT_CACHE:
+      if (!p->table) return fail(FS_INVALID_ARG, "direct plan needs its table");
+      if (p->q < 1) return fail(FS_INVALID_ARG, "gap must be >= 1");
+      if (p->algorithm == FS_ALGO_DIRECT_CACHE && p->q != 1)
+        return fail(FS_INVALID_ARG, "fused records pair with the gap-1 kernel");
+      break;
+    case FS_ALGO_BITSET2:
+    case FS_ALGO_EYTZINGER:
+      if (!p->table) return fail(FS_INVALID_ARG, "plan needs its padded/tree table");
+      if (p->pbits < 1 || p->pbits > 31) return fail(FS_INVALID_ARG, "pbits out of range");
+      break;
+    case FS_ALGO_CLASSIC:
+    case FS_ALGO_BITSET1:
+    case FS_ALGO_BITSET3:
+    case FS_ALGO_OFFSET:
+      if (p->pbits < 1 || p->pbits > 32) return fail(FS_INVALID_ARG, "pbits out of range");
+      break;
+    default:
+      return fail(FS_INVALID_ARG, "unknown algorithm");
+  }
+  return FS_OK;
+}
+
+Placement place(const fs_plan* p) {
+  Placement pl;
+  const size_t es = p->dtype == FS_F32 ? 4 : 8;
+  const size_t budget = smem_budget();
+  const bool force_global = p->smem_policy == 1;
+  switch (p->algorithm) {
+    case FS_ALGO_DIRECT:
+    case FS_ALGO_DIRECT_GAP2:
+    case FS_ALGO_DIRECT_GENERIC: {
+      const uint64_t xb = p->n1 * es, kb = (p->r + 1) * 4;
+      if (force_global || p->r >= (1ull << 32)) break;
+      if (align128(xb) + kb <= budget) {
+        pl.xs = pl.ks = true;
+      } else if (xb <= budget) {
+        pl.xs = true;
+      } else if (kb <= budget) {
+        pl.ks = true;
+      }
+      if (pl.xs) {
+        pl.x_bytes = (uint32_t)xb;
+        pl.seg0_src = p->x;
+        pl.seg0_bytes = (uint32_t)xb;
+        pl.nseg = 1;
+        pl.flags |= FS_PLACE_SMEM_X;
+      }
+      if (pl.ks) {
+        pl.table_bytes = (uint32_t)kb;
+        if (pl.xs) {
+          pl.seg1_src = p->table;
+          pl.seg1_bytes = (uint32_t)kb;
+          pl.nseg = 2;
+        } else {
+          pl.seg0_src = p->table;
+          pl.seg0_bytes = (uint32_t)kb;
+          pl.nseg = 1;
+        }
+        pl.flags |= FS_PLACE_SMEM_K;
+      }
+      pl.smem = pl.xs && pl.ks ? align128(pl.x_bytes) + pl.table_bytes : (pl.xs ? pl.x_bytes : pl.table_bytes);
+      break;
+    }
+    case FS_ALGO_DIRECT_CACHE: {
+      const uint64_t rb = (p->r + 1) * (es == 4 ? 8 : 16);
+      if (!force_global && p->r < (1ull << 32) && rb <= budget) {
+        pl.ks = true;
+        pl.table_bytes = (uint32_t)rb;
+        pl.seg0_src = p->table;
+        pl.seg0_bytes = (uint32_t)rb;
+        pl.nseg = 1;
+        pl.smem = rb;
+        pl.flags |= FS_PLACE_SMEM_K;
+      }
+      break;
+    }
+    case FS_ALGO_BITSET2: {
+      if (force_global) break;
+      const uint64_t full = (1ull << p->pbits) * es;
+      pl.top = true;
+      if (full <= budget) {
+        pl.top_bits = p->pbits;
+        pl.x_bytes = (uint32_t)full;
+        pl.seg0_src = p->table;
+        pl.seg0_bytes = (uint32_t)full;
+        pl.nseg = 1;
+        pl.smem = full;
+        pl.flags |= FS_PLACE_SMEM_X;
+      } else {
+        int tb = bit_length(budget / es) - 1;
+        tb = std::min(tb, p->pbits);
+        pl.top_bits = tb;
+        pl.x_bytes = (uint32_t)((1ull << tb) * es);
+        pl.smem = pl.x_bytes;
+        pl.flags |= FS_PLACE_SMEM_TOP;
+      }
+      break;
+    }
+    default: {  // classic / bitset1 / bitset3 / offset on X; eytzinger on its tree
+      if (force_global) break;
+      const bool tree = p->algorithm == FS_ALGO_EYTZINGER;
+      const uint64_t xb = tree ? ((1ull << p->pbits) - 1) * es : p->n1 * es;
+      if (xb <= budget) {
+        pl.xs = true;
+        pl.x_bytes = (uint32_t)xb;
+        pl.seg0_src = tree ? p->table : p->x;
+        pl.seg0_bytes = (uint32_t)xb;
+        pl.nseg = 1;
+        pl.smem = xb;
+        pl.flags |= FS_PLACE_SMEM_X;
+      }
+      break;
+    }
+  }
+  return pl;
+}
+
+// ---------------------------------------------------------------------------
+// Launch
+// ---------------------------------------------------------------------------
+constexpr int kUnroll = 4;
+
+template <typename T, typename OutT, typename Probe>
+int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t m, OutT* out,
+                 unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
+  auto kern = search_kernel<T, OutT, Probe, kUnroll>;
+  const size_t smem = pl.smem;
+  if (smem > 0) FS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // One CTA per SM with a big staged table wants the widest CTA the register
+  // file allows; otherwise 512 threads and several CTAs per SM.
+  int threads = 0, per_sm = 0;
+  const int cands_big[] = {1024, 512, 256, 128};
+  const int cands_small[] = {512, 256, 128, 0};
+  const int* cands = pl.smem > 113 * 1024 ? cands_big : cands_small;
+  for (int c = 0; c < 4 && cands[c]; ++c) {
+    FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cands[c], smem));
+    if (per_sm >= 1) {
+      threads = cands[c];
+      break;
+    }
+  }
+  if (per_sm < 1) return fail(FS_TOO_LARGE, "search kernel does not fit on an SM with this table placement");
+
+  StreamShape sh;
+  sh.m = m;
+  sh.base = base;
+  const uintptr_t za = reinterpret_cast<uintptr_t>(z);
+  uint64_t head = ((16 - (za & 15)) & 15) / sizeof(T);
+  if (head > m) head = m;
+  sh.head = head;
+  sh.nvec = (m - head) / 4;
+  DevPlan<T> d = dp;
+  d.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) + head * sizeof(OutT)) & 15) == 0;
+
+  const uint64_t full = (uint64_t)per_sm * sm_count();
+  uint64_t want = (sh.nvec + (uint64_t)threads * kUnroll - 1) / ((uint64_t)threads * kUnroll);
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(full, want));
+
+  StageSeg s0{nullptr, pl.seg0_src, pl.seg0_bytes};
+  StageSeg s1{nullptr, pl.seg1_src, pl.seg1_bytes};
+  kern<<<grid, threads, smem, st>>>(z, out, sh, d, first_bad, s0, s1, pl.nseg);
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+template <typename T>
+DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
+  DevPlan<T> d{};
+  d.x = static_cast<const T*>(p->x);
+  d.table = p->table;
+  d.n1 = p->n1;
+  d.r = p->r;
+  d.h = (T)p->h;
+  d.x0 = (T)p->x0;
+  d.xn = (T)p->xn;
+  d.q = p->q;
+  d.pbits = p->pbits;
+  d.top_bits = pl.top_bits;
+  const uint64_t n = p->n1 - 1;
+  d.off_f = (uint32_t)((n + 1) >> 1);
+  d.off_s = (uint32_t)(n + 1 - d.off_f);
+  d.off_j = (uint32_t)(bit_length(n + 1) - 1);
+  d.x_smem_bytes = pl.xs || pl.top ? pl.x_bytes : 0;
+  d.table_smem_bytes = pl.ks ? pl.table_bytes : 0;
+  // With only K staged it sits at offset 0.
+  if (!pl.xs && !pl.top) d.x_smem_bytes = 0;
+  return d;
+}
+
+template <typename T, typename OutT, typename J, int GAP>
+int dispatch_direct(const DevPlan<T>& d, const Placement& pl, const T* z, uint64_t m, OutT* out,
+                    unsigned long long* fb, uint64_t base, cudaStream_t st) {
+  if (pl.xs && pl.ks) return launch_probe<T, OutT, DirectProbe<T, J, GAP, true, true>>(d, pl, z, m, out, fb, base, st);
+  if (pl.xs) return launch_probe<T, OutT, DirectProbe<T, J, GAP, true, false>>(d, pl, z, m, out, fb, base, st);
+  if (pl.ks) return launch_probe<T, OutT, DirectProbe<T, J, GAP, false, true>>(d, pl, z, m, out, fb, base, st);
+  return launch_probe<T, OutT, DirectProbe<T, J, GAP, false, false>>(d, pl, z, m, out, fb, base, st);
+}
+
+template <typename T, typename OutT, int ALGO>
+int dispatch_compare(const DevPlan<T>& d, const Placement& pl, const T* z, uint64_t m, OutT* out,
+                     unsigned long long* fb, uint64_t base, cudaStream_t st) {
+  if (pl.xs) return launch_probe<T, OutT, CompareProbe<T, ALGO, true>>(d, pl, z, m, out, fb, base, st);
+  return launch_probe<T, OutT, CompareProbe<T, ALGO, false>>(d, pl, z, m, out, fb, base, st);
+}
+
+template <typename T, typename OutT>
+int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT* out, unsigned long long* fb,
+             uint64_t base, cudaStream_t st) {
+  const DevPlan<T> d = make_devplan<T>(p, pl);
+  const bool wide = p->r >= (1ull << 32);
+  switch (p->algorithm) {
+    case FS_ALGO_DIRECT:
+      if (wide) return launch_probe<T, OutT, DirectProbe<T, uint64_t, 1, false, false>>(d, pl, z, m, out, fb, base, st);
+      return dispatch_direct<T, OutT, uint32_t, 1>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_DIRECT_GAP2:
+      if (wide) return launch_probe<T, OutT, DirectProbe<T, uint64_t, 2, false, false>>(d, pl, z, m, out, fb, base, st);
+      return dispatch_direct<T, OutT, uint32_t, 2>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_DIRECT_GENERIC:
+      if (wide) return launch_probe<T, OutT, DirectProbe<T, uint64_t, 3, false, false>>(d, pl, z, m, out, fb, base, st);
+      return dispatch_direct<T, OutT, uint32_t, 3>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_DIRECT_CACHE:
+      if (wide) return launch_probe<T, OutT, CacheProbe<T, uint64_t, false>>(d, pl, z, m, out, fb, base, st);
+      if (pl.ks) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
+      return launch_probe<T, OutT, CacheProbe<T, uint32_t, false>>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_BITSET2:
+      if (pl.top) return launch_probe<T, OutT, Bitset2Probe<T, true>>(d, pl, z, m, out, fb, base, st);
+      return launch_probe<T, OutT, Bitset2Probe<T, false>>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_CLASSIC: return dispatch_compare<T, OutT, 0>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_BITSET1: return dispatch_compare<T, OutT, 1>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_BITSET3: return dispatch_compare<T, OutT, 3>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_OFFSET: return dispatch_compare<T, OutT, 4>(d, pl, z, m, out, fb, base, st);
+    case FS_ALGO_EYTZINGER: return dispatch_compare<T, OutT, 5>(d, pl, z, m, out, fb, base, st);
+  }
+  return fail(FS_INVALID_ARG, "unknown algorithm");
+}
+
+// Launch the search over z[0..m) (global positions base..base+m); no memset.
+int launch_search(const fs_plan* p, const Placement& pl, const void* z, uint64_t m, void* out, int out_bytes,
+                  unsigned long long* fb, uint64_t base, cudaStream_t st) {
+  if (m == 0) return FS_OK;
+  if (p->dtype == FS_F32) {
+    if (out_bytes == 4)
+      return dispatch<float, int32_t>(p, pl, static_cast<const float*>(z), m, static_cast<int32_t*>(out), fb, base, st);
+    return dispatch<float, int64_t>(p, pl, static_cast<const float*>(z), m, static_cast<int64_t*>(out), fb, base, st);
+  }
+  if (out_bytes == 4)
+    return dispatch<double, int32_t>(p, pl, static_cast<const double*>(z), m, static_cast<int32_t*>(out), fb, base, st);
+  return dispatch<double, int64_t>(p, pl, static_cast<const double*>(z), m, static_cast<int64_t*>(out), fb, base, st);
+}
+
+int check_search_args(const fs_plan* p, const void* z, uint64_t m, const void* out, int out_bytes,
+                      const void* fb) {
+  int rc = validate_plan(p);
+  if (rc) return rc;
+  if (out_bytes != 4 && out_bytes != 8) return fail(FS_INVALID_ARG, "out_bytes must be 4 (int32) or 8 (int64)");
+  if (!fb) return fail(FS_INVALID_ARG, "first_bad word is NULL");
+  if (m && (!z || !out)) return fail(FS_INVALID_ARG, "query/output pointer is NULL");
+  const size_t es = p->dtype == FS_F32 ? 4 : 8;
+  if (reinterpret_cast<uintptr_t>(z) % es || reinterpret_cast<uintptr_t>(out) % out_bytes)
+    return fail(FS_INVALID_ARG, "query/output arrays must be element-aligned");
+  return FS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Certification driver
+// ---------------------------------------------------------------------------
+template <typename T>
+int certify_impl(const T* x, uint64_t n1, int qbits, int q, CertStatus* st, T* h_out, T* h_start_out,
+                 uint64_t* r_out, uint32_t* incr_out, int64_t* pos_out, cudaStream_t s) {
+  constexpr int NT = 256;
+  const uint64_t n = n1 - 1;
+  const uint64_t basis = std::min<uint64_t>((uint64_t)q, n);
+  const int grid = grid_1d(n1, NT);
+  cert_init_kernel<<<1, 1, 0, s>>>(st);
+  certify_prep<T, NT><<<grid, NT, 0, s>>>(x, n1, (uint64_t)q, basis, st);
+  certify_finalize<T><<<1, 1, 0, s>>>(x, n1, qbits, st);
+  certify_check<T, NT><<<grid, NT, 0, s>>>(x, n1, (uint64_t)q, st);
+  FS_CUDA(cudaGetLastError());
+  CertStatus hs;
+  for (;;) {
+    FS_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaStreamSynchronize(s));
+    if (hs.status != 0 || hs.fail == 0) break;
+    certify_grow<T><<<1, 1, 0, s>>>(x, n1, qbits, st);
+    certify_check<T, NT><<<grid, NT, 0, s>>>(x, n1, (uint64_t)q, st);
+    FS_CUDA(cudaGetLastError());
+  }
+  if (h_out) *h_out = (T)hs.h;
+  if (h_start_out) *h_start_out = (T)hs.h_start;
+  if (incr_out) *incr_out = hs.increments;
+  if (hs.status == 1) {
+    if (pos_out) *pos_out = (int64_t)hs.collide_pos;
+    return fail(FS_NOT_DISTINGUISHABLE, "rounded offsets collide");
+  }
+  if (hs.status == 2) return fail(FS_OVERFLOW, "floor(H * D_N) >= 2**qbits");
+  if (r_out) *r_out = (uint64_t)hs.r_float;
+  return FS_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* fs_version(void) { return "fsgpu 0.1.0 (sm_100a)"; }
+
+const char* fs_last_error(void) { return g_last_error.c_str(); }
+
+size_t fs_workspace_bytes(void) { return (sizeof(CertStatus) + 255) & ~(size_t)255; }
+
+int fs_certify(int32_t dtype, const void* x_dev, uint64_t n1, int32_t qbits, int32_t q, void* ws_dev, void* h_out,
+               void* h_start_out, uint64_t* r_out, uint32_t* increments_out, int64_t* pos_out, void* stream) {
+  if (qbits != 32 && qbits != 64) return fail(FS_INVALID_ARG, "qbits must be 32 or 64");
+  if (q < 1) return fail(FS_INVALID_ARG, "gap must be >= 1");
+  if (n1 < 2) return fail(FS_INVALID_ARG, "a partition needs at least two values");
+  if (!x_dev || !ws_dev) return fail(FS_INVALID_ARG, "NULL pointer");
+  auto* st = static_cast<CertStatus*>(ws_dev);
+  if (dtype == FS_F32)
+    return certify_impl<float>(static_cast<const float*>(x_dev), n1, qbits, q, st, static_cast<float*>(h_out),
+                               static_cast<float*>(h_start_out), r_out, increments_out, pos_out, as_stream(stream));
+  if (dtype == FS_F64)
+    return certify_impl<double>(static_cast<const double*>(x_dev), n1, qbits, q, st, static_cast<double*>(h_out),
+                                static_cast<double*>(h_start_out), r_out, increments_out, pos_out, as_stream(stream));
+  return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+}
+
+int fs_build_table(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t q, uint32_t* k_dev,
+                   uint64_t* f_scratch_dev, void* ws_dev, void* stream) {
+  if (n1 < 2) return fail(FS_INVALID_ARG, "a partition needs at least two values");
+  if (n1 - 1 >= (1ull << 32)) return fail(FS_INVALID_ARG, "table entries are 32-bit; partition is too large");
+  if (q < 1) return fail(FS_INVALID_ARG, "gap must be >= 1");
+  if (!x_dev || !k_dev || !f_scratch_dev || !ws_dev) return fail(FS_INVALID_ARG, "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  auto* st = static_cast<CertStatus*>(ws_dev);
+  cert_init_kernel<<<1, 1, 0, s>>>(st);
+  const int g = grid_1d(n1, 256);
+  if (dtype == FS_F32)
+    knot_buckets_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(x_dev), n1, (float)h, r, f_scratch_dev, st);
+  else if (dtype == FS_F64)
+    knot_buckets_kernel<double><<<g, 256, 0, s>>>(static_cast<const double*>(x_dev), n1, h, r, f_scratch_dev, st);
+  else
+    return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  FS_CUDA(cudaGetLastError());
+  unsigned long long inconsistent = 0;
+  FS_CUDA(cudaMemcpyAsync(&inconsistent, &st->inconsistent, sizeof(inconsistent), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  if (inconsistent) return fail(FS_INCONSISTENT, "(h, r) pair is inconsistent with this partition");
+  constexpr int NT = 256, ITEMS = 16;
+  const uint64_t tiles = (r + 1 + (uint64_t)NT * ITEMS - 1) / ((uint64_t)NT * ITEMS);
+  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)sm_count() * 8);
+  if (q == 1)
+    fill_table_kernel<NT, ITEMS, false><<<grid, NT, 0, s>>>(f_scratch_dev, n1, r, k_dev);
+  else
+    fill_table_kernel<NT, ITEMS, true><<<grid, NT, 0, s>>>(f_scratch_dev, n1, r, k_dev);
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t* f_dev, void* stream) {
+  if (!x_dev || !f_dev || n1 < 1) return fail(FS_INVALID_ARG, "bad arguments");
+  cudaStream_t s = as_stream(stream);
+  const int g = grid_1d(n1, 256);
+  // r = ~0 never matches, and the status pointer is unused when NULL-checked below
+  if (dtype == FS_F32)
+    knot_buckets_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(x_dev), n1, (float)h, ~0ull, f_dev, nullptr);
+  else if (dtype == FS_F64)
+    knot_buckets_kernel<double><<<g, 256, 0, s>>>(static_cast<const double*>(x_dev), n1, h, ~0ull, f_dev, nullptr);
+  else
+    return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_build_fused(int32_t dtype, const void* x_dev, uint64_t n1, const uint32_t* k_dev, uint64_t r, void* rec_dev,
+                   void* stream) {
+  if (!x_dev || !k_dev || !rec_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  cudaStream_t s = as_stream(stream);
+  const int g = grid_1d(r + 1, 256);
+  if (dtype == FS_F32)
+    fill_fused_f32<<<g, 256, 0, s>>>(static_cast<const float*>(x_dev), k_dev, r, static_cast<uint2*>(rec_dev));
+  else if (dtype == FS_F64)
+    fill_fused_f64<<<g, 256, 0, s>>>(static_cast<const double*>(x_dev), k_dev, r, static_cast<double2*>(rec_dev));
+  else
+    return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_build_padded(int32_t dtype, const void* x_dev, uint64_t n1, int32_t pbits, void* xpad_dev, void* stream) {
+  if (!x_dev || !xpad_dev || n1 < 2 || pbits < 1 || pbits > 40 || (1ull << pbits) < n1)
+    return fail(FS_INVALID_ARG, "bad arguments");
+  cudaStream_t s = as_stream(stream);
+  const uint64_t len = 1ull << pbits;
+  const int g = grid_1d(len, 256);
+  if (dtype == FS_F32)
+    pad_right_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(x_dev), n1, len, static_cast<float*>(xpad_dev));
+  else if (dtype == FS_F64)
+    pad_right_kernel<double><<<g, 256, 0, s>>>(static_cast<const double*>(x_dev), n1, len, static_cast<double*>(xpad_dev));
+  else
+    return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_build_eytzinger(int32_t dtype, const void* x_dev, uint64_t n1, int32_t depth, void* tree_dev, void* stream) {
+  if (!x_dev || !tree_dev || n1 < 2 || depth < 1 || depth > 40 || ((1ull << depth) - 1) < n1)
+    return fail(FS_INVALID_ARG, "bad arguments");
+  cudaStream_t s = as_stream(stream);
+  const int g = grid_1d((1ull << depth) - 1, 256);
+  if (dtype == FS_F32)
+    eytzinger_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(x_dev), n1, depth, static_cast<float*>(tree_dev));
+  else if (dtype == FS_F64)
+    eytzinger_kernel<double><<<g, 256, 0, s>>>(static_cast<const double*>(x_dev), n1, depth, static_cast<double*>(tree_dev));
+  else
+    return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* out_dev, int32_t out_bytes,
+                     unsigned long long* first_bad_dev, void* stream) {
+  int rc = check_search_args(plan, z_dev, m, out_dev, out_bytes, first_bad_dev);
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
+  return launch_search(plan, place(plan), z_dev, m, out_dev, out_bytes, first_bad_dev, 0, s);
+}
+
+int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host, int32_t out_bytes, void* z_dev,
+                   void* out_dev, unsigned long long* first_bad_dev, uint64_t chunk_elems, int64_t* pos_out,
+                   void* stream, void* copy_stream) {
+  int rc = check_search_args(plan, z_dev, m, out_dev, out_bytes, first_bad_dev);
+  if (rc) return rc;
+  if (m && (!z_host || !out_host)) return fail(FS_INVALID_ARG, "host pointer is NULL");
+  cudaStream_t s = as_stream(stream), cs = as_stream(copy_stream);
+  const size_t es = plan->dtype == FS_F32 ? 4 : 8;
+  if (chunk_elems == 0) chunk_elems = (64ull << 20) / es;
+  chunk_elems = (chunk_elems + 3) & ~3ull;  // keep every chunk 16-B aligned on device
+  const Placement pl = place(plan);
+  FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
+  cudaEvent_t ev;
+  FS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  int status = FS_OK;
+  for (uint64_t off = 0; off < m && status == FS_OK; off += chunk_elems) {
+    const uint64_t n = std::min(chunk_elems, m - off);
+    const char* src = static_cast<const char*>(z_host) + off * es;
+    char* dst = static_cast<char*>(z_dev) + off * es;
+    cudaError_t e = cudaMemcpyAsync(dst, src, n * es, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev, 0);
+    if (e != cudaSuccess) {
+      status = fail(FS_CUDA_ERROR, std::string("chunk upload: ") + cudaGetErrorString(e));
+      break;
+    }
+    status = launch_search(plan, pl, dst, n, static_cast<char*>(out_dev) + off * out_bytes, out_bytes, first_bad_dev,
+                           off, s);
+  }
+  unsigned long long bad = ~0ull;
+  if (status == FS_OK) {
+    cudaError_t e = cudaMemcpyAsync(&bad, first_bad_dev, sizeof(bad), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("first-bad readback: ") + cudaGetErrorString(e));
+  }
+  cudaEventDestroy(ev);
+  if (status != FS_OK) return status;
+  if (bad != ~0ull) {
+    if (pos_out) *pos_out = (int64_t)bad;
+    return fail(FS_OUT_OF_DOMAIN, "query outside [X0, XN)");
+  }
+  if (m) {
+    FS_CUDA(cudaMemcpyAsync(out_host, out_dev, m * (uint64_t)out_bytes, cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaStreamSynchronize(s));
+  }
+  return FS_OK;
+}
+
+int fs_plan_placement(const fs_plan* plan, int32_t* placement_out, uint64_t* smem_bytes_out) {
+  int rc = validate_plan(plan);
+  if (rc) return rc;
+  const Placement pl = place(plan);
+  if (placement_out) *placement_out = pl.flags;
+  if (smem_bytes_out) *smem_bytes_out = pl.smem;
+  return FS_OK;
+}
+
+int fs_search_launches(const fs_plan* plan, uint64_t m) {
+  (void)plan;
+  return m ? 1 : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,361 @@
+// search.cuh — batch search kernels (the hot path).
+//
+// One persistent, grid-stride kernel template streams the query array Z
+// (128-bit evict-first loads, 128-bit streaming stores) and resolves each
+// query with an `Algo` probe.  Tables are staged into shared memory by the
+// bulk-copy engine when they fit, otherwise gathered
+// through L2 with ld.global.nc.  The out-of-domain check of batch_search
+// (batch.py:411-413) is fused: each lane keeps the smallest bad position it
+// saw and one atomicMin per warp folds it into a global word.
+//
+// Probes (each cites the reference kernel it restates):
+//   Direct<gap 1>     batch.py:315-317 / direct.py:570-574
+//   Direct<gap 2>     batch.py:341-343 / direct.py:577-589
+//   Direct<generic q> direct.py:592-598
+//   DirectCache       batch.py:368-371 / direct.py:601-610
+//   Bitset2           batch.py:193-200 / binsearch.py:72-86
+//   Bitset1 / Bitset3 batch.py:176-185, 208-216 / binsearch.py:60-69, 89-99
+//   Offset            batch.py:224-234 / binsearch.py:102-114
+//   Eytzinger         batch.py:242-246 / eytzinger.py:84-89
+//   Classic           binsearch.py:48-57
+#pragma once
+
+#include "common.cuh"
+
+namespace fsg {
+
+// Device image of fs_plan with typed scalars.
+template <typename T>
+struct DevPlan {
+  const T* x;            // knots
+  const void* table;     // K / records / padded / tree
+  uint64_t n1;           // N+1
+  uint64_t r;            // R (direct family)
+  T h, x0, xn;           // scale, domain
+  int32_t q;             // gap
+  int32_t pbits;         // bitset / eytzinger depth
+  int32_t top_bits;      // bitset2: levels served from smem
+  uint32_t off_f, off_s, off_j;  // offset search constants
+  uint32_t x_smem_bytes;     // bytes of X (or padded / tree / top table) staged; 0 = global
+  uint32_t table_smem_bytes; // bytes of K / records staged; 0 = global
+  int32_t out_vec_ok;        // output pointer co-aligned with the 16-B query groups
+  __host__ __device__ __forceinline__ uint32_t x_smem_bytes_aligned() const {
+    return (x_smem_bytes + 127u) & ~127u;
+  }
+};
+
+template <bool S, typename V>
+__device__ __forceinline__ V tload(const V* p, uint64_t i) {
+  if constexpr (S) return p[i];
+  else return __ldg(p + i);
+}
+
+// ---------------------------------------------------------------------------
+// Direct search, gap 1 / 2 / generic.  j = trunc(RN(RN(z - x0) * h)) in the
+// partition's precision (Appendix A.1), clamped to R so out-of-domain lanes
+// stay in bounds (in-domain j <= R always: RN is monotone and z < XN).
+// ---------------------------------------------------------------------------
+template <typename T, typename J, int GAP, bool XS, bool KS>
+struct DirectProbe {
+  const T* X;
+  const uint32_t* K;
+  T h, x0;
+  J r;
+  int q;
+  __device__ __forceinline__ DirectProbe(const DevPlan<T>& p, unsigned char* smem) {
+    X = XS ? reinterpret_cast<const T*>(smem) : p.x;
+    K = KS ? reinterpret_cast<const uint32_t*>(smem + p.x_smem_bytes_aligned()) : static_cast<const uint32_t*>(p.table);
+    h = p.h;
+    x0 = p.x0;
+    r = (J)p.r;
+    q = p.q;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    J j = trunc_to<J>(mul_rn(sub_rn(z, x0), h));
+    j = j < r ? j : r;
+    const uint32_t t = tload<KS>(K, j);
+    if constexpr (GAP == 1) {
+      return (int64_t)t - (z < tload<XS>(X, t) ? 1 : 0);
+    } else if constexpr (GAP == 2) {
+      // xpad[w+1] = X_w with xpad[0] = X0 (left_pad): the read of X_{t-1} is
+      // clamped to X0, which never satisfies z < X0 for in-domain z.
+      const uint32_t tm = t ? t - 1 : 0;
+      return (int64_t)t - (z < tload<XS>(X, t) ? 1 : 0) - (z < tload<XS>(X, tm) ? 1 : 0);
+    } else {
+      int64_t hits = 0;
+      for (int m = 0; m < q; ++m) {
+        const int64_t w = (int64_t)t - m;
+        hits += z < tload<XS>(X, (uint64_t)(w > 0 ? w : 0)) ? 1 : 0;
+      }
+      return (int64_t)t - hits;
+    }
+  }
+};
+
+// Cache-fused records: {u32 idx, f32 val} (8 B) / {u32 idx, u32 pad, f64 val}
+// (16 B), direct.py:337-342.  One gather resolves the query.
+template <typename T, typename J, bool RS>
+struct CacheProbe;
+
+template <typename J, bool RS>
+struct CacheProbe<float, J, RS> {
+  const uint2* R;
+  float h, x0;
+  J r;
+  __device__ __forceinline__ CacheProbe(const DevPlan<float>& p, unsigned char* smem) {
+    R = RS ? reinterpret_cast<const uint2*>(smem) : static_cast<const uint2*>(p.table);
+    h = p.h;
+    x0 = p.x0;
+    r = (J)p.r;
+  }
+  __device__ __forceinline__ int64_t operator()(float z) const {
+    J j = trunc_to<J>(mul_rn(sub_rn(z, x0), h));
+    j = j < r ? j : r;
+    const uint2 rec = tload<RS>(R, j);
+    return (int64_t)rec.x - (z < __uint_as_float(rec.y) ? 1 : 0);
+  }
+};
+
+template <typename J, bool RS>
+struct CacheProbe<double, J, RS> {
+  const double2* R;
+  double h, x0;
+  J r;
+  __device__ __forceinline__ CacheProbe(const DevPlan<double>& p, unsigned char* smem) {
+    R = RS ? reinterpret_cast<const double2*>(smem) : static_cast<const double2*>(p.table);
+    h = p.h;
+    x0 = p.x0;
+    r = (J)p.r;
+  }
+  __device__ __forceinline__ int64_t operator()(double z) const {
+    J j = trunc_to<J>(mul_rn(sub_rn(z, x0), h));
+    j = j < r ? j : r;
+    const double2 rec = tload<RS>(R, j);
+    const uint32_t idx = (uint32_t)(unsigned long long)__double_as_longlong(rec.x);
+    return (int64_t)idx - (z < rec.y ? 1 : 0);
+  }
+};
+
+// Branch-free bit-setting search over the right-padded array (Alg 3).
+// The first `top_bits` levels read a shared-memory copy of the padded array
+// subsampled at stride 2^(pbits-top_bits) (exactly the nodes those levels
+// can touch); deeper levels gather from global.  With top_bits == pbits the
+// whole padded array is in shared memory.
+template <typename T, bool TOP>
+struct Bitset2Probe {
+  const T* top;
+  const T* xpad;
+  int pbits, top_bits, shift;
+  __device__ __forceinline__ Bitset2Probe(const DevPlan<T>& p, unsigned char* smem) {
+    top = reinterpret_cast<const T*>(smem);
+    xpad = static_cast<const T*>(p.table);
+    pbits = p.pbits;
+    top_bits = TOP ? p.top_bits : 0;
+    shift = p.pbits - top_bits;
+  }
+  // Levels served from smem when the padded array itself does not fit: copy
+  // the strided subsample xpad[m << shift] cooperatively (plain loads).
+  static __device__ __forceinline__ void prologue(const DevPlan<T>& p, unsigned char* smem) {
+    if constexpr (TOP) {
+      if (p.top_bits < p.pbits) {
+        T* dst = reinterpret_cast<T*>(smem);
+        const T* src = static_cast<const T*>(p.table);
+        const int sh = p.pbits - p.top_bits;
+        for (uint32_t m = threadIdx.x; m < (1u << p.top_bits); m += blockDim.x) dst[m] = __ldg(src + ((uint64_t)m << sh));
+        __syncthreads();
+      }
+    }
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    uint32_t i = 0;
+    int lvl = 0;
+    if constexpr (TOP) {
+      for (; lvl < top_bits; ++lvl) {
+        const uint32_t r = i | (1u << (pbits - 1 - lvl));
+        if (z >= top[r >> shift]) i = r;
+      }
+    }
+    for (; lvl < pbits; ++lvl) {
+      const uint32_t r = i | (1u << (pbits - 1 - lvl));
+      if (z >= __ldg(xpad + r)) i = r;
+    }
+    return (int64_t)i;
+  }
+};
+
+// The other comparison kernels of batch.ALGORITHMS, on X in smem or global.
+template <typename T, int ALGO, bool XS>
+struct CompareProbe {
+  const T* X;
+  uint32_t n;
+  int pbits;
+  uint32_t F, S, Jc;
+  __device__ __forceinline__ CompareProbe(const DevPlan<T>& p, unsigned char* smem) {
+    X = XS ? reinterpret_cast<const T*>(smem)
+           : (ALGO == 5 ? static_cast<const T*>(p.table) : p.x);
+    n = (uint32_t)(p.n1 - 1);
+    pbits = p.pbits;
+    F = p.off_f;
+    S = p.off_s;
+    Jc = p.off_j;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    if constexpr (ALGO == 0) {  // classic, binsearch.py:48-57
+      uint32_t low = 0, high = n;
+      while (high - low > 1) {
+        const uint32_t mid = (low + high) >> 1;
+        if (z < tload<XS>(X, mid)) high = mid;
+        else low = mid;
+      }
+      return low;
+    } else if constexpr (ALGO == 1) {  // bitset1, binsearch.py:60-69
+      uint32_t i = 0;
+      for (uint32_t k = 1u << (pbits - 1); k; k >>= 1) {
+        const uint32_t r = i | k;
+        if (r < n && z >= tload<XS>(X, r)) i = r;
+      }
+      return i;
+    } else if constexpr (ALGO == 3) {  // bitset3, binsearch.py:89-99
+      uint32_t i = 0;
+      for (uint32_t k = 1u << (pbits - 1); k; k >>= 1) {
+        const uint32_t r = i | k;
+        const uint32_t w = r < n ? r : n;
+        if (z >= tload<XS>(X, w)) i = r;
+      }
+      return i;
+    } else if constexpr (ALGO == 4) {  // offset, binsearch.py:102-114
+      uint32_t i = z >= tload<XS>(X, F) ? F : 0;
+      uint32_t s = S;
+      for (uint32_t it = 0; it < Jc; ++it) {
+        const uint32_t half = s >> 1;
+        uint32_t f = i + half;
+        f = f < n ? f : n;  // never binds in domain; keeps bad lanes in bounds
+        if (z >= tload<XS>(X, f)) i = f;
+        s -= half;
+      }
+      return i;
+    } else {  // eytzinger, eytzinger.py:84-89 (X points at the tree)
+      uint64_t k = 1;
+      for (int l = 0; l < pbits; ++l) k = 2 * k + (z >= tload<XS>(X, k - 1) ? 1 : 0);
+      return (int64_t)k - (int64_t(1) << pbits) - 1;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Streaming driver
+// ---------------------------------------------------------------------------
+template <typename T> struct Vec4;
+template <> struct Vec4<float> {
+  float v[4];
+  __device__ __forceinline__ void load(const float* p) {
+    float4 a = ld_stream(reinterpret_cast<const float4*>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+};
+template <> struct Vec4<double> {
+  double v[4];
+  __device__ __forceinline__ void load(const double* p) {
+    double2 a = ld_stream(reinterpret_cast<const double2*>(p));
+    double2 b = ld_stream(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+};
+
+__device__ __forceinline__ void store4(int32_t* p, const int64_t (&o)[4], bool vec) {
+  if (vec) {
+    st_stream(reinterpret_cast<int4*>(p), make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) st_stream(p + e, (int32_t)o[e]);
+  }
+}
+__device__ __forceinline__ void store4(int64_t* p, const int64_t (&o)[4], bool vec) {
+  if (vec) {
+    st_stream(reinterpret_cast<longlong2*>(p), make_longlong2(o[0], o[1]));
+    st_stream(reinterpret_cast<longlong2*>(p) + 1, make_longlong2(o[2], o[3]));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) st_stream(p + e, o[e]);
+  }
+}
+
+// Probes without a prologue
+template <typename P, typename T>
+__device__ __forceinline__ auto run_prologue(const DevPlan<T>& p, unsigned char* smem, int)
+    -> decltype(P::prologue(p, smem), void()) {
+  P::prologue(p, smem);
+}
+template <typename P, typename T>
+__device__ __forceinline__ void run_prologue(const DevPlan<T>&, unsigned char*, long) {}
+
+struct StreamShape {
+  uint64_t m;      // total queries
+  uint64_t head;   // scalar queries before the first 16-B aligned group
+  uint64_t nvec;   // groups of 4 (vector path)
+  uint64_t base;   // global position of z[0] (for first-bad reporting)
+};
+
+template <typename T, typename OutT, typename Probe, int UNROLL>
+__global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh,
+                              DevPlan<T> plan, unsigned long long* __restrict__ first_bad,
+                              StageSeg seg0, StageSeg seg1, int nseg) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bar;
+  if (nseg > 0) {
+    StageSeg segs[2] = {seg0, seg1};
+    segs[0].dst = smem;
+    segs[1].dst = smem + plan.x_smem_bytes_aligned();
+    stage_tables(segs, nseg, &bar);
+  }
+  run_prologue<Probe>(plan, smem, 0);
+  const Probe probe(plan, smem);
+  const T x0 = plan.x0, xn = plan.xn;
+  unsigned long long mybad = ~0ull;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+
+  auto one = [&](uint64_t pos) {
+    const T v = ld_stream(z + pos);
+    const bool bad = !(v >= x0 && v < xn);
+    if (bad && pos < mybad) mybad = pos;
+    out[pos] = (OutT)probe(v);
+  };
+
+  {
+    // scalar head (< 4 queries) and tail (< 4 queries)
+    const uint64_t tail0 = sh.head + 4 * sh.nvec;
+    if (tid < sh.head) one(tid);
+    if (tid < sh.m - tail0) one(tail0 + tid);
+    const bool vec_out = plan.out_vec_ok != 0;
+    const T* zv = z + sh.head;
+    OutT* ov = out + sh.head;
+    for (uint64_t g0 = tid; g0 < sh.nvec; g0 += stride * UNROLL) {
+      Vec4<T> buf[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint64_t g = g0 + u * stride;
+        if (g < sh.nvec) buf[u].load(zv + 4 * g);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint64_t g = g0 + u * stride;
+        if (g < sh.nvec) {
+          int64_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const T v = buf[u].v[e];
+            const bool bad = !(v >= x0 && v < xn);
+            const uint64_t pos = sh.head + 4 * g + e;
+            if (bad && pos < mybad) mybad = pos;
+            o[e] = probe(v);
+          }
+          store4(ov + 4 * g, o, vec_out);
+        }
+      }
+    }
+  }
+  flush_first_bad(mybad == ~0ull ? ~0ull : mybad + sh.base, first_bad);
+}
+
+}  // namespace fsg
