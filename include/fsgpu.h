@@ -92,7 +92,14 @@ typedef struct fs_plan {
   int32_t q;          /* direct family: gap (1, 2, >2 generic)                   */
   int32_t pbits;      /* bitset family: bit_length(N); eytzinger: depth L   */
   int32_t smem_policy;/* 0 auto, 1 force global (L2) gathers                      */
-  int32_t reserved;
+  int32_t tune;       /* launch-geometry override for tuning runs, 0 = auto:
+                         bits 0-11 threads per CTA, bits 12-19 max CTAs per SM   */
+  const void* rank;   /* direct (gap 1) only, optional: rank directory of K
+                         (fs_build_rank); when set the kernel reads it instead
+                         of K.  NULL = read K.                                    */
+  const void* records;/* direct (gap 1) only, optional: fused (K[j], X[K[j]])
+                         records (fs_build_fused); used, staged in shared
+                         memory, when they fit there.  NULL = unused.            */
 } fs_plan;
 
 /* Library identification. */
@@ -136,6 +143,19 @@ int fs_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
 int fs_build_table(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
                    int32_t q, uint32_t* k_dev, uint64_t* f_scratch_dev, void* ws_dev,
                    void* stream);
+
+/*
+ * Rank directory of the gap-1 table: the same K in 2 bits per bucket.
+ * For a certified gap-1 index every bucket holds at most one knot, so
+ * K[j] = #{i : f_i < j} steps by 0 or 1 per bucket.  Word w (buckets
+ * 32w..32w+31) is {mask_w, base_w} (8 B): bit b of mask_w is set iff some
+ * f_i == 32w + b, and base_w = K[32w].  Then K[j] = base_w + popc(mask_w &
+ * (2^b - 1)) exactly, and when bit b is clear the fix-up comparison of
+ * batch.py:317 is known to hold (z < X[K[j]]) without reading X.
+ * dir_dev holds (r >> 5) + 1 uint2 words; f_scratch_dev n1 uint64.
+ */
+int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
+                  uint64_t* f_scratch_dev, void* dir_dev, void* stream);
 
 /*
  * Cache-fused (idx, val) records.  Replaces direct.with_fused

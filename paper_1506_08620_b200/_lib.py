@@ -57,6 +57,7 @@ EXPORTED = (
     "fs_certify",
     "fs_knot_buckets",
     "fs_build_table",
+    "fs_build_rank",
     "fs_build_fused",
     "fs_build_padded",
     "fs_build_eytzinger",
@@ -83,7 +84,9 @@ class FsPlan(ctypes.Structure):
         ("q", ctypes.c_int32),
         ("pbits", ctypes.c_int32),
         ("smem_policy", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("tune", ctypes.c_int32),
+        ("rank", ctypes.c_void_p),
+        ("records", ctypes.c_void_p),
     ]
 
 
@@ -112,6 +115,8 @@ def _declare(lib):
     lib.fs_knot_buckets.argtypes = [_i32, _vp, _u64, ctypes.c_double, _vp, _vp]
     lib.fs_build_table.restype = ctypes.c_int
     lib.fs_build_table.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp, _vp]
+    lib.fs_build_rank.restype = ctypes.c_int
+    lib.fs_build_rank.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _vp, _vp, _vp]
     lib.fs_build_fused.restype = ctypes.c_int
     lib.fs_build_fused.argtypes = [_i32, _vp, _u64, _vp, _u64, _vp, _vp]
     lib.fs_build_padded.restype = ctypes.c_int

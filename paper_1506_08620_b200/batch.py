@@ -54,6 +54,10 @@ THREADS_ENV = "FASTSEARCH_THREADS"
 #: host->device chunk for the end-to-end path (elements); ~64 MB of queries
 HOST_CHUNK_BYTES = 64 << 20
 
+#: fused (K[j], X[K[j]]) records are built for the direct kernel when they can
+#: be staged in shared memory (227 KB per CTA on sm_100a, less static use)
+SMEM_RECORDS_MAX = 226 * 1024
+
 _copy_streams: dict = {}
 
 
@@ -252,8 +256,35 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32) -> PreparedKern
     else:
         raise ValueError(f"unknown algorithm {algorithm!r}; pick one of {ALGORITHMS}")
     plan, keep = _plan_for(algorithm, structure, p)
+    if algorithm == "direct" and structure.q == 1:
+        rec_bytes = 8 if p.precision == "single" else 16
+        if (structure.r + 1) * rec_bytes <= SMEM_RECORDS_MAX:
+            rec = _device.empty((structure.r + 1) * rec_bytes, np.uint8)
+            rc = _lib.load().fs_build_fused(fs_dtype(p.precision), p.device_values().data_ptr(), len(p.values),
+                                            structure.k_dev.data_ptr(), structure.r, rec.data_ptr(),
+                                            _device.stream_ptr())
+            _lib.check(rc, what="fs_build_fused")
+            plan.records = rec.data_ptr()
+            keep.append(rec)
+        rank = build_rank_directory(p, structure)
+        plan.rank = rank.data_ptr()
+        keep.append(rank)
     scalar, lanes = _make_callables(plan, p)
     return PreparedKernel(algorithm, p, structure, scalar, lanes, plan=plan, buffers=tuple(keep))
+
+
+def build_rank_directory(p: SortedPartition, idx: DirectIndex):
+    """Device rank directory of the gap-1 table (fs_build_rank): K in 2 bits
+    per bucket, 8-B words {mask, K[32w]}.  The search kernel recovers K[j]
+    exactly from it and skips the X comparison for buckets without a knot."""
+    x = p.device_values()
+    f = _device.empty(len(p.values), np.uint64)
+    words = (idx.r >> 5) + 1
+    d = _device.empty(2 * words, np.uint32)
+    rc = _lib.load().fs_build_rank(fs_dtype(p.precision), x.data_ptr(), len(p.values), float(idx.h), idx.r,
+                                   f.data_ptr(), d.data_ptr(), _device.stream_ptr())
+    _lib.check(rc, what="fs_build_rank")
+    return d
 
 
 def prepare_with_fallback(p: SortedPartition, qbits: int = 32, algorithm: str = "direct",

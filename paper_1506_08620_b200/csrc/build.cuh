@@ -192,6 +192,24 @@ __global__ void __launch_bounds__(NT) fill_table_kernel(const uint64_t* __restri
   }
 }
 
+// Rank directory of the gap-1 table (see fs_build_rank in fsgpu.h): word w
+// = {mask of buckets 32w..32w+31 holding a knot, K[32w]}.  One thread per
+// word: K[32w] = lower_bound(f, 32w), then at most 32 knots set bits.
+__global__ void fill_rank_kernel(const uint64_t* __restrict__ f, uint64_t n1, uint64_t r, uint2* __restrict__ dir) {
+  const uint64_t words = (r >> 5) + 1;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j0 = w << 5;
+    const uint64_t base = bound_search<false>(f, 0, n1, j0);
+    uint32_t mask = 0;
+    for (uint64_t i = base; i < n1; ++i) {
+      const uint64_t fi = __ldg(f + i);
+      if (fi >= j0 + 32) break;
+      mask |= 1u << (uint32_t)(fi - j0);
+    }
+    dir[w] = make_uint2(mask, (uint32_t)base);
+  }
+}
+
 // Fused (idx, val) records.  direct.py:553-561.
 __global__ void fill_fused_f32(const float* __restrict__ x, const uint32_t* __restrict__ K, uint64_t r,
                                uint2* __restrict__ rec) {

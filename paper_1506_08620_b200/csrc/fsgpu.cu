@@ -75,6 +75,8 @@ struct Placement {
   const void* seg1_src = nullptr;
   uint32_t seg0_bytes = 0, seg1_bytes = 0;
   int nseg = 0;
+  int tune = 0;          // fs_plan.tune (launch-geometry override)
+  bool records = false;  // direct served from fused records in smem
 };
 
 int validate_plan(const fs_plan* p) {
@@ -112,17 +114,39 @@ int validate_plan(const fs_plan* p) {
 
 Placement place(const fs_plan* p) {
   Placement pl;
+  pl.tune = p->tune;
   const size_t es = p->dtype == FS_F32 ? 4 : 8;
   const size_t budget = smem_budget();
   const bool force_global = p->smem_policy == 1;
-  switch (p->algorithm) {
+  // direct (gap 1): fused records staged in smem when they fit (one 8/16-B
+  // conflict-light gather per query); else the rank directory; else K.
+  if (p->algorithm == FS_ALGO_DIRECT && p->records && p->q == 1 && !force_global && p->r < (1ull << 32)) {
+    const uint64_t rb = (p->r + 1) * (es == 4 ? 8 : 16);
+    if (rb <= budget) {
+      pl.records = pl.ks = true;
+      pl.table_bytes = (uint32_t)rb;
+      pl.seg0_src = p->records;
+      pl.seg0_bytes = (uint32_t)rb;
+      pl.nseg = 1;
+      pl.smem = rb;
+      pl.flags |= FS_PLACE_SMEM_K;
+      return pl;
+    }
+  }
+  const bool use_rank = p->algorithm == FS_ALGO_DIRECT && p->rank != nullptr && p->q == 1;
+  switch (use_rank ? -1 : p->algorithm) {
+    case -1:  // direct, gap 1, over the rank directory: X and/or directory in smem
     case FS_ALGO_DIRECT:
     case FS_ALGO_DIRECT_GAP2:
     case FS_ALGO_DIRECT_GENERIC: {
-      const uint64_t xb = p->n1 * es, kb = (p->r + 1) * 4;
+      const uint64_t xb = p->n1 * es;
+      const uint64_t kb = use_rank ? ((p->r >> 5) + 1) * 8 : (p->r + 1) * 4;
+      const void* tab = use_rank ? p->rank : p->table;
       if (force_global || p->r >= (1ull << 32)) break;
       if (align128(xb) + kb <= budget) {
         pl.xs = pl.ks = true;
+      } else if (use_rank && kb <= budget) {
+        pl.ks = true;  // every query reads the directory, few read X
       } else if (xb <= budget) {
         pl.xs = true;
       } else if (kb <= budget) {
@@ -138,11 +162,11 @@ Placement place(const fs_plan* p) {
       if (pl.ks) {
         pl.table_bytes = (uint32_t)kb;
         if (pl.xs) {
-          pl.seg1_src = p->table;
+          pl.seg1_src = tab;
           pl.seg1_bytes = (uint32_t)kb;
           pl.nseg = 2;
         } else {
-          pl.seg0_src = p->table;
+          pl.seg0_src = tab;
           pl.seg0_bytes = (uint32_t)kb;
           pl.nseg = 1;
         }
@@ -216,12 +240,16 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
   auto kern = search_kernel<T, OutT, Probe, kUnroll>;
   const size_t smem = pl.smem;
   if (smem > 0) FS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // One CTA per SM with a big staged table wants the widest CTA the register
-  // file allows; otherwise 512 threads and several CTAs per SM.
+  // Kernels that stage tables in shared memory run best with ~1024 threads
+  // per SM in one wide CTA (measured on cfg3: 1x1024 95% of HBM peak vs
+  // 3x512 86%; fewer resident warps contend less for the smem crossbar the
+  // table gathers share with the stream).  L2-gather kernels use 512-thread
+  // CTAs at full occupancy (geometry-insensitive within 1%).
   int threads = 0, per_sm = 0;
   const int cands_big[] = {1024, 512, 256, 128};
   const int cands_small[] = {512, 256, 128, 0};
-  const int* cands = pl.smem > 113 * 1024 ? cands_big : cands_small;
+  const int cands_tuned[] = {pl.tune & 0xfff, 0, 0, 0};
+  const int* cands = (pl.tune & 0xfff) ? cands_tuned : (pl.smem > 0 ? cands_big : cands_small);
   for (int c = 0; c < 4 && cands[c]; ++c) {
     FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cands[c], smem));
     if (per_sm >= 1) {
@@ -230,6 +258,9 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
     }
   }
   if (per_sm < 1) return fail(FS_TOO_LARGE, "search kernel does not fit on an SM with this table placement");
+  int cap = (pl.tune >> 12) & 0xff;
+  if (!pl.tune && pl.smem > 0) cap = std::max(1, 1024 / threads);  // ~1024 threads per SM
+  if (cap && per_sm > cap) per_sm = cap;
 
   StreamShape sh;
   sh.m = m;
@@ -258,6 +289,7 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   DevPlan<T> d{};
   d.x = static_cast<const T*>(p->x);
   d.table = p->table;
+  d.rank = static_cast<const uint2*>(p->rank);
   d.n1 = p->n1;
   d.r = p->r;
   d.h = (T)p->h;
@@ -300,6 +332,14 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
   const bool wide = p->r >= (1ull << 32);
   switch (p->algorithm) {
     case FS_ALGO_DIRECT:
+      if (pl.records) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
+      if (p->rank && p->q == 1) {
+        if (wide) return launch_probe<T, OutT, RankProbe<T, uint64_t, false, false>>(d, pl, z, m, out, fb, base, st);
+        if (pl.xs && pl.ks) return launch_probe<T, OutT, RankProbe<T, uint32_t, true, true>>(d, pl, z, m, out, fb, base, st);
+        if (pl.xs) return launch_probe<T, OutT, RankProbe<T, uint32_t, true, false>>(d, pl, z, m, out, fb, base, st);
+        if (pl.ks) return launch_probe<T, OutT, RankProbe<T, uint32_t, false, true>>(d, pl, z, m, out, fb, base, st);
+        return launch_probe<T, OutT, RankProbe<T, uint32_t, false, false>>(d, pl, z, m, out, fb, base, st);
+      }
       if (wide) return launch_probe<T, OutT, DirectProbe<T, uint64_t, 1, false, false>>(d, pl, z, m, out, fb, base, st);
       return dispatch_direct<T, OutT, uint32_t, 1>(d, pl, z, m, out, fb, base, st);
     case FS_ALGO_DIRECT_GAP2:
@@ -459,6 +499,19 @@ int fs_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
     knot_buckets_kernel<double><<<g, 256, 0, s>>>(static_cast<const double*>(x_dev), n1, h, ~0ull, f_dev, nullptr);
   else
     return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t* f_scratch_dev,
+                  void* dir_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !dir_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  if (n1 - 1 >= (1ull << 32)) return fail(FS_INVALID_ARG, "table entries are 32-bit; partition is too large");
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  const uint64_t words = (r >> 5) + 1;
+  fill_rank_kernel<<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint2*>(dir_dev));
   FS_CUDA(cudaGetLastError());
   return FS_OK;
 }

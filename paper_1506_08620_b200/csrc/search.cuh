@@ -29,6 +29,7 @@ template <typename T>
 struct DevPlan {
   const T* x;            // knots
   const void* table;     // K / records / padded / tree
+  const uint2* rank;     // rank directory of K (direct, gap 1) or NULL
   uint64_t n1;           // N+1
   uint64_t r;            // R (direct family)
   T h, x0, xn;           // scale, domain
@@ -89,6 +90,38 @@ struct DirectProbe {
       }
       return (int64_t)t - hits;
     }
+  }
+};
+
+// Direct search (gap 1) over the rank directory of K: identical answers to
+// DirectProbe<GAP=1> (t = K[j] is recovered exactly; when bucket j holds no
+// knot, z < X[t] is implied by the monotone bucket function, so the X read
+// is skipped).  One 8-B gather per query, plus an X read only for queries
+// whose bucket holds a knot (#knots / R of them).
+template <typename T, typename J, bool XS, bool DS>
+struct RankProbe {
+  const T* X;
+  const uint2* D;
+  T h, x0;
+  J r;
+  __device__ __forceinline__ RankProbe(const DevPlan<T>& p, unsigned char* smem) {
+    X = XS ? reinterpret_cast<const T*>(smem) : p.x;
+    D = DS ? reinterpret_cast<const uint2*>(smem + p.x_smem_bytes_aligned()) : p.rank;
+    h = p.h;
+    x0 = p.x0;
+    r = (J)p.r;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    J j = trunc_to<J>(mul_rn(sub_rn(z, x0), h));
+    j = j < r ? j : r;
+    const uint2 d = tload<DS>(D, (uint64_t)(j >> 5));
+    const uint32_t b = (uint32_t)j & 31u;
+    const uint32_t t = d.y + __popc(d.x & ((1u << b) - 1u));
+    const bool knot = (d.x >> b) & 1u;
+    // lanes whose bucket holds no knot read X[0] (a broadcast), never a
+    // conflicting bank, and their answer is t - 1 regardless
+    const T xv = tload<XS>(X, knot ? t : 0u);
+    return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
   }
 };
 

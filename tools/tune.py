@@ -1,0 +1,106 @@
+"""Launch-geometry / algorithm sweep for the search kernels (tuning aid, not
+part of the product).  Times each variant with CUDA events over device-
+resident queries and prints one JSON line per variant.
+
+    python tools/tune.py [--configs cfg3,cfg4] [--geometry] [--steps 10]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import paper_1506_08620_b200 as fs  # noqa: E402
+from paper_1506_08620_b200 import workloads  # noqa: E402
+
+PEAK = 6461.2
+
+
+def time_launch(fn, steps, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / 1e3 / steps
+
+
+def verify(p, z, out):
+    x = p.device_values()
+    o = out.long().clamp(0, p.n_intervals - 1)
+    return bool(((x[o] <= z) & (z < x[o + 1])).all().item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="cfg3")
+    ap.add_argument("--algos", default="direct,direct-cache,bitset2")
+    ap.add_argument("--geometry", action="store_true")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--m", type=int, default=0)
+    ap.add_argument("--out-bytes", type=int, default=4)
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    for spec in args.configs.split(","):
+        name, _, arg = spec.partition(":")
+        kw = {"n1": int(arg)} if name == "cfg5" and arg else ({"seed": int(arg)} if arg else {})
+        p = workloads.knots(name, **kw)
+        m = args.m or workloads.CONFIGS[name].m
+        z = workloads.queries_device(name, p, m, seed=1)
+        out = torch.empty(m, dtype=torch.int32 if args.out_bytes == 4 else torch.int64, device="cuda")
+        fb = torch.empty(1, dtype=torch.uint64, device="cuda")
+        qbytes = z.element_size() + out.element_size()
+        if name == "cfg3" or args.geometry:
+            zi = z.view(torch.int32) if z.element_size() == 4 else z.view(torch.int64)
+            oo = out if z.element_size() == out.element_size() else out
+            t = time_launch(lambda: oo.copy_(zi[: oo.numel()].to(oo.dtype)) if False else oo.copy_(zi.to(oo.dtype, copy=False)), args.steps)
+            print(json.dumps({"config": spec, "variant": "torch copy ceiling", "ms": t * 1e3,
+                              "gbs": qbytes * m / t / 1e9, "frac": qbytes * m / t / 1e9 / PEAK}), flush=True)
+        for algo in args.algos.split(","):
+            try:
+                prep = fs.prepare("direct" if algo in ("direct-k", "direct-rank") else algo, p)
+                if algo == "direct-k":  # plain K table instead of rank directory / records
+                    prep.plan.rank = None
+                    prep.plan.records = None
+                if algo == "direct-rank":
+                    prep.plan.records = None
+            except fs.InfeasibleError as e:
+                print(json.dumps({"config": spec, "algo": algo, "infeasible": type(e).__name__}), flush=True)
+                continue
+            geos = [0]
+            if args.geometry:
+                geos = [0] + [thr | (cap << 12) for thr in (256, 512, 1024) for cap in (0, 1, 2, 3, 4, 6, 8)]
+            for tune in geos:
+                prep.plan.tune = tune
+                try:
+                    t = time_launch(lambda: prep.launch(z, out, fb), args.steps)
+                except Exception as e:  # geometry that does not fit
+                    print(json.dumps({"config": spec, "algo": algo, "tune": tune, "error": str(e)[:80]}), flush=True)
+                    continue
+                ok = int(fb.view(torch.int64).item()) == -1 and verify(p, z, out)
+                gbs = qbytes * m / t / 1e9
+                print(json.dumps({
+                    "config": spec, "algo": algo, "threads": tune & 0xfff, "cap": tune >> 12, "m": m,
+                    "ms": round(t * 1e3, 4), "gqs": round(m / t / 1e9, 2), "gbs": round(gbs, 1),
+                    "frac": round(gbs / PEAK, 4), "ok": ok, "placement": prep.placement(),
+                    "r": getattr(prep.structure, "r", None),
+                }), flush=True)
+            prep.plan.tune = 0
+        del z, out
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
