@@ -1,0 +1,103 @@
+"""The C-ABI library loads on a CPU-only host and exports exactly what
+include/fsgpu.h declares; the ctypes mirror of fs_plan matches the C layout.
+No compute call is made (there is no GPU here)."""
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_1506_08620_b200 import _lib
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "fsgpu.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+char\s*\*|int|size_t)\s+(fs_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_and_binding_agree():
+    assert declared_functions() == sorted(_lib.EXPORTED)
+
+
+def test_library_loads_and_exports_every_symbol():
+    lib = _lib.load()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s+(fs_\w+)$", nm, flags=re.M))
+    assert set(declared_functions()) <= exported
+
+
+def test_version_and_workspace():
+    lib = _lib.load()
+    assert b"sm_100a" in lib.fs_version()
+    assert lib.fs_workspace_bytes() >= 64
+
+
+def test_library_is_sm100a_code():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_argument_validation_without_gpu():
+    """Invalid arguments are rejected before any CUDA call (ValueError contract)."""
+    lib = _lib.load()
+    pos = ctypes.c_int64(-1)
+    assert lib.fs_certify(0, None, 4, 16, 1, None, None, None, None, None, ctypes.byref(pos), None) == _lib.FS_INVALID_ARG
+    assert b"qbits" in lib.fs_last_error()
+    assert lib.fs_certify(0, None, 4, 32, 0, None, None, None, None, None, ctypes.byref(pos), None) == _lib.FS_INVALID_ARG
+    plan = _lib.FsPlan()
+    plan.algorithm = 99
+    plan.dtype = 0
+    plan.n1 = 4
+    plan.x = 1
+    assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, None, None) == _lib.FS_INVALID_ARG
+    plan.algorithm = _lib.ALGO_CODES["direct"]
+    plan.table = 1
+    plan.q = 1
+    assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 3, 1, None) == _lib.FS_INVALID_ARG
+    assert b"out_bytes" in lib.fs_last_error()
+    plan.algorithm = _lib.ALGO_CODES["direct-cache"]
+    plan.q = 2
+    assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
+
+
+def test_status_codes_map_to_reference_exceptions():
+    import paper_1506_08620_b200 as fs
+
+    with pytest.raises(fs.NotDistinguishable) as e:
+        _lib.check(_lib.FS_NOT_DISTINGUISHABLE, pos=2)
+    assert e.value.position == 2
+    with pytest.raises(fs.Overflow):
+        _lib.check(_lib.FS_OVERFLOW)
+    with pytest.raises(fs.OutOfDomain) as e:
+        _lib.check(_lib.FS_OUT_OF_DOMAIN, pos=7)
+    assert e.value.position == 7
+    with pytest.raises(ValueError):
+        _lib.check(_lib.FS_INVALID_ARG)
+    with pytest.raises(ValueError):
+        _lib.check(_lib.FS_INCONSISTENT)
+    with pytest.raises(fs.DeviceError):
+        _lib.check(_lib.FS_CUDA_ERROR)
+
+
+def test_fs_plan_layout_matches_c(tmp_path):
+    fields = [f for f, _ in _lib.FsPlan._fields_]
+    src = tmp_path / "layout.c"
+    body = "\n".join(f'  printf("{f} %zu\\n", offsetof(fs_plan, {f}));' for f in fields)
+    src.write_text(
+        "#include <stdio.h>\n#include <stddef.h>\n#include \"fsgpu.h\"\n"
+        "int main(void) {\n  printf(\"sizeof %zu\\n\", sizeof(fs_plan));\n" + body + "\n  return 0;\n}\n"
+    )
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    out = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split("\n") if line)
+    assert int(out["sizeof"]) == ctypes.sizeof(_lib.FsPlan)
+    for f in fields:
+        assert int(out[f]) == getattr(_lib.FsPlan, f).offset, f
