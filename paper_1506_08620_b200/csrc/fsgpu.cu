@@ -190,14 +190,12 @@ Placement place(const fs_plan* p) {
     }
     case FS_ALGO_BITSET2: {
       if (force_global) break;
+      // the probed nodes are staged in level order by the kernel prologue
       const uint64_t full = (1ull << p->pbits) * es;
       pl.top = true;
       if (full <= budget) {
         pl.top_bits = p->pbits;
         pl.x_bytes = (uint32_t)full;
-        pl.seg0_src = p->table;
-        pl.seg0_bytes = (uint32_t)full;
-        pl.nseg = 1;
         pl.smem = full;
         pl.flags |= FS_PLACE_SMEM_X;
       } else {

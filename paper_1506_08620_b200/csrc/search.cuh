@@ -186,27 +186,37 @@ struct Bitset2Probe {
     top_bits = TOP ? p.top_bits : 0;
     shift = p.pbits - top_bits;
   }
-  // Levels served from smem when the padded array itself does not fit: copy
-  // the strided subsample xpad[m << shift] cooperatively (plain loads).
+  // The nodes the first `top_bits` levels can probe are staged in LEVEL
+  // ORDER: level l's 2^l candidates r = (m << (p-l)) | 2^(p-1-l) sit at
+  // [2^l - 1, 2^(l+1) - 1).  In the sorted padded array every node of a level
+  // l <= 7 shares one bank (stride >= 32 words), up to 32-way conflicts; in
+  // level order they are consecutive words.  Same comparisons, same values.
   static __device__ __forceinline__ void prologue(const DevPlan<T>& p, unsigned char* smem) {
     if constexpr (TOP) {
-      if (p.top_bits < p.pbits) {
-        T* dst = reinterpret_cast<T*>(smem);
-        const T* src = static_cast<const T*>(p.table);
-        const int sh = p.pbits - p.top_bits;
-        for (uint32_t m = threadIdx.x; m < (1u << p.top_bits); m += blockDim.x) dst[m] = __ldg(src + ((uint64_t)m << sh));
-        __syncthreads();
+      T* dst = reinterpret_cast<T*>(smem);
+      const T* src = static_cast<const T*>(p.table);
+      const uint32_t nodes = (1u << p.top_bits) - 1;
+      for (uint32_t s = threadIdx.x; s < nodes; s += blockDim.x) {
+        const int l = 31 - __clz(s + 1);
+        const uint32_t m = s + 1 - (1u << l);
+        const uint64_t r = ((uint64_t)m << (p.pbits - l)) | (1ull << (p.pbits - 1 - l));
+        dst[s] = __ldg(src + r);
       }
+      __syncthreads();
     }
   }
   __device__ __forceinline__ int64_t operator()(T z) const {
     uint32_t i = 0;
     int lvl = 0;
     if constexpr (TOP) {
-      for (; lvl < top_bits; ++lvl) {
-        const uint32_t r = i | (1u << (pbits - 1 - lvl));
-        if (z >= top[r >> shift]) i = r;
-      }
+      // Level-order descent: the node of (level l, path m) is s = 2^l - 1 + m
+      // and its children are 2s + 1 (bit clear) / 2s + 2 (bit set), so each
+      // level is one LDS, one compare and one LEA.
+      uint32_t s = 0;
+#pragma unroll 4
+      for (int l = 0; l < top_bits; ++l) s = 2 * s + 1 + (z >= top[s] ? 1u : 0u);
+      i = (s - ((1u << top_bits) - 1)) << (pbits - top_bits);
+      lvl = top_bits;
     }
     for (; lvl < pbits; ++lvl) {
       const uint32_t r = i | (1u << (pbits - 1 - lvl));
