@@ -299,14 +299,25 @@ def main():
         te.append(time.perf_counter() - a)
     barrier()
     t_e2e = float(np.median(te))
+    # opt-in speculative write-back (atomic=False): both PCIe directions overlap
+    fs.batch_search(cfg, zh, oh, atomic=False)
+    barrier()
+    to = []
+    for _ in range(e2e_steps):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        fs.batch_search(cfg, zh, oh, atomic=False)
+        to.append(time.perf_counter() - a)
+    barrier()
+    t_e2e_ov = float(np.median(to))
 
-    times = torch.tensor([t_dir, t_bs, t_e2e], dtype=torch.float64, device="cuda")
+    times = torch.tensor([t_dir, t_bs, t_e2e, t_e2e_ov], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
         v = torch.tensor([1 if verified else 0], device="cuda")
         dist.all_reduce(v, op=dist.ReduceOp.MIN)
         verified = bool(v.item())
-    t_dir, t_bs, t_e2e = times.tolist()
+    t_dir, t_bs, t_e2e, t_e2e_ov = times.tolist()
 
     if rank == 0:
         total = m * world
@@ -366,6 +377,13 @@ def main():
                 "d2h_bytes_per_step": 4 * m,
                 "api": "paper_1506_08620_b200.batch_search(LaneConfig(d=65536,'direct'), pinned numpy z, pinned numpy int32 out)",
                 "ms_per_step": 1e3 * t_e2e,
+                "contract": "reference batch_search guarantee kept: nothing written to out on OutOfDomain "
+                            "(H2D of all queries, then D2H)",
+                "overlapped": {
+                    "value": total / t_e2e_ov,
+                    "ms_per_step": 1e3 * t_e2e_ov,
+                    "api": "batch_search(..., atomic=False): chunk results written back while later chunks upload",
+                },
             },
             "gpu_launches": args.steps * prep.launches_per_batch(m),
             "clocks": clocks,

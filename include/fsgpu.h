@@ -198,11 +198,18 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
  * copies the results to out_host (nothing is written on error, as
  * batch.py:404 promises).  z_dev/out_dev are device scratch of m elements.
  * SYNC.  On FS_OUT_OF_DOMAIN *pos_out is the first offending position.
+ *
+ * flags & FS_HOST_OVERLAP: speculative write-back -- each chunk's results
+ * are copied to out_host as soon as its kernel finishes, so the D2H stream
+ * overlaps the H2D stream (PCIe is full duplex: ~2x end to end).  On
+ * FS_OUT_OF_DOMAIN the error and position are the same, but out_host may
+ * hold results for some chunks (opt-in relaxation of batch.py:404).
  */
+#define FS_HOST_OVERLAP 1
 int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host,
                    int32_t out_bytes, void* z_dev, void* out_dev,
                    unsigned long long* first_bad_dev, uint64_t chunk_elems,
-                   int64_t* pos_out, void* stream, void* copy_stream);
+                   int64_t* pos_out, void* stream, void* copy_stream, int32_t flags);
 
 /* Placement the search kernel will use for this plan (FS_PLACE_* bit set),
  * plus the dynamic shared memory bytes per CTA it stages. */

@@ -32,6 +32,8 @@ FS_TOO_LARGE = 7
 FS_F32 = 0
 FS_F64 = 1
 
+FS_HOST_OVERLAP = 1
+
 ALGO_CODES = {
     "classic": 0,
     "bitset1": 1,
@@ -127,7 +129,7 @@ def _declare(lib):
     lib.fs_search_device.argtypes = [ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp]
     lib.fs_search_host.restype = ctypes.c_int
     lib.fs_search_host.argtypes = [
-        ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp, _vp, _u64, _p_i64, _vp, _vp,
+        ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp, _vp, _u64, _p_i64, _vp, _vp, _i32,
     ]
     lib.fs_plan_placement.restype = ctypes.c_int
     lib.fs_plan_placement.argtypes = [ctypes.POINTER(FsPlan), _p_i32, _p_u64]

@@ -109,8 +109,10 @@ def _plan_for(algorithm: str, structure, p: SortedPartition):
     return plan, keep
 
 
-def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = HOST_CHUNK_BYTES) -> None:
-    """End-to-end search of host queries into host ``out[:m]`` (fs_search_host)."""
+def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = HOST_CHUNK_BYTES,
+                       overlap: bool = False) -> None:
+    """End-to-end search of host queries into host ``out[:m]`` (fs_search_host).
+    ``overlap`` = speculative per-chunk write-back (FS_HOST_OVERLAP)."""
     m = len(z)
     if m == 0:
         return
@@ -126,7 +128,7 @@ def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = 
     rc = _lib.load().fs_search_host(
         ctypes.byref(plan), z.ctypes.data, m, target.ctypes.data, ob, z_dev.data_ptr(), o_dev.data_ptr(),
         fb.data_ptr(), max(4, chunk_bytes // z.dtype.itemsize), ctypes.byref(pos), _device.stream_ptr(),
-        _device.stream_ptr(_copy_stream()),
+        _device.stream_ptr(_copy_stream()), _lib.FS_HOST_OVERLAP if overlap else 0,
     )
     _lib.check(rc, pos=pos.value, what="fs_search_host")
     if not direct_out:
@@ -308,12 +310,16 @@ def resolve_threads(threads: int | None) -> int:
     return max(1, int(env)) if env else 1
 
 
-def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None) -> int:
+def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None, *, atomic: bool = True) -> int:
     """Resolve every query into ``out``; returns the number resolved
     (batch.py:399-441).
 
     Raises OutOfDomain(position) for the first query outside [X_0, X_N);
-    a host ``out`` is left untouched in that case.
+    a host ``out`` is left untouched in that case.  ``atomic=False`` (not in
+    the reference) relaxes only that last guarantee for host arrays: results
+    are written back chunk by chunk while later chunks are still uploading,
+    overlapping the two PCIe directions (~2x end to end); the exception and
+    its position are unchanged.
     """
     kern = cfg.structure
     resolve_threads(threads)
@@ -339,7 +345,7 @@ def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None) -> i
         _search_device_tensor(kern.plan, z.contiguous(), out[:m])
         return m
     zz = coerce_queries(z, p.values.dtype)
-    _search_host_array(kern.plan, zz, out)
+    _search_host_array(kern.plan, zz, out, overlap=not atomic)
     return m
 
 

@@ -571,23 +571,28 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
 
 int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host, int32_t out_bytes, void* z_dev,
                    void* out_dev, unsigned long long* first_bad_dev, uint64_t chunk_elems, int64_t* pos_out,
-                   void* stream, void* copy_stream) {
+                   void* stream, void* copy_stream, int32_t flags) {
   int rc = check_search_args(plan, z_dev, m, out_dev, out_bytes, first_bad_dev);
   if (rc) return rc;
   if (m && (!z_host || !out_host)) return fail(FS_INVALID_ARG, "host pointer is NULL");
   cudaStream_t s = as_stream(stream), cs = as_stream(copy_stream);
+  const bool overlap = (flags & FS_HOST_OVERLAP) != 0;
   const size_t es = plan->dtype == FS_F32 ? 4 : 8;
   if (chunk_elems == 0) chunk_elems = (64ull << 20) / es;
   chunk_elems = (chunk_elems + 3) & ~3ull;  // keep every chunk 16-B aligned on device
   const Placement pl = place(plan);
   FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
-  cudaEvent_t ev;
+  cudaEvent_t ev, evk;
+  cudaStream_t ds = nullptr;
   FS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  FS_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
+  if (overlap) FS_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
   int status = FS_OK;
   for (uint64_t off = 0; off < m && status == FS_OK; off += chunk_elems) {
     const uint64_t n = std::min(chunk_elems, m - off);
     const char* src = static_cast<const char*>(z_host) + off * es;
     char* dst = static_cast<char*>(z_dev) + off * es;
+    char* odev = static_cast<char*>(out_dev) + off * out_bytes;
     cudaError_t e = cudaMemcpyAsync(dst, src, n * es, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaEventRecord(ev, cs);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev, 0);
@@ -595,22 +600,37 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
       status = fail(FS_CUDA_ERROR, std::string("chunk upload: ") + cudaGetErrorString(e));
       break;
     }
-    status = launch_search(plan, pl, dst, n, static_cast<char*>(out_dev) + off * out_bytes, out_bytes, first_bad_dev,
-                           off, s);
+    status = launch_search(plan, pl, dst, n, odev, out_bytes, first_bad_dev, off, s);
+    if (status == FS_OK && overlap) {
+      // speculative write-back on a third stream: D2H of chunk c runs while
+      // the H2D of chunk c+1 is in flight (the two copy engines are independent)
+      e = cudaEventRecord(evk, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(ds, evk, 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(static_cast<char*>(out_host) + off * out_bytes, odev, n * (uint64_t)out_bytes,
+                            cudaMemcpyDeviceToHost, ds);
+      if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("chunk download: ") + cudaGetErrorString(e));
+    }
   }
   unsigned long long bad = ~0ull;
   if (status == FS_OK) {
     cudaError_t e = cudaMemcpyAsync(&bad, first_bad_dev, sizeof(bad), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && ds) e = cudaStreamSynchronize(ds);
     if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("first-bad readback: ") + cudaGetErrorString(e));
   }
+  if (ds) {
+    cudaStreamSynchronize(ds);
+    cudaStreamDestroy(ds);
+  }
   cudaEventDestroy(ev);
+  cudaEventDestroy(evk);
   if (status != FS_OK) return status;
   if (bad != ~0ull) {
     if (pos_out) *pos_out = (int64_t)bad;
     return fail(FS_OUT_OF_DOMAIN, "query outside [X0, XN)");
   }
-  if (m) {
+  if (m && !overlap) {
     FS_CUDA(cudaMemcpyAsync(out_host, out_dev, m * (uint64_t)out_bytes, cudaMemcpyDeviceToHost, s));
     FS_CUDA(cudaStreamSynchronize(s));
   }

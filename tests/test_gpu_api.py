@@ -1,0 +1,253 @@
+"""GPU tests of the API surfaces around the hot path: device tensors,
+misaligned views, lane/thread invariance, the speculative write-back mode,
+the direct->bitset2 fallback policy, placement variants, and full-size
+configs checked by the bracket property (unique answer => equals oracle)."""
+
+import numpy as np
+import pytest
+
+import golden_data as gd
+from oracle import fs_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _fs():
+    import paper_1506_08620_b200 as fs
+
+    return fs
+
+
+def _bracket_ok(p, z, out):
+    import torch
+
+    x = p.device_values()
+    o = out.long()
+    ok = (o >= 0) & (o < p.n_intervals)
+    o = o.clamp(0, p.n_intervals - 1)
+    return bool((ok & (x[o] <= z) & (z < x[o + 1])).all().item())
+
+
+@pytest.fixture(scope="module")
+def sweep4095():
+    case = next(c for c in gd.query_cases() if c["name"] == "sweep_single_4095")
+    xs = gd.knots_for(case)
+    return case, xs, gd.queries_for(case, xs)
+
+
+def test_device_tensor_path(cuda, sweep4095):
+    import torch
+
+    fs = _fs()
+    case, xs, z = sweep4095
+    p = fs.validate_partition(xs)
+    zt = torch.from_numpy(z).to(cuda)
+    for algo in ("direct", "bitset2", "direct-cache", "eytzinger"):
+        prep = fs.prepare(algo, p)
+        for odt in (torch.int32, torch.int64):
+            out = torch.empty(len(z), dtype=odt, device=cuda)
+            assert fs.batch_search(fs.LaneConfig(8, algo, prep), zt, out) == len(z)
+            gd.check_answers(case, out.cpu().numpy())
+        gd.check_answers(case, fs.run_batch(prep, zt).cpu().numpy())
+        gd.check_answers(case, prep.lanes(zt).cpu().numpy())
+
+
+def test_misaligned_views_and_odd_sizes(cuda, sweep4095):
+    """Every head/tail peel and the non-vector store path."""
+    import torch
+
+    fs = _fs()
+    case, xs, z = sweep4095
+    p = fs.validate_partition(xs)
+    want = orc.rank_oracle(xs, z)
+    zt = torch.from_numpy(z).to(cuda)
+    prep = fs.prepare("direct", p)
+    for a in range(0, 5):
+        for b in (len(z), len(z) - 1, len(z) - 3, a + 1, a + 7):
+            for oshift in (0, 1, 2, 3):
+                out = torch.full((b - a + oshift,), -9, dtype=torch.int32, device=cuda)
+                fs.batch_search(fs.LaneConfig(1, "direct", prep), zt[a:b], out[oshift:])
+                got = out[oshift:].cpu().numpy()
+                assert np.array_equal(got, want[a:b]), (a, b, oshift)
+                assert (out[:oshift].cpu().numpy() == -9).all()
+    # host arrays: odd lengths, non-contiguous out, other integer dtypes
+    for m in (1, 2, 3, 5, 4001):
+        out = np.empty(m, dtype=np.int16) if m < 3000 else np.empty(m, dtype=np.uint32)
+        fs.batch_search(fs.LaneConfig(3, "direct", prep), z[:m], out)
+        assert np.array_equal(out.astype(np.int64), want[:m])
+    out = np.zeros(2 * 101, dtype=np.int64)[::2]
+    fs.batch_search(fs.LaneConfig(3, "direct", prep), z[:101], out)
+    assert np.array_equal(out, want[:101])
+
+
+def test_empty_batch_and_capacity(cuda, sweep4095):
+    fs = _fs()
+    _, xs, z = sweep4095
+    prep = fs.prepare("direct", fs.validate_partition(xs))
+    assert fs.batch_search(fs.LaneConfig(4, "direct", prep), z[:0], np.empty(0, np.int64)) == 0
+    with pytest.raises(ValueError):
+        fs.batch_search(fs.LaneConfig(4, "direct", prep), z[:10], np.empty(9, np.int64))
+
+
+def test_lane_and_thread_invariance(cuda, sweep4095):
+    """test_batch.py:32-52, 115-123: d and threads never change results."""
+    fs = _fs()
+    case, xs, z = sweep4095
+    p = fs.validate_partition(xs)
+    for algo in fs.ALGORITHMS:
+        prep = fs.prepare(algo, p)
+        base = fs.run_batch(prep, z, d=1)
+        for d in (2, 3, 64, 4001, 100_000):
+            assert np.array_equal(fs.run_batch(prep, z, d=d, threads=3), base)
+        gd.check_answers(case, base)
+
+
+def test_speculative_write_back(cuda, sweep4095):
+    fs = _fs()
+    case, xs, z = sweep4095
+    p = fs.validate_partition(xs)
+    prep = fs.prepare("direct", p)
+    out = np.empty(len(z), dtype=np.int32)
+    from paper_1506_08620_b200 import batch as fb
+
+    fb._search_host_array(prep.plan, z, out, chunk_bytes=4096, overlap=True)  # many chunks
+    gd.check_answers(case, out)
+    bad = z.copy()
+    bad[77_777] = np.nan
+    bad[90_000] = xs[-1]
+    with pytest.raises(fs.OutOfDomain) as e:
+        fb._search_host_array(prep.plan, bad, out, chunk_bytes=4096, overlap=True)
+    assert e.value.position == 77_777
+    with pytest.raises(fs.OutOfDomain) as e:
+        fs.batch_search(fs.LaneConfig(4, "direct", prep), bad, out, atomic=False)
+    assert e.value.position == 77_777
+
+
+def test_atomic_contract_with_chunks(cuda, sweep4095):
+    """Default mode: many chunks, a bad query in the last one, out untouched."""
+    fs = _fs()
+    _, xs, z = sweep4095
+    prep = fs.prepare("bitset2", fs.validate_partition(xs))
+    bad = z.copy()
+    bad[-1] = -1.0
+    out = np.full(len(z), 123, dtype=np.int64)
+    from paper_1506_08620_b200 import batch as fb
+
+    with pytest.raises(fs.OutOfDomain) as e:
+        fb._search_host_array(prep.plan, bad, out, chunk_bytes=4096)
+    assert e.value.position == len(z) - 1
+    assert (out == 123).all()
+
+
+def test_fallback_policy(cuda):
+    """infeasible direct layouts fall back to bitset2."""
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots("cfg5", n1=1_048_577, filtered=False)
+    with pytest.raises(fs.Overflow):
+        fs.prepare("direct", p)
+    prep = fs.prepare_with_fallback(p)
+    assert prep.algorithm == "bitset2"
+    z = workloads.queries_host("cfg5", p, 300_001, seed=9)
+    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(p.values, z))
+    collide = fs.validate_partition(np.array([-1e9, 0.0, 1.0], dtype=np.float32))
+    assert fs.prepare_with_fallback(collide).algorithm == "bitset2"
+    assert fs.prepare_with_fallback(collide, algorithm="direct-gap2").algorithm == "direct-gap2"
+
+
+@pytest.mark.parametrize("variant", ["records", "rank", "k", "global"])
+def test_direct_table_variants_agree(cuda, variant):
+    """The direct kernel's table encodings (fused records in smem, rank
+    directory, plain K, forced L2) give identical answers."""
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    for name, kw in (("cfg3", {}), ("cfg1", {}), ("cfg5", {"n1": 33}), ("cfg4", {})):
+        p = workloads.knots(name, **kw)
+        z = workloads.queries_host(name, p, 500_003, seed=4)
+        prep = fs.prepare("direct", p)
+        if variant in ("rank", "k", "global"):
+            prep.plan.records = None
+        if variant in ("k", "global"):
+            prep.plan.rank = None
+        if variant == "global":
+            prep.plan.smem_policy = 1
+        assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(p.values, z)), (name, variant)
+
+
+def test_scalar_entry_points(cuda):
+    """binsearch.py / eytzinger.py scalar wrappers (test_binsearch.py:43-79)."""
+    fs = _fs()
+    p = fs.validate_partition([0, 1, 2, 3])
+    assert fs.classic_search(p, 2.9) == 2 and fs.classic_search(p, 0.0) == 0
+    assert fs.bitset_search_v1(p, fs.probe_constant(3), 1.5) == 1
+    assert fs.bitset_search_v2(fs.pad_right_pow2(p), 2.5) == 2
+    assert fs.bitset_search_v3(p, fs.probe_constant(3), 1.0) == 1
+    assert fs.offset_search(p, fs.offset_constants(3), 2.2) == 2
+    assert fs.eytzinger_search(fs.build_layout(p), 2.5) == 2
+    p9 = fs.gen_uniform_gap_partition(9, 1, 5, seed=9)
+    zt = np.nextafter(p9.values[-1], -np.inf)
+    assert fs.bitset_search_v1(p9, fs.probe_constant(8), zt) == 7
+    assert fs.bitset_search_v2(fs.pad_right_pow2(p9), zt) == 7
+    pp = fs.pad_right_pow2(fs.gen_uniform_gap_partition(17, 1, 5, seed=1))
+    assert len(pp.padded) == 32 and pp.p == 5 and pp.probe == 16
+    for search in (lambda z: fs.classic_search(p, z), lambda z: fs.bitset_search_v2(fs.pad_right_pow2(p), z)):
+        with pytest.raises(fs.OutOfDomain):
+            search(3.0)
+    # gap-2 / generic (test_direct.py:73-79, 110-116, 266-289)
+    pc = fs.validate_partition(np.array([-1e9, 0.0, 1.0], dtype=np.float32))
+    idx2, _ = fs.build(pc, q=2)
+    for z in orc.boundary_probes(pc.values):
+        assert fs.direct_search_gap2(idx2, pc, z) == orc.linear_scan(pc.values, z)
+    p3 = fs.gen_uniform_gap_partition(63, 1, 5, seed=8)
+    idx3, _ = fs.build(p3, q=3)
+    for z in orc.boundary_probes(p3.values)[::7]:
+        assert fs.direct_search_generic(idx3, p3, z) == orc.linear_scan(p3.values, z)
+    pw = fs.validate_partition([0.0, 2.5])
+    idxw, _ = fs.build(pw, q=2)
+    assert fs.direct_search_gap2(idxw, pw, 1.0) == 0
+
+
+def test_float64_queries_on_float32_partition(cuda):
+    fs = _fs()
+    xs = orc.gen_uniform_gap(300, 1, 5, 3, np.float32)
+    p = fs.validate_partition(xs)
+    rng = np.random.default_rng(0)
+    z64 = np.concatenate([rng.uniform(float(xs[0]), float(xs[-1]), 100_000),
+                          np.nextafter(xs[1:].astype(np.float64), -np.inf)])
+    exact = np.searchsorted(xs.astype(np.float64), z64, side="right") - 1
+    for algo in ("direct", "bitset2"):
+        assert np.array_equal(fs.run_batch(fs.prepare(algo, p), z64), exact)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,kw,m", [
+    ("cfg3", {}, 1 << 30),
+    ("cfg4", {}, 1 << 28),
+    ("cfg2", {"seed": 0}, 100_000_000),
+    ("cfg5", {"n1": 1_048_577}, 1 << 28),
+    ("cfg5", {"n1": 33}, 1 << 28),
+])
+def test_full_size_configs(cuda, name, kw, m):
+    """BASELINE sizes: every answer satisfies X[i] <= z < X[i+1] (bracket
+    property, exact float compares), direct == bitset2 elementwise, and a 1e6
+    sample equals the CPU oracle."""
+    import torch
+
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots(name, **kw)
+    z = workloads.queries_device(name, p, m, seed=3)
+    outs = []
+    for algo in ("direct", "bitset2"):
+        prep = fs.prepare(algo, p)
+        out = torch.empty(m, dtype=torch.int32, device=cuda)
+        fs.batch_search(fs.LaneConfig(65536, algo, prep), z, out)
+        assert _bracket_ok(p, z, out), algo
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    idx = torch.randint(0, m, (1_000_000,), device=cuda)
+    zs = z[idx].cpu().numpy()
+    assert np.array_equal(outs[0][idx].cpu().numpy(), orc.rank_oracle(p.values, zs))
