@@ -20,6 +20,8 @@
 //   Classic           binsearch.py:48-57
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace fsg {
@@ -205,6 +207,33 @@ struct Bitset2Probe {
       __syncthreads();
     }
   }
+  // N queries descend in lockstep: N independent smem/L2 loads per level.
+  template <int N>
+  __device__ __forceinline__ void batch(const T (&z)[N], int64_t (&o)[N]) const {
+    uint32_t s[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) s[q] = 0;
+    int lvl = 0;
+    if constexpr (TOP) {
+      for (int l = 0; l < top_bits; ++l) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) s[q] = 2 * s[q] + 1 + (z[q] >= top[s[q]] ? 1u : 0u);
+      }
+#pragma unroll
+      for (int q = 0; q < N; ++q) s[q] = (s[q] - ((1u << top_bits) - 1)) << (pbits - top_bits);
+      lvl = top_bits;
+    }
+    for (; lvl < pbits; ++lvl) {
+      const uint32_t bit = 1u << (pbits - 1 - lvl);
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        const uint32_t r = s[q] | bit;
+        if (z[q] >= __ldg(xpad + r)) s[q] = r;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) o[q] = (int64_t)s[q];
+  }
   __device__ __forceinline__ int64_t operator()(T z) const {
     uint32_t i = 0;
     int lvl = 0;
@@ -332,6 +361,24 @@ __device__ __forceinline__ auto run_prologue(const DevPlan<T>& p, unsigned char*
 template <typename P, typename T>
 __device__ __forceinline__ void run_prologue(const DevPlan<T>&, unsigned char*, long) {}
 
+// Probes that define `template <int N> batch(const T (&)[N], int64_t (&)[N])`
+// resolve a group of independent queries in lockstep (ILP across queries
+// for multi-step searches); the others are applied one query at a time.
+template <typename P, typename = void>
+struct has_batch : std::false_type {};
+template <typename P>
+struct has_batch<P, std::void_t<decltype(&P::template batch<16>)>> : std::true_type {};
+
+template <typename P, typename T, int N>
+__device__ __forceinline__ void probe_batch(const P& p, const T (&z)[N], int64_t (&o)[N]) {
+  if constexpr (has_batch<P>::value) {
+    p.template batch<N>(z, o);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) o[i] = p(z[i]);
+  }
+}
+
 struct StreamShape {
   uint64_t m;      // total queries
   uint64_t head;   // scalar queries before the first 16-B aligned group
@@ -374,26 +421,31 @@ __global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, S
     const T* zv = z + sh.head;
     OutT* ov = out + sh.head;
     for (uint64_t g0 = tid; g0 < sh.nvec; g0 += stride * UNROLL) {
-      Vec4<T> buf[UNROLL];
+      T zz[UNROLL * 4];
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const uint64_t g = g0 + u * stride;
-        if (g < sh.nvec) buf[u].load(zv + 4 * g);
+        Vec4<T> b;
+        if (g < sh.nvec) b.load(zv + 4 * g);
+        else b.v[0] = b.v[1] = b.v[2] = b.v[3] = x0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) zz[4 * u + e] = b.v[e];
       }
+      int64_t o[UNROLL * 4];
+      probe_batch<Probe, T, UNROLL * 4>(probe, zz, o);
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const uint64_t g = g0 + u * stride;
         if (g < sh.nvec) {
-          int64_t o[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const T v = buf[u].v[e];
+            const T v = zz[4 * u + e];
             const bool bad = !(v >= x0 && v < xn);
             const uint64_t pos = sh.head + 4 * g + e;
             if (bad && pos < mybad) mybad = pos;
-            o[e] = probe(v);
           }
-          store4(ov + 4 * g, o, vec_out);
+          const int64_t(&ou)[4] = *reinterpret_cast<const int64_t(*)[4]>(o + 4 * u);
+          store4(ov + 4 * g, ou, vec_out);
         }
       }
     }
