@@ -211,6 +211,19 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
                    unsigned long long* first_bad_dev, uint64_t chunk_elems,
                    int64_t* pos_out, void* stream, void* copy_stream, int32_t flags);
 
+/* ---------------------------------------------------------------------------
+ * Index persistence (bench/persist.py:1-112)
+ * ------------------------------------------------------------------------ */
+
+/*
+ * zlib-compatible CRC-32 of `bytes` bytes of device memory: the K-payload
+ * checksum of the FBSIDX1 index file (persist.py:63, 91), computed on the
+ * GPU (chunked slice-by-4 + GF(2) combine tree) so a loaded payload is
+ * verified where it lands.  ws_dev: fs_crc32_ws_bytes(bytes) bytes.  SYNC.
+ */
+size_t fs_crc32_ws_bytes(uint64_t bytes);
+int fs_crc32(const void* data_dev, uint64_t bytes, void* ws_dev, uint32_t* crc_out, void* stream);
+
 /* Placement the search kernel will use for this plan (FS_PLACE_* bit set),
  * plus the dynamic shared memory bytes per CTA it stages. */
 int fs_plan_placement(const fs_plan* plan, int32_t* placement_out, uint64_t* smem_bytes_out);

@@ -65,6 +65,8 @@ EXPORTED = (
     "fs_build_eytzinger",
     "fs_search_device",
     "fs_search_host",
+    "fs_crc32_ws_bytes",
+    "fs_crc32",
     "fs_plan_placement",
     "fs_search_launches",
 )
@@ -131,6 +133,10 @@ def _declare(lib):
     lib.fs_search_host.argtypes = [
         ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp, _vp, _u64, _p_i64, _vp, _vp, _i32,
     ]
+    lib.fs_crc32_ws_bytes.restype = ctypes.c_size_t
+    lib.fs_crc32_ws_bytes.argtypes = [_u64]
+    lib.fs_crc32.restype = ctypes.c_int
+    lib.fs_crc32.argtypes = [_vp, _u64, _vp, _p_u32, _vp]
     lib.fs_plan_placement.restype = ctypes.c_int
     lib.fs_plan_placement.argtypes = [ctypes.POINTER(FsPlan), _p_i32, _p_u64]
     lib.fs_search_launches.restype = ctypes.c_int

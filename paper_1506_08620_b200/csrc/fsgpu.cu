@@ -15,6 +15,7 @@
 #include "../../include/fsgpu.h"
 #include "build.cuh"
 #include "common.cuh"
+#include "crc32.cuh"
 #include "search.cuh"
 
 using namespace fsg;
@@ -634,6 +635,33 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
     FS_CUDA(cudaMemcpyAsync(out_host, out_dev, m * (uint64_t)out_bytes, cudaMemcpyDeviceToHost, s));
     FS_CUDA(cudaStreamSynchronize(s));
   }
+  return FS_OK;
+}
+
+size_t fs_crc32_ws_bytes(uint64_t bytes) {
+  const uint64_t nchunks = (bytes + kCrcChunk - 1) / kCrcChunk;
+  return (size_t)std::max<uint64_t>(nchunks, 1) * sizeof(uint32_t);
+}
+
+int fs_crc32(const void* data_dev, uint64_t bytes, void* ws_dev, uint32_t* crc_out, void* stream) {
+  if (!crc_out || (bytes && (!data_dev || !ws_dev))) return fail(FS_INVALID_ARG, "NULL pointer");
+  if (bytes == 0) {
+    *crc_out = 0;
+    return FS_OK;
+  }
+  cudaStream_t s = as_stream(stream);
+  uint32_t* c = static_cast<uint32_t*>(ws_dev);
+  const uint64_t nchunks = (bytes + kCrcChunk - 1) / kCrcChunk;
+  crc32_chunks_kernel<<<grid_1d(nchunks, 256), 256, 0, s>>>(static_cast<const unsigned char*>(data_dev), bytes, c,
+                                                           nchunks);
+  FS_CUDA(cudaGetLastError());
+  for (uint64_t step = 1; step < nchunks; step *= 2) {
+    const uint64_t pairs = (nchunks + 2 * step - 1) / (2 * step);
+    crc32_combine_kernel<<<grid_1d(pairs, 256), 256, 0, s>>>(c, nchunks, step, bytes);
+    FS_CUDA(cudaGetLastError());
+  }
+  FS_CUDA(cudaMemcpyAsync(crc_out, c, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
   return FS_OK;
 }
 
