@@ -217,6 +217,63 @@ def time_device(prep, z, out, fb, steps: int, warmup: int, barrier):
     return start.elapsed_time(stop) / 1e3  # seconds for `steps` launches
 
 
+PER_CONFIG = (
+    # (label, config, knot-recipe kwargs, queries per GPU): BASELINE.json configs[0..4]
+    ("cfg1", "cfg1", {"seed": 0}, 1_000_000),
+    ("cfg2_s0", "cfg2", {"seed": 0}, 100_000_000),
+    ("cfg3", "cfg3", {"seed": 0}, 1 << 30),
+    ("cfg4", "cfg4", {}, 1 << 28),
+    ("cfg5_33", "cfg5", {"n1": 33}, 1 << 28),
+    ("cfg5_1025", "cfg5", {"n1": 1025}, 1 << 28),
+    ("cfg5_32769", "cfg5", {"n1": 32_769}, 1 << 28),
+    ("cfg5_1048577", "cfg5", {"n1": 1_048_577}, 1 << 28),
+)
+
+
+def per_config(steps: int, barrier, world: int):
+    """Every BASELINE config on this GPU: direct (or its fall-back) vs
+    bitset2, device-resident, CUDA events, answers verified by the bracket
+    property.  Returns {label: {...}} with per-rank times max-reduced."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1506_08620_b200 as fs
+    from paper_1506_08620_b200 import workloads
+
+    pk = peaks()["hbm_gbs"]
+    res = {}
+    for label, cfg, kw, m in PER_CONFIG:
+        p = workloads.knots(cfg, **kw)
+        z = workloads.queries_device(cfg, p, m, seed=11)
+        out = torch.empty(m, dtype=torch.int32, device=z.device)
+        fb = torch.empty(1, dtype=torch.uint64, device=z.device)
+        qb = z.element_size() + 4
+        row = {"queries_per_gpu": m, "dtype": "f32" if p.precision == "single" else "f64", "bytes_per_query": qb}
+        for name in ("direct", "bitset2"):
+            prep = fs.prepare_with_fallback(p) if name == "direct" else fs.prepare("bitset2", p)
+            n = steps * (1 if m >= (1 << 30) else 4) * (1 if m >= (1 << 26) else 10)
+            t = time_device(prep, z, out, fb, n, 3, barrier) / n
+            ok = int(fb.view(torch.int64).item()) == -1 and verify_bracket(p, z, out)
+            tt = torch.tensor([t, 0.0 if ok else 1.0], dtype=torch.float64, device=z.device)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t, bad = tt.tolist()
+            row[name] = {
+                "algorithm": prep.algorithm,
+                "gqs": world * m / t / 1e9,
+                "ms": 1e3 * t,
+                "roofline_frac": qb * m / t / 1e9 / pk,
+                "placement": prep.placement(),
+                "verified": bad == 0,
+            }
+            if name == "direct" and prep.algorithm.startswith("direct"):
+                row["R"] = prep.structure.r
+        res[label] = row
+        del z, out
+        torch.cuda.empty_cache()
+    return res
+
+
 def verify_bracket(p, z, out) -> bool:
     """X[out] <= z < X[out+1] for every query (unique answer => equals the
     oracle's max{i : X_i <= z}); exact float compares on the device."""
@@ -239,6 +296,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--m", type=int, default=M_PER_GPU, help="queries per GPU")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config sweep (cfg1..cfg5)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -318,6 +376,10 @@ def main():
         dist.all_reduce(v, op=dist.ReduceOp.MIN)
         verified = bool(v.item())
     t_dir, t_bs, t_e2e, t_e2e_ov = times.tolist()
+    z_cpu, o_cpu = zh[:CPU_SAMPLE].copy(), oh[:CPU_SAMPLE].copy()
+    del zh_t, oh_t, zh, oh
+    torch.cuda.empty_cache()
+    configs = None if args.no_configs else per_config(max(3, min(args.steps, 10)), barrier, world)
 
     if rank == 0:
         total = m * world
@@ -388,10 +450,12 @@ def main():
             "gpu_launches": args.steps * prep.launches_per_batch(m),
             "clocks": clocks,
         }
+        if configs is not None:
+            line["per_config"] = configs
         if not args.no_cpu_baseline:
             from oracle import fs_oracle as orc  # noqa: F401  (cpu_baseline leg only)
 
-            zs = zh[:CPU_SAMPLE]
+            zs = z_cpu
             rate, threads, reps, outc = cpu_reference_rate(p.values, zs, "direct", 3, 1, min_time=10.0)
             line["cpu_baseline"] = {
                 "value": rate,
@@ -402,7 +466,7 @@ def main():
                           f"(batch.py:315-317, restated in oracle/fs_oracle.py), d=65536, {threads} threads, "
                           f"median of {reps} passes",
             }
-            line["config"]["cpu_sample_matches_gpu"] = bool(np.array_equal(outc, oh[:CPU_SAMPLE]))
+            line["config"]["cpu_sample_matches_gpu"] = bool(np.array_equal(outc, o_cpu))
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
