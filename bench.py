@@ -452,7 +452,7 @@ def main():
         }
         if configs is not None:
             line["per_config"] = configs
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
             from oracle import fs_oracle as orc  # noqa: F401  (cpu_baseline leg only)
 
             zs = z_cpu
