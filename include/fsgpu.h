@@ -68,7 +68,8 @@ enum {
   FS_PLACE_GLOBAL = 0,  /* tables gathered through L2 (ld.global.nc)               */
   FS_PLACE_SMEM_X = 1,  /* knots (or padded/tree array) staged in shared memory   */
   FS_PLACE_SMEM_K = 2,  /* bucket table / fused records staged in shared memory   */
-  FS_PLACE_SMEM_TOP = 4 /* bitset2: top levels in smem, bottom levels via L2      */
+  FS_PLACE_SMEM_TOP = 4,/* bitset2: top levels in smem, bottom levels via L2      */
+  FS_PLACE_SMEM_HOT = 8 /* direct: hot window of directory + knots in smem        */
 };
 
 /*
@@ -100,6 +101,10 @@ typedef struct fs_plan {
   const void* records;/* direct (gap 1) only, optional: fused (K[j], X[K[j]])
                          records (fs_build_fused); used, staged in shared
                          memory, when they fit there.  NULL = unused.            */
+  uint64_t hot_word0, hot_words;  /* direct over `rank`, optional: directory words
+                         [hot_word0, +hot_words) staged in shared memory ...     */
+  uint64_t hot_knot0, hot_knots;  /* ... with knots X[hot_knot0, +hot_knots);
+                         hot_words = 0: no hot window (fs_build_hot_window).     */
 } fs_plan;
 
 /* Library identification. */
@@ -156,6 +161,20 @@ int fs_build_table(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint
  */
 int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
                   uint64_t* f_scratch_dev, void* dir_dev, void* stream);
+
+/*
+ * Hot window of a rank directory for shared-memory staging: among all
+ * contiguous directory ranges whose words plus referenced knots fit in
+ * `budget_bytes`, the one holding the most knots (ties: lowest start).
+ * Queries distributed like the knots (the interpolation use of the paper)
+ * then mostly hit shared memory.  dir_dev: (r >> 5) + 1 words; ws_dev:
+ * fs_workspace_bytes().  Writes the window; *knots_in_window_out = knots
+ * whose bucket lies inside.  SYNC.
+ */
+int fs_build_hot_window(int32_t dtype, const void* dir_dev, uint64_t r, uint64_t budget_bytes,
+                        void* ws_dev, uint64_t* word0_out, uint64_t* words_out,
+                        uint64_t* knot0_out, uint64_t* knots_out,
+                        uint64_t* knots_in_window_out, void* stream);
 
 /*
  * Cache-fused (idx, val) records.  Replaces direct.with_fused

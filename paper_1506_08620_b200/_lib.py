@@ -50,6 +50,7 @@ ALGO_CODES = {
 PLACE_SMEM_X = 1
 PLACE_SMEM_K = 2
 PLACE_SMEM_TOP = 4
+PLACE_SMEM_HOT = 8
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (
@@ -60,6 +61,7 @@ EXPORTED = (
     "fs_knot_buckets",
     "fs_build_table",
     "fs_build_rank",
+    "fs_build_hot_window",
     "fs_build_fused",
     "fs_build_padded",
     "fs_build_eytzinger",
@@ -91,6 +93,10 @@ class FsPlan(ctypes.Structure):
         ("tune", ctypes.c_int32),
         ("rank", ctypes.c_void_p),
         ("records", ctypes.c_void_p),
+        ("hot_word0", ctypes.c_uint64),
+        ("hot_words", ctypes.c_uint64),
+        ("hot_knot0", ctypes.c_uint64),
+        ("hot_knots", ctypes.c_uint64),
     ]
 
 
@@ -121,6 +127,8 @@ def _declare(lib):
     lib.fs_build_table.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp, _vp]
     lib.fs_build_rank.restype = ctypes.c_int
     lib.fs_build_rank.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _vp, _vp, _vp]
+    lib.fs_build_hot_window.restype = ctypes.c_int
+    lib.fs_build_hot_window.argtypes = [_i32, _vp, _u64, _u64, _vp, _p_u64, _p_u64, _p_u64, _p_u64, _p_u64, _vp]
     lib.fs_build_fused.restype = ctypes.c_int
     lib.fs_build_fused.argtypes = [_i32, _vp, _u64, _vp, _u64, _vp, _vp]
     lib.fs_build_padded.restype = ctypes.c_int

@@ -191,6 +191,7 @@ class PreparedKernel:
             "smem_x": bool(f & _lib.PLACE_SMEM_X),
             "smem_table": bool(f & _lib.PLACE_SMEM_K),
             "smem_top": bool(f & _lib.PLACE_SMEM_TOP),
+            "smem_hot": bool(f & _lib.PLACE_SMEM_HOT),
             "smem_bytes": int(smem.value),
         }
 
@@ -235,11 +236,14 @@ def _make_callables(plan, p: SortedPartition):
     return scalar, lanes
 
 
-def prepare(algorithm: str, p: SortedPartition, qbits: int = 32) -> PreparedKernel:
+def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: bool = False) -> PreparedKernel:
     """Build the device search structure for ``algorithm`` (batch.py:156-255).
 
     Direct-family preparation propagates NotDistinguishable/Overflow from
-    index construction, as the reference does.
+    index construction, as the reference does.  ``hot_window`` (direct only,
+    opt-in) stages the knot-densest slice of a directory too large for
+    shared memory (fs_build_hot_window); measured neutral on cfg4, whose
+    dense queries already share L1 lines, so it is off by default.
     """
     n = p.n_intervals
     if algorithm == "classic":
@@ -271,8 +275,45 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32) -> PreparedKern
         rank = build_rank_directory(p, structure)
         plan.rank = rank.data_ptr()
         keep.append(rank)
+        if hot_window:
+            _set_hot_window(plan, p, structure, rank)
     scalar, lanes = _make_callables(plan, p)
     return PreparedKernel(algorithm, p, structure, scalar, lanes, plan=plan, buffers=tuple(keep))
+
+
+#: hot-window staging budget: small enough that the L2-gather kernel keeps
+#: full occupancy (3-4 CTAs per SM) for the queries outside the window
+HOT_WINDOW_BYTES = 48 * 1024
+#: used only for skewed tables: knots per byte inside the window at least
+#: this multiple of the table-wide average (uniform layouts gain nothing)
+HOT_WINDOW_MIN_DENSITY_RATIO = 4.0
+
+
+def _smem_budget() -> int:
+    import torch
+
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    return int(getattr(props, "shared_memory_per_block_optin", 227 * 1024)) - 1024
+
+
+def _set_hot_window(plan, p: SortedPartition, idx: DirectIndex, rank) -> None:
+    """When neither records nor the whole directory fit in shared memory,
+    stage the directory window (and the knots it references) holding the
+    most knots: queries distributed like the knots then resolve from smem
+    (fs_build_hot_window)."""
+    dir_bytes = ((idx.r >> 5) + 1) * 8
+    if plan.records or dir_bytes <= _smem_budget() or idx.r >= (1 << 32):
+        return
+    out = [ctypes.c_uint64(0) for _ in range(5)]
+    ws = _device.Workspace.get()
+    rc = _lib.load().fs_build_hot_window(fs_dtype(p.precision), rank.data_ptr(), idx.r, HOT_WINDOW_BYTES,
+                                         ws.data_ptr(), *[ctypes.byref(o) for o in out], _device.stream_ptr())
+    _lib.check(rc, what="fs_build_hot_window")
+    w0, nw, t0, nt, inside = (o.value for o in out)
+    table_bytes = dir_bytes + p.values.dtype.itemsize * len(p.values)
+    density_ratio = (inside / HOT_WINDOW_BYTES) / (p.n_intervals / table_bytes)
+    if nw and density_ratio >= HOT_WINDOW_MIN_DENSITY_RATIO:
+        plan.hot_word0, plan.hot_words, plan.hot_knot0, plan.hot_knots = w0, nw, t0, nt
 
 
 def build_rank_directory(p: SortedPartition, idx: DirectIndex):

@@ -210,6 +210,54 @@ __global__ void fill_rank_kernel(const uint64_t* __restrict__ f, uint64_t n1, ui
   }
 }
 
+// Hot window of the rank directory: for every start word a, the longest
+// window [a, b) whose directory words plus the X range they reference,
+// [base_a, base_b], fit in `budget` bytes; the window holding the most
+// knots wins (ties -> lowest a).  Packed key (knots << 32 | ~a) max-reduced.
+__global__ void hot_window_kernel(const uint2* __restrict__ dir, uint64_t words, uint32_t es, uint64_t budget,
+                                  unsigned long long* __restrict__ best) {
+  unsigned long long mine = 0;
+  for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < words; a += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t base_a = __ldg(&dir[a].y);
+    // cost(a, b) = 8 (b - a) + es (base_b - base_a + 1) is monotone in b
+    uint64_t lo = a, hi = words - 1;  // largest b in [a, words-1] with cost <= budget
+    if (8ull + es * 1ull > budget) continue;
+    while (lo < hi) {
+      const uint64_t mid = lo + ((hi - lo + 1) >> 1);
+      const uint64_t cost = 8ull * (mid - a) + (uint64_t)es * ((uint64_t)__ldg(&dir[mid].y) - base_a + 1);
+      if (cost <= budget) lo = mid;
+      else hi = mid - 1;
+    }
+    const uint64_t knots = (uint64_t)__ldg(&dir[lo].y) - base_a;
+    if (lo > a && a <= 0xffffffffull) {
+      const unsigned long long key = (knots << 32) | (0xffffffffull - a);
+      mine = key > mine ? key : mine;
+    }
+  }
+  // warp max, then one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mine, o);
+    mine = w > mine ? w : mine;
+  }
+  if ((threadIdx.x & 31) == 0 && mine) atomicMax(best, mine);
+}
+
+// Window end for the chosen start word (single thread): out = {b, base_a, base_b}.
+__global__ void hot_window_finish(const uint2* __restrict__ dir, uint64_t words, uint32_t es, uint64_t budget,
+                                  uint64_t a, uint64_t* __restrict__ out) {
+  const uint64_t base_a = dir[a].y;
+  uint64_t lo = a, hi = words - 1;
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo + 1) >> 1);
+    const uint64_t cost = 8ull * (mid - a) + (uint64_t)es * ((uint64_t)dir[mid].y - base_a + 1);
+    if (cost <= budget) lo = mid;
+    else hi = mid - 1;
+  }
+  out[0] = lo;
+  out[1] = base_a;
+  out[2] = dir[lo].y;
+}
+
 // Fused (idx, val) records.  direct.py:553-561.
 __global__ void fill_fused_f32(const float* __restrict__ x, const uint32_t* __restrict__ K, uint64_t r,
                                uint2* __restrict__ rec) {

@@ -78,6 +78,7 @@ struct Placement {
   int nseg = 0;
   int tune = 0;          // fs_plan.tune (launch-geometry override)
   bool records = false;  // direct served from fused records in smem
+  bool hot = false;      // direct over the rank directory with a smem hot window
 };
 
 int validate_plan(const fs_plan* p) {
@@ -135,6 +136,23 @@ Placement place(const fs_plan* p) {
     }
   }
   const bool use_rank = p->algorithm == FS_ALGO_DIRECT && p->rank != nullptr && p->q == 1;
+  // rank directory too big for smem but a hot window is set: stage the window
+  if (use_rank && p->hot_words && !force_global && p->r < (1ull << 32) && ((p->r >> 5) + 1) * 8 > budget) {
+    const uint64_t xb = p->hot_knots * es, db = p->hot_words * 8;
+    if (align128(xb) + db <= budget) {
+      pl.hot = pl.xs = pl.ks = true;
+      pl.x_bytes = (uint32_t)xb;
+      pl.table_bytes = (uint32_t)db;
+      pl.seg0_src = static_cast<const char*>(p->x) + p->hot_knot0 * es;
+      pl.seg0_bytes = (uint32_t)xb;
+      pl.seg1_src = static_cast<const char*>(p->rank) + p->hot_word0 * 8;
+      pl.seg1_bytes = (uint32_t)db;
+      pl.nseg = 2;
+      pl.smem = align128(xb) + db;
+      pl.flags |= FS_PLACE_SMEM_HOT;
+      return pl;
+    }
+  }
   switch (use_rank ? -1 : p->algorithm) {
     case -1:  // direct, gap 1, over the rank directory: X and/or directory in smem
     case FS_ALGO_DIRECT:
@@ -248,7 +266,8 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
   const int cands_big[] = {1024, 512, 256, 128};
   const int cands_small[] = {512, 256, 128, 0};
   const int cands_tuned[] = {pl.tune & 0xfff, 0, 0, 0};
-  const int* cands = (pl.tune & 0xfff) ? cands_tuned : (pl.smem > 0 ? cands_big : cands_small);
+  const bool smem_resident = pl.smem > 0 && !pl.hot;  // a hot window still gathers through L2
+  const int* cands = (pl.tune & 0xfff) ? cands_tuned : (smem_resident ? cands_big : cands_small);
   for (int c = 0; c < 4 && cands[c]; ++c) {
     FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cands[c], smem));
     if (per_sm >= 1) {
@@ -258,7 +277,7 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
   }
   if (per_sm < 1) return fail(FS_TOO_LARGE, "search kernel does not fit on an SM with this table placement");
   int cap = (pl.tune >> 12) & 0xff;
-  if (!pl.tune && pl.smem > 0) cap = std::max(1, 1024 / threads);  // ~1024 threads per SM
+  if (!pl.tune && smem_resident) cap = std::max(1, 1024 / threads);  // ~1024 threads per SM
   if (cap && per_sm > cap) per_sm = cap;
 
   StreamShape sh;
@@ -301,6 +320,10 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   d.off_f = (uint32_t)((n + 1) >> 1);
   d.off_s = (uint32_t)(n + 1 - d.off_f);
   d.off_j = (uint32_t)(bit_length(n + 1) - 1);
+  d.hot_w0 = (uint32_t)p->hot_word0;
+  d.hot_nw = pl.hot ? (uint32_t)p->hot_words : 0;
+  d.hot_t0 = (uint32_t)p->hot_knot0;
+  d.hot_nt = pl.hot ? (uint32_t)p->hot_knots : 0;
   d.x_smem_bytes = pl.xs || pl.top ? pl.x_bytes : 0;
   d.table_smem_bytes = pl.ks ? pl.table_bytes : 0;
   // With only K staged it sits at offset 0.
@@ -332,6 +355,7 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
   switch (p->algorithm) {
     case FS_ALGO_DIRECT:
       if (pl.records) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
+      if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (p->rank && p->q == 1) {
         if (wide) return launch_probe<T, OutT, RankProbe<T, uint64_t, false, false>>(d, pl, z, m, out, fb, base, st);
         if (pl.xs && pl.ks) return launch_probe<T, OutT, RankProbe<T, uint32_t, true, true>>(d, pl, z, m, out, fb, base, st);
@@ -512,6 +536,42 @@ int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
   const uint64_t words = (r >> 5) + 1;
   fill_rank_kernel<<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint2*>(dir_dev));
   FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_build_hot_window(int32_t dtype, const void* dir_dev, uint64_t r, uint64_t budget_bytes, void* ws_dev,
+                        uint64_t* word0_out, uint64_t* words_out, uint64_t* knot0_out, uint64_t* knots_out,
+                        uint64_t* knots_in_window_out, void* stream) {
+  if (!dir_dev || !ws_dev) return fail(FS_INVALID_ARG, "NULL pointer");
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  cudaStream_t s = as_stream(stream);
+  const uint64_t words = (r >> 5) + 1;
+  const uint32_t es = dtype == FS_F32 ? 4 : 8;
+  const uint64_t budget = budget_bytes > 256 ? budget_bytes - 256 : 0;  // alignment slack
+  auto* scratch = static_cast<unsigned long long*>(ws_dev);           // [0]: best key, [1..3]: window
+  FS_CUDA(cudaMemsetAsync(scratch, 0, sizeof(unsigned long long), s));
+  const auto* dir = static_cast<const uint2*>(dir_dev);
+  hot_window_kernel<<<grid_1d(words, 256), 256, 0, s>>>(dir, words, es, budget, scratch);
+  FS_CUDA(cudaGetLastError());
+  unsigned long long key = 0;
+  FS_CUDA(cudaMemcpyAsync(&key, scratch, sizeof(key), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  if (!key) {
+    *word0_out = *words_out = *knot0_out = *knots_out = 0;
+    if (knots_in_window_out) *knots_in_window_out = 0;
+    return FS_OK;
+  }
+  const uint64_t a = 0xffffffffull - (key & 0xffffffffull);
+  hot_window_finish<<<1, 1, 0, s>>>(dir, words, es, budget, a, reinterpret_cast<uint64_t*>(scratch) + 1);
+  FS_CUDA(cudaGetLastError());
+  uint64_t fin[3];
+  FS_CUDA(cudaMemcpyAsync(fin, scratch + 1, sizeof(fin), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  *word0_out = a;
+  *words_out = fin[0] - a;
+  *knot0_out = fin[1];
+  *knots_out = fin[2] - fin[1] + 1;
+  if (knots_in_window_out) *knots_in_window_out = key >> 32;
   return FS_OK;
 }
 

@@ -24,6 +24,12 @@
 
 #include "common.cuh"
 
+// Queries per two-phase group in the rank-directory probe (gathers in flight
+// per thread vs live registers / occupancy).
+#ifndef FSG_RANK_GROUP
+#define FSG_RANK_GROUP 8
+#endif
+
 namespace fsg {
 
 // Device image of fs_plan with typed scalars.
@@ -42,6 +48,8 @@ struct DevPlan {
   uint32_t x_smem_bytes;     // bytes of X (or padded / tree / top table) staged; 0 = global
   uint32_t table_smem_bytes; // bytes of K / records staged; 0 = global
   int32_t out_vec_ok;        // output pointer co-aligned with the 16-B query groups
+  uint32_t hot_w0, hot_nw;   // rank-directory hot window (words) staged in smem
+  uint32_t hot_t0, hot_nt;   // knot window X[t0, t0 + nt) staged in smem
   __host__ __device__ __forceinline__ uint32_t x_smem_bytes_aligned() const {
     return (x_smem_bytes + 127u) & ~127u;
   }
@@ -123,6 +131,75 @@ struct RankProbe {
     // lanes whose bucket holds no knot read X[0] (a broadcast), never a
     // conflicting bank, and their answer is t - 1 regardless
     const T xv = tload<XS>(X, knot ? t : 0u);
+    return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
+  }
+#if FSG_RANK_GROUP > 0
+  // Two phases over N queries: every directory gather is in flight before
+  // the first is consumed; X is then read only for buckets holding a knot
+  // (predicated load, no memory traffic for the other lanes).
+  template <int N>
+  __device__ __forceinline__ void batch(const T (&z)[N], int64_t (&o)[N]) const {
+    constexpr int G = N < FSG_RANK_GROUP ? N : FSG_RANK_GROUP;  // live-register bound
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += G) {
+      uint2 d[G];
+      uint32_t b[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        J j = trunc_to<J>(mul_rn(sub_rn(z[g0 + q], x0), h));
+        j = j < r ? j : r;
+        b[q] = (uint32_t)j & 31u;
+        d[q] = tload<DS>(D, (uint64_t)(j >> 5));
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        const uint32_t t = d[q].y + __popc(d[q].x & ((1u << b[q]) - 1u));
+        const bool knot = (d[q].x >> b[q]) & 1u;
+        T xv = z[g0 + q];
+        if (knot) xv = tload<XS>(X, t);
+        o[g0 + q] = (int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0);
+      }
+    }
+  }
+#endif
+};
+
+// RankProbe with a shared-memory hot window: directory words [w0, w0 + nw)
+// and knots X[t0 .. t0 + nt) are staged (X window at smem offset 0, the
+// directory window after it); lanes outside the window gather through L2.
+// Same answers as RankProbe -- only where each word is read from differs.
+template <typename T>
+struct HotRankProbe {
+  const T* X;
+  const uint2* D;
+  const T* Xs;
+  const uint2* Ds;
+  T h, x0;
+  uint32_t r, w0, nw, t0, nt;
+  __device__ __forceinline__ HotRankProbe(const DevPlan<T>& p, unsigned char* smem) {
+    X = p.x;
+    D = p.rank;
+    Xs = reinterpret_cast<const T*>(smem);
+    Ds = reinterpret_cast<const uint2*>(smem + p.x_smem_bytes_aligned());
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+    w0 = p.hot_w0;
+    nw = p.hot_nw;
+    t0 = p.hot_t0;
+    nt = p.hot_nt;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
+    j = j < r ? j : r;
+    const uint32_t w = j >> 5, wl = w - w0;
+    const uint2 d = wl < nw ? Ds[wl] : __ldg(D + w);
+    const uint32_t b = j & 31u;
+    const uint32_t t = d.y + __popc(d.x & ((1u << b) - 1u));
+    const bool knot = (d.x >> b) & 1u;
+    const uint32_t tl = t - t0;
+    T xv = z;  // any value: unused unless `knot`
+    if (knot) xv = tl < nt ? Xs[tl] : __ldg(X + t);
     return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
   }
 };

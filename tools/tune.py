@@ -70,12 +70,14 @@ def main():
                               "gbs": qbytes * m / t / 1e9, "frac": qbytes * m / t / 1e9 / PEAK}), flush=True)
         for algo in args.algos.split(","):
             try:
-                prep = fs.prepare("direct" if algo in ("direct-k", "direct-rank") else algo, p)
+                prep = fs.prepare("direct" if algo in ("direct-k", "direct-rank", "direct-hot") else algo, p)
                 if algo == "direct-k":  # plain K table instead of rank directory / records
                     prep.plan.rank = None
                     prep.plan.records = None
                 if algo == "direct-rank":
                     prep.plan.records = None
+                if algo == "direct-hot":
+                    prep = fs.prepare("direct", p, hot_window=True)
             except fs.InfeasibleError as e:
                 print(json.dumps({"config": spec, "algo": algo, "infeasible": type(e).__name__}), flush=True)
                 continue
