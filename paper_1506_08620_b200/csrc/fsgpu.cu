@@ -249,12 +249,19 @@ Placement place(const fs_plan* p) {
 // ---------------------------------------------------------------------------
 // Launch
 // ---------------------------------------------------------------------------
-constexpr int kUnroll = 4;
+#ifndef FSG_UNROLL
+#define FSG_UNROLL 3  // 4-query groups in flight per thread per iteration (f32; 3 > 4 > 2 measured on cfg3)
+#endif
+#ifndef FSG_UNROLL_F64
+#define FSG_UNROLL_F64 2  // f64: same bytes in flight, half the live registers
+#endif
+template <typename T>
+constexpr int kUnroll = sizeof(T) == 8 ? FSG_UNROLL_F64 : FSG_UNROLL;
 
 template <typename T, typename OutT, typename Probe>
 int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t m, OutT* out,
                  unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
-  auto kern = search_kernel<T, OutT, Probe, kUnroll>;
+  auto kern = search_kernel<T, OutT, Probe, kUnroll<T>>;
   const size_t smem = pl.smem;
   if (smem > 0) FS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // Kernels that stage tables in shared memory run best with ~1024 threads
@@ -292,7 +299,7 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
   d.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) + head * sizeof(OutT)) & 15) == 0;
 
   const uint64_t full = (uint64_t)per_sm * sm_count();
-  uint64_t want = (sh.nvec + (uint64_t)threads * kUnroll - 1) / ((uint64_t)threads * kUnroll);
+  uint64_t want = (sh.nvec + (uint64_t)threads * kUnroll<T> - 1) / ((uint64_t)threads * kUnroll<T>);
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(full, want));
 
   StageSeg s0{nullptr, pl.seg0_src, pl.seg0_bytes};

@@ -137,8 +137,8 @@ struct RankProbe {
   // Two phases over N queries: every directory gather is in flight before
   // the first is consumed; X is then read only for buckets holding a knot
   // (predicated load, no memory traffic for the other lanes).
-  template <int N>
-  __device__ __forceinline__ void batch(const T (&z)[N], int64_t (&o)[N]) const {
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
     constexpr int G = N < FSG_RANK_GROUP ? N : FSG_RANK_GROUP;  // live-register bound
 #pragma unroll
     for (int g0 = 0; g0 < N; g0 += G) {
@@ -146,6 +146,7 @@ struct RankProbe {
       uint32_t b[G];
 #pragma unroll
       for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;  // N need not be a multiple of G (compile-time)
         J j = trunc_to<J>(mul_rn(sub_rn(z[g0 + q], x0), h));
         j = j < r ? j : r;
         b[q] = (uint32_t)j & 31u;
@@ -153,11 +154,12 @@ struct RankProbe {
       }
 #pragma unroll
       for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
         const uint32_t t = d[q].y + __popc(d[q].x & ((1u << b[q]) - 1u));
         const bool knot = (d[q].x >> b[q]) & 1u;
         T xv = z[g0 + q];
         if (knot) xv = tload<XS>(X, t);
-        o[g0 + q] = (int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0);
+        o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
       }
     }
   }
@@ -285,8 +287,8 @@ struct Bitset2Probe {
     }
   }
   // N queries descend in lockstep: N independent smem/L2 loads per level.
-  template <int N>
-  __device__ __forceinline__ void batch(const T (&z)[N], int64_t (&o)[N]) const {
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
     uint32_t s[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) s[q] = 0;
@@ -309,7 +311,7 @@ struct Bitset2Probe {
       }
     }
 #pragma unroll
-    for (int q = 0; q < N; ++q) o[q] = (int64_t)s[q];
+    for (int q = 0; q < N; ++q) o[q] = (R)s[q];
   }
   __device__ __forceinline__ int64_t operator()(T z) const {
     uint32_t i = 0;
@@ -411,12 +413,12 @@ template <> struct Vec4<double> {
   }
 };
 
-__device__ __forceinline__ void store4(int32_t* p, const int64_t (&o)[4], bool vec) {
+__device__ __forceinline__ void store4(int32_t* p, const int32_t (&o)[4], bool vec) {
   if (vec) {
-    st_stream(reinterpret_cast<int4*>(p), make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]));
+    st_stream(reinterpret_cast<int4*>(p), make_int4(o[0], o[1], o[2], o[3]));
   } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) st_stream(p + e, (int32_t)o[e]);
+    for (int e = 0; e < 4; ++e) st_stream(p + e, o[e]);
   }
 }
 __device__ __forceinline__ void store4(int64_t* p, const int64_t (&o)[4], bool vec) {
@@ -444,15 +446,15 @@ __device__ __forceinline__ void run_prologue(const DevPlan<T>&, unsigned char*, 
 template <typename P, typename = void>
 struct has_batch : std::false_type {};
 template <typename P>
-struct has_batch<P, std::void_t<decltype(&P::template batch<16>)>> : std::true_type {};
+struct has_batch<P, std::void_t<decltype(&P::template batch<16, int64_t>)>> : std::true_type {};
 
-template <typename P, typename T, int N>
-__device__ __forceinline__ void probe_batch(const P& p, const T (&z)[N], int64_t (&o)[N]) {
+template <typename P, typename T, typename R, int N>
+__device__ __forceinline__ void probe_batch(const P& p, const T (&z)[N], R (&o)[N]) {
   if constexpr (has_batch<P>::value) {
-    p.template batch<N>(z, o);
+    p.template batch<N, R>(z, o);
   } else {
 #pragma unroll
-    for (int i = 0; i < N; ++i) o[i] = p(z[i]);
+    for (int i = 0; i < N; ++i) o[i] = (R)p(z[i]);
   }
 }
 
@@ -508,8 +510,10 @@ __global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, S
 #pragma unroll
         for (int e = 0; e < 4; ++e) zz[4 * u + e] = b.v[e];
       }
-      int64_t o[UNROLL * 4];
-      probe_batch<Probe, T, UNROLL * 4>(probe, zz, o);
+      // results in the output's width: int32 halves the live registers
+      using R = std::conditional_t<sizeof(OutT) == 4, int32_t, int64_t>;
+      R o[UNROLL * 4];
+      probe_batch<Probe, T, R, UNROLL * 4>(probe, zz, o);
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const uint64_t g = g0 + u * stride;
@@ -521,7 +525,7 @@ __global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, S
             const uint64_t pos = sh.head + 4 * g + e;
             if (bad && pos < mybad) mybad = pos;
           }
-          const int64_t(&ou)[4] = *reinterpret_cast<const int64_t(*)[4]>(o + 4 * u);
+          const R ou[4] = {o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]};
           store4(ov + 4 * g, ou, vec_out);
         }
       }
