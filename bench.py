@@ -246,14 +246,14 @@ def per_config(steps: int, barrier, world: int):
         p = workloads.knots(cfg, **kw)
         z = workloads.queries_device(cfg, p, m, seed=11)
         out = torch.empty(m, dtype=torch.int32, device=z.device)
-        fb = torch.empty(1, dtype=torch.uint64, device=z.device)
+        fb = fs.new_status(z.device)
         qb = z.element_size() + 4
         row = {"queries_per_gpu": m, "dtype": "f32" if p.precision == "single" else "f64", "bytes_per_query": qb}
         for name in ("direct", "bitset2"):
             prep = fs.prepare_with_fallback(p) if name == "direct" else fs.prepare("bitset2", p)
             n = steps * (1 if m >= (1 << 30) else 4) * (1 if m >= (1 << 26) else 10)
             t = time_device(prep, z, out, fb, n, 3, barrier) / n
-            ok = int(fb.view(torch.int64).item()) == -1 and verify_bracket(p, z, out)
+            ok = fs.first_bad_of(fb) is None and verify_bracket(p, z, out)
             tt = torch.tensor([t, 0.0 if ok else 1.0], dtype=torch.float64, device=z.device)
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -328,12 +328,12 @@ def main():
     prep_b = fs.prepare("bitset2", p)
     z = workloads.queries_device("cfg3", p, m, seed=1 + rank)
     out = torch.empty(m, dtype=torch.int32, device=z.device)
-    fb = torch.empty(1, dtype=torch.uint64, device=z.device)
+    fb = fs.new_status(z.device)
 
     with ClockSampler(local) as clk:
         t_dir = time_device(prep, z, out, fb, args.steps, args.warmup, barrier)
     clocks = clk.summary()
-    bad = int(fb.view(torch.int64).item())
+    bad = -1 if fs.first_bad_of(fb) is None else 0
     verified = bad == -1 and verify_bracket(p, z, out)
     t_bs = time_device(prep_b, z, out, fb, max(3, args.steps // 5), 3, barrier)
     verified &= verify_bracket(p, z, out)

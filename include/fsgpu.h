@@ -16,7 +16,9 @@
  *  - Every call is stream-ordered on the cudaStream_t passed as `void*`
  *    (NULL = legacy default stream).  Calls marked SYNC synchronise that
  *    stream before returning; all others are asynchronous.
- *  - No global mutable state; calls are thread-safe.
+ *  - Calls are thread-safe.  The only process-wide state is an idempotent,
+ *    mutex-guarded cache of launch geometry (occupancy results and the
+ *    dynamic-shared-memory attribute) per (device, kernel, smem size).
  *  - Return value: an fs_status code.  Positions (first offending element)
  *    are written through `pos_out` where the reference exception carries a
  *    `position` attribute (errors.py:28-62).
@@ -199,15 +201,26 @@ int fs_build_eytzinger(int32_t dtype, const void* x_dev, uint64_t n1, int32_t de
  * ------------------------------------------------------------------------ */
 
 /*
+ * Status workspace of the search calls: FS_SEARCH_WS_WORDS uint64 words of
+ * device memory, ZERO-INITIALISED ONCE by its owner and then reusable by any
+ * number of stream-ordered searches (not by concurrent ones).  After a
+ * search, word 0 holds the first out-of-domain position or UINT64_MAX;
+ * words 1-2 are the kernel's CTA ticket counter and running first-bad
+ * fold, both left at 0 by every launch.
+ */
+#define FS_SEARCH_WS_WORDS 4
+size_t fs_search_ws_words(void);
+
+/*
  * Resolve m device-resident queries into device `out` (out_bytes = 4 for
  * int32, 8 for int64).  Replaces PreparedKernel.lanes + the domain check of
  * batch_search (batch.py:411-413): the first query with !(X0 <= z < XN)
- * (NaN included) is atomically min-reduced into *first_bad_dev, which this
- * call initialises to UINT64_MAX.  `out` is unspecified where a query is
- * out of domain.  ASYNC: one kernel launch (plus a 8-byte memset).
+ * (NaN included) is written to status word 0 by the kernel's last CTA (no
+ * memset node).  `out` is unspecified where a query is out of domain.
+ * ASYNC: exactly one kernel launch (m > 0).
  */
 int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* out_dev,
-                     int32_t out_bytes, unsigned long long* first_bad_dev, void* stream);
+                     int32_t out_bytes, unsigned long long* status_dev, void* stream);
 
 /*
  * End-to-end host-buffer search: the whole batch_search contract
@@ -227,7 +240,7 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
 #define FS_HOST_OVERLAP 1
 int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host,
                    int32_t out_bytes, void* z_dev, void* out_dev,
-                   unsigned long long* first_bad_dev, uint64_t chunk_elems,
+                   unsigned long long* status_dev, uint64_t chunk_elems,
                    int64_t* pos_out, void* stream, void* copy_stream, int32_t flags);
 
 /* ---------------------------------------------------------------------------

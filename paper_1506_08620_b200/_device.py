@@ -33,9 +33,17 @@ def require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None, device_index: int | None = None) -> int:
+    """cudaStream_t of ``stream`` or of the current stream (raw pointer; the
+    fast path skips building a torch Stream object on every launch)."""
+    if stream is not None:
+        return int(stream.cuda_stream)
+    if _raw_stream is not None:
+        return int(_raw_stream(torch.cuda.current_device() if device_index is None else device_index))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def torch_dtype(dtype) -> torch.dtype:

@@ -65,6 +65,7 @@ EXPORTED = (
     "fs_build_fused",
     "fs_build_padded",
     "fs_build_eytzinger",
+    "fs_search_ws_words",
     "fs_search_device",
     "fs_search_host",
     "fs_crc32_ws_bytes",
@@ -135,6 +136,8 @@ def _declare(lib):
     lib.fs_build_padded.argtypes = [_i32, _vp, _u64, _i32, _vp, _vp]
     lib.fs_build_eytzinger.restype = ctypes.c_int
     lib.fs_build_eytzinger.argtypes = [_i32, _vp, _u64, _i32, _vp, _vp]
+    lib.fs_search_ws_words.restype = ctypes.c_size_t
+    lib.fs_search_ws_words.argtypes = []
     lib.fs_search_device.restype = ctypes.c_int
     lib.fs_search_device.argtypes = [ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp]
     lib.fs_search_host.restype = ctypes.c_int

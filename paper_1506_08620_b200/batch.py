@@ -123,7 +123,7 @@ def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = 
     ob = target.dtype.itemsize
     z_dev = _device.empty(m, z.dtype)
     o_dev = _device.empty(m, target.dtype)
-    fb = _device.empty(1, np.uint64)
+    fb = _cached_status(z_dev.device, _device.stream_ptr())
     pos = ctypes.c_int64(-1)
     rc = _lib.load().fs_search_host(
         ctypes.byref(plan), z.ctypes.data, m, target.ctypes.data, ob, z_dev.data_ptr(), o_dev.data_ptr(),
@@ -135,21 +135,55 @@ def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = 
         out[:m] = target
 
 
-def _launch_device(plan, z, out, first_bad) -> None:
-    """Asynchronous device search (fs_search_device); first_bad is a 1-element
-    uint64 CUDA tensor that receives the first out-of-domain position."""
-    rc = _lib.load().fs_search_device(ctypes.byref(plan), z.data_ptr(), z.numel(), out.data_ptr(),
-                                      out.element_size(), first_bad.data_ptr(), _device.stream_ptr())
-    _lib.check(rc, what="fs_search_device")
+def new_status(device=None):
+    """A zeroed search status workspace (FS_SEARCH_WS_WORDS uint64) for
+    PreparedKernel.launch: word 0 receives the first out-of-domain position
+    (UINT64_MAX when clean).  Reusable by stream-ordered searches, not by
+    concurrent ones."""
+    import torch
+
+    dev = device if device is not None else _device.require_cuda()
+    return torch.zeros(int(_lib.load().fs_search_ws_words()), dtype=torch.uint64, device=dev)
+
+
+_status_cache: dict = {}
+
+
+def _cached_status(device, stream_ptr: int):
+    """One status workspace per (device, stream): calls on a stream are
+    ordered, so they can share it."""
+    key = (device.index, stream_ptr)
+    s = _status_cache.get(key)
+    if s is None:
+        s = new_status(device)
+        _status_cache[key] = s
+    return s
+
+
+def _launch_device(plan, z, out, status) -> None:
+    """Asynchronous device search (fs_search_device): exactly one kernel;
+    status[0] receives the first out-of-domain position."""
+    lib = _lib._lib or _lib.load()
+    rc = lib.fs_search_device(ctypes.byref(plan), z.data_ptr(), z.numel(), out.data_ptr(), out.element_size(),
+                              status.data_ptr(), _device.stream_ptr(device_index=z.get_device()))
+    if rc:
+        _lib.check(rc, what="fs_search_device")
+
+
+def first_bad_of(status):
+    """Read the first out-of-domain position from a status workspace (syncs);
+    None when every query was in domain."""
+    import torch
+
+    bad = int(status[:1].view(torch.int64).item())
+    return None if bad == -1 else bad
 
 
 def _search_device_tensor(plan, z, out) -> None:
-    import torch
-
-    fb = torch.empty(1, dtype=torch.uint64, device=z.device)
-    _launch_device(plan, z, out, fb)
-    bad = int(fb.view(torch.int64).item())
-    if bad != -1:
+    st = _cached_status(z.device, _device.stream_ptr())
+    _launch_device(plan, z, out, st)
+    bad = first_bad_of(st)
+    if bad is not None:
         raise OutOfDomain(position=bad)
 
 
@@ -173,12 +207,15 @@ class PreparedKernel:
     buffers: tuple = field(default=(), repr=False, compare=False)
 
     # -- device-level API (no host copies, no synchronisation) -------------
-    def launch(self, z, out, first_bad) -> None:
-        """Enqueue one search kernel on the current stream.  ``z``: CUDA tensor
-        of the partition's dtype; ``out``: int32/int64 CUDA tensor; ``first_bad``:
-        1-element uint64 CUDA tensor (UINT64_MAX when every query is in
-        domain).  ``out`` is unspecified for out-of-domain queries."""
-        _launch_device(self.plan, z, out, first_bad)
+    def launch(self, z, out, status) -> None:
+        """Enqueue exactly one search kernel on the current stream.  ``z``:
+        CUDA tensor of the partition's dtype; ``out``: int32/int64 CUDA
+        tensor; ``status``: a workspace from ``new_status()`` whose word 0
+        receives the first out-of-domain position (UINT64_MAX when clean;
+        read it with ``first_bad_of``).  ``out`` is unspecified for
+        out-of-domain queries.  No host synchronisation; capturable in a
+        CUDA graph."""
+        _launch_device(self.plan, z, out, status)
 
     def placement(self) -> dict:
         """Where the kernel keeps its tables: {'smem_x', 'smem_table',

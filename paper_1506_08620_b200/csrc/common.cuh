@@ -210,12 +210,36 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
   return v;
 }
 
-// Fold a lane's first-bad candidate into the global word (one atomic per
-// warp that saw a bad query; nothing on the clean path but a vote).
-__device__ __forceinline__ void flush_first_bad(unsigned long long mine, unsigned long long* first_bad) {
+// Status workspace of one search (fs_search_ws_words() u64 words, zeroed
+// once by its owner): [0] result (first out-of-domain position or ~0),
+// [1] CTA ticket counter, [2] running max of ~position over the CTAs that
+// saw a bad query; [1] and [2] are left at 0 after every launch.
+constexpr int kStatusHeader = 3;
+
+// Fold every lane's first-bad candidate into status[0] without a prior
+// memset.  Warps that saw a bad query fold ~pos into status[2] (atomicMax,
+// so the zero-initialised word means "none"); every CTA takes a ticket and
+// the last one turns status[2] into the result (merge != 0: min with the
+// current value, for several launches over one batch) and rewinds [1], [2].
+__device__ __forceinline__ void finalize_first_bad(unsigned long long mine, unsigned long long* status, int merge) {
+  __shared__ int s_last;
   if (__any_sync(0xffffffffu, mine != ~0ull)) {
-    unsigned long long w = warp_min_u64(mine);
-    if ((threadIdx.x & 31) == 0) atomicMin(first_bad, w);
+    const unsigned long long w = warp_min_u64(mine);
+    if ((threadIdx.x & 31) == 0 && w != ~0ull) atomicMax(status + 2, ~w);
+  }
+  __syncthreads();  // every warp's fold is issued before the CTA's ticket
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int ticket = atomicAdd(reinterpret_cast<unsigned int*>(status + 1), 1u);
+    s_last = ticket == gridDim.x - 1;
+    if (s_last) {
+      __threadfence();
+      const unsigned long long first = ~__ldcg(status + 2);
+      if (merge) atomicMin(status, first);
+      else status[0] = first;
+      status[2] = 0;
+      *reinterpret_cast<volatile unsigned int*>(status + 1) = 0u;
+    }
   }
 }
 

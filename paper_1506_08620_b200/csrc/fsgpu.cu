@@ -10,7 +10,10 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "../../include/fsgpu.h"
 #include "build.cuh"
@@ -79,6 +82,7 @@ struct Placement {
   int tune = 0;          // fs_plan.tune (launch-geometry override)
   bool records = false;  // direct served from fused records in smem
   bool hot = false;      // direct over the rank directory with a smem hot window
+  int merge = 0;         // status[0] = min(status[0], result) (chunked host path)
 };
 
 int validate_plan(const fs_plan* p) {
@@ -246,6 +250,25 @@ Placement place(const fs_plan* p) {
   return pl;
 }
 
+// Small batches of the direct family skip table staging: when staging the
+// tables into every CTA would move more bytes than the queries themselves,
+// L2 gathers win (measured on cfg1, 1e6 queries: 122 vs 109 Gq/s).  The
+// comparison searches keep their smem placement (their L2 path is far slower).
+Placement place_for_batch(const fs_plan* p, uint64_t m) {
+  Placement pl = place(p);
+  const bool direct_family = p->algorithm == FS_ALGO_DIRECT || p->algorithm == FS_ALGO_DIRECT_CACHE ||
+                             p->algorithm == FS_ALGO_DIRECT_GAP2 || p->algorithm == FS_ALGO_DIRECT_GENERIC;
+  if (!direct_family || pl.smem == 0 || p->smem_policy != 0 || pl.hot) return pl;
+  const uint64_t query_bytes = m * ((p->dtype == FS_F32 ? 4 : 8) + 4);
+  const uint64_t staging_bytes = (uint64_t)pl.smem * sm_count() / 2;
+  if (query_bytes >= staging_bytes) return pl;
+  fs_plan g = *p;
+  g.smem_policy = 1;
+  Placement gl = place(&g);
+  gl.tune = pl.tune;
+  return gl;
+}
+
 // ---------------------------------------------------------------------------
 // Launch
 // ---------------------------------------------------------------------------
@@ -258,31 +281,67 @@ Placement place(const fs_plan* p) {
 template <typename T>
 constexpr int kUnroll = sizeof(T) == 8 ? FSG_UNROLL_F64 : FSG_UNROLL;
 
-template <typename T, typename OutT, typename Probe>
-int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t m, OutT* out,
-                 unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
-  auto kern = search_kernel<T, OutT, Probe, kUnroll<T>>;
-  const size_t smem = pl.smem;
-  if (smem > 0) FS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // Kernels that stage tables in shared memory run best with ~1024 threads
-  // per SM in one wide CTA (measured on cfg3: 1x1024 95% of HBM peak vs
-  // 3x512 86%; fewer resident warps contend less for the smem crossbar the
-  // table gathers share with the stream).  L2-gather kernels use 512-thread
-  // CTAs at full occupancy (geometry-insensitive within 1%).
-  int threads = 0, per_sm = 0;
+
+// Launch geometry per (device, kernel, dynamic smem, candidate set), and the
+// largest dynamic-smem attribute set per (device, kernel): process-wide,
+// idempotent caches so a launch costs no runtime queries after the first
+// (the occupancy calculator and cudaFuncSetAttribute were ~10 us per call).
+std::mutex g_geo_mu;
+std::map<std::tuple<const void*, int, size_t, int>, std::pair<int, int>> g_geo;
+std::map<std::pair<const void*, int>, size_t> g_smem_attr;
+
+int launch_geometry(const void* fn, size_t smem, int mode, int* threads_out, int* per_sm_out) {
+  int dev = 0;
+  FS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_geo_mu);
+  const auto key = std::make_tuple(fn, dev, smem, mode);
+  auto it = g_geo.find(key);
+  if (it != g_geo.end()) {
+    *threads_out = it->second.first;
+    *per_sm_out = it->second.second;
+    return FS_OK;
+  }
+  if (smem > 0) {
+    size_t& cur = g_smem_attr[std::make_pair(fn, dev)];
+    if (smem > cur) {
+      FS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cur = smem;
+    }
+  }
   const int cands_big[] = {1024, 512, 256, 128};
   const int cands_small[] = {512, 256, 128, 0};
-  const int cands_tuned[] = {pl.tune & 0xfff, 0, 0, 0};
-  const bool smem_resident = pl.smem > 0 && !pl.hot;  // a hot window still gathers through L2
-  const int* cands = (pl.tune & 0xfff) ? cands_tuned : (smem_resident ? cands_big : cands_small);
+  const int cands_tuned[] = {mode > 0 ? mode : 0, 0, 0, 0};
+  const int* cands = mode > 0 ? cands_tuned : (mode == -1 ? cands_big : cands_small);
+  int threads = 0, per_sm = 0;
   for (int c = 0; c < 4 && cands[c]; ++c) {
-    FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, cands[c], smem));
+    FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, cands[c], smem));
     if (per_sm >= 1) {
       threads = cands[c];
       break;
     }
   }
   if (per_sm < 1) return fail(FS_TOO_LARGE, "search kernel does not fit on an SM with this table placement");
+  g_geo[key] = std::make_pair(threads, per_sm);
+  *threads_out = threads;
+  *per_sm_out = per_sm;
+  return FS_OK;
+}
+
+template <typename T, typename OutT, typename Probe>
+int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t m, OutT* out,
+                 unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
+  auto kern = search_kernel<T, OutT, Probe, kUnroll<T>>;
+  const size_t smem = pl.smem;
+  // Kernels that stage tables in shared memory run best with ~1024 threads
+  // per SM in one wide CTA (measured on cfg3: 1x1024 95% of HBM peak vs
+  // 3x512 86%; fewer resident warps contend less for the smem crossbar the
+  // table gathers share with the stream).  L2-gather kernels use 512-thread
+  // CTAs at full occupancy (geometry-insensitive within 1%).
+  const bool smem_resident = pl.smem > 0 && !pl.hot;  // a hot window still gathers through L2
+  const int mode = (pl.tune & 0xfff) ? (pl.tune & 0xfff) : (smem_resident ? -1 : -2);
+  int threads = 0, per_sm = 0;
+  int rc = launch_geometry(reinterpret_cast<const void*>(kern), smem, mode, &threads, &per_sm);
+  if (rc) return rc;
   int cap = (pl.tune >> 12) & 0xff;
   if (!pl.tune && smem_resident) cap = std::max(1, 1024 / threads);  // ~1024 threads per SM
   if (cap && per_sm > cap) per_sm = cap;
@@ -304,7 +363,7 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
 
   StageSeg s0{nullptr, pl.seg0_src, pl.seg0_bytes};
   StageSeg s1{nullptr, pl.seg1_src, pl.seg1_bytes};
-  kern<<<grid, threads, smem, st>>>(z, out, sh, d, first_bad, s0, s1, pl.nseg);
+  kern<<<grid, threads, smem, st>>>(z, out, sh, d, first_bad, pl.merge, s0, s1, pl.nseg);
   FS_CUDA(cudaGetLastError());
   return FS_OK;
 }
@@ -633,9 +692,12 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
   int rc = check_search_args(plan, z_dev, m, out_dev, out_bytes, first_bad_dev);
   if (rc) return rc;
   cudaStream_t s = as_stream(stream);
-  FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
-  return launch_search(plan, place(plan), z_dev, m, out_dev, out_bytes, first_bad_dev, 0, s);
+  // the kernel's last CTA writes status[0]; only an empty batch needs a write here
+  if (m == 0) FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
+  return launch_search(plan, place_for_batch(plan, m), z_dev, m, out_dev, out_bytes, first_bad_dev, 0, s);
 }
+
+size_t fs_search_ws_words(void) { return FS_SEARCH_WS_WORDS; }
 
 int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host, int32_t out_bytes, void* z_dev,
                    void* out_dev, unsigned long long* first_bad_dev, uint64_t chunk_elems, int64_t* pos_out,
@@ -648,7 +710,8 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   const size_t es = plan->dtype == FS_F32 ? 4 : 8;
   if (chunk_elems == 0) chunk_elems = (64ull << 20) / es;
   chunk_elems = (chunk_elems + 3) & ~3ull;  // keep every chunk 16-B aligned on device
-  const Placement pl = place(plan);
+  Placement pl = place_for_batch(plan, m);
+  pl.merge = 1;  // every chunk min-merges into status[0]
   FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
   cudaEvent_t ev, evk;
   cudaStream_t ds = nullptr;

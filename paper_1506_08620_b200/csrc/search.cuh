@@ -467,7 +467,7 @@ struct StreamShape {
 
 template <typename T, typename OutT, typename Probe, int UNROLL>
 __global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh,
-                              DevPlan<T> plan, unsigned long long* __restrict__ first_bad,
+                              DevPlan<T> plan, unsigned long long* __restrict__ status, int merge,
                               StageSeg seg0, StageSeg seg1, int nseg) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bar;
@@ -531,7 +531,7 @@ __global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, S
       }
     }
   }
-  flush_first_bad(mybad == ~0ull ? ~0ull : mybad + sh.base, first_bad);
+  finalize_first_bad(mybad == ~0ull ? ~0ull : mybad + sh.base, status, merge);
 }
 
 }  // namespace fsg

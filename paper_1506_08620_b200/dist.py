@@ -14,6 +14,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
+from .batch import first_bad_of, new_status
 from .errors import OutOfDomain
 
 NO_BAD = (1 << 63) - 1  # int64 sentinel ("no out-of-domain query")
@@ -56,10 +57,10 @@ def sharded_batch_search(prepared, z_local, out_local, offset: int, group=None) 
     [offset, offset + len) of the global batch.  Raises OutOfDomain with the
     global first position on every rank if any rank saw a bad query.
     """
-    fb = torch.empty(1, dtype=torch.uint64, device=z_local.device)
+    fb = new_status(z_local.device)
     prepared.launch(z_local, out_local, fb)
-    local = int(fb.view(torch.int64).item())
-    first = global_first_bad(None if local == -1 else local, offset, group=group, device=z_local.device)
+    local = first_bad_of(fb)
+    first = global_first_bad(local, offset, group=group, device=z_local.device)
     if first is not None:
         raise OutOfDomain(position=first)
     return z_local.numel()

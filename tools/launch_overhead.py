@@ -17,7 +17,7 @@ p = workloads.knots("cfg1", seed=0)
 for m in (10_000, 100_000, 1_000_000, 10_000_000):
     z = workloads.queries_device("cfg1", p, m, seed=1)
     out = torch.empty(m, dtype=torch.int32, device="cuda")
-    fb = torch.empty(1, dtype=torch.uint64, device="cuda")
+    fb = fs.new_status()
     for algo in ("direct", "direct-cache", "bitset2"):
         prep = fs.prepare(algo, p)
         for policy in (0, 1):
