@@ -70,7 +70,9 @@ def main():
                               "gbs": qbytes * m / t / 1e9, "frac": qbytes * m / t / 1e9 / PEAK}), flush=True)
         for algo in args.algos.split(","):
             try:
-                prep = fs.prepare("direct" if algo in ("direct-k", "direct-rank", "direct-hot") else algo, p)
+                base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct",
+                        "bitset2-sorted": "bitset2"}.get(algo, algo)
+                prep = fs.prepare(base, p)
                 if algo == "direct-k":  # plain K table instead of rank directory / records
                     prep.plan.rank = None
                     prep.plan.records = None
@@ -78,6 +80,9 @@ def main():
                     prep.plan.records = None
                 if algo == "direct-hot":
                     prep = fs.prepare("direct", p, hot_window=True)
+                if algo == "bitset2-sorted":  # bottom levels from the sorted padded array
+                    prep = fs.prepare("bitset2", p)
+                    prep.plan.aux = None
             except fs.InfeasibleError as e:
                 print(json.dumps({"config": spec, "algo": algo, "infeasible": type(e).__name__}), flush=True)
                 continue
