@@ -238,6 +238,14 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
  * hold results for some chunks (opt-in relaxation of batch.py:404).
  */
 #define FS_HOST_OVERLAP 1
+/*
+ * Pageable (not page-locked) host buffers of 4 MB or more are staged by the
+ * library through a cached ring of pinned slots filled and drained by a pool
+ * of host threads (parallel memcpy overlapped with the DMA); the contract is
+ * the same.  flags & FS_HOST_NO_STAGING: hand pageable buffers to the
+ * driver's bounce buffer instead.
+ */
+#define FS_HOST_NO_STAGING 2
 int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host,
                    int32_t out_bytes, void* z_dev, void* out_dev,
                    unsigned long long* status_dev, uint64_t chunk_elems,

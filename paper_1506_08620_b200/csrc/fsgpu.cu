@@ -19,6 +19,7 @@
 #include "build.cuh"
 #include "common.cuh"
 #include "crc32.cuh"
+#include "host_staging.h"
 #include "search.cuh"
 
 using namespace fsg;
@@ -699,6 +700,92 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
 
 size_t fs_search_ws_words(void) { return FS_SEARCH_WS_WORDS; }
 
+namespace {
+
+// End-to-end search of PAGEABLE host buffers through pinned staging slots:
+// phase 1 streams queries pageable -> pinned slot (host threads) -> device
+// (copy engine) with the search kernel of each chunk queued behind its
+// upload; after the first-bad readback (nothing is written on error), phase
+// 2 drains results device -> pinned slot -> pageable out the same way.
+int search_host_staged(const fs_plan* plan, Placement pl, const void* z_host, uint64_t m, void* out_host, int ob,
+                       void* z_dev, void* out_dev, unsigned long long* fb, int64_t* pos_out, cudaStream_t s,
+                       cudaStream_t cs) {
+  constexpr int kSlots = 3;
+  const size_t es = plan->dtype == FS_F32 ? 4 : 8;
+  const uint64_t chunk = ((16ull << 20) / es + 3) & ~3ull;  // 16 MB of queries per slot
+  const size_t slot_bytes = chunk * std::max<size_t>(es, (size_t)ob);
+  void* slot[kSlots] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[kSlots] = {nullptr, nullptr, nullptr};
+  int status = FS_OK;
+  for (int i = 0; i < kSlots && status == FS_OK; ++i) {
+    slot[i] = PinnedSlots::acquire(slot_bytes);
+    if (!slot[i]) status = fail(FS_CUDA_ERROR, "pinned staging allocation failed");
+    else if (cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess)
+      status = fail(FS_CUDA_ERROR, "event creation failed");
+  }
+  CopyPool pool(host_copy_threads());
+  pl.merge = 1;
+  if (status == FS_OK && cudaMemsetAsync(fb, 0xff, sizeof(unsigned long long), s) != cudaSuccess)
+    status = fail(FS_CUDA_ERROR, "status reset failed");
+  // phase 1: upload + search
+  uint64_t c = 0;
+  for (uint64_t off = 0; off < m && status == FS_OK; off += chunk, ++c) {
+    const uint64_t n = std::min(chunk, m - off);
+    const int k = (int)(c % kSlots);
+    if (c >= kSlots && cudaEventSynchronize(ev[k]) != cudaSuccess) {
+      status = fail(FS_CUDA_ERROR, "staging slot wait failed");
+      break;
+    }
+    pool.copy(slot[k], static_cast<const char*>(z_host) + off * es, n * es);
+    char* dst = static_cast<char*>(z_dev) + off * es;
+    cudaError_t e = cudaMemcpyAsync(dst, slot[k], n * es, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[k], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[k], 0);
+    if (e != cudaSuccess) {
+      status = fail(FS_CUDA_ERROR, std::string("staged upload: ") + cudaGetErrorString(e));
+      break;
+    }
+    status = launch_search(plan, pl, dst, n, static_cast<char*>(out_dev) + off * ob, ob, fb, off, s);
+  }
+  unsigned long long bad = ~0ull;
+  if (status == FS_OK) {
+    cudaError_t e = cudaMemcpyAsync(&bad, fb, sizeof(bad), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("first-bad readback: ") + cudaGetErrorString(e));
+  }
+  if (status == FS_OK && bad != ~0ull) {
+    if (pos_out) *pos_out = (int64_t)bad;
+    status = fail(FS_OUT_OF_DOMAIN, "query outside [X0, XN)");
+  }
+  // phase 2: download (only for a clean batch)
+  if (status == FS_OK) {
+    const uint64_t nch = (m + chunk - 1) / chunk;
+    for (uint64_t i = 0; i <= nch && status == FS_OK; ++i) {
+      if (i < nch) {  // DMA of chunk i into its slot
+        const uint64_t off = i * chunk, n = std::min(chunk, m - off);
+        cudaError_t e = cudaMemcpyAsync(slot[i % kSlots], static_cast<const char*>(out_dev) + off * ob, n * ob,
+                                        cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[i % kSlots], cs);
+        if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("staged download: ") + cudaGetErrorString(e));
+      }
+      if (i >= 1 && status == FS_OK) {  // host copy of chunk i-1 while chunk i is in flight
+        const uint64_t off = (i - 1) * chunk, n = std::min(chunk, m - off);
+        const int k = (int)((i - 1) % kSlots);
+        if (cudaEventSynchronize(ev[k]) != cudaSuccess) status = fail(FS_CUDA_ERROR, "staging slot wait failed");
+        else pool.copy(static_cast<char*>(out_host) + off * ob, slot[k], n * ob);
+      }
+    }
+  }
+  cudaStreamSynchronize(cs);
+  for (int i = 0; i < kSlots; ++i) {
+    if (ev[i]) cudaEventDestroy(ev[i]);
+    if (slot[i]) PinnedSlots::release(slot[i]);
+  }
+  return status;
+}
+
+}  // namespace
+
 int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host, int32_t out_bytes, void* z_dev,
                    void* out_dev, unsigned long long* first_bad_dev, uint64_t chunk_elems, int64_t* pos_out,
                    void* stream, void* copy_stream, int32_t flags) {
@@ -706,6 +793,11 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   if (rc) return rc;
   if (m && (!z_host || !out_host)) return fail(FS_INVALID_ARG, "host pointer is NULL");
   cudaStream_t s = as_stream(stream), cs = as_stream(copy_stream);
+  // pageable buffers of any real size go through the library's own pinned staging
+  if (m * (uint64_t)out_bytes >= (4ull << 20) && !(flags & FS_HOST_NO_STAGING) &&
+      !(is_pinned(z_host) && is_pinned(out_host)))
+    return search_host_staged(plan, place_for_batch(plan, m), z_host, m, out_host, out_bytes, z_dev, out_dev,
+                              first_bad_dev, pos_out, s, cs);
   const bool overlap = (flags & FS_HOST_OVERLAP) != 0;
   const size_t es = plan->dtype == FS_F32 ? 4 : 8;
   if (chunk_elems == 0) chunk_elems = (64ull << 20) / es;

@@ -139,6 +139,33 @@ def test_atomic_contract_with_chunks(cuda, sweep4095):
     assert (out == 123).all()
 
 
+@pytest.mark.parametrize("prec,odt", [("single", np.int32), ("double", np.int64)])
+def test_pageable_staged_host_path(cuda, prec, odt):
+    """Pageable numpy buffers >= 4 MB go through the library's pinned staging
+    ring (several 16 MB slots): answers exact, OutOfDomain in the last chunk
+    leaves `out` untouched, atomic=False still reports the position."""
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots("cfg3") if prec == "single" else workloads.knots("cfg5", n1=1025)
+    name = "cfg3" if prec == "single" else "cfg5"
+    z = workloads.queries_host(name, p, 10_000_003, seed=8)
+    want = orc.rank_oracle(p.values, z)
+    prep = fs.prepare("direct", p)
+    out = np.empty(len(z), dtype=odt)
+    fs.batch_search(fs.LaneConfig(64, "direct", prep), z, out)
+    assert np.array_equal(out, want)
+    bad = z.copy()
+    bad[-2] = np.nan
+    out2 = np.full(len(z), 7, dtype=odt)
+    with pytest.raises(fs.OutOfDomain) as e:
+        fs.batch_search(fs.LaneConfig(64, "direct", prep), bad, out2)
+    assert e.value.position == len(z) - 2 and (out2 == 7).all()
+    with pytest.raises(fs.OutOfDomain) as e:
+        fs.batch_search(fs.LaneConfig(64, "direct", prep), bad, out2, atomic=False)
+    assert e.value.position == len(z) - 2
+
+
 def test_fallback_policy(cuda):
     """infeasible direct layouts fall back to bitset2."""
     fs = _fs()
