@@ -423,7 +423,12 @@ def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None, *, a
         _search_device_tensor(kern.plan, z.contiguous(), out[:m])
         return m
     zz = coerce_queries(z, p.values.dtype)
-    _search_host_array(kern.plan, zz, out, overlap=not atomic)
+    if isinstance(out, np.ndarray):
+        _search_host_array(kern.plan, zz, out, overlap=not atomic)
+    else:  # any mutable sequence, as the reference's slice assignment allows (batch.py:423)
+        tmp = np.empty(m, dtype=np.int64)
+        _search_host_array(kern.plan, zz, tmp)
+        out[:m] = tmp.tolist()
     return m
 
 

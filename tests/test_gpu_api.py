@@ -80,6 +80,23 @@ def test_misaligned_views_and_odd_sizes(cuda, sweep4095):
     assert np.array_equal(out, want[:101])
 
 
+def test_python_sequences(cuda, sweep4095):
+    """Queries as a Python list / QueryBatch, out as a Python list
+    (the reference's slice assignment, batch.py:423)."""
+    fs = _fs()
+    _, xs, z = sweep4095
+    p = fs.validate_partition(xs)
+    want = orc.rank_oracle(xs, z[:1000])
+    prep = fs.prepare("direct", p)
+    out = [None] * 1002
+    assert fs.batch_search(fs.LaneConfig(4, "direct", prep), z[:1000].tolist(), out) == 1000
+    assert out[:1000] == want.tolist() and out[1000:] == [None, None]
+    qb = fs.QueryBatch(values=z[:1000], precision="single")
+    assert np.array_equal(fs.run_batch(prep, qb), want)
+    assert prep.scalar(float(z[5])) == want[5]
+    assert np.array_equal(prep.lanes(z[:1000]), want)
+
+
 def test_empty_batch_and_capacity(cuda, sweep4095):
     fs = _fs()
     _, xs, z = sweep4095
