@@ -71,7 +71,8 @@ enum {
   FS_PLACE_SMEM_X = 1,  /* knots (or padded/tree array) staged in shared memory   */
   FS_PLACE_SMEM_K = 2,  /* bucket table / fused records staged in shared memory   */
   FS_PLACE_SMEM_TOP = 4,/* bitset2: top levels in smem, bottom levels via L2      */
-  FS_PLACE_SMEM_HOT = 8 /* direct: hot window of directory + knots in smem        */
+  FS_PLACE_SMEM_HOT = 8,/* direct: hot window of directory + knots in smem        */
+  FS_PLACE_SMEM_SPARSE = 16 /* direct: two-level sparse table in smem              */
 };
 
 /*
@@ -107,6 +108,11 @@ typedef struct fs_plan {
                          [hot_word0, +hot_words) staged in shared memory ...     */
   uint64_t hot_knot0, hot_knots;  /* ... with knots X[hot_knot0, +hot_knots);
                          hot_words = 0: no hot window (fs_build_hot_window).     */
+  const void* sparse; /* direct (gap 1) only, optional: two-level sparse table
+                         (fs_build_sparse); staged in shared memory when the
+                         rank directory does not fit there.  NULL = unused.      */
+  int32_t sparse_shift;/* super-bucket = 2^sparse_shift buckets (1..16)           */
+  int32_t reserved;
 } fs_plan;
 
 /* Library identification. */
@@ -163,6 +169,21 @@ int fs_build_table(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint
  */
 int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
                   uint64_t* f_scratch_dev, void* dir_dev, void* stream);
+
+/*
+ * Two-level sparse encoding of the gap-1 table, for R >> N: super-bucket J
+ * (2^shift buckets) stores C[J] = K[J 2^shift] (uint32, (r >> shift) + 2
+ * entries, the last = n1), each knot i stores F[i] = f_i mod 2^shift
+ * (uint16, n1 entries) right after C.  Then K[j] = C[j >> shift] +
+ * #{i in [C[J], C[J+1]) : F[i] < j mod 2^shift} exactly, and bucket j holds
+ * knot t = K[j] iff F[t] == j mod 2^shift.  fs_sparse_bytes: buffer size;
+ * fs_sparse_shift: smallest shift whose table (plus X when with_x) fits in
+ * budget_bytes, or -1.  f_scratch_dev: n1 uint64.
+ */
+uint64_t fs_sparse_bytes(uint64_t n1, uint64_t r, int32_t shift);
+int fs_sparse_shift(int32_t dtype, uint64_t n1, uint64_t r, uint64_t budget_bytes, int32_t with_x);
+int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t shift,
+                    uint64_t* f_scratch_dev, void* sparse_dev, void* stream);
 
 /*
  * Hot window of a rank directory for shared-memory staging: among all

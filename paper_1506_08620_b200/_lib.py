@@ -51,6 +51,7 @@ PLACE_SMEM_X = 1
 PLACE_SMEM_K = 2
 PLACE_SMEM_TOP = 4
 PLACE_SMEM_HOT = 8
+PLACE_SMEM_SPARSE = 16
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (
@@ -61,6 +62,9 @@ EXPORTED = (
     "fs_knot_buckets",
     "fs_build_table",
     "fs_build_rank",
+    "fs_sparse_bytes",
+    "fs_sparse_shift",
+    "fs_build_sparse",
     "fs_build_hot_window",
     "fs_build_fused",
     "fs_build_padded",
@@ -98,6 +102,9 @@ class FsPlan(ctypes.Structure):
         ("hot_words", ctypes.c_uint64),
         ("hot_knot0", ctypes.c_uint64),
         ("hot_knots", ctypes.c_uint64),
+        ("sparse", ctypes.c_void_p),
+        ("sparse_shift", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -128,6 +135,12 @@ def _declare(lib):
     lib.fs_build_table.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp, _vp]
     lib.fs_build_rank.restype = ctypes.c_int
     lib.fs_build_rank.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _vp, _vp, _vp]
+    lib.fs_sparse_bytes.restype = ctypes.c_uint64
+    lib.fs_sparse_bytes.argtypes = [_u64, _u64, _i32]
+    lib.fs_sparse_shift.restype = ctypes.c_int
+    lib.fs_sparse_shift.argtypes = [_i32, _u64, _u64, _u64, _i32]
+    lib.fs_build_sparse.restype = ctypes.c_int
+    lib.fs_build_sparse.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp]
     lib.fs_build_hot_window.restype = ctypes.c_int
     lib.fs_build_hot_window.argtypes = [_i32, _vp, _u64, _u64, _vp, _p_u64, _p_u64, _p_u64, _p_u64, _p_u64, _vp]
     lib.fs_build_fused.restype = ctypes.c_int

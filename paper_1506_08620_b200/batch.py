@@ -229,6 +229,7 @@ class PreparedKernel:
             "smem_table": bool(f & _lib.PLACE_SMEM_K),
             "smem_top": bool(f & _lib.PLACE_SMEM_TOP),
             "smem_hot": bool(f & _lib.PLACE_SMEM_HOT),
+            "smem_sparse": bool(f & _lib.PLACE_SMEM_SPARSE),
             "smem_bytes": int(smem.value),
         }
 
@@ -312,11 +313,18 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
         rank = build_rank_directory(p, structure)
         plan.rank = rank.data_ptr()
         keep.append(rank)
+        if not plan.records:
+            _set_sparse_table(plan, p, structure, keep)
         if hot_window:
             _set_hot_window(plan, p, structure, rank)
     scalar, lanes = _make_callables(plan, p)
     return PreparedKernel(algorithm, p, structure, scalar, lanes, plan=plan, buffers=tuple(keep))
 
+
+#: the sparse two-level table is used only when no super-bucket holds more
+#: knots than this (in-super-bucket search of at most ~6 steps); measured:
+#: cfg2/cfg5 (max a few) 1.4-2.9x faster than L2 gathers, cfg4 (max 512) 2x slower
+SPARSE_MAX_OCCUPANCY = 64
 
 #: hot-window staging budget: small enough that the L2-gather kernel keeps
 #: full occupancy (3-4 CTAs per SM) for the queries outside the window
@@ -351,6 +359,38 @@ def _set_hot_window(plan, p: SortedPartition, idx: DirectIndex, rank) -> None:
     density_ratio = (inside / HOT_WINDOW_BYTES) / (p.n_intervals / table_bytes)
     if nw and density_ratio >= HOT_WINDOW_MIN_DENSITY_RATIO:
         plan.hot_word0, plan.hot_words, plan.hot_knot0, plan.hot_knots = w0, nw, t0, nt
+
+
+def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:
+    """For R >> N, the two-level sparse encoding of K (fs_build_sparse) fits
+    in shared memory where the rank directory does not; the kernel picks it
+    over L2 gathers when the directory (plus X) cannot be staged."""
+    if idx.r >= (1 << 32):
+        return
+    lib = _lib.load()
+    budget = _smem_budget() - 512
+    dt = fs_dtype(p.precision)
+    n1 = len(p.values)
+    shift = int(lib.fs_sparse_shift(dt, n1, idx.r, budget, 1))
+    if shift < 0:
+        shift = int(lib.fs_sparse_shift(dt, n1, idx.r, budget, 0))
+    if shift < 0:
+        return
+    buf = _device.empty(int(lib.fs_sparse_bytes(n1, idx.r, shift)), np.uint8)
+    f = _device.empty(n1, np.uint64)
+    rc = lib.fs_build_sparse(dt, p.device_values().data_ptr(), n1, float(idx.h), idx.r, shift, f.data_ptr(),
+                             buf.data_ptr(), _device.stream_ptr())
+    _lib.check(rc, what="fs_build_sparse")
+    # a query searches its super-bucket's knots: dense regions (cfg4's
+    # 1-knot-per-bucket start) make that search deep, and L2 gathers win
+    import torch
+
+    c = buf[: 4 * ((idx.r >> shift) + 2)].view(torch.int32)
+    if int((c[1:] - c[:-1]).max().item()) > SPARSE_MAX_OCCUPANCY:
+        return
+    plan.sparse = buf.data_ptr()
+    plan.sparse_shift = shift
+    keep.append(buf)
 
 
 def build_rank_directory(p: SortedPartition, idx: DirectIndex):

@@ -210,6 +210,22 @@ __global__ void fill_rank_kernel(const uint64_t* __restrict__ f, uint64_t n1, ui
   }
 }
 
+// Two-level sparse encoding of the gap-1 table for R >> N: super-bucket J
+// (buckets J 2^s .. (J+1) 2^s - 1) stores C[J] = K[J 2^s] = lower_bound(f,
+// J 2^s); every knot i stores F[i] = f_i mod 2^s (16 bit).  The knots of
+// super-bucket J are exactly [C[J], C[J+1]), so K[j] = C[j >> s] +
+// #{i in it : F[i] < j mod 2^s}.  C has (r >> s) + 2 entries, the last = n1.
+__global__ void fill_sparse_kernel(const uint64_t* __restrict__ f, uint64_t n1, uint64_t r, int s,
+                                   uint32_t* __restrict__ C, uint16_t* __restrict__ F) {
+  const uint64_t nc = (r >> s) + 2;
+  const uint64_t mask = (1ull << s) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nc || i < n1;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i < nc) C[i] = i == nc - 1 ? (uint32_t)n1 : (uint32_t)bound_search<false>(f, 0, n1, i << s);
+    if (i < n1) F[i] = (uint16_t)(__ldg(f + i) & mask);
+  }
+}
+
 // Hot window of the rank directory: for every start word a, the longest
 // window [a, b) whose directory words plus the X range they reference,
 // [base_a, base_b], fit in `budget` bytes; the window holding the most

@@ -83,6 +83,7 @@ struct Placement {
   int tune = 0;          // fs_plan.tune (launch-geometry override)
   bool records = false;  // direct served from fused records in smem
   bool hot = false;      // direct over the rank directory with a smem hot window
+  bool sparse = false;   // direct over the two-level sparse table in smem
   int merge = 0;         // status[0] = min(status[0], result) (chunked host path)
 };
 
@@ -141,6 +142,36 @@ Placement place(const fs_plan* p) {
     }
   }
   const bool use_rank = p->algorithm == FS_ALGO_DIRECT && p->rank != nullptr && p->q == 1;
+  // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
+  if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->q == 1 && !force_global && p->r < (1ull << 32) &&
+      p->sparse_shift >= 1 && p->sparse_shift <= 16) {
+    const uint64_t xb = p->n1 * es;
+    const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
+    const uint64_t cfb = fs_sparse_bytes(p->n1, p->r, p->sparse_shift);
+    const bool rank_fits = use_rank && align128(xb) + dir_b <= budget;
+    if (!rank_fits && cfb <= budget) {
+      pl.sparse = pl.ks = true;
+      pl.xs = align128(xb) + cfb <= budget;
+      pl.x_bytes = pl.xs ? (uint32_t)xb : 0;
+      pl.table_bytes = (uint32_t)cfb;
+      if (pl.xs) {
+        pl.seg0_src = p->x;
+        pl.seg0_bytes = (uint32_t)xb;
+        pl.seg1_src = p->sparse;
+        pl.seg1_bytes = (uint32_t)cfb;
+        pl.nseg = 2;
+        pl.smem = align128(xb) + cfb;
+        pl.flags |= FS_PLACE_SMEM_X;
+      } else {
+        pl.seg0_src = p->sparse;
+        pl.seg0_bytes = (uint32_t)cfb;
+        pl.nseg = 1;
+        pl.smem = cfb;
+      }
+      pl.flags |= FS_PLACE_SMEM_SPARSE;
+      return pl;
+    }
+  }
   // rank directory too big for smem but a hot window is set: stage the window
   if (use_rank && p->hot_words && !force_global && p->r < (1ull << 32) && ((p->r >> 5) + 1) * 8 > budget) {
     const uint64_t xb = p->hot_knots * es, db = p->hot_words * 8;
@@ -387,6 +418,7 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   d.off_f = (uint32_t)((n + 1) >> 1);
   d.off_s = (uint32_t)(n + 1 - d.off_f);
   d.off_j = (uint32_t)(bit_length(n + 1) - 1);
+  d.sparse_shift = p->sparse_shift;
   d.hot_w0 = (uint32_t)p->hot_word0;
   d.hot_nw = pl.hot ? (uint32_t)p->hot_words : 0;
   d.hot_t0 = (uint32_t)p->hot_knot0;
@@ -423,6 +455,10 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
     case FS_ALGO_DIRECT:
       if (pl.records) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
+      if (pl.sparse) {
+        if (pl.xs) return launch_probe<T, OutT, SparseProbe<T, true>>(d, pl, z, m, out, fb, base, st);
+        return launch_probe<T, OutT, SparseProbe<T, false>>(d, pl, z, m, out, fb, base, st);
+      }
       if (p->rank && p->q == 1) {
         if (wide) return launch_probe<T, OutT, RankProbe<T, uint64_t, false, false>>(d, pl, z, m, out, fb, base, st);
         if (pl.xs && pl.ks) return launch_probe<T, OutT, RankProbe<T, uint32_t, true, true>>(d, pl, z, m, out, fb, base, st);
@@ -602,6 +638,35 @@ int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
   cudaStream_t s = as_stream(stream);
   const uint64_t words = (r >> 5) + 1;
   fill_rank_kernel<<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint2*>(dir_dev));
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+uint64_t fs_sparse_bytes(uint64_t n1, uint64_t r, int32_t shift) {
+  if (shift < 1 || shift > 16) return 0;
+  return (4 * ((r >> shift) + 2) + 2 * n1 + 15) & ~15ull;
+}
+
+int fs_sparse_shift(int32_t dtype, uint64_t n1, uint64_t r, uint64_t budget_bytes, int32_t with_x) {
+  const uint64_t es = dtype == FS_F32 ? 4 : 8;
+  const uint64_t xb = with_x ? align128(n1 * es) : 0;
+  for (int s = 1; s <= 16; ++s)
+    if (xb + fs_sparse_bytes(n1, r, s) <= budget_bytes) return s;
+  return -1;
+}
+
+int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t shift,
+                    uint64_t* f_scratch_dev, void* sparse_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !sparse_dev || n1 < 2 || shift < 1 || shift > 16)
+    return fail(FS_INVALID_ARG, "bad arguments");
+  if (n1 - 1 >= (1ull << 32) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "sparse table needs R, N < 2^32");
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  const uint64_t nc = (r >> shift) + 2;
+  uint32_t* C = static_cast<uint32_t*>(sparse_dev);
+  uint16_t* F = reinterpret_cast<uint16_t*>(C + nc);
+  fill_sparse_kernel<<<grid_1d(std::max(nc, n1), 256), 256, 0, s>>>(f_scratch_dev, n1, r, shift, C, F);
   FS_CUDA(cudaGetLastError());
   return FS_OK;
 }

@@ -48,6 +48,7 @@ struct DevPlan {
   uint32_t x_smem_bytes;     // bytes of X (or padded / tree / top table) staged; 0 = global
   uint32_t table_smem_bytes; // bytes of K / records staged; 0 = global
   int32_t out_vec_ok;        // output pointer co-aligned with the 16-B query groups
+  int32_t sparse_shift;      // sparse two-level table: super-bucket = 2^shift buckets
   uint32_t hot_w0, hot_nw;   // rank-directory hot window (words) staged in smem
   uint32_t hot_t0, hot_nt;   // knot window X[t0, t0 + nt) staged in smem
   __host__ __device__ __forceinline__ uint32_t x_smem_bytes_aligned() const {
@@ -164,6 +165,48 @@ struct RankProbe {
     }
   }
 #endif
+};
+
+// Direct search (gap 1) over the two-level sparse encoding of K (fill_sparse_
+// kernel), staged in shared memory: C (super-bucket ranks) and F (16-bit
+// knot offsets) after X when X fits (else X via L2 -- read only for buckets
+// holding a knot).  t = K[j] = C[J] + lower_bound(F[C[J] .. C[J+1]), j mod 2^s)
+// exactly; bucket j holds knot t iff F[t] == j mod 2^s; identical answers to
+// DirectProbe<GAP=1> (batch.py:315-317).
+template <typename T, bool XS>
+struct SparseProbe {
+  const T* X;
+  const uint32_t* C;
+  const uint16_t* F;
+  T h, x0;
+  uint32_t r, s, mask;
+  __device__ __forceinline__ SparseProbe(const DevPlan<T>& p, unsigned char* smem) {
+    X = XS ? reinterpret_cast<const T*>(smem) : p.x;
+    unsigned char* cf = smem + p.x_smem_bytes_aligned();
+    C = reinterpret_cast<const uint32_t*>(cf);
+    F = reinterpret_cast<const uint16_t*>(cf + 4 * (((uint64_t)p.r >> p.sparse_shift) + 2));
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+    s = (uint32_t)p.sparse_shift;
+    mask = (1u << s) - 1u;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
+    j = j < r ? j : r;
+    const uint32_t J = j >> s, jl = j & mask;
+    uint32_t lo = C[J], hi = C[J + 1];
+    const uint32_t end = hi;
+    while (lo < hi) {  // lower_bound of jl in F[lo, hi)
+      const uint32_t mid = (lo + hi) >> 1;
+      if (F[mid] < jl) lo = mid + 1;
+      else hi = mid;
+    }
+    const bool knot = lo < end && F[lo] == jl;
+    T xv = z;
+    if (knot) xv = tload<XS>(X, lo);
+    return (int64_t)lo - ((!knot || z < xv) ? 1 : 0);
+  }
 };
 
 // RankProbe with a shared-memory hot window: directory words [w0, w0 + nw)

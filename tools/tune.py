@@ -78,6 +78,7 @@ def main():
                     prep.plan.records = None
                 if algo == "direct-rank":
                     prep.plan.records = None
+                    prep.plan.sparse = None
                 if algo == "direct-hot":
                     prep = fs.prepare("direct", p, hot_window=True)
                 if algo == "bitset2-sorted":  # bottom levels from the sorted padded array
