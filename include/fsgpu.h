@@ -111,8 +111,8 @@ typedef struct fs_plan {
   const void* sparse; /* direct (gap 1) only, optional: two-level sparse table
                          (fs_build_sparse); staged in shared memory when the
                          rank directory does not fit there.  NULL = unused.      */
-  int32_t sparse_shift;/* super-bucket = 2^sparse_shift buckets (1..16)           */
-  int32_t reserved;
+  int32_t sparse_shift;/* super-bucket = 2^sparse_shift buckets (5..16)           */
+  uint32_t sparse_ndense; /* dense (bitmask) super-buckets in `sparse`            */
 } fs_plan;
 
 /* Library identification. */
@@ -171,17 +171,26 @@ int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
                   uint64_t* f_scratch_dev, void* dir_dev, void* stream);
 
 /*
- * Two-level sparse encoding of the gap-1 table, for R >> N: super-bucket J
+ * Two-level sparse encoding of the gap-1 table, for R >> N.  Super-bucket J
  * (2^shift buckets) stores C[J] = K[J 2^shift] (uint32, (r >> shift) + 2
- * entries, the last = n1), each knot i stores F[i] = f_i mod 2^shift
- * (uint16, n1 entries) right after C.  Then K[j] = C[j >> shift] +
+ * entries, the last = n1); each knot i stores F[i] = f_i mod 2^shift
+ * (uint16, n1 entries) after C.  Then K[j] = C[j >> shift] +
  * #{i in [C[J], C[J+1]) : F[i] < j mod 2^shift} exactly, and bucket j holds
- * knot t = K[j] iff F[t] == j mod 2^shift.  fs_sparse_bytes: buffer size;
- * fs_sparse_shift: smallest shift whose table (plus X when with_x) fits in
- * budget_bytes, or -1.  f_scratch_dev: n1 uint64.
+ * knot t = K[j] iff F[t] == j mod 2^shift.  Super-buckets with more than 64
+ * knots are DENSE: bit 31 of C[J] is set, F[C[J]] holds a slot, and the
+ * slot's 2^shift-bit knot mask (uint32 words) and per-word prefix counts
+ * (uint16) follow F -- K[j] = C[J] + prefix + popc(mask below j), as in the
+ * rank directory.  Layout: C | F | pad to 4 | masks | prefixes.
+ *   fs_sparse_bytes: buffer size for (shift, ndense).
+ *   fs_plan_sparse: smallest shift (5..16) whose table (plus X when with_x)
+ *     fits in budget_bytes -> shift, ndense, bytes; FS_TOO_LARGE if none.  SYNC.
+ *   fs_build_sparse: fill the buffer for that shift.  SYNC.
+ * f_scratch_dev: n1 uint64.
  */
-uint64_t fs_sparse_bytes(uint64_t n1, uint64_t r, int32_t shift);
-int fs_sparse_shift(int32_t dtype, uint64_t n1, uint64_t r, uint64_t budget_bytes, int32_t with_x);
+uint64_t fs_sparse_bytes(uint64_t n1, uint64_t r, int32_t shift, uint64_t ndense);
+int fs_plan_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                   int32_t with_x, uint64_t* f_scratch_dev, int32_t* shift_out, uint64_t* ndense_out,
+                   uint64_t* bytes_out, void* stream);
 int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t shift,
                     uint64_t* f_scratch_dev, void* sparse_dev, void* stream);
 

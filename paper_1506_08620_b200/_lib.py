@@ -63,7 +63,7 @@ EXPORTED = (
     "fs_build_table",
     "fs_build_rank",
     "fs_sparse_bytes",
-    "fs_sparse_shift",
+    "fs_plan_sparse",
     "fs_build_sparse",
     "fs_build_hot_window",
     "fs_build_fused",
@@ -104,7 +104,7 @@ class FsPlan(ctypes.Structure):
         ("hot_knots", ctypes.c_uint64),
         ("sparse", ctypes.c_void_p),
         ("sparse_shift", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("sparse_ndense", ctypes.c_uint32),
     ]
 
 
@@ -136,9 +136,10 @@ def _declare(lib):
     lib.fs_build_rank.restype = ctypes.c_int
     lib.fs_build_rank.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _vp, _vp, _vp]
     lib.fs_sparse_bytes.restype = ctypes.c_uint64
-    lib.fs_sparse_bytes.argtypes = [_u64, _u64, _i32]
-    lib.fs_sparse_shift.restype = ctypes.c_int
-    lib.fs_sparse_shift.argtypes = [_i32, _u64, _u64, _u64, _i32]
+    lib.fs_sparse_bytes.argtypes = [_u64, _u64, _i32, _u64]
+    lib.fs_plan_sparse.restype = ctypes.c_int
+    lib.fs_plan_sparse.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _u64, _i32, _vp, _p_i32, _p_u64, _p_u64,
+                                   _vp]
     lib.fs_build_sparse.restype = ctypes.c_int
     lib.fs_build_sparse.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp]
     lib.fs_build_hot_window.restype = ctypes.c_int

@@ -321,10 +321,9 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
     return PreparedKernel(algorithm, p, structure, scalar, lanes, plan=plan, buffers=tuple(keep))
 
 
-#: the sparse two-level table is used only when no super-bucket holds more
-#: knots than this (in-super-bucket search of at most ~6 steps); measured:
-#: cfg2/cfg5 (max a few) 1.4-2.9x faster than L2 gathers, cfg4 (max 512) 2x slower
-SPARSE_MAX_OCCUPANCY = 64
+#: the sparse two-level table is used when its dense (bitmask) super-buckets
+#: hold at most this fraction of the knots
+SPARSE_MAX_DENSE_KNOT_FRACTION = 0.25
 
 #: hot-window staging budget: small enough that the L2-gather kernel keeps
 #: full occupancy (3-4 CTAs per SM) for the queries outside the window
@@ -365,31 +364,44 @@ def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) ->
     """For R >> N, the two-level sparse encoding of K (fs_build_sparse) fits
     in shared memory where the rank directory does not; the kernel picks it
     over L2 gathers when the directory (plus X) cannot be staged."""
-    if idx.r >= (1 << 32):
+    if idx.r >= (1 << 32) or len(p.values) >= (1 << 31):
         return
     lib = _lib.load()
     budget = _smem_budget() - 512
     dt = fs_dtype(p.precision)
     n1 = len(p.values)
-    shift = int(lib.fs_sparse_shift(dt, n1, idx.r, budget, 1))
-    if shift < 0:
-        shift = int(lib.fs_sparse_shift(dt, n1, idx.r, budget, 0))
-    if shift < 0:
-        return
-    buf = _device.empty(int(lib.fs_sparse_bytes(n1, idx.r, shift)), np.uint8)
+    x = p.device_values()
     f = _device.empty(n1, np.uint64)
-    rc = lib.fs_build_sparse(dt, p.device_values().data_ptr(), n1, float(idx.h), idx.r, shift, f.data_ptr(),
-                             buf.data_ptr(), _device.stream_ptr())
-    _lib.check(rc, what="fs_build_sparse")
-    # a query searches its super-bucket's knots: dense regions (cfg4's
-    # 1-knot-per-bucket start) make that search deep, and L2 gathers win
-    import torch
-
-    c = buf[: 4 * ((idx.r >> shift) + 2)].view(torch.int32)
-    if int((c[1:] - c[:-1]).max().item()) > SPARSE_MAX_OCCUPANCY:
+    shift, ndense, nbytes = ctypes.c_int32(-1), ctypes.c_uint64(0), ctypes.c_uint64(0)
+    for with_x in (1, 0):  # X staged beside the table if possible, else X via L2
+        rc = lib.fs_plan_sparse(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, with_x, f.data_ptr(),
+                                ctypes.byref(shift), ctypes.byref(ndense), ctypes.byref(nbytes),
+                                _device.stream_ptr())
+        if rc == _lib.FS_OK:
+            break
+        if rc != _lib.FS_TOO_LARGE:
+            _lib.check(rc, what="fs_plan_sparse")
+    else:
         return
+    buf = _device.empty(int(nbytes.value), np.uint8)
+    rc = lib.fs_build_sparse(dt, x.data_ptr(), n1, float(idx.h), idx.r, shift.value, f.data_ptr(), buf.data_ptr(),
+                             _device.stream_ptr())
+    _lib.check(rc, what="fs_build_sparse")
+    if ndense.value:
+        # queries in dense super-buckets still read X through L2 for almost
+        # every bucket; when those regions hold many knots (cfg4's start:
+        # 31%) the L2-gather kernel at full occupancy is faster (measured
+        # 354 vs 214 Gq/s), so the sparse table is kept for mostly-sparse
+        # layouts only
+        import torch
+
+        c = buf[: 4 * ((idx.r >> shift.value) + 2)].view(torch.int32).long() & 0x7FFFFFFF
+        occ = c[1:] - c[:-1]
+        if int(occ[occ > 64].sum().item()) > SPARSE_MAX_DENSE_KNOT_FRACTION * n1:
+            return
     plan.sparse = buf.data_ptr()
-    plan.sparse_shift = shift
+    plan.sparse_shift = shift.value
+    plan.sparse_ndense = ndense.value
     keep.append(buf)
 
 

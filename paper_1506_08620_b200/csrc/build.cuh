@@ -226,6 +226,37 @@ __global__ void fill_sparse_kernel(const uint64_t* __restrict__ f, uint64_t n1, 
   }
 }
 
+// Dense super-buckets of the sparse table (more than kDenseOcc knots): one
+// CTA per dense slot builds the 2^s-bit knot mask of super-bucket
+// J = dense_j[slot] in W = 2^(s-5) words plus per-word knot prefix counts,
+// then flags C[J] (bit 31) and stores the slot in F[C[J]], which the dense
+// path never reads as an offset.
+
+__global__ void fill_dense_kernel(uint32_t* __restrict__ C, uint16_t* __restrict__ F, const uint32_t* __restrict__ dense_j,
+                                  uint64_t ndense, int s, uint32_t* __restrict__ dmask, uint16_t* __restrict__ dpre) {
+  const uint32_t W = 1u << (s - 5);
+  for (uint64_t slot = blockIdx.x; slot < ndense; slot += gridDim.x) {
+    const uint32_t J = dense_j[slot];
+    const uint32_t lo = C[J] & ~kDenseFlag, hi = C[J + 1] & ~kDenseFlag;
+    for (uint32_t w = threadIdx.x; w < W; w += blockDim.x) {
+      uint32_t m = 0, pre = 0;
+      for (uint32_t i = lo; i < hi; ++i) {
+        const uint32_t off = F[i];
+        if ((off >> 5) == w) m |= 1u << (off & 31);
+        else if ((off >> 5) < w) ++pre;
+      }
+      dmask[slot * W + w] = m;
+      dpre[slot * W + w] = (uint16_t)pre;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      F[lo] = (uint16_t)slot;
+      C[J] = lo | kDenseFlag;
+    }
+    __syncthreads();
+  }
+}
+
 // Hot window of the rank directory: for every start word a, the longest
 // window [a, b) whose directory words plus the X range they reference,
 // [base_a, base_b], fit in `budget` bytes; the window holding the most

@@ -13,6 +13,12 @@
 
 namespace fsg {
 
+// Sparse two-level table: bit 31 of a super-bucket rank C[J] marks a dense
+// (bitmask) super-bucket (knot indices stay below 2^31).
+constexpr uint32_t kDenseFlag = 0x80000000u;
+// Super-buckets holding more knots than this are stored densely.
+constexpr uint32_t kDenseOcc = 64;
+
 // ---------------------------------------------------------------------------
 // Exact arithmetic in the partition's precision
 // ---------------------------------------------------------------------------

@@ -14,6 +14,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include "../../include/fsgpu.h"
 #include "build.cuh"
@@ -144,10 +145,10 @@ Placement place(const fs_plan* p) {
   const bool use_rank = p->algorithm == FS_ALGO_DIRECT && p->rank != nullptr && p->q == 1;
   // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
   if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->q == 1 && !force_global && p->r < (1ull << 32) &&
-      p->sparse_shift >= 1 && p->sparse_shift <= 16) {
+      p->sparse_shift >= 5 && p->sparse_shift <= 16) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
-    const uint64_t cfb = fs_sparse_bytes(p->n1, p->r, p->sparse_shift);
+    const uint64_t cfb = fs_sparse_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense);
     const bool rank_fits = use_rank && align128(xb) + dir_b <= budget;
     if (!rank_fits && cfb <= budget) {
       pl.sparse = pl.ks = true;
@@ -419,6 +420,7 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   d.off_s = (uint32_t)(n + 1 - d.off_f);
   d.off_j = (uint32_t)(bit_length(n + 1) - 1);
   d.sparse_shift = p->sparse_shift;
+  d.sparse_ndense = p->sparse_ndense;
   d.hot_w0 = (uint32_t)p->hot_word0;
   d.hot_nw = pl.hot ? (uint32_t)p->hot_words : 0;
   d.hot_t0 = (uint32_t)p->hot_knot0;
@@ -456,8 +458,12 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       if (pl.records) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (pl.sparse) {
-        if (pl.xs) return launch_probe<T, OutT, SparseProbe<T, true>>(d, pl, z, m, out, fb, base, st);
-        return launch_probe<T, OutT, SparseProbe<T, false>>(d, pl, z, m, out, fb, base, st);
+        if (p->sparse_ndense) {
+          if (pl.xs) return launch_probe<T, OutT, SparseProbe<T, true, true>>(d, pl, z, m, out, fb, base, st);
+          return launch_probe<T, OutT, SparseProbe<T, false, true>>(d, pl, z, m, out, fb, base, st);
+        }
+        if (pl.xs) return launch_probe<T, OutT, SparseProbe<T, true, false>>(d, pl, z, m, out, fb, base, st);
+        return launch_probe<T, OutT, SparseProbe<T, false, false>>(d, pl, z, m, out, fb, base, st);
       }
       if (p->rank && p->q == 1) {
         if (wide) return launch_probe<T, OutT, RankProbe<T, uint64_t, false, false>>(d, pl, z, m, out, fb, base, st);
@@ -642,24 +648,48 @@ int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
   return FS_OK;
 }
 
-uint64_t fs_sparse_bytes(uint64_t n1, uint64_t r, int32_t shift) {
-  if (shift < 1 || shift > 16) return 0;
-  return (4 * ((r >> shift) + 2) + 2 * n1 + 15) & ~15ull;
+uint64_t fs_sparse_bytes(uint64_t n1, uint64_t r, int32_t shift, uint64_t ndense) {
+  if (shift < 5 || shift > 16) return 0;
+  const uint64_t nc = (r >> shift) + 2, words = ndense << (shift - 5);
+  const uint64_t head = (4 * nc + 2 * n1 + 3) & ~3ull;  // C | F | pad to 4
+  return (head + words * 4 + words * 2 + 15) & ~15ull;  // | masks | prefixes
 }
 
-int fs_sparse_shift(int32_t dtype, uint64_t n1, uint64_t r, uint64_t budget_bytes, int32_t with_x) {
-  const uint64_t es = dtype == FS_F32 ? 4 : 8;
-  const uint64_t xb = with_x ? align128(n1 * es) : 0;
-  for (int s = 1; s <= 16; ++s)
-    if (xb + fs_sparse_bytes(n1, r, s) <= budget_bytes) return s;
-  return -1;
+int fs_plan_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                   int32_t with_x, uint64_t* f_scratch_dev, int32_t* shift_out, uint64_t* ndense_out,
+                   uint64_t* bytes_out, void* stream) {
+  if (!x_dev || !f_scratch_dev || n1 < 2 || !shift_out) return fail(FS_INVALID_ARG, "bad arguments");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "sparse table needs R < 2^32, N < 2^31");
+  const uint64_t xb = with_x ? align128(n1 * (dtype == FS_F32 ? 4 : 8)) : 0;
+  if (xb + 2 * n1 > budget_bytes) return fail(FS_TOO_LARGE, "knot offsets alone exceed the budget");
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
+  if (rc) return rc;
+  std::vector<uint64_t> f(n1);
+  FS_CUDA(cudaMemcpyAsync(f.data(), f_scratch_dev, n1 * 8, cudaMemcpyDeviceToHost, as_stream(stream)));
+  FS_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  for (int s = 5; s <= 16; ++s) {
+    const uint64_t nc = (r >> s) + 2;
+    if (xb + fs_sparse_bytes(n1, r, s, 0) > budget_bytes) continue;  // C + F alone too big
+    std::vector<uint32_t> occ(nc, 0);
+    for (uint64_t i = 0; i < n1; ++i) ++occ[f[i] >> s];
+    uint64_t ndense = 0;
+    for (uint32_t o : occ) ndense += o > kDenseOcc;
+    const uint64_t bytes = fs_sparse_bytes(n1, r, s, ndense);
+    if (ndense <= 65535 && xb + bytes <= budget_bytes) {
+      *shift_out = s;
+      if (ndense_out) *ndense_out = ndense;
+      if (bytes_out) *bytes_out = bytes;
+      return FS_OK;
+    }
+  }
+  return fail(FS_TOO_LARGE, "no sparse layout fits the budget");
 }
 
 int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t shift,
                     uint64_t* f_scratch_dev, void* sparse_dev, void* stream) {
-  if (!x_dev || !f_scratch_dev || !sparse_dev || n1 < 2 || shift < 1 || shift > 16)
+  if (!x_dev || !f_scratch_dev || !sparse_dev || n1 < 2 || shift < 5 || shift > 16)
     return fail(FS_INVALID_ARG, "bad arguments");
-  if (n1 - 1 >= (1ull << 32) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "sparse table needs R, N < 2^32");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "sparse table needs R < 2^32, N < 2^31");
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
   if (rc) return rc;
   cudaStream_t s = as_stream(stream);
@@ -668,6 +698,26 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
   uint16_t* F = reinterpret_cast<uint16_t*>(C + nc);
   fill_sparse_kernel<<<grid_1d(std::max(nc, n1), 256), 256, 0, s>>>(f_scratch_dev, n1, r, shift, C, F);
   FS_CUDA(cudaGetLastError());
+  // dense super-buckets: slot order = increasing J (the same count fs_plan_sparse made)
+  std::vector<uint32_t> c(nc);
+  FS_CUDA(cudaMemcpyAsync(c.data(), C, nc * 4, cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint32_t> dense_j;
+  for (uint64_t J = 0; J + 1 < nc; ++J)
+    if (c[J + 1] - c[J] > kDenseOcc) dense_j.push_back((uint32_t)J);
+  if (dense_j.empty()) return FS_OK;
+  if (dense_j.size() > 65535) return fail(FS_TOO_LARGE, "too many dense super-buckets");
+  const uint64_t words = (uint64_t)dense_j.size() << (shift - 5);
+  const uint64_t head = (4 * nc + 2 * n1 + 3) & ~3ull;
+  uint32_t* dmask = reinterpret_cast<uint32_t*>(static_cast<char*>(sparse_dev) + head);
+  uint16_t* dpre = reinterpret_cast<uint16_t*>(dmask + words);
+  // the f scratch is free again: it carries the dense super-bucket list
+  FS_CUDA(cudaMemcpyAsync(f_scratch_dev, dense_j.data(), dense_j.size() * 4, cudaMemcpyHostToDevice, s));
+  const int grid = (int)std::min<uint64_t>(dense_j.size(), (uint64_t)sm_count() * 8);
+  fill_dense_kernel<<<grid, 128, 0, s>>>(C, F, reinterpret_cast<const uint32_t*>(f_scratch_dev), dense_j.size(), shift,
+                                        dmask, dpre);
+  FS_CUDA(cudaGetLastError());
+  FS_CUDA(cudaStreamSynchronize(s));
   return FS_OK;
 }
 

@@ -49,6 +49,7 @@ struct DevPlan {
   uint32_t table_smem_bytes; // bytes of K / records staged; 0 = global
   int32_t out_vec_ok;        // output pointer co-aligned with the 16-B query groups
   int32_t sparse_shift;      // sparse two-level table: super-bucket = 2^shift buckets
+  uint32_t sparse_ndense;    // ... and its number of dense (bitmask) super-buckets
   uint32_t hot_w0, hot_nw;   // rank-directory hot window (words) staged in smem
   uint32_t hot_t0, hot_nt;   // knot window X[t0, t0 + nt) staged in smem
   __host__ __device__ __forceinline__ uint32_t x_smem_bytes_aligned() const {
@@ -173,39 +174,58 @@ struct RankProbe {
 // holding a knot).  t = K[j] = C[J] + lower_bound(F[C[J] .. C[J+1]), j mod 2^s)
 // exactly; bucket j holds knot t iff F[t] == j mod 2^s; identical answers to
 // DirectProbe<GAP=1> (batch.py:315-317).
-template <typename T, bool XS>
+template <typename T, bool XS, bool DENSE>
 struct SparseProbe {
   const T* X;
   const uint32_t* C;
   const uint16_t* F;
+  const uint32_t* Dm;  // dense super-buckets: knot masks, W words each
+  const uint16_t* Dp;  //                     per-word knot prefix counts
   T h, x0;
-  uint32_t r, s, mask;
+  uint32_t r, s, mask, wshift;
   __device__ __forceinline__ SparseProbe(const DevPlan<T>& p, unsigned char* smem) {
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
     unsigned char* cf = smem + p.x_smem_bytes_aligned();
+    const uint64_t nc = ((uint64_t)p.r >> p.sparse_shift) + 2;
     C = reinterpret_cast<const uint32_t*>(cf);
-    F = reinterpret_cast<const uint16_t*>(cf + 4 * (((uint64_t)p.r >> p.sparse_shift) + 2));
+    F = reinterpret_cast<const uint16_t*>(cf + 4 * nc);
+    const uint64_t dm_off = (4 * nc + 2 * p.n1 + 3) & ~3ull;
+    Dm = reinterpret_cast<const uint32_t*>(cf + dm_off);
+    Dp = reinterpret_cast<const uint16_t*>(cf + dm_off + 4ull * p.sparse_ndense * (1ull << (p.sparse_shift - 5)));
     h = p.h;
     x0 = p.x0;
     r = (uint32_t)p.r;
     s = (uint32_t)p.sparse_shift;
     mask = (1u << s) - 1u;
+    wshift = s - 5;
   }
   __device__ __forceinline__ int64_t operator()(T z) const {
     uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
     j = j < r ? j : r;
     const uint32_t J = j >> s, jl = j & mask;
-    uint32_t lo = C[J], hi = C[J + 1];
-    const uint32_t end = hi;
-    while (lo < hi) {  // lower_bound of jl in F[lo, hi)
-      const uint32_t mid = (lo + hi) >> 1;
-      if (F[mid] < jl) lo = mid + 1;
-      else hi = mid;
+    const uint32_t c = C[J];
+    uint32_t t;
+    bool knot;
+    if (DENSE && (c & kDenseFlag)) {  // dense super-bucket: mask word + prefix, like the rank directory
+      const uint32_t lo = c & ~kDenseFlag;
+      const uint32_t widx = ((uint32_t)F[lo] << wshift) + (jl >> 5);
+      const uint32_t m = Dm[widx], b = jl & 31u;
+      t = lo + Dp[widx] + __popc(m & ((1u << b) - 1u));
+      knot = (m >> b) & 1u;
+    } else {  // lower_bound of jl among the super-bucket's knot offsets
+      uint32_t lo = c, hi = DENSE ? C[J + 1] & ~kDenseFlag : C[J + 1];
+      const uint32_t end = hi;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (F[mid] < jl) lo = mid + 1;
+        else hi = mid;
+      }
+      t = lo;
+      knot = lo < end && F[lo] == jl;
     }
-    const bool knot = lo < end && F[lo] == jl;
     T xv = z;
-    if (knot) xv = tload<XS>(X, lo);
-    return (int64_t)lo - ((!knot || z < xv) ? 1 : 0);
+    if (knot) xv = tload<XS>(X, t);
+    return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
   }
 };
 

@@ -220,6 +220,27 @@ def test_direct_table_variants_agree(cuda, variant):
         assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(p.values, z)), (name, variant)
 
 
+def test_sparse_table_with_dense_super_buckets(cuda):
+    """A mostly-sparse layout with one tight cluster: the two-level sparse
+    table with dense (bitmask) super-buckets is chosen and is exact."""
+    fs = _fs()
+    rng = np.random.default_rng(17)
+    base = np.sort(rng.uniform(0.0, 1.0, 1000))
+    base = base[np.concatenate([[True], np.diff(base) > 1e-5])]
+    cluster = 0.5 + 1e-7 * np.arange(1, 201)
+    xs = np.unique(np.concatenate([base[(base < 0.5) | (base > 0.5 + 1e-4)], cluster, [0.0, 1.0]]))
+    p = fs.validate_partition(xs)
+    prep = fs.prepare("direct", p)
+    assert prep.placement()["smem_sparse"] and prep.plan.sparse_ndense > 0
+    z = np.concatenate([orc.random_queries(xs, 300_000, seed=2), orc.boundary_probes(xs),
+                        np.random.default_rng(3).uniform(0.5, 0.5 + 2.1e-5, 100_000)])
+    z = z[(z >= xs[0]) & (z < xs[-1])]
+    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
+    # and the same answers with the dense path's competitors
+    prep.plan.sparse = None
+    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
+
+
 def test_scalar_entry_points(cuda):
     """binsearch.py / eytzinger.py scalar wrappers (test_binsearch.py:43-79)."""
     fs = _fs()
