@@ -17,7 +17,9 @@ same metric through the public drop-in API (``batch_search`` on pinned host
 numpy arrays: H2D copies, kernel and D2H inside every step); ``bsearch`` =
 the branchless binary search (Alg 3, bitset2) timed identically -- the
 "direct vs binary search" half of the metric.  Inputs are 4 GiB + 4 GiB of
-output per GPU, far larger than the 126 MB L2, so no flush is needed.
+output per GPU, far larger than the 126 MB L2, so no flush is needed; the
+``per_config`` sweep flushes L2 before every launch of a stream that fits in
+it (cfg1).
 
 ``--impl reference`` times the reference's CPU path (its numpy lane kernel
 and thread-span driver, restated in oracle/fs_oracle.py -- the reference
@@ -194,9 +196,12 @@ def run_reference(args):
     return 0
 
 
-def time_device(prep, z, out, fb, steps: int, warmup: int, barrier):
+def time_device(prep, z, out, fb, steps: int, warmup: int, barrier, flush=None):
     """Warm up, then time exactly ``steps`` launches with CUDA events on the
-    launching stream, bracketed by barrier + synchronize."""
+    launching stream, bracketed by barrier + synchronize.  With ``flush`` (a
+    device buffer larger than L2), every launch is preceded by an untimed
+    write of that buffer and timed by its own event pair, so a stream that
+    fits in L2 is read cold each time."""
     import torch
 
     for _ in range(warmup):
@@ -205,6 +210,17 @@ def time_device(prep, z, out, fb, steps: int, warmup: int, barrier):
     barrier()
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
+    if flush is not None:
+        pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in pairs:
+            flush.zero_()
+            a.record(s)
+            prep.launch(z, out, fb)
+            b.record(s)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in pairs) / 1e3
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     start.record(s)
@@ -215,6 +231,9 @@ def time_device(prep, z, out, fb, steps: int, warmup: int, barrier):
     barrier()
     torch.cuda.synchronize()
     return start.elapsed_time(stop) / 1e3  # seconds for `steps` launches
+
+
+L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2
 
 
 PER_CONFIG = (
@@ -249,10 +268,13 @@ def per_config(steps: int, barrier, world: int):
         fb = fs.new_status(z.device)
         qb = z.element_size() + 4
         row = {"queries_per_gpu": m, "dtype": "f32" if p.precision == "single" else "f64", "bytes_per_query": qb}
+        # streams that fit in L2 are read cold: the L2 is flushed before every launch
+        flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=z.device) if qb * m < L2_FLUSH_BYTES else None
+        row["l2"] = "flushed before each launch" if flush is not None else "stream > L2, no flush"
         for name in ("direct", "bitset2"):
             prep = fs.prepare_with_fallback(p) if name == "direct" else fs.prepare("bitset2", p)
             n = steps * (1 if m >= (1 << 30) else 4) * (1 if m >= (1 << 26) else 10)
-            t = time_device(prep, z, out, fb, n, 3, barrier) / n
+            t = time_device(prep, z, out, fb, n, 3, barrier, flush) / n
             ok = fs.first_bad_of(fb) is None and verify_bracket(p, z, out)
             tt = torch.tensor([t, 0.0 if ok else 1.0], dtype=torch.float64, device=z.device)
             if world > 1:
@@ -269,7 +291,7 @@ def per_config(steps: int, barrier, world: int):
             if name == "direct" and prep.algorithm.startswith("direct"):
                 row["R"] = prep.structure.r
         res[label] = row
-        del z, out
+        del z, out, flush
         torch.cuda.empty_cache()
     return res
 
