@@ -276,6 +276,16 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
  * driver's bounce buffer instead.
  */
 #define FS_HOST_NO_STAGING 2
+/*
+ * Default (atomic) mode over two or more chunks of page-locked (or small)
+ * buffers: host threads check every query's domain while the uploads run;
+ * once no query is bad, each chunk's results are copied back as soon as its
+ * kernel finishes, overlapping the remaining uploads (nothing is written if
+ * a query is bad -- the contract is unchanged).  flags & FS_HOST_NO_PRECHECK:
+ * wait for the device's first-bad word before any write-back instead.
+ * FS_INCONSISTENT if the two checks disagree (z_host modified during the call).
+ */
+#define FS_HOST_NO_PRECHECK 4
 int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host,
                    int32_t out_bytes, void* z_dev, void* out_dev,
                    unsigned long long* status_dev, uint64_t chunk_elems,

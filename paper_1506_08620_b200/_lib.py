@@ -33,6 +33,8 @@ FS_F32 = 0
 FS_F64 = 1
 
 FS_HOST_OVERLAP = 1
+FS_HOST_NO_STAGING = 2
+FS_HOST_NO_PRECHECK = 4
 
 ALGO_CODES = {
     "classic": 0,

@@ -110,9 +110,11 @@ def _plan_for(algorithm: str, structure, p: SortedPartition):
 
 
 def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = HOST_CHUNK_BYTES,
-                       overlap: bool = False) -> None:
+                       overlap: bool = False, precheck: bool = True) -> None:
     """End-to-end search of host queries into host ``out[:m]`` (fs_search_host).
-    ``overlap`` = speculative per-chunk write-back (FS_HOST_OVERLAP)."""
+    ``overlap`` = speculative per-chunk write-back (FS_HOST_OVERLAP);
+    ``precheck=False`` = wait for the device's domain check before any
+    write-back (FS_HOST_NO_PRECHECK)."""
     m = len(z)
     if m == 0:
         return
@@ -128,7 +130,8 @@ def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = 
     rc = _lib.load().fs_search_host(
         ctypes.byref(plan), z.ctypes.data, m, target.ctypes.data, ob, z_dev.data_ptr(), o_dev.data_ptr(),
         fb.data_ptr(), max(4, chunk_bytes // z.dtype.itemsize), ctypes.byref(pos), _device.stream_ptr(),
-        _device.stream_ptr(_copy_stream()), _lib.FS_HOST_OVERLAP if overlap else 0,
+        _device.stream_ptr(_copy_stream()),
+        (_lib.FS_HOST_OVERLAP if overlap else 0) | (0 if precheck else _lib.FS_HOST_NO_PRECHECK),
     )
     _lib.check(rc, pos=pos.value, what="fs_search_host")
     if not direct_out:

@@ -919,13 +919,19 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   chunk_elems = (chunk_elems + 3) & ~3ull;  // keep every chunk 16-B aligned on device
   Placement pl = place_for_batch(plan, m);
   pl.merge = 1;  // every chunk min-merges into status[0]
+  // atomic mode over several chunks: host threads check the domain while the
+  // chunks upload, so write-back can start before the last upload
+  const uint64_t nch = (m + chunk_elems - 1) / chunk_elems;
+  const bool precheck = !overlap && !(flags & FS_HOST_NO_PRECHECK) && nch >= 2;
   FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
   cudaEvent_t ev, evk;
   cudaStream_t ds = nullptr;
+  std::vector<cudaEvent_t> done;  // precheck: kernel of chunk c finished
   FS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   FS_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
-  if (overlap) FS_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+  if (overlap || precheck) FS_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
   int status = FS_OK;
+  bool wrote = false;
   for (uint64_t off = 0; off < m && status == FS_OK; off += chunk_elems) {
     const uint64_t n = std::min(chunk_elems, m - off);
     const char* src = static_cast<const char*>(z_host) + off * es;
@@ -949,6 +955,34 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
                             cudaMemcpyDeviceToHost, ds);
       if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("chunk download: ") + cudaGetErrorString(e));
     }
+    if (status == FS_OK && precheck) {
+      cudaEvent_t d;
+      cudaError_t e = cudaEventCreateWithFlags(&d, cudaEventDisableTiming);
+      if (e == cudaSuccess) {
+        done.push_back(d);
+        e = cudaEventRecord(d, s);
+      }
+      if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("chunk event: ") + cudaGetErrorString(e));
+    }
+  }
+  // every upload and search is queued: check the domain on the host meanwhile,
+  // then queue each chunk's write-back behind its kernel
+  if (status == FS_OK && precheck) {
+    const uint64_t hb =
+        plan->dtype == FS_F32
+            ? host_first_bad<float>(static_cast<const float*>(z_host), m, (float)plan->x0, (float)plan->xn,
+                                    host_scan_threads())
+            : host_first_bad<double>(static_cast<const double*>(z_host), m, plan->x0, plan->xn, host_scan_threads());
+    for (uint64_t c = 0; hb == ~0ull && c < done.size() && status == FS_OK; ++c) {
+      const uint64_t off = c * chunk_elems, n = std::min(chunk_elems, m - off);
+      cudaError_t e = cudaStreamWaitEvent(ds, done[c], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(static_cast<char*>(out_host) + off * out_bytes,
+                            static_cast<const char*>(out_dev) + off * out_bytes, n * (uint64_t)out_bytes,
+                            cudaMemcpyDeviceToHost, ds);
+      if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("chunk download: ") + cudaGetErrorString(e));
+      wrote = true;
+    }
   }
   unsigned long long bad = ~0ull;
   if (status == FS_OK) {
@@ -961,14 +995,16 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
     cudaStreamSynchronize(ds);
     cudaStreamDestroy(ds);
   }
+  for (cudaEvent_t d : done) cudaEventDestroy(d);
   cudaEventDestroy(ev);
   cudaEventDestroy(evk);
   if (status != FS_OK) return status;
   if (bad != ~0ull) {
     if (pos_out) *pos_out = (int64_t)bad;
+    if (wrote) return fail(FS_INCONSISTENT, "host and device domain checks disagree (queries modified during the call?)");
     return fail(FS_OUT_OF_DOMAIN, "query outside [X0, XN)");
   }
-  if (m && !overlap) {
+  if (m && !overlap && !wrote) {
     FS_CUDA(cudaMemcpyAsync(out_host, out_dev, m * (uint64_t)out_bytes, cudaMemcpyDeviceToHost, s));
     FS_CUDA(cudaStreamSynchronize(s));
   }

@@ -142,6 +142,73 @@ inline bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// ---------------------------------------------------------------------------
+// Host-side domain check of the queries (the compare of batch.py:411-413,
+// NaN included), run while the uploads and searches of the same call are in
+// flight.  It lets the default (atomic) end-to-end path start writing results
+// back before the last chunk has been uploaded: "nothing is written on
+// OutOfDomain" only needs to know that no query is bad, and the host can
+// establish that at ~100 GB/s (16 threads, AVX2), faster than PCIe uploads
+// the queries.  The device kernels still perform their own fused check and
+// report the position.
+// ---------------------------------------------------------------------------
+template <typename T>
+inline uint64_t scan_span_generic(const T* z, uint64_t a, uint64_t b, T x0, T xn) {
+  constexpr uint64_t kBlock = 4096;
+  for (uint64_t i = a; i < b; i += kBlock) {
+    const uint64_t e = std::min(b, i + kBlock);
+    int bad = 0;
+    for (uint64_t k = i; k < e; ++k) bad |= (int)!(z[k] >= x0) | (int)!(z[k] < xn);
+    if (bad)
+      for (uint64_t k = i; k < e; ++k)
+        if (!(z[k] >= x0 && z[k] < xn)) return k;
+  }
+  return ~0ull;
+}
+
+template <typename T>
+__attribute__((target("avx2"), optimize("O3"))) uint64_t scan_span_avx2(const T* z, uint64_t a, uint64_t b, T x0,
+                                                                          T xn) {
+  constexpr uint64_t kBlock = 4096;
+  for (uint64_t i = a; i < b; i += kBlock) {
+    const uint64_t e = std::min(b, i + kBlock);
+    int bad = 0;
+    for (uint64_t k = i; k < e; ++k) bad |= (int)!(z[k] >= x0) | (int)!(z[k] < xn);
+    if (bad)
+      for (uint64_t k = i; k < e; ++k)
+        if (!(z[k] >= x0 && z[k] < xn)) return k;
+  }
+  return ~0ull;
+}
+
+// First position in z[0, m) outside [x0, xn), ~0 if none; n threads over
+// contiguous spans (the smallest bad position wins).
+template <typename T>
+uint64_t host_first_bad(const T* z, uint64_t m, T x0, T xn, int n) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  auto scan = [&](uint64_t a, uint64_t b) {
+    return avx2 ? scan_span_avx2<T>(z, a, b, x0, xn) : scan_span_generic<T>(z, a, b, x0, xn);
+  };
+  if (n <= 1 || m < (1u << 20)) return scan(0, m);
+  std::vector<uint64_t> res(n, ~0ull);
+  std::vector<std::thread> th;
+  const uint64_t per = (m + n - 1) / n;
+  for (int i = 1; i < n; ++i)
+    th.emplace_back([&, i] { res[i] = scan(std::min(m, per * i), std::min(m, per * (i + 1))); });
+  res[0] = scan(0, std::min(m, per));
+  for (auto& t : th) t.join();
+  return *std::min_element(res.begin(), res.end());
+}
+
+inline int host_scan_threads() {
+  if (const char* e = std::getenv("FSG_SCAN_THREADS")) {  // tuning override
+    const int n = std::atoi(e);
+    if (n > 0) return std::min(n, 64);
+  }
+  const unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(32u, hc ? hc : 4u));
+}
+
 inline int host_copy_threads() {
   if (const char* e = std::getenv("FSG_COPY_THREADS")) {  // tuning override
     const int n = std::atoi(e);

@@ -156,6 +156,63 @@ def test_atomic_contract_with_chunks(cuda, sweep4095):
     assert (out == 123).all()
 
 
+@pytest.mark.parametrize("precheck", [True, False])
+@pytest.mark.parametrize("where", ["first", "middle", "last", "nan", "none"])
+def test_host_precheck_atomic_contract(cuda, sweep4095, precheck, where):
+    """Atomic mode over many chunks, with and without the host-side domain
+    pre-check that lets write-back overlap the uploads: exact answers when
+    clean; the device's first-bad position and an untouched `out` when not."""
+    fs = _fs()
+    from paper_1506_08620_b200 import batch as fb
+
+    _, xs, z = sweep4095
+    p = fs.validate_partition(xs)
+    prep = fs.prepare("direct", p)
+    bad = z.copy()
+    pos = {"first": 0, "middle": len(z) // 2, "last": len(z) - 1, "nan": len(z) // 3, "none": None}[where]
+    if pos is not None:
+        bad[pos] = np.nan if where == "nan" else xs[-1]
+        bad[pos + 1:] = np.where(np.arange(len(z) - pos - 1) % 7 == 0, -1.0, bad[pos + 1:]).astype(z.dtype)
+    out = np.full(len(z), 123, dtype=np.int32)
+    if pos is None:
+        fb._search_host_array(prep.plan, bad, out, chunk_bytes=4096, precheck=precheck)
+        assert np.array_equal(out, orc.rank_oracle(p.values, z))
+    else:
+        with pytest.raises(fs.OutOfDomain) as e:
+            fb._search_host_array(prep.plan, bad, out, chunk_bytes=4096, precheck=precheck)
+        assert e.value.position == pos
+        assert (out == 123).all()
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_host_precheck_pinned_threads(cuda, prec):
+    """Page-locked buffers of several million queries: the host check runs
+    on many threads; a bad query deep in a later thread's span is reported
+    at its position with `out` untouched, and a clean batch is exact."""
+    import torch
+
+    fs = _fs()
+    from paper_1506_08620_b200 import batch as fb
+    from paper_1506_08620_b200 import workloads
+
+    name = "cfg3" if prec == "single" else "cfg5"
+    p = workloads.knots(name) if prec == "single" else workloads.knots("cfg5", n1=1025)
+    m = 3_000_017
+    zh = workloads.queries_host(name, p, m, seed=12)
+    z = torch.from_numpy(zh).pin_memory().numpy()
+    out = torch.full((m,), 5, dtype=torch.int32).pin_memory().numpy()
+    prep = fs.prepare("direct", p)
+    fb._search_host_array(prep.plan, z, out, chunk_bytes=1 << 20)
+    assert np.array_equal(out, orc.rank_oracle(p.values, zh))
+    out[:] = 5
+    z[2_345_678] = -np.inf
+    z[2_999_999] = np.nan
+    with pytest.raises(fs.OutOfDomain) as e:
+        fb._search_host_array(prep.plan, z, out, chunk_bytes=1 << 20)
+    assert e.value.position == 2_345_678
+    assert (out == 5).all()
+
+
 @pytest.mark.parametrize("prec,odt", [("single", np.int32), ("double", np.int64)])
 def test_pageable_staged_host_path(cuda, prec, odt):
     """Pageable numpy buffers >= 4 MB go through the library's pinned staging
