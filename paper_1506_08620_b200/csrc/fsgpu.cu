@@ -926,7 +926,10 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
   cudaEvent_t ev, evk;
   cudaStream_t ds = nullptr;
-  std::vector<cudaEvent_t> done;  // precheck: kernel of chunk c finished
+  std::vector<cudaEvent_t> done;  // precheck: kernel of chunk c finished ...
+  unsigned long long* prefix_bad = nullptr;  // ... with this first-bad word (pinned)
+  if (precheck && !(prefix_bad = static_cast<unsigned long long*>(PinnedSlots::acquire(nch * 8))))
+    return fail(FS_CUDA_ERROR, "pinned status allocation failed");
   FS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   FS_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
   if (overlap || precheck) FS_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
@@ -955,9 +958,11 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
                             cudaMemcpyDeviceToHost, ds);
       if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("chunk download: ") + cudaGetErrorString(e));
     }
-    if (status == FS_OK && precheck) {
+    if (status == FS_OK && precheck) {  // the device's verdict on chunks 0..c, then done[c]
       cudaEvent_t d;
-      cudaError_t e = cudaEventCreateWithFlags(&d, cudaEventDisableTiming);
+      cudaError_t e = cudaMemcpyAsync(&prefix_bad[done.size()], first_bad_dev, sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d, cudaEventDisableTiming);
       if (e == cudaSuccess) {
         done.push_back(d);
         e = cudaEventRecord(d, s);
@@ -965,15 +970,17 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
       if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("chunk event: ") + cudaGetErrorString(e));
     }
   }
-  // every upload and search is queued: check the domain on the host meanwhile,
-  // then queue each chunk's write-back behind its kernel
+  // every upload and search is queued: establish "no query is bad" from both
+  // ends meanwhile, then queue each chunk's write-back behind its kernel
   if (status == FS_OK && precheck) {
-    const uint64_t hb =
+    const int64_t nd = (int64_t)done.size();
+    const bool clean =
         plan->dtype == FS_F32
-            ? host_first_bad<float>(static_cast<const float*>(z_host), m, (float)plan->x0, (float)plan->xn,
-                                    host_scan_threads())
-            : host_first_bad<double>(static_cast<const double*>(z_host), m, plan->x0, plan->xn, host_scan_threads());
-    for (uint64_t c = 0; hb == ~0ull && c < done.size() && status == FS_OK; ++c) {
+            ? domain_clean_two_sided<float>(static_cast<const float*>(z_host), m, chunk_elems, (float)plan->x0,
+                                            (float)plan->xn, host_scan_threads(), done.data(), prefix_bad, nd)
+            : domain_clean_two_sided<double>(static_cast<const double*>(z_host), m, chunk_elems, plan->x0, plan->xn,
+                                             host_scan_threads(), done.data(), prefix_bad, nd);
+    for (uint64_t c = 0; clean && c < done.size() && status == FS_OK; ++c) {
       const uint64_t off = c * chunk_elems, n = std::min(chunk_elems, m - off);
       cudaError_t e = cudaStreamWaitEvent(ds, done[c], 0);
       if (e == cudaSuccess)
@@ -996,6 +1003,7 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
     cudaStreamDestroy(ds);
   }
   for (cudaEvent_t d : done) cudaEventDestroy(d);
+  if (prefix_bad) PinnedSlots::release(prefix_bad);
   cudaEventDestroy(ev);
   cudaEventDestroy(evk);
   if (status != FS_OK) return status;

@@ -1,4 +1,5 @@
-// host_staging.h — host side of the end-to-end path for PAGEABLE buffers.
+// host_staging.h — host side of the end-to-end path: pinned staging of
+// PAGEABLE buffers, and the host half of the two-sided domain check.
 //
 // cudaMemcpyAsync from pageable memory goes through the driver's bounce
 // buffer at ~14 GB/s here (measured: 1.7 G queries/s end to end on cfg3
@@ -12,6 +13,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <memory>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -147,14 +151,14 @@ inline bool is_pinned(const void* p) {
 // NaN included), run while the uploads and searches of the same call are in
 // flight.  It lets the default (atomic) end-to-end path start writing results
 // back before the last chunk has been uploaded: "nothing is written on
-// OutOfDomain" only needs to know that no query is bad, and the host can
-// establish that at ~100 GB/s (16 threads, AVX2), faster than PCIe uploads
-// the queries.  The device kernels still perform their own fused check and
-// report the position.
+// OutOfDomain" only needs to know that no query is bad, and host threads
+// (AVX2, ~100 GB/s with 16 threads) scanning from the end meet the device's
+// own fused check, which advances from the start at the PCIe upload rate.
+// The device still reports the position.
 // ---------------------------------------------------------------------------
 template <typename T>
-inline uint64_t scan_span_generic(const T* z, uint64_t a, uint64_t b, T x0, T xn) {
-  constexpr uint64_t kBlock = 4096;
+__attribute__((always_inline)) inline uint64_t scan_span_body(const T* z, uint64_t a, uint64_t b, T x0, T xn) {
+  constexpr uint64_t kBlock = 4096;  // branch-free (vectorised) test per block, exact scan only if it fails
   for (uint64_t i = a; i < b; i += kBlock) {
     const uint64_t e = std::min(b, i + kBlock);
     int bad = 0;
@@ -165,39 +169,68 @@ inline uint64_t scan_span_generic(const T* z, uint64_t a, uint64_t b, T x0, T xn
   }
   return ~0ull;
 }
-
+template <typename T>
+uint64_t scan_span_generic(const T* z, uint64_t a, uint64_t b, T x0, T xn) {
+  return scan_span_body<T>(z, a, b, x0, xn);
+}
 template <typename T>
 __attribute__((target("avx2"), optimize("O3"))) uint64_t scan_span_avx2(const T* z, uint64_t a, uint64_t b, T x0,
                                                                           T xn) {
-  constexpr uint64_t kBlock = 4096;
-  for (uint64_t i = a; i < b; i += kBlock) {
-    const uint64_t e = std::min(b, i + kBlock);
-    int bad = 0;
-    for (uint64_t k = i; k < e; ++k) bad |= (int)!(z[k] >= x0) | (int)!(z[k] < xn);
-    if (bad)
-      for (uint64_t k = i; k < e; ++k)
-        if (!(z[k] >= x0 && z[k] < xn)) return k;
-  }
-  return ~0ull;
+  return scan_span_body<T>(z, a, b, x0, xn);
 }
 
-// First position in z[0, m) outside [x0, xn), ~0 if none; n threads over
-// contiguous spans (the smallest bad position wins).
+// Two-sided domain check of the atomic host path.  The device checks every
+// chunk as it arrives: prefix_bad[c] (copied to pinned memory before done[c]
+// fires) is the first bad position in chunks 0..c, so the device covers a
+// prefix that grows at the PCIe upload rate.  Host threads scan chunks from
+// the END at host-memory speed.  Returns true once the two meet with no bad
+// query; false as soon as either side sees one (the caller then reports the
+// device's position and writes nothing).
 template <typename T>
-uint64_t host_first_bad(const T* z, uint64_t m, T x0, T xn, int n) {
+bool domain_clean_two_sided(const T* z, uint64_t m, uint64_t chunk, T x0, T xn, int nthreads,
+                            const cudaEvent_t* done, const volatile unsigned long long* prefix_bad, int64_t nch) {
   static const bool avx2 = __builtin_cpu_supports("avx2");
-  auto scan = [&](uint64_t a, uint64_t b) {
-    return avx2 ? scan_span_avx2<T>(z, a, b, x0, xn) : scan_span_generic<T>(z, a, b, x0, xn);
+  constexpr uint64_t kSlice = 1u << 20;  // elements between stop checks
+  std::atomic<int64_t> next{nch - 1}, gpu_upto{-1};
+  std::atomic<bool> stop{false}, bad{false};
+  std::unique_ptr<std::atomic<char>[]> clean(new std::atomic<char>[nch]);
+  for (int64_t c = 0; c < nch; ++c) clean[c].store(0, std::memory_order_relaxed);
+  auto worker = [&] {
+    for (;;) {
+      const int64_t c = next.fetch_sub(1);
+      if (c < 0 || c <= gpu_upto.load()) return;
+      const uint64_t e = std::min(m, (uint64_t)(c + 1) * chunk);
+      for (uint64_t a = (uint64_t)c * chunk; a < e; a += kSlice) {
+        if (stop.load(std::memory_order_relaxed)) return;
+        const uint64_t b = std::min(e, a + kSlice);
+        if ((avx2 ? scan_span_avx2<T>(z, a, b, x0, xn) : scan_span_generic<T>(z, a, b, x0, xn)) != ~0ull) {
+          bad.store(true);
+          stop.store(true);
+          return;
+        }
+      }
+      clean[c].store(1);
+    }
   };
-  if (n <= 1 || m < (1u << 20)) return scan(0, m);
-  std::vector<uint64_t> res(n, ~0ull);
   std::vector<std::thread> th;
-  const uint64_t per = (m + n - 1) / n;
-  for (int i = 1; i < n; ++i)
-    th.emplace_back([&, i] { res[i] = scan(std::min(m, per * i), std::min(m, per * (i + 1))); });
-  res[0] = scan(0, std::min(m, per));
+  for (int i = 0; i < std::max(1, nthreads); ++i) th.emplace_back(worker);
+  int64_t g = -1;  // chunks [0, g] verified by the device
+  while (!bad.load()) {
+    while (g + 1 < nch && cudaEventQuery(done[g + 1]) == cudaSuccess) {
+      if (prefix_bad[g + 1] != ~0ull) {
+        bad.store(true);
+        break;
+      }
+      gpu_upto.store(++g);
+    }
+    bool covered = true;
+    for (int64_t c = g + 1; c < nch && covered; ++c) covered = clean[c].load() != 0;
+    if (covered) break;
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  stop.store(true);
   for (auto& t : th) t.join();
-  return *std::min_element(res.begin(), res.end());
+  return !bad.load();
 }
 
 inline int host_scan_threads() {
