@@ -44,7 +44,8 @@ typedef enum fs_status {
   FS_OUT_OF_DOMAIN = 3,       /* errors.OutOfDomain(position)                 */
   FS_INVALID_ARG = 4,         /* ValueError (qbits, q, sizes, dtype, ...)     */
   FS_CUDA_ERROR = 5,          /* CUDA runtime failure; see fs_last_error()    */
-  FS_INCONSISTENT = 6,        /* build_index: "(h, r) pair is inconsistent"  */
+  FS_INCONSISTENT = 6,        /* build_index: "(h, r) pair is inconsistent";
+                                 fs_search_host: host/device checks disagree */
   FS_TOO_LARGE = 7            /* table/workspace does not fit the device path */
 } fs_status;
 
@@ -278,10 +279,12 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
 #define FS_HOST_NO_STAGING 2
 /*
  * Default (atomic) mode over two or more chunks of page-locked (or small)
- * buffers: host threads check every query's domain while the uploads run;
- * once no query is bad, each chunk's results are copied back as soon as its
- * kernel finishes, overlapping the remaining uploads (nothing is written if
- * a query is bad -- the contract is unchanged).  flags & FS_HOST_NO_PRECHECK:
+ * buffers: while the uploads run, "no query is bad" is established from both
+ * ends -- the device's per-chunk verdicts cover a growing prefix, host
+ * threads scan chunks from the end; once they meet, each chunk's results are
+ * copied back as soon as its kernel finishes, overlapping the remaining
+ * uploads (nothing is written if a query is bad -- the contract is
+ * unchanged).  flags & FS_HOST_NO_PRECHECK:
  * wait for the device's first-bad word before any write-back instead.
  * FS_INCONSISTENT if the two checks disagree (z_host modified during the call).
  */
