@@ -6,6 +6,8 @@ and hands raw pointers to the C-ABI (``_lib``).
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -72,16 +74,20 @@ def ptr(t: torch.Tensor | None) -> int | None:
 
 
 class Workspace:
-    """Small per-device status block of the build entry points."""
+    """Small status block of the build entry points, one per (thread,
+    device): concurrent builds on a shared stream must not share it."""
 
-    _cache: dict[int, torch.Tensor] = {}
+    _tls = threading.local()
 
     @classmethod
     def get(cls) -> torch.Tensor:
         dev = require_cuda()
-        ws = cls._cache.get(dev.index)
+        cache = getattr(cls._tls, "ws", None)
+        if cache is None:
+            cache = cls._tls.ws = {}
+        ws = cache.get(dev.index)
         if ws is None:
             nbytes = int(_lib.load().fs_workspace_bytes())
             ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-            cls._cache[dev.index] = ws
+            cache[dev.index] = ws
         return ws

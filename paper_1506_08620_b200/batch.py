@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -149,17 +150,22 @@ def new_status(device=None):
     return torch.zeros(int(_lib.load().fs_search_ws_words()), dtype=torch.uint64, device=dev)
 
 
-_status_cache: dict = {}
+_tls = threading.local()
 
 
 def _cached_status(device, stream_ptr: int):
-    """One status workspace per (device, stream): calls on a stream are
-    ordered, so they can share it."""
+    """One status workspace per (thread, device, stream).  One thread's calls
+    on a stream are ordered, so they can share it; two threads on the same
+    stream must not, or one's launch could land between the other's kernel
+    and its read-back of the first-bad word."""
+    cache = getattr(_tls, "status", None)
+    if cache is None:
+        cache = _tls.status = {}
     key = (device.index, stream_ptr)
-    s = _status_cache.get(key)
+    s = cache.get(key)
     if s is None:
         s = new_status(device)
-        _status_cache[key] = s
+        cache[key] = s
     return s
 
 

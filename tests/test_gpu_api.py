@@ -213,6 +213,60 @@ def test_host_precheck_pinned_threads(cuda, prec):
     assert (out == 5).all()
 
 
+def test_concurrent_callers_share_a_stream(cuda):
+    """fsgpu.h "calls are thread-safe" / partition.py:9-10: six threads on the
+    SAME (default) stream each build their own index and run device,
+    pageable-staged and chunked host searches with out-of-domain queries at
+    thread-specific positions; each sees exactly its own answers and
+    positions (no shared status word between callers)."""
+    import threading
+
+    import torch
+
+    fs = _fs()
+    from paper_1506_08620_b200 import batch as fb
+    from paper_1506_08620_b200 import workloads
+
+    errors = []
+
+    def work(k):
+        try:
+            p = workloads.knots("cfg3", seed=k)
+            prep = fs.prepare("direct", p)
+            cfg = fs.LaneConfig(64, "direct", prep)
+            for it in range(4):
+                z = workloads.queries_host("cfg3", p, 1_200_000 + 1000 * k, seed=100 * k + it)
+                want = orc.rank_oracle(p.values, z)
+                out = np.empty(len(z), np.int32)
+                fs.batch_search(cfg, z, out)
+                assert np.array_equal(out, want), "pageable"
+                ot = torch.empty(len(z), dtype=torch.int32, device=cuda)
+                fs.batch_search(cfg, torch.from_numpy(z).to(cuda), ot)
+                assert np.array_equal(ot.cpu().numpy(), want), "device"
+                pos = 1000 * k + 17 * it + 1
+                bad = z.copy()
+                bad[pos] = np.nan
+                with pytest.raises(fs.OutOfDomain) as e:
+                    fs.batch_search(cfg, torch.from_numpy(bad).to(cuda), ot)
+                assert e.value.position == pos, "device position"
+                out2 = np.full(len(z), 9, np.int32)
+                with pytest.raises(fs.OutOfDomain) as e:
+                    fs.batch_search(cfg, bad, out2)
+                assert e.value.position == pos and (out2 == 9).all(), "staged"
+                with pytest.raises(fs.OutOfDomain) as e:
+                    fb._search_host_array(prep.plan, bad, out2, chunk_bytes=1 << 20)
+                assert e.value.position == pos and (out2 == 9).all(), "chunked"
+        except BaseException as ex:  # noqa: BLE001 -- reported by the main thread
+            errors.append((k, repr(ex)))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+
+
 @pytest.mark.parametrize("prec,odt", [("single", np.int32), ("double", np.int64)])
 def test_pageable_staged_host_path(cuda, prec, odt):
     """Pageable numpy buffers >= 4 MB go through the library's pinned staging
