@@ -213,6 +213,40 @@ def test_host_precheck_pinned_threads(cuda, prec):
     assert (out == 5).all()
 
 
+def test_batch_beyond_2_pow_32(cuda):
+    """Positions and offsets are 64-bit: one batch of 2^32 + 9 queries (16 GiB
+    in, 16 GiB out).  Every answer satisfies the bracket property, the tail
+    (positions > 2^32) equals the oracle, and a bad query at 2^32 + 3 is
+    reported there by both the direct and the bitset2 kernels."""
+    import torch
+
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots("cfg3")
+    m = (1 << 32) + 9
+    z = workloads.queries_device("cfg3", p, m, seed=21)
+    out = torch.empty(m, dtype=torch.int32, device=cuda)
+    direct = fs.LaneConfig(64, "direct", fs.prepare("direct", p))
+    fs.batch_search(direct, z, out)
+    x = p.device_values()
+    step = 1 << 28
+    for a in range(0, m, step):
+        zz, o = z[a:a + step], out[a:a + step].long()
+        assert bool(((o >= 0) & (o < p.n_intervals)).all())
+        assert bool(((x[o] <= zz) & (zz < x[o + 1])).all())
+    tail = z[-100_000:].cpu().numpy()
+    assert np.array_equal(out[-100_000:].cpu().numpy(), orc.rank_oracle(p.values, tail))
+    pos = (1 << 32) + 3
+    z[pos] = float("nan")
+    for cfg in (direct, fs.LaneConfig(64, "bitset2", fs.prepare("bitset2", p))):
+        with pytest.raises(fs.OutOfDomain) as e:
+            fs.batch_search(cfg, z, out)
+        assert e.value.position == pos
+    del z, out
+    torch.cuda.empty_cache()
+
+
 def test_concurrent_callers_share_a_stream(cuda):
     """fsgpu.h "calls are thread-safe" / partition.py:9-10: six threads on the
     SAME (default) stream each build their own index and run device,
