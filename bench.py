@@ -168,9 +168,11 @@ def run_reference(args):
     from paper_1506_08620_b200 import workloads
 
     p = workloads.knots("cfg3", seed=0)
-    z = workloads.queries_host("cfg3", p, CPU_SAMPLE, seed=1)
-    rate, threads, reps, _ = cpu_reference_rate(p.values, z, "direct", args.steps, args.warmup, min_time=10.0)
-    sample = (f"cfg3 direct lane path (batch.py:315-317 via oracle/fs_oracle.py), {CPU_SAMPLE} queries "
+    n = args.ref_sample
+    z = workloads.queries_host("cfg3", p, n, seed=1)
+    rate, threads, reps, _ = cpu_reference_rate(p.values, z, "direct", args.steps, args.warmup,
+                                                min_time=args.ref_min_time)
+    sample = (f"cfg3 direct lane path (batch.py:315-317 via oracle/fs_oracle.py), {n} queries "
               f"per step, d=65536, {threads} threads, median of {reps} passes")
     line = {
         "impl": "reference",
@@ -180,13 +182,13 @@ def run_reference(args):
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1e3 * CPU_SAMPLE / rate,
+        "ms_per_step": 1e3 * n / rate,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded cfg3 recipe)",
-        "config": {"workload": "cfg3: f32 N+1=4097 gaps 0.5+U[0,1); uniform queries", "queries_per_step": CPU_SAMPLE,
+        "config": {"workload": "cfg3: f32 N+1=4097 gaps 0.5+U[0,1); uniform queries", "queries_per_step": n,
                    "algorithm": "direct"},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -319,6 +321,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--m", type=int, default=M_PER_GPU, help="queries per GPU")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config sweep (cfg1..cfg5)")
+    ap.add_argument("--ref-sample", type=int, default=CPU_SAMPLE, help="--impl reference: queries per step")
+    ap.add_argument("--ref-min-time", type=float, default=10.0, help="--impl reference: minimum seconds sampled")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
