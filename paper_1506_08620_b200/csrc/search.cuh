@@ -357,12 +357,28 @@ struct Bitset2Probe {
     for (int q = 0; q < N; ++q) s[q] = 0;
     int lvl = 0;
     if constexpr (TOP) {
+      // node s carried as its shared-window address a = base + s * sizeof(T):
+      // the children 2s+1 / 2s+2 are 2a + sizeof(T) - base (+ sizeof(T)), so a
+      // level is LDS, compare, select, one 3-input add
+      constexpr uint32_t sz = sizeof(T);
+      const uint32_t base = (uint32_t)__cvta_generic_to_shared(top);
+      const uint32_t c1 = sz - base, c2 = 2 * sz - base;
+#pragma unroll
+      for (int q = 0; q < N; ++q) s[q] = base;
       for (int l = 0; l < top_bits; ++l) {
 #pragma unroll
-        for (int q = 0; q < N; ++q) s[q] = 2 * s[q] + 1 + (z[q] >= top[s[q]] ? 1u : 0u);
+        for (int q = 0; q < N; ++q) {
+          T v;
+          if constexpr (sizeof(T) == 4) {
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(s[q]));
+          } else {
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(s[q]));
+          }
+          s[q] = s[q] + s[q] + (z[q] >= v ? c2 : c1);
+        }
       }
 #pragma unroll
-      for (int q = 0; q < N; ++q) s[q] = (s[q] - ((1u << top_bits) - 1)) << (pbits - top_bits);
+      for (int q = 0; q < N; ++q) s[q] = ((s[q] - base) / sz - ((1u << top_bits) - 1)) << (pbits - top_bits);
       lvl = top_bits;
     }
     for (; lvl < pbits; ++lvl) {
