@@ -70,10 +70,23 @@ int grid_1d(uint64_t work, int threads) {
 // ---------------------------------------------------------------------------
 // Placement
 // ---------------------------------------------------------------------------
+#ifndef FSG_B2_REPLICATE
+#define FSG_B2_REPLICATE 1
+#endif
+constexpr bool kB2Replicate = FSG_B2_REPLICATE != 0;
+constexpr int kB2ConflictFree = 6;  // levels 0..5: at most 32 consecutive words
+
+// bitset2's staged top levels: levels [0, top) in level order, levels
+// [l1, l2) stored as 32 bank-private copies (Bitset2Probe).
+inline uint64_t b2_smem_bytes(int top, int l1, int l2, size_t es) {
+  return (((1ull << l1) - 1) + ((1ull << l2) - (1ull << l1)) * 32 + ((1ull << top) - (1ull << l2))) * es;
+}
+
 struct Placement {
   uint32_t x_bytes = 0;      // bytes staged at smem offset 0 (X / padded / tree / top)
   uint32_t table_bytes = 0;  // bytes staged after align128(x_bytes) (K / records)
-  int top_bits = 0;          // bitset2
+  int top_bits = 0;          // bitset2: levels staged in smem ...
+  int b2_l1 = 0, b2_l2 = 0;  // ... of which [b2_l1, b2_l2) replicated per bank
   bool xs = false, ks = false, top = false;
   int flags = FS_PLACE_GLOBAL;
   size_t smem = 0;
@@ -246,22 +259,21 @@ Placement place(const fs_plan* p) {
     }
     case FS_ALGO_BITSET2: {
       if (force_global) break;
-      // the probed nodes are staged in level order by the kernel prologue
-      const uint64_t full = (1ull << p->pbits) * es;
+      // the probed nodes are staged by the kernel prologue (Bitset2Probe):
+      // as many levels as fit, then bank-private copies of the levels below
+      // the conflict-free top six, as far as the remaining budget allows
       pl.top = true;
-      if (full <= budget) {
-        pl.top_bits = p->pbits;
-        pl.x_bytes = (uint32_t)full;
-        pl.smem = full;
-        pl.flags |= FS_PLACE_SMEM_X;
-      } else {
-        int tb = bit_length(budget / es) - 1;
-        tb = std::min(tb, p->pbits);
-        pl.top_bits = tb;
-        pl.x_bytes = (uint32_t)((1ull << tb) * es);
-        pl.smem = pl.x_bytes;
-        pl.flags |= FS_PLACE_SMEM_TOP;
-      }
+      int tb = std::min(bit_length(budget / es + 1) - 1, p->pbits);
+      pl.top_bits = tb;
+      pl.flags |= tb == p->pbits ? FS_PLACE_SMEM_X : FS_PLACE_SMEM_TOP;
+      pl.b2_l1 = pl.b2_l2 = std::min(kB2ConflictFree, tb);
+      // (only when every level is in smem: with global levels below, the L1
+      // the larger carve-out takes away costs more than the conflicts)
+      while (kB2Replicate && tb == p->pbits && pl.b2_l2 < tb &&
+             b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2 + 1, es) <= budget)
+        ++pl.b2_l2;
+      pl.x_bytes = (uint32_t)b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2, es);
+      pl.smem = pl.x_bytes;
       break;
     }
     default: {  // classic / bitset1 / bitset3 / offset on X; eytzinger on its tree
@@ -289,6 +301,18 @@ Placement place(const fs_plan* p) {
 // comparison searches keep their smem placement (their L2 path is far slower).
 Placement place_for_batch(const fs_plan* p, uint64_t m) {
   Placement pl = place(p);
+  if (pl.top && pl.b2_l2 > pl.b2_l1) {
+    // the replicated levels cost every CTA an L2 -> smem copy; a batch smaller
+    // than that traffic keeps the plain level-order layout
+    const size_t es = p->dtype == FS_F32 ? 4 : 8;
+    const uint64_t query_bytes = m * (es + 4);
+    if (query_bytes < (uint64_t)pl.smem * sm_count()) {
+      pl.b2_l2 = pl.b2_l1;
+      pl.x_bytes = (uint32_t)b2_smem_bytes(pl.top_bits, pl.b2_l1, pl.b2_l2, es);
+      pl.smem = pl.x_bytes;
+    }
+    return pl;
+  }
   const bool direct_family = p->algorithm == FS_ALGO_DIRECT || p->algorithm == FS_ALGO_DIRECT_CACHE ||
                              p->algorithm == FS_ALGO_DIRECT_GAP2 || p->algorithm == FS_ALGO_DIRECT_GENERIC;
   if (!direct_family || pl.smem == 0 || p->smem_policy != 0 || pl.hot) return pl;
@@ -415,6 +439,8 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   d.q = p->q;
   d.pbits = p->pbits;
   d.top_bits = pl.top_bits;
+  d.b2_l1 = pl.b2_l1;
+  d.b2_l2 = pl.b2_l2;
   const uint64_t n = p->n1 - 1;
   d.off_f = (uint32_t)((n + 1) >> 1);
   d.off_s = (uint32_t)(n + 1 - d.off_f);

@@ -44,6 +44,7 @@ struct DevPlan {
   int32_t q;             // gap
   int32_t pbits;         // bitset / eytzinger depth
   int32_t top_bits;      // bitset2: levels served from smem
+  int32_t b2_l1, b2_l2;  // bitset2: levels [b2_l1, b2_l2) replicated per bank in smem
   uint32_t off_f, off_s, off_j;  // offset search constants
   uint32_t x_smem_bytes;     // bytes of X (or padded / tree / top table) staged; 0 = global
   uint32_t table_smem_bytes; // bytes of K / records staged; 0 = global
@@ -314,40 +315,157 @@ struct CacheProbe<double, J, RS> {
 };
 
 // Branch-free bit-setting search over the right-padded array (Alg 3).
-// The first `top_bits` levels read a shared-memory copy of the padded array
-// subsampled at stride 2^(pbits-top_bits) (exactly the nodes those levels
-// can touch); deeper levels gather from global.  With top_bits == pbits the
-// whole padded array is in shared memory.
+// The first `top_bits` levels read a shared-memory copy of the nodes those
+// levels can touch; deeper levels gather from global.  With top_bits ==
+// pbits the whole padded array is in shared memory.
+//
+// Shared layout of the top levels (filled by the prologue), three regions:
+//   P1  levels [0, l1)       level order: level l's 2^l candidates
+//                            r = (m << (p-l)) | 2^(p-1-l) at [2^l - 1, 2^(l+1) - 1).
+//                            In the sorted padded array every node of a level
+//                            l <= 7 shares one bank; in level order they are
+//                            consecutive words (l1 <= 6: at most 32 of them,
+//                            conflict-free).
+//   R   levels [l1, l2)      level order, each node replicated 32 times and
+//                            interleaved (word = node * 32 + copy): lane c reads
+//                            copy c, always bank c, so these levels are
+//                            conflict-free for random queries.
+//   P2  levels [l2, top)     level order again (too large to replicate).
+// In every region a node is carried as its shared-window address, and the
+// child step is a' = 2a + (z >= node ? c2 : c1) with region constants (the
+// regions are stacked in level order, which makes c1 / c2 level-independent):
+// one LDS, one compare, one select, one 3-input add per level.  Same
+// comparisons, same values as binsearch.py:72-86.
 template <typename T, bool TOP>
 struct Bitset2Probe {
   const T* top;
   const T* xpad;
-  int pbits, top_bits, shift;
+  int pbits, top_bits, l1, l2;
   __device__ __forceinline__ Bitset2Probe(const DevPlan<T>& p, unsigned char* smem) {
     top = reinterpret_cast<const T*>(smem);
     xpad = static_cast<const T*>(p.table);
     pbits = p.pbits;
     top_bits = TOP ? p.top_bits : 0;
-    shift = p.pbits - top_bits;
+    l1 = TOP ? p.b2_l1 : 0;
+    l2 = TOP ? p.b2_l2 : 0;
   }
-  // The nodes the first `top_bits` levels can probe are staged in LEVEL
-  // ORDER: level l's 2^l candidates r = (m << (p-l)) | 2^(p-1-l) sit at
-  // [2^l - 1, 2^(l+1) - 1).  In the sorted padded array every node of a level
-  // l <= 7 shares one bank (stride >= 32 words), up to 32-way conflicts; in
-  // level order they are consecutive words.  Same comparisons, same values.
   static __device__ __forceinline__ void prologue(const DevPlan<T>& p, unsigned char* smem) {
     if constexpr (TOP) {
       T* dst = reinterpret_cast<T*>(smem);
       const T* src = static_cast<const T*>(p.table);
-      const uint32_t nodes = (1u << p.top_bits) - 1;
-      for (uint32_t s = threadIdx.x; s < nodes; s += blockDim.x) {
-        const int l = 31 - __clz(s + 1);
-        const uint32_t m = s + 1 - (1u << l);
+      const uint32_t n1w = (1u << p.b2_l1) - 1;                                   // P1 words
+      const uint32_t nrw = ((1u << p.b2_l2) - (1u << p.b2_l1)) * 32u;            // R words
+      const uint32_t total = n1w + nrw + ((1u << p.top_bits) - (1u << p.b2_l2));  // + P2 words
+      for (uint32_t w = threadIdx.x; w < total; w += blockDim.x) {
+        // level-order node index of word w (P1 | R: 32 copies per node | P2)
+        const uint32_t node = w < n1w         ? w
+                              : w < n1w + nrw ? n1w + ((w - n1w) >> 5)
+                                              : (1u << p.b2_l2) - 1 + (w - n1w - nrw);
+        const int l = 31 - __clz(node + 1);
+        const uint32_t m = node + 1 - (1u << l);
         const uint64_t r = ((uint64_t)m << (p.pbits - l)) | (1ull << (p.pbits - 1 - l));
-        dst[s] = __ldg(src + r);
+        dst[w] = __ldg(src + r);
       }
       __syncthreads();
     }
+  }
+  static __device__ __forceinline__ T lds(uint32_t a) {
+    T v;
+    if constexpr (sizeof(T) == 4) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    else asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+  }
+#ifndef FSG_B2_PIPE_MIX
+#define FSG_B2_PIPE_MIX 1
+#endif
+  // One level: a' = 2a + (z >= node(a) ? c2 : c1).  The compare is an ALU
+  // op; the rest is either ALU (select + 3-input add) or, through an opaque
+  // multiplier ptxas cannot strength-reduce, the FMA pipe's IMAD.  ncu shows
+  // the all-ALU form saturating the ALU pipe (91%) with FMA idle (6%);
+  // alternating two forms across the lockstep queries balances the pipes
+  // (f32; profiles/r01/tune_bitset2_pipes.txt):
+  //   FORM 0: FSETP, SEL, IMAD            (ALU 2, FMA 1)
+  //   FORM 1: FSETP, IMAD, predicated IMAD (ALU 1, FMA 2)
+  template <int FORM>
+  static __device__ __forceinline__ uint32_t step(uint32_t a, T z, uint32_t c1, uint32_t c2, uint32_t two,
+                                                  uint32_t one) {
+    const T v = lds(a);
+#if FSG_B2_PIPE_MIX
+    // f64 compares issue on the FP64 pipe, which leaves the ALU room: the
+    // all-ALU form measures best there
+    if constexpr (sizeof(T) == 8) {
+      return a + a + (z >= v ? c2 : c1);
+    } else {
+      uint32_t r;
+      if constexpr (FORM == 0) {
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(two), "r"(z >= v ? c2 : c1));
+      } else {
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(two), "r"(c1));
+        asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, %2;\n\t@p mad.lo.u32 %0, %3, %4, %0;\n\t}"
+            : "+r"(r) : "f"(z), "f"(v), "r"(c2 - c1), "r"(one));
+      }
+      return r;
+    }
+#else
+    return a + a + (z >= v ? c2 : c1);
+#endif
+  }
+  // Levels [0, top_bits) for N queries in lockstep; returns, per query, the
+  // bit prefix i (the index reached after top_bits levels, low bits clear).
+  template <int N>
+  __device__ __forceinline__ void descend_top(const T (&z)[N], uint32_t (&i)[N]) const {
+    constexpr uint32_t sz = sizeof(T);
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(top);
+    uint32_t two, one;  // opaque to ptxas: keeps the IMADs on the FMA pipe
+    asm volatile("mov.u32 %0, 2;" : "=r"(two));
+    asm volatile("mov.u32 %0, 1;" : "=r"(one));
+    uint32_t a[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) a[q] = base;
+    {  // P1: a = base + s * sz
+      const uint32_t c1 = sz - base, c2 = 2 * sz - base;
+      for (int l = 0; l < l1; ++l) {
+#pragma unroll
+        for (int q = 0; q + 1 < N; q += 2) {
+          a[q] = step<0>(a[q], z[q], c1, c2, two, one);
+          a[q + 1] = step<1>(a[q + 1], z[q + 1], c1, c2, two, one);
+        }
+        if constexpr (N & 1) a[N - 1] = step<0>(a[N - 1], z[N - 1], c1, c2, two, one);
+      }
+    }
+    uint32_t b2 = base, s0 = 0;  // the P2 region: a = b2 + (s - s0) * sz
+    if (l2 > l1) {  // R: a = B_l + m * 32sz + lane * sz, B_l = rb + (2^l - 2^l1) * 32sz
+      const uint32_t lane = threadIdx.x & 31u;
+      const uint32_t rb = base + ((1u << l1) - 1) * sz;
+      const uint32_t c1 = (1u << l1) * 32u * sz - rb - lane * sz, c2 = c1 + 32u * sz;
+#pragma unroll
+      for (int q = 0; q < N; ++q) a[q] = rb + ((a[q] - base) / sz - ((1u << l1) - 1)) * 32u * sz + lane * sz;
+      for (int l = l1; l < l2; ++l) {
+#pragma unroll
+        for (int q = 0; q + 1 < N; q += 2) {
+          a[q] = step<0>(a[q], z[q], c1, c2, two, one);
+          a[q + 1] = step<1>(a[q + 1], z[q + 1], c1, c2, two, one);
+        }
+        if constexpr (N & 1) a[N - 1] = step<0>(a[N - 1], z[N - 1], c1, c2, two, one);
+      }
+      b2 = rb + ((1u << l2) - (1u << l1)) * 32u * sz;  // B_l2: P2 starts here
+      s0 = (1u << l2) - 1;
+#pragma unroll
+      for (int q = 0; q < N; ++q) a[q] = b2 + (a[q] - b2 - lane * sz) / (32u * sz) * sz;
+    }
+    {  // P2 (or the rest of P1 when nothing is replicated)
+      const uint32_t c1 = (s0 + 1) * sz - b2, c2 = c1 + sz;
+      for (int l = l2 > l1 ? l2 : l1; l < top_bits; ++l) {
+#pragma unroll
+        for (int q = 0; q + 1 < N; q += 2) {
+          a[q] = step<0>(a[q], z[q], c1, c2, two, one);
+          a[q + 1] = step<1>(a[q + 1], z[q + 1], c1, c2, two, one);
+        }
+        if constexpr (N & 1) a[N - 1] = step<0>(a[N - 1], z[N - 1], c1, c2, two, one);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) i[q] = ((a[q] - b2) / sz + s0 - ((1u << top_bits) - 1)) << (pbits - top_bits);
   }
   // N queries descend in lockstep: N independent smem/L2 loads per level.
   template <int N, typename R>
@@ -355,33 +473,8 @@ struct Bitset2Probe {
     uint32_t s[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) s[q] = 0;
-    int lvl = 0;
-    if constexpr (TOP) {
-      // node s carried as its shared-window address a = base + s * sizeof(T):
-      // the children 2s+1 / 2s+2 are 2a + sizeof(T) - base (+ sizeof(T)), so a
-      // level is LDS, compare, select, one 3-input add
-      constexpr uint32_t sz = sizeof(T);
-      const uint32_t base = (uint32_t)__cvta_generic_to_shared(top);
-      const uint32_t c1 = sz - base, c2 = 2 * sz - base;
-#pragma unroll
-      for (int q = 0; q < N; ++q) s[q] = base;
-      for (int l = 0; l < top_bits; ++l) {
-#pragma unroll
-        for (int q = 0; q < N; ++q) {
-          T v;
-          if constexpr (sizeof(T) == 4) {
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(s[q]));
-          } else {
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(s[q]));
-          }
-          s[q] = s[q] + s[q] + (z[q] >= v ? c2 : c1);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < N; ++q) s[q] = ((s[q] - base) / sz - ((1u << top_bits) - 1)) << (pbits - top_bits);
-      lvl = top_bits;
-    }
-    for (; lvl < pbits; ++lvl) {
+    if constexpr (TOP) descend_top<N>(z, s);
+    for (int lvl = top_bits; lvl < pbits; ++lvl) {
       const uint32_t bit = 1u << (pbits - 1 - lvl);
 #pragma unroll
       for (int q = 0; q < N; ++q) {
@@ -393,23 +486,10 @@ struct Bitset2Probe {
     for (int q = 0; q < N; ++q) o[q] = (R)s[q];
   }
   __device__ __forceinline__ int64_t operator()(T z) const {
-    uint32_t i = 0;
-    int lvl = 0;
-    if constexpr (TOP) {
-      // Level-order descent: the node of (level l, path m) is s = 2^l - 1 + m
-      // and its children are 2s + 1 (bit clear) / 2s + 2 (bit set), so each
-      // level is one LDS, one compare and one LEA.
-      uint32_t s = 0;
-#pragma unroll 4
-      for (int l = 0; l < top_bits; ++l) s = 2 * s + 1 + (z >= top[s] ? 1u : 0u);
-      i = (s - ((1u << top_bits) - 1)) << (pbits - top_bits);
-      lvl = top_bits;
-    }
-    for (; lvl < pbits; ++lvl) {
-      const uint32_t r = i | (1u << (pbits - 1 - lvl));
-      if (z >= __ldg(xpad + r)) i = r;
-    }
-    return (int64_t)i;
+    const T zz[1] = {z};
+    int64_t o[1];
+    batch<1, int64_t>(zz, o);
+    return o[0];
   }
 };
 

@@ -213,6 +213,24 @@ def test_host_precheck_pinned_threads(cuda, prec):
     assert (out == 5).all()
 
 
+@pytest.mark.parametrize("name,kw", [("cfg3", {}), ("cfg5", {"n1": 1025}), ("cfg2", {})])
+def test_bitset2_bank_replicated_layout(cuda, name, kw):
+    """Large batches of fully smem-resident bitset2 tables use the bank-
+    private replicated middle levels (Bitset2Probe); answers equal the
+    oracle exactly, and a small batch (plain layout) agrees."""
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots(name, **kw)
+    prep = fs.prepare("bitset2", p)
+    plain = ((1 << p.n_intervals.bit_length()) - 1) * p.values.dtype.itemsize
+    assert prep.placement()["smem_bytes"] > plain  # replication planned
+    z = workloads.queries_host(name, p, 6_000_001, seed=31)
+    want = orc.rank_oracle(p.values, z)
+    assert np.array_equal(fs.run_batch(prep, z), want)
+    assert np.array_equal(fs.run_batch(prep, z[:5000]), want[:5000])
+
+
 def test_batch_beyond_2_pow_32(cuda):
     """Positions and offsets are 64-bit: one batch of 2^32 + 9 queries (16 GiB
     in, 16 GiB out).  Every answer satisfies the bracket property, the tail
