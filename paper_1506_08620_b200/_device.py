@@ -69,10 +69,6 @@ def download(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
 
 
-def ptr(t: torch.Tensor | None) -> int | None:
-    return None if t is None else int(t.data_ptr())
-
-
 class Workspace:
     """Small status block of the build entry points, one per (thread,
     device): concurrent builds on a shared stream must not share it."""

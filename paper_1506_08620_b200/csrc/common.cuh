@@ -108,9 +108,6 @@ __device__ __forceinline__ void st_stream(int64_t* p, int64_t v) {
   __stcs(reinterpret_cast<long long*>(p), (long long)v);
 }
 
-// Read-only table gathers through L2 (tables are re-read by every query).
-template <typename T> __device__ __forceinline__ T ld_table(const T* p) { return __ldg(p); }
-
 // ---------------------------------------------------------------------------
 // Shared-memory staging with the bulk-copy engine (cp.async.bulk + mbarrier)
 // ---------------------------------------------------------------------------

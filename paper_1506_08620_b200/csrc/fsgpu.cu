@@ -949,16 +949,37 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   // chunks upload, so write-back can start before the last upload
   const uint64_t nch = (m + chunk_elems - 1) / chunk_elems;
   const bool precheck = !overlap && !(flags & FS_HOST_NO_PRECHECK) && nch >= 2;
+  // Per-call resources.  On every exit the streams are drained before
+  // anything is released: no copy may still read the caller's buffers or
+  // write a pinned slot that is back in the process-wide cache.
+  struct CallState {
+    cudaStream_t s, cs, ds = nullptr;
+    cudaEvent_t ev = nullptr, evk = nullptr;
+    std::vector<cudaEvent_t> done;  // precheck: kernel of chunk c finished ...
+    unsigned long long* prefix_bad = nullptr;  // ... with this first-bad word (pinned)
+    ~CallState() {
+      cudaStreamSynchronize(s);
+      cudaStreamSynchronize(cs);
+      if (ds) {
+        cudaStreamSynchronize(ds);
+        cudaStreamDestroy(ds);
+      }
+      for (cudaEvent_t d : done) cudaEventDestroy(d);
+      if (ev) cudaEventDestroy(ev);
+      if (evk) cudaEventDestroy(evk);
+      if (prefix_bad) PinnedSlots::release(prefix_bad);
+    }
+  } st{s, cs};
   FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
-  cudaEvent_t ev, evk;
-  cudaStream_t ds = nullptr;
-  std::vector<cudaEvent_t> done;  // precheck: kernel of chunk c finished ...
-  unsigned long long* prefix_bad = nullptr;  // ... with this first-bad word (pinned)
-  if (precheck && !(prefix_bad = static_cast<unsigned long long*>(PinnedSlots::acquire(nch * 8))))
+  if (precheck && !(st.prefix_bad = static_cast<unsigned long long*>(PinnedSlots::acquire(nch * 8))))
     return fail(FS_CUDA_ERROR, "pinned status allocation failed");
-  FS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  FS_CUDA(cudaEventCreateWithFlags(&evk, cudaEventDisableTiming));
-  if (overlap || precheck) FS_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+  FS_CUDA(cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming));
+  FS_CUDA(cudaEventCreateWithFlags(&st.evk, cudaEventDisableTiming));
+  if (overlap || precheck) FS_CUDA(cudaStreamCreateWithFlags(&st.ds, cudaStreamNonBlocking));
+  cudaEvent_t ev = st.ev, evk = st.evk;
+  cudaStream_t ds = st.ds;
+  std::vector<cudaEvent_t>& done = st.done;
+  unsigned long long* prefix_bad = st.prefix_bad;
   int status = FS_OK;
   bool wrote = false;
   for (uint64_t off = 0; off < m && status == FS_OK; off += chunk_elems) {
@@ -1024,14 +1045,6 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
     if (e == cudaSuccess && ds) e = cudaStreamSynchronize(ds);
     if (e != cudaSuccess) status = fail(FS_CUDA_ERROR, std::string("first-bad readback: ") + cudaGetErrorString(e));
   }
-  if (ds) {
-    cudaStreamSynchronize(ds);
-    cudaStreamDestroy(ds);
-  }
-  for (cudaEvent_t d : done) cudaEventDestroy(d);
-  if (prefix_bad) PinnedSlots::release(prefix_bad);
-  cudaEventDestroy(ev);
-  cudaEventDestroy(evk);
   if (status != FS_OK) return status;
   if (bad != ~0ull) {
     if (pos_out) *pos_out = (int64_t)bad;

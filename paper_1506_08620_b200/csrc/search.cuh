@@ -6,7 +6,9 @@
 // bulk-copy engine when they fit, otherwise gathered
 // through L2 with ld.global.nc.  The out-of-domain check of batch_search
 // (batch.py:411-413) is fused: each lane keeps the smallest bad position it
-// saw and one atomicMin per warp folds it into a global word.
+// saw, one atomic per warp folds it into the status workspace, and the CTA
+// that finishes last publishes the batch's first bad position
+// (finalize_first_bad, common.cuh).
 //
 // Probes (each cites the reference kernel it restates):
 //   Direct<gap 1>     batch.py:315-317 / direct.py:570-574
