@@ -116,6 +116,13 @@ int validate_plan(const fs_plan* p) {
       if (p->q < 1) return fail(FS_INVALID_ARG, "gap must be >= 1");
       if (p->algorithm == FS_ALGO_DIRECT_CACHE && p->q != 1)
         return fail(FS_INVALID_ARG, "fused records pair with the gap-1 kernel");
+      // optional accelerators: their extents must lie inside the tables they index
+      if (p->hot_words && (p->hot_word0 > (p->r >> 5) + 1 || p->hot_words > (p->r >> 5) + 1 - p->hot_word0 ||
+                           p->hot_knot0 > p->n1 || p->hot_knots > p->n1 - p->hot_knot0))
+        return fail(FS_INVALID_ARG, "hot window outside the rank directory / knots");
+      if (p->sparse && (p->sparse_shift < 5 || p->sparse_shift > 16 ||
+                        p->sparse_ndense > (p->r >> p->sparse_shift) + 2))
+        return fail(FS_INVALID_ARG, "sparse table parameters out of range");
       break;
     case FS_ALGO_BITSET2:
     case FS_ALGO_EYTZINGER:

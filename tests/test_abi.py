@@ -66,6 +66,22 @@ def test_argument_validation_without_gpu():
     plan.algorithm = _lib.ALGO_CODES["direct-cache"]
     plan.q = 2
     assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
+    # optional accelerators whose extents would index outside their tables
+    plan.algorithm = _lib.ALGO_CODES["direct"]
+    plan.q = 1
+    plan.r = 1000  # directory of (1000 >> 5) + 1 = 32 words
+    plan.rank = 1
+    plan.hot_word0, plan.hot_words, plan.hot_knot0, plan.hot_knots = 30, 5, 0, 2
+    assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
+    assert b"hot window" in lib.fs_last_error()
+    plan.hot_word0, plan.hot_words, plan.hot_knot0, plan.hot_knots = 0, 32, 3, 2  # knots past n1 = 4
+    assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
+    plan.hot_words = 0
+    plan.sparse = 1
+    for shift, ndense in ((4, 0), (17, 0), (5, 40)):
+        plan.sparse_shift, plan.sparse_ndense = shift, ndense
+        assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
+        assert b"sparse" in lib.fs_last_error()
 
 
 def test_status_codes_map_to_reference_exceptions():
