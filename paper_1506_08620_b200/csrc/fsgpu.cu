@@ -344,6 +344,22 @@ Placement place_for_batch(const fs_plan* p, uint64_t m) {
 #endif
 template <typename T>
 constexpr int kUnroll = sizeof(T) == 8 ? FSG_UNROLL_F64 : FSG_UNROLL;
+// Per-probe override: f64 probes whose whole table sits in smem have short,
+// latency-light chains and take one more 4-query group in flight
+// (profiles/r01/tune_unroll_f64.txt: records +2.6%, sparse with X in smem
+// +3.6%; the L2-gathering and bitset2 probes lose with it).
+template <typename T, typename Probe>
+struct UnrollFor {
+  static constexpr int value = kUnroll<T>;
+};
+template <typename J>
+struct UnrollFor<double, CacheProbe<double, J, true>> {
+  static constexpr int value = 3;
+};
+template <bool DENSE>
+struct UnrollFor<double, SparseProbe<double, true, DENSE>> {
+  static constexpr int value = 3;
+};
 
 
 // Launch geometry per (device, kernel, dynamic smem, candidate set), and the
@@ -394,7 +410,8 @@ int launch_geometry(const void* fn, size_t smem, int mode, int* threads_out, int
 template <typename T, typename OutT, typename Probe>
 int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t m, OutT* out,
                  unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
-  auto kern = search_kernel<T, OutT, Probe, kUnroll<T>>;
+  constexpr int kU = UnrollFor<T, Probe>::value;
+  auto kern = search_kernel<T, OutT, Probe, kU>;
   const size_t smem = pl.smem;
   // Kernels that stage tables in shared memory run best with ~1024 threads
   // per SM in one wide CTA (measured on cfg3: 1x1024 95% of HBM peak vs
@@ -422,7 +439,7 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
   d.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) + head * sizeof(OutT)) & 15) == 0;
 
   const uint64_t full = (uint64_t)per_sm * sm_count();
-  uint64_t want = (sh.nvec + (uint64_t)threads * kUnroll<T> - 1) / ((uint64_t)threads * kUnroll<T>);
+  uint64_t want = (sh.nvec + (uint64_t)threads * kU - 1) / ((uint64_t)threads * kU);
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(full, want));
 
   StageSeg s0{nullptr, pl.seg0_src, pl.seg0_bytes};
