@@ -360,6 +360,19 @@ template <bool DENSE>
 struct UnrollFor<double, SparseProbe<double, true, DENSE>> {
   static constexpr int value = 3;
 };
+// Probes launched through the 1024-thread-bounded entry point: the sparse
+// probe with X in smem exceeds 64 registers with int64 outputs and gains
+// from 1024-thread CTAs despite small spills (cfg2 int64 222 -> 264 Gq/s);
+// the f64 records probe loses (399 -> 335), so the default stays unbounded
+// (profiles/r01/tune_launch_bounds.txt).
+template <typename T, typename Probe>
+struct BoundedFor {
+  static constexpr bool value = false;
+};
+template <typename T, bool DENSE>
+struct BoundedFor<T, SparseProbe<T, true, DENSE>> {
+  static constexpr bool value = true;
+};
 
 
 // Launch geometry per (device, kernel, dynamic smem, candidate set), and the
@@ -411,7 +424,10 @@ template <typename T, typename OutT, typename Probe>
 int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t m, OutT* out,
                  unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
   constexpr int kU = UnrollFor<T, Probe>::value;
-  auto kern = search_kernel<T, OutT, Probe, kU>;
+  auto kern = [] {
+    if constexpr (BoundedFor<T, Probe>::value) return search_kernel_1k<T, OutT, Probe, kU>;
+    else return search_kernel<T, OutT, Probe, kU>;
+  }();
   const size_t smem = pl.smem;
   // Kernels that stage tables in shared memory run best with ~1024 threads
   // per SM in one wide CTA (measured on cfg3: 1x1024 95% of HBM peak vs

@@ -627,9 +627,9 @@ struct StreamShape {
 };
 
 template <typename T, typename OutT, typename Probe, int UNROLL>
-__global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh,
-                              DevPlan<T> plan, unsigned long long* __restrict__ status, int merge,
-                              StageSeg seg0, StageSeg seg1, int nseg) {
+__device__ __forceinline__ void search_body(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh,
+                                            DevPlan<T> plan, unsigned long long* __restrict__ status, int merge,
+                                            StageSeg seg0, StageSeg seg1, int nseg) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bar;
   if (nseg > 0) {
@@ -693,6 +693,23 @@ __global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, S
     }
   }
   finalize_first_bad(mybad == ~0ull ? ~0ull : mybad + sh.base, status, merge);
+}
+
+// The kernel entry points: the register budget is left to ptxas (a kernel
+// above 64 registers then runs 512-thread CTAs), or bounded so that one
+// 1024-thread CTA fits per SM (at most 64 registers, small spills allowed);
+// which one a probe uses is measured (BoundedFor, fsgpu.cu).
+template <typename T, typename OutT, typename Probe, int UNROLL>
+__global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh, DevPlan<T> plan,
+                              unsigned long long* __restrict__ status, int merge, StageSeg seg0, StageSeg seg1,
+                              int nseg) {
+  search_body<T, OutT, Probe, UNROLL>(z, out, sh, plan, status, merge, seg0, seg1, nseg);
+}
+template <typename T, typename OutT, typename Probe, int UNROLL>
+__global__ void __launch_bounds__(1024, 1)
+    search_kernel_1k(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh, DevPlan<T> plan,
+                     unsigned long long* __restrict__ status, int merge, StageSeg seg0, StageSeg seg1, int nseg) {
+  search_body<T, OutT, Probe, UNROLL>(z, out, sh, plan, status, merge, seg0, seg1, nseg);
 }
 
 }  // namespace fsg
