@@ -117,3 +117,17 @@ def test_fs_plan_layout_matches_c(tmp_path):
     assert int(out["sizeof"]) == ctypes.sizeof(_lib.FsPlan)
     for f in fields:
         assert int(out[f]) == getattr(_lib.FsPlan, f).offset, f
+
+
+def test_integration_stub_matches_c_layout():
+    """The maintainer-side ctypes stub printed in INTEGRATION.md declares the
+    same fs_plan as the library (field names, types and offsets)."""
+    text = (ROOT / "INTEGRATION.md").read_text()
+    block = text.split("class fs_plan(ctypes.Structure):")[1].split("]\n", 1)[0] + "]"
+    ns = {"ctypes": ctypes}
+    exec("class fs_plan(ctypes.Structure):" + block, ns)
+    stub = ns["fs_plan"]
+    assert [f for f, _ in stub._fields_] == [f for f, _ in _lib.FsPlan._fields_]
+    assert ctypes.sizeof(stub) == ctypes.sizeof(_lib.FsPlan)
+    for f, _ in stub._fields_:
+        assert getattr(stub, f).offset == getattr(_lib.FsPlan, f).offset, f
