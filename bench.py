@@ -375,48 +375,40 @@ def main():
     cfg = fs.LaneConfig(d=65536, kernel="direct", structure=prep)
     del z, out
     torch.cuda.empty_cache()
-    fs.batch_search(cfg, zh, oh)  # warm-up (allocator, copy stream)
-    barrier()
-    te = []
-    for _ in range(e2e_steps):
-        torch.cuda.synchronize()
-        a = time.perf_counter()
-        fs.batch_search(cfg, zh, oh)
-        te.append(time.perf_counter() - a)
-    barrier()
-    t_e2e = float(np.median(te))
+    def timed_calls(call, n):
+        """Median seconds of n synchronous public-API calls, each bracketed by
+        CUDA events on the current stream (device clock; the call returns only
+        after its results are in host memory)."""
+        call()  # warm-up (allocator, copy stream, pinned staging slots)
+        barrier()
+        ts = []
+        for _ in range(n):
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            call()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        barrier()
+        return float(np.median(ts))
+
+    t_e2e = timed_calls(lambda: fs.batch_search(cfg, zh, oh), e2e_steps)
     # opt-in speculative write-back (atomic=False): both PCIe directions overlap
-    fs.batch_search(cfg, zh, oh, atomic=False)
-    barrier()
-    to = []
-    for _ in range(e2e_steps):
-        torch.cuda.synchronize()
-        a = time.perf_counter()
-        fs.batch_search(cfg, zh, oh, atomic=False)
-        to.append(time.perf_counter() - a)
-    barrier()
-    t_e2e_ov = float(np.median(to))
+    t_e2e_ov = timed_calls(lambda: fs.batch_search(cfg, zh, oh, atomic=False), e2e_steps)
     # what a drop-in numpy user passes: ordinary pageable arrays (staged by the library)
     zpg = zh.copy()
     opg = np.empty_like(oh)
-    fs.batch_search(cfg, zpg, opg)
-    barrier()
-    tp = []
-    for _ in range(3):
-        a = time.perf_counter()
-        fs.batch_search(cfg, zpg, opg)
-        tp.append(time.perf_counter() - a)
-    barrier()
-    t_e2e_pg = float(np.median(tp))
+    t_e2e_pg = timed_calls(lambda: fs.batch_search(cfg, zpg, opg), 3)
     del zpg, opg
 
-    times = torch.tensor([t_dir, t_bs, t_e2e, t_e2e_ov], dtype=torch.float64, device="cuda")
+    times = torch.tensor([t_dir, t_bs, t_e2e, t_e2e_ov, t_e2e_pg], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
         v = torch.tensor([1 if verified else 0], device="cuda")
         dist.all_reduce(v, op=dist.ReduceOp.MIN)
         verified = bool(v.item())
-    t_dir, t_bs, t_e2e, t_e2e_ov = times.tolist()
+    t_dir, t_bs, t_e2e, t_e2e_ov, t_e2e_pg = times.tolist()
     z_cpu, o_cpu = zh[:CPU_SAMPLE].copy(), oh[:CPU_SAMPLE].copy()
     del zh_t, oh_t, zh, oh
     torch.cuda.empty_cache()
