@@ -114,6 +114,11 @@ typedef struct fs_plan {
                          rank directory does not fit there.  NULL = unused.      */
   int32_t sparse_shift;/* super-bucket = 2^sparse_shift buckets (5..16)           */
   uint32_t sparse_ndense; /* dense (bitmask) super-buckets in `sparse`            */
+  const void* b2_deep;  /* bitset2 only, optional: subtree records of the levels
+                           below the shared-memory top (fs_build_b2_deep); one
+                           32-B gather resolves b2_deep_k levels.  NULL = unused. */
+  int32_t b2_deep_top;  /* ... built for this many staged top levels             */
+  int32_t b2_deep_k;    /* ... levels per record (3 for f32, 2 for f64)           */
 } fs_plan;
 
 /* Library identification. */
@@ -221,6 +226,21 @@ int fs_build_fused(int32_t dtype, const void* x_dev, uint64_t n1, const uint32_t
  * (partition.py:163-171). */
 int fs_build_padded(int32_t dtype, const void* x_dev, uint64_t n1, int32_t pbits,
                     void* xpad_dev, void* stream);
+
+/*
+ * Subtree records for bitset2's global levels (a device layout of the same
+ * padded array; no reference counterpart).  Below the `top_bits` levels the
+ * kernel stages in shared memory, each remaining level pair (f64) / triple
+ * (f32) becomes one 32-B record per node: the node's padded value and its
+ * descendants' down to k levels, in BFS order.  One 256-bit gather then
+ * resolves k levels with exactly the comparisons of binsearch.py:72-86; a
+ * leftover single level reads xpad itself.  fs_b2_deep_bytes returns the
+ * buffer size (0 = nothing to build) and the top_bits / k the search kernel
+ * will use for this plan; fs_build_b2_deep fills it.
+ */
+uint64_t fs_b2_deep_bytes(int32_t dtype, int32_t pbits, int32_t* top_bits_out, int32_t* k_out);
+int fs_build_b2_deep(int32_t dtype, const void* xpad_dev, int32_t pbits, int32_t top_bits, int32_t k,
+                     void* deep_dev, void* stream);
 
 /* Heap-order (Eytzinger) tree of depth L.  Replaces eytzinger.build_layout
  * (eytzinger.py:45-63). tree_dev holds 2^L - 1 elements. */

@@ -70,6 +70,8 @@ EXPORTED = (
     "fs_build_hot_window",
     "fs_build_fused",
     "fs_build_padded",
+    "fs_b2_deep_bytes",
+    "fs_build_b2_deep",
     "fs_build_eytzinger",
     "fs_search_ws_words",
     "fs_search_device",
@@ -107,6 +109,9 @@ class FsPlan(ctypes.Structure):
         ("sparse", ctypes.c_void_p),
         ("sparse_shift", ctypes.c_int32),
         ("sparse_ndense", ctypes.c_uint32),
+        ("b2_deep", ctypes.c_void_p),
+        ("b2_deep_top", ctypes.c_int32),
+        ("b2_deep_k", ctypes.c_int32),
     ]
 
 
@@ -150,6 +155,10 @@ def _declare(lib):
     lib.fs_build_fused.argtypes = [_i32, _vp, _u64, _vp, _u64, _vp, _vp]
     lib.fs_build_padded.restype = ctypes.c_int
     lib.fs_build_padded.argtypes = [_i32, _vp, _u64, _i32, _vp, _vp]
+    lib.fs_b2_deep_bytes.restype = ctypes.c_uint64
+    lib.fs_b2_deep_bytes.argtypes = [_i32, _i32, _p_i32, _p_i32]
+    lib.fs_build_b2_deep.restype = ctypes.c_int
+    lib.fs_build_b2_deep.argtypes = [_i32, _vp, _i32, _i32, _i32, _vp, _vp]
     lib.fs_build_eytzinger.restype = ctypes.c_int
     lib.fs_build_eytzinger.argtypes = [_i32, _vp, _u64, _i32, _vp, _vp]
     lib.fs_search_ws_words.restype = ctypes.c_size_t

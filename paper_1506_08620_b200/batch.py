@@ -102,6 +102,7 @@ def _plan_for(algorithm: str, structure, p: SortedPartition):
         plan.table = pp.padded_dev.data_ptr()
         plan.pbits = pp.p
         keep.append(pp.padded_dev)
+        _set_b2_deep(plan, pp, keep)
     elif algorithm == "eytzinger":
         lay: EytzingerLayout = structure
         plan.table = lay.tree_dev.data_ptr()
@@ -367,6 +368,26 @@ def _set_hot_window(plan, p: SortedPartition, idx: DirectIndex, rank) -> None:
     density_ratio = (inside / HOT_WINDOW_BYTES) / (p.n_intervals / table_bytes)
     if nw and density_ratio >= HOT_WINDOW_MIN_DENSITY_RATIO:
         plan.hot_word0, plan.hot_words, plan.hot_knot0, plan.hot_knots = w0, nw, t0, nt
+
+
+def _set_b2_deep(plan, pp: PaddedPartition, keep: list) -> None:
+    """bitset2 levels below the shared-memory top as 32-B subtree records
+    (fs_build_b2_deep): one gather per 2 (f64) / 3 (f32) levels instead of
+    one per level.  Same comparisons as binsearch.py:72-86."""
+    lib = _lib.load()
+    dt = fs_dtype(pp.base.precision)
+    top, k = ctypes.c_int32(0), ctypes.c_int32(0)
+    nbytes = int(lib.fs_b2_deep_bytes(dt, pp.p, ctypes.byref(top), ctypes.byref(k)))
+    if nbytes == 0:
+        return
+    buf = _device.empty(nbytes, np.uint8)
+    rc = lib.fs_build_b2_deep(dt, pp.padded_dev.data_ptr(), pp.p, top.value, k.value, buf.data_ptr(),
+                              _device.stream_ptr())
+    _lib.check(rc, what="fs_build_b2_deep")
+    plan.b2_deep = buf.data_ptr()
+    plan.b2_deep_top = top.value
+    plan.b2_deep_k = k.value
+    keep.append(buf)
 
 
 def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:

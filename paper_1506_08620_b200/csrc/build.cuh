@@ -343,4 +343,32 @@ __global__ void eytzinger_kernel(const T* __restrict__ x, uint64_t n1, int depth
   }
 }
 
+// ---------------------------------------------------------------------------
+// bitset2 subtree records for the global levels (fs_build_b2_deep).  Chunk c
+// starts at level l_c and spans k_c levels; record m of the chunk holds, in
+// BFS order, the padded values the bit-setting walk (binsearch.py:72-86)
+// can probe in levels l_c .. l_c + k_c - 1 when its first l_c decisions are
+// the bits of m: slot s at relative depth d = floor(log2(s + 1)), path q =
+// s + 1 - 2^d reads xpad[(m << (p - l)) | (q << (p - l - d)) | 2^(p - l - d - 1)].
+// One thread per record slot; unused slots are zero.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void b2_deep_kernel(const T* __restrict__ xpad, int pbits, int level, int kc, uint64_t nrec,
+                               T* __restrict__ rec) {
+  constexpr int kSlots = 32 / sizeof(T);
+  const uint64_t total = nrec * kSlots;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t m = w / kSlots;
+    const int s = (int)(w % kSlots);
+    T v = T(0);
+    if (s < (1 << kc) - 1) {
+      const int d = 31 - __clz(s + 1);
+      const uint64_t q = (uint64_t)(s + 1 - (1 << d));
+      const int sh = pbits - level;
+      v = xpad[(m << sh) | (q << (sh - d)) | (1ull << (sh - d - 1))];
+    }
+    rec[w] = v;
+  }
+}
+
 }  // namespace fsg

@@ -78,6 +78,25 @@ constexpr int kB2ConflictFree = 6;  // levels 0..5: at most 32 consecutive words
 
 // bitset2's staged top levels: levels [0, top) in level order, levels
 // [l1, l2) stored as 32 bank-private copies (Bitset2Probe).
+// bitset2's global levels as subtree records (fs_build_b2_deep): chunks of
+// k levels from `top` down while at least two levels remain; 32 B per record,
+// 2^level records per chunk.
+constexpr int kB2DeepMinLevels = 2;
+inline int b2_deep_k(int dtype) { return dtype == FS_F32 ? 3 : 2; }
+// Fewest global levels worth records: two f32 levels read 8 B of the padded
+// array per query, which on clustered streams stays L1-resident better than
+// a 32-B record (cfg4: 166 vs 137 Gq/s); from three f32 / two f64 levels
+// the records win (2^20 f32 knots 42 -> 91, cfg5 N+1 = 32769 85 -> 98,
+// N+1 = 1048577 33 -> 50; profiles/r01/tune_bitset2_deep.txt).
+inline int b2_deep_min_levels(int dtype) { return dtype == FS_F32 ? 3 : 2; }
+inline uint64_t b2_deep_total_bytes(int pbits, int top, int k) {
+  uint64_t bytes = 0;
+  for (int l = top; pbits - l >= kB2DeepMinLevels; l += std::min(k, pbits - l)) bytes += (1ull << l) * 32;
+  return bytes;
+}
+inline int b2_top_bits(int pbits, size_t es) {
+  return std::min(bit_length(smem_budget() / es + 1) - 1, pbits);
+}
 inline uint64_t b2_smem_bytes(int top, int l1, int l2, size_t es) {
   return (((1ull << l1) - 1) + ((1ull << l2) - (1ull << l1)) * 32 + ((1ull << top) - (1ull << l2))) * es;
 }
@@ -270,7 +289,7 @@ Placement place(const fs_plan* p) {
       // as many levels as fit, then bank-private copies of the levels below
       // the conflict-free top six, as far as the remaining budget allows
       pl.top = true;
-      int tb = std::min(bit_length(budget / es + 1) - 1, p->pbits);
+      const int tb = b2_top_bits(p->pbits, es);
       pl.top_bits = tb;
       pl.flags |= tb == p->pbits ? FS_PLACE_SMEM_X : FS_PLACE_SMEM_TOP;
       pl.b2_l1 = pl.b2_l2 = std::min(kB2ConflictFree, tb);
@@ -373,6 +392,7 @@ template <typename T, bool DENSE>
 struct BoundedFor<T, SparseProbe<T, true, DENSE>> {
   static constexpr bool value = true;
 };
+
 
 
 // Launch geometry per (device, kernel, dynamic smem, candidate set), and the
@@ -481,6 +501,11 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   d.top_bits = pl.top_bits;
   d.b2_l1 = pl.b2_l1;
   d.b2_l2 = pl.b2_l2;
+  // subtree records apply only to the staged-top split they were built for
+  const bool deep = pl.top && p->b2_deep && p->b2_deep_top == pl.top_bits &&
+                    p->b2_deep_k == b2_deep_k(p->dtype);
+  d.b2_deep = deep ? p->b2_deep : nullptr;
+  d.b2_deep_k = deep ? p->b2_deep_k : 0;
   const uint64_t n = p->n1 - 1;
   d.off_f = (uint32_t)((n + 1) >> 1);
   d.off_s = (uint32_t)(n + 1 - d.off_f);
@@ -551,6 +576,7 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       if (pl.ks) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
       return launch_probe<T, OutT, CacheProbe<T, uint32_t, false>>(d, pl, z, m, out, fb, base, st);
     case FS_ALGO_BITSET2:
+      if (pl.top && d.b2_deep) return launch_probe<T, OutT, Bitset2Probe<T, true, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.top) return launch_probe<T, OutT, Bitset2Probe<T, true>>(d, pl, z, m, out, fb, base, st);
       return launch_probe<T, OutT, Bitset2Probe<T, false>>(d, pl, z, m, out, fb, base, st);
     case FS_ALGO_CLASSIC: return dispatch_compare<T, OutT, 0>(d, pl, z, m, out, fb, base, st);
@@ -866,6 +892,41 @@ int fs_build_eytzinger(int32_t dtype, const void* x_dev, uint64_t n1, int32_t de
   else
     return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
   FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+uint64_t fs_b2_deep_bytes(int32_t dtype, int32_t pbits, int32_t* top_bits_out, int32_t* k_out) {
+  if ((dtype != FS_F32 && dtype != FS_F64) || pbits < 1 || pbits > 31) return 0;
+  const int top = b2_top_bits(pbits, dtype == FS_F32 ? 4 : 8), k = b2_deep_k(dtype);
+  if (top_bits_out) *top_bits_out = top;
+  if (k_out) *k_out = k;
+  if (pbits - top < b2_deep_min_levels(dtype)) return 0;
+  return b2_deep_total_bytes(pbits, top, k);
+}
+
+int fs_build_b2_deep(int32_t dtype, const void* xpad_dev, int32_t pbits, int32_t top_bits, int32_t k,
+                     void* deep_dev, void* stream) {
+  if (!xpad_dev || !deep_dev || pbits < 1 || pbits > 31 || top_bits < 0 || top_bits >= pbits || k < 2 || k > 3 ||
+      (dtype == FS_F64 && k > 2))
+    return fail(FS_INVALID_ARG, "bad arguments");
+  cudaStream_t s = as_stream(stream);
+  uint64_t off = 0;
+  for (int l = top_bits; pbits - l >= kB2DeepMinLevels; l += std::min<int>(k, pbits - l)) {
+    const int kc = std::min<int>(k, pbits - l);
+    const uint64_t nrec = 1ull << l;
+    char* dst = static_cast<char*>(deep_dev) + off;
+    const int g = grid_1d(nrec * 8, 256);
+    if (dtype == FS_F32)
+      b2_deep_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(xpad_dev), pbits, l, kc, nrec,
+                                              reinterpret_cast<float*>(dst));
+    else if (dtype == FS_F64)
+      b2_deep_kernel<double><<<g, 256, 0, s>>>(static_cast<const double*>(xpad_dev), pbits, l, kc, nrec,
+                                               reinterpret_cast<double*>(dst));
+    else
+      return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+    FS_CUDA(cudaGetLastError());
+    off += nrec * 32;
+  }
   return FS_OK;
 }
 

@@ -47,6 +47,8 @@ struct DevPlan {
   int32_t pbits;         // bitset / eytzinger depth
   int32_t top_bits;      // bitset2: levels served from smem
   int32_t b2_l1, b2_l2;  // bitset2: levels [b2_l1, b2_l2) replicated per bank in smem
+  const void* b2_deep;   // bitset2: subtree records of the levels below top_bits, or NULL
+  int32_t b2_deep_k;     // ... levels per record
   uint32_t off_f, off_s, off_j;  // offset search constants
   uint32_t x_smem_bytes;     // bytes of X (or padded / tree / top table) staged; 0 = global
   uint32_t table_smem_bytes; // bytes of K / records staged; 0 = global
@@ -338,11 +340,12 @@ struct CacheProbe<double, J, RS> {
 // regions are stacked in level order, which makes c1 / c2 level-independent):
 // one LDS, one compare, one select, one 3-input add per level.  Same
 // comparisons, same values as binsearch.py:72-86.
-template <typename T, bool TOP>
+template <typename T, bool TOP, bool DEEP = false>
 struct Bitset2Probe {
   const T* top;
   const T* xpad;
-  int pbits, top_bits, l1, l2;
+  const char* deep;  // subtree records of the global levels (fs_build_b2_deep) or NULL
+  int pbits, top_bits, l1, l2, deep_k;
   __device__ __forceinline__ Bitset2Probe(const DevPlan<T>& p, unsigned char* smem) {
     top = reinterpret_cast<const T*>(smem);
     xpad = static_cast<const T*>(p.table);
@@ -350,6 +353,40 @@ struct Bitset2Probe {
     top_bits = TOP ? p.top_bits : 0;
     l1 = TOP ? p.b2_l1 : 0;
     l2 = TOP ? p.b2_l2 : 0;
+    deep = DEEP ? static_cast<const char*>(p.b2_deep) : nullptr;
+    deep_k = DEEP ? p.b2_deep_k : 0;
+  }
+  // One 32-B subtree record: 8 f32 / 4 f64 values, BFS order.
+  struct Rec {
+    T v[32 / sizeof(T)];
+  };
+  static __device__ __forceinline__ Rec ld_rec(const char* p) {
+    Rec r;
+    if constexpr (sizeof(T) == 4) {
+      asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                     "=f"(r.v[6]), "=f"(r.v[7])
+                   : "l"(p));
+    } else {
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                   : "l"(p));
+    }
+    return r;
+  }
+  // k_c levels of one record, selects only (no local-memory indexing):
+  // returns the k_c decision bits, first decision in the high bit.
+  static __device__ __forceinline__ uint32_t walk_rec(const Rec& r, T z, int kc) {
+    const uint32_t b0 = z >= r.v[0];
+    const T v1 = b0 ? r.v[2] : r.v[1];
+    const uint32_t b1 = z >= v1;
+    if constexpr (sizeof(T) == 4) {
+      if (kc == 3) {
+        const T v2 = b0 ? (b1 ? r.v[6] : r.v[5]) : (b1 ? r.v[4] : r.v[3]);
+        return (b0 << 2) | (b1 << 1) | (uint32_t)(z >= v2);
+      }
+    }
+    return (b0 << 1) | b1;
   }
   static __device__ __forceinline__ void prologue(const DevPlan<T>& p, unsigned char* smem) {
     if constexpr (TOP) {
@@ -475,8 +512,33 @@ struct Bitset2Probe {
     uint32_t s[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) s[q] = 0;
-    if constexpr (TOP) descend_top<N>(z, s);
-    for (int lvl = top_bits; lvl < pbits; ++lvl) {
+    int lvl = top_bits;
+    if constexpr (TOP) {
+      descend_top<N>(z, s);
+    }
+    if constexpr (DEEP) {
+      {  // global levels in k-level chunks: one 32-B gather per chunk
+        uint64_t off = 0;
+        for (; pbits - lvl >= 2; ) {
+          const int kc = pbits - lvl < deep_k ? pbits - lvl : deep_k;
+          const int sh = pbits - lvl;
+          constexpr int G = N < 4 ? N : 4;  // records in flight per group (32 B each)
+#pragma unroll
+          for (int g0 = 0; g0 < N; g0 += G) {
+            Rec r[G];
+#pragma unroll
+            for (int q = 0; q < G; ++q)
+              if (g0 + q < N) r[q] = ld_rec(deep + off + (uint64_t)(s[g0 + q] >> sh) * 32);
+#pragma unroll
+            for (int q = 0; q < G; ++q)
+              if (g0 + q < N) s[g0 + q] |= walk_rec(r[q], z[g0 + q], kc) << (sh - kc);
+          }
+          off += (32ull << lvl);
+          lvl += kc;
+        }
+      }
+    }
+    for (; lvl < pbits; ++lvl) {
       const uint32_t bit = 1u << (pbits - 1 - lvl);
 #pragma unroll
       for (int q = 0; q < N; ++q) {

@@ -231,6 +231,25 @@ def test_bitset2_bank_replicated_layout(cuda, name, kw):
     assert np.array_equal(fs.run_batch(prep, z[:5000]), want[:5000])
 
 
+@pytest.mark.parametrize("dtype,n1", [(np.float32, (1 << 18) + 1), (np.float32, (1 << 19) + 1),
+                                       (np.float32, (1 << 20) + 1), (np.float64, (1 << 16) + 1),
+                                       (np.float64, (1 << 17) + 1)])
+def test_bitset2_subtree_records(cuda, dtype, n1):
+    """bitset2 on tables too large for shared memory reads its global levels
+    through 32-B subtree records (fs_build_b2_deep): 3 levels per f32 record,
+    2 per f64, a leftover level from the padded array.  These sizes cover
+    every chunk split (f32: 3+1, 3+2, 3+3; f64: 2+1, 2+2); answers equal the
+    oracle on random queries, every knot and its neighbours."""
+    fs = _fs()
+    rng = np.random.default_rng(n1)
+    xs = np.unique(rng.uniform(0.0, 1.0, n1 + n1 // 4).astype(dtype))[:n1]
+    p = fs.validate_partition(xs)
+    prep = fs.prepare("bitset2", p)
+    assert prep.plan.b2_deep  # records built and used
+    z = np.concatenate([orc.random_queries(xs, 1_000_000, seed=3), orc.boundary_probes(xs)])
+    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
+
+
 def test_batch_beyond_2_pow_32(cuda):
     """Positions and offsets are 64-bit: one batch of 2^32 + 9 queries (16 GiB
     in, 16 GiB out).  Every answer satisfies the bracket property, the tail

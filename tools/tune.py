@@ -15,6 +15,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_1506_08620_b200 as fs  # noqa: E402
@@ -56,6 +57,27 @@ def main():
     for spec in args.configs.split(","):
         name, _, arg = spec.partition(":")
         kw = {"n1": int(arg)} if name == "cfg5" and arg else ({"seed": int(arg)} if arg else {})
+        if name == "cfg5u":  # the unfiltered cfg5 draw: direct raises Overflow, bitset2 is the fallback
+            name, kw = "cfg5", {"n1": int(arg or 1048577), "filtered": False}
+        if name == "big32":  # f32 sorted U[0,1) with 2^20 / 2^22 knots: bitset2 with several global levels
+            n1 = int(arg or 1048577)
+            rng = np.random.default_rng(5)
+            xs = np.unique(rng.uniform(0, 1, n1 + n1 // 8).astype(np.float32))[:n1]
+            p = fs.validate_partition(xs)
+            z = (torch.rand(1 << 28, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
+                 * float(xs[-1] - xs[0]) + float(xs[0])).float()
+            z = torch.clamp(z, max=float(np.nextafter(xs[-1], np.float32(0))))
+            out = torch.empty(z.numel(), dtype=torch.int32, device="cuda")
+            fb = fs.new_status()
+            for algo in args.algos.split(","):
+                if algo not in ("bitset2",):
+                    continue
+                prep = fs.prepare(algo, p)
+                t = time_launch(lambda: prep.launch(z, out, fb), args.steps)
+                ok = fs.first_bad_of(fb) is None and verify(p, z, out)
+                print(json.dumps({"config": spec, "algo": algo, "m": z.numel(), "gqs": round(z.numel() / t / 1e9, 2),
+                                  "ok": ok, "placement": prep.placement()}), flush=True)
+            continue
         p = workloads.knots(name, **kw)
         m = args.m or workloads.CONFIGS[name].m
         z = workloads.queries_device(name, p, m, seed=1)
