@@ -741,12 +741,17 @@ __device__ __forceinline__ void search_body(const T* __restrict__ z, OutT* __res
       for (int u = 0; u < UNROLL; ++u) {
         const uint64_t g = g0 + u * stride;
         if (g < sh.nvec) {
+          // domain check: a 4-bit mask per group; the position is formed and
+          // min-merged only for a group holding a bad query (rare)
+          uint32_t badmask = 0;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const T v = zz[4 * u + e];
-            const bool bad = !(v >= x0 && v < xn);
-            const uint64_t pos = sh.head + 4 * g + e;
-            if (bad && pos < mybad) mybad = pos;
+            badmask |= (uint32_t)!(v >= x0 && v < xn) << e;
+          }
+          if (badmask) {
+            const uint64_t pos = sh.head + 4 * g + (uint32_t)__ffs(badmask) - 1;
+            if (pos < mybad) mybad = pos;
           }
           const R ou[4] = {o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]};
           store4(ov + 4 * g, ou, vec_out);

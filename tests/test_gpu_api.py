@@ -250,6 +250,36 @@ def test_bitset2_subtree_records(cuda, dtype, n1):
     assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
 
 
+@pytest.mark.parametrize("algo", ["direct", "bitset2", "classic"])
+def test_first_bad_across_tail_and_vector_body(cuda, algo):
+    """The scalar head/tail queries of a batch are checked before the vector
+    body by the same threads: a bad tail query must not hide a smaller bad
+    position in the body (thread tid owns tail query tail0 + tid and vector
+    group tid).  Every tail length 1..3 and head offset 0..3."""
+    import torch
+
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots("cfg3")
+    prep = fs.prepare(algo, p)
+    base = workloads.queries_device("cfg3", p, 100_000 + 8, seed=4)
+    out = torch.empty(base.numel(), dtype=torch.int32, device=cuda)
+    for off in range(4):  # head = (4 - off) % 4 queries before the first 16-B group
+        for tail in (1, 2, 3):
+            m = 4 * 20_000 + tail + (4 - off) % 4
+            zz = base.clone()[off:off + m]
+            head = (4 - (zz.data_ptr() // 4) % 4) % 4
+            tail0 = head + 4 * ((m - head) // 4)
+            tid = (m - 1) - tail0
+            body = head + 4 * tid + 2  # vector group tid of thread tid, element 2
+            zz[m - 1] = float("nan")
+            zz[body] = -1.0
+            with pytest.raises(fs.OutOfDomain) as e:
+                fs.batch_search(fs.LaneConfig(4, algo, prep), zz, out[off:off + m])
+            assert e.value.position == body, (off, tail, head)
+
+
 def test_batch_beyond_2_pow_32(cuda):
     """Positions and offsets are 64-bit: one batch of 2^32 + 9 queries (16 GiB
     in, 16 GiB out).  Every answer satisfies the bracket property, the tail
