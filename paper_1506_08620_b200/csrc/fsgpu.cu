@@ -305,13 +305,17 @@ Placement place(const fs_plan* p) {
     default: {  // classic / bitset1 / bitset3 / offset on X; eytzinger on its tree
       if (force_global) break;
       const bool tree = p->algorithm == FS_ALGO_EYTZINGER;
-      const uint64_t xb = tree ? ((1ull << p->pbits) - 1) * es : p->n1 * es;
+      // sorted X is staged XOR-swizzled by the kernel prologue (whole 128-B
+      // rows, CompareProbe::swz); the Eytzinger tree by the bulk copy
+      const uint64_t xb = tree ? ((1ull << p->pbits) - 1) * es : align128(p->n1 * es);
       if (xb <= budget) {
         pl.xs = true;
         pl.x_bytes = (uint32_t)xb;
-        pl.seg0_src = tree ? p->table : p->x;
-        pl.seg0_bytes = (uint32_t)xb;
-        pl.nseg = 1;
+        if (tree) {
+          pl.seg0_src = p->table;
+          pl.seg0_bytes = (uint32_t)xb;
+          pl.nseg = 1;
+        }
         pl.smem = xb;
         pl.flags |= FS_PLACE_SMEM_X;
       }

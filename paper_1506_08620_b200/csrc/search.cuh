@@ -564,6 +564,28 @@ struct CompareProbe {
   uint32_t n;
   int pbits;
   uint32_t F, S, Jc;
+  // Sorted X in shared memory is stored XOR-swizzled within 128-B rows:
+  // element i sits at i ^ (hash(i >> R) & (2^R - 1)).  The searches probe
+  // elements 2^k apart, which in plain order share one bank (up to 32-way
+  // conflicts, ~63 G queries/s on cfg3); swizzled they spread over the
+  // banks.  The Eytzinger tree is already in level order and is not swizzled.
+  static constexpr bool kSwz = XS && ALGO != 5;
+  static __device__ __forceinline__ uint32_t swz(uint32_t i) {
+    constexpr int R = sizeof(T) == 4 ? 5 : 4;  // elements per 128-B row: 2^R
+    const uint32_t hi = i >> R;
+    return i ^ ((hi ^ (hi >> R) ^ (hi >> (2 * R)) ^ (hi >> (3 * R))) & ((1u << R) - 1));
+  }
+  __device__ __forceinline__ T x(uint32_t i) const {
+    if constexpr (kSwz) return X[swz(i)];
+    else return tload<XS>(X, i);
+  }
+  static __device__ __forceinline__ void prologue(const DevPlan<T>& p, unsigned char* smem) {
+    if constexpr (kSwz) {
+      T* dst = reinterpret_cast<T*>(smem);
+      for (uint32_t i = threadIdx.x; i < p.n1; i += blockDim.x) dst[swz(i)] = __ldg(p.x + i);
+      __syncthreads();
+    }
+  }
   __device__ __forceinline__ CompareProbe(const DevPlan<T>& p, unsigned char* smem) {
     X = XS ? reinterpret_cast<const T*>(smem)
            : (ALGO == 5 ? static_cast<const T*>(p.table) : p.x);
@@ -578,7 +600,7 @@ struct CompareProbe {
       uint32_t low = 0, high = n;
       while (high - low > 1) {
         const uint32_t mid = (low + high) >> 1;
-        if (z < tload<XS>(X, mid)) high = mid;
+        if (z < x(mid)) high = mid;
         else low = mid;
       }
       return low;
@@ -586,7 +608,7 @@ struct CompareProbe {
       uint32_t i = 0;
       for (uint32_t k = 1u << (pbits - 1); k; k >>= 1) {
         const uint32_t r = i | k;
-        if (r < n && z >= tload<XS>(X, r)) i = r;
+        if (r < n && z >= x(r)) i = r;
       }
       return i;
     } else if constexpr (ALGO == 3) {  // bitset3, binsearch.py:89-99
@@ -594,17 +616,17 @@ struct CompareProbe {
       for (uint32_t k = 1u << (pbits - 1); k; k >>= 1) {
         const uint32_t r = i | k;
         const uint32_t w = r < n ? r : n;
-        if (z >= tload<XS>(X, w)) i = r;
+        if (z >= x(w)) i = r;
       }
       return i;
     } else if constexpr (ALGO == 4) {  // offset, binsearch.py:102-114
-      uint32_t i = z >= tload<XS>(X, F) ? F : 0;
+      uint32_t i = z >= x(F) ? F : 0;
       uint32_t s = S;
       for (uint32_t it = 0; it < Jc; ++it) {
         const uint32_t half = s >> 1;
         uint32_t f = i + half;
         f = f < n ? f : n;  // never binds in domain; keeps bad lanes in bounds
-        if (z >= tload<XS>(X, f)) i = f;
+        if (z >= x(f)) i = f;
         s -= half;
       }
       return i;
@@ -612,6 +634,61 @@ struct CompareProbe {
       uint64_t k = 1;
       for (int l = 0; l < pbits; ++l) k = 2 * k + (z >= tload<XS>(X, k - 1) ? 1 : 0);
       return (int64_t)k - (int64_t(1) << pbits) - 1;
+    }
+  }
+  // N queries in lockstep (independent load chains per step), the same
+  // comparisons per query as operator(); classic keeps one query at a time
+  // (its masked lockstep measured 15% slower).
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    if constexpr (ALGO == 0) {  // data-dependent trip count: one query at a time measures best
+#pragma unroll
+      for (int q = 0; q < N; ++q) o[q] = (R)(*this)(z[q]);
+    } else if constexpr (ALGO == 1 || ALGO == 3) {
+      uint32_t i[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) i[q] = 0;
+      for (uint32_t k = 1u << (pbits - 1); k; k >>= 1) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          const uint32_t r = i[q] | k;
+          if constexpr (ALGO == 1) {
+            if (r < n && z[q] >= x(r)) i[q] = r;
+          } else {
+            if (z[q] >= x(r < n ? r : n)) i[q] = r;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < N; ++q) o[q] = (R)i[q];
+    } else if constexpr (ALGO == 4) {
+      uint32_t i[N];
+      const T xf = x(F);
+#pragma unroll
+      for (int q = 0; q < N; ++q) i[q] = z[q] >= xf ? F : 0;
+      uint32_t s = S;
+      for (uint32_t it = 0; it < Jc; ++it) {
+        const uint32_t half = s >> 1;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          uint32_t f = i[q] + half;
+          f = f < n ? f : n;
+          if (z[q] >= x(f)) i[q] = f;
+        }
+        s -= half;
+      }
+#pragma unroll
+      for (int q = 0; q < N; ++q) o[q] = (R)i[q];
+    } else {
+      uint64_t k[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) k[q] = 1;
+      for (int l = 0; l < pbits; ++l) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) k[q] = 2 * k[q] + (z[q] >= tload<XS>(X, k[q] - 1) ? 1 : 0);
+      }
+#pragma unroll
+      for (int q = 0; q < N; ++q) o[q] = (R)((int64_t)k[q] - (int64_t(1) << pbits) - 1);
     }
   }
 };
