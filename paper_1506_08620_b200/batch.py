@@ -310,8 +310,18 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
     else:
         raise ValueError(f"unknown algorithm {algorithm!r}; pick one of {ALGORITHMS}")
     plan, keep = _plan_for(algorithm, structure, p)
-    if algorithm == "direct" and structure.q == 1:
-        rec_bytes = 8 if p.precision == "single" else 16
+    rec_bytes = 8 if p.precision == "single" else 16
+    if algorithm == "direct-cache" and (structure.r + 1) * rec_bytes > SMEM_RECORDS_MAX:
+        # Records that cannot be staged would be gathered 16 B at a time
+        # through L2 (cfg5 N+1 = 1025: 89 G queries/s).  The cache lane's
+        # answers are the gap-1 direct answers by definition (direct.py:
+        # 601-610 vs 570-574), so the device plan uses direct's layouts over
+        # the same index (K, rank directory, sparse table); the structure
+        # and its fused host view are unchanged.
+        plan.algorithm = _lib.ALGO_CODES["direct"]
+        plan.table = structure.k_dev.data_ptr()
+        keep.append(structure.k_dev)
+    if plan.algorithm == _lib.ALGO_CODES["direct"] and structure.q == 1:
         if (structure.r + 1) * rec_bytes <= SMEM_RECORDS_MAX:
             rec = _device.empty((structure.r + 1) * rec_bytes, np.uint8)
             rc = _lib.load().fs_build_fused(fs_dtype(p.precision), p.device_values().data_ptr(), len(p.values),

@@ -280,6 +280,25 @@ def test_first_bad_across_tail_and_vector_body(cuda, algo):
             assert e.value.position == body, (off, tail, head)
 
 
+def test_direct_cache_with_records_too_large_for_smem(cuda):
+    """prepare("direct-cache") keeps the reference structure (fused records,
+    host view, scalar cache lane) but, when the records cannot be staged,
+    searches through direct's device layouts: same answers (direct.py:601-610
+    equals 570-574 by construction), no 16-B L2 record gathers."""
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots("cfg5", n1=1025)
+    prep = fs.prepare("direct-cache", p)
+    assert prep.algorithm == "direct-cache"
+    assert prep.structure.fused is not None and prep.structure.fused.dtype.itemsize == 16
+    assert prep.placement()["smem_sparse"]
+    z = workloads.queries_host("cfg5", p, 1_000_003, seed=17)
+    want = orc.rank_oracle(p.values, z)
+    assert np.array_equal(fs.run_batch(prep, z), want)
+    assert [fs.direct_search_cache(prep.structure, v) for v in z[:50]] == want[:50].tolist()
+
+
 def test_batch_beyond_2_pow_32(cuda):
     """Positions and offsets are 64-bit: one batch of 2^32 + 9 queries (16 GiB
     in, 16 GiB out).  Every answer satisfies the bracket property, the tail
