@@ -46,6 +46,7 @@ METRIC = "queries/sec and achieved HBM GB/s (fraction of roofline), direct vs bi
 UNIT = "queries/s"
 M_PER_GPU = 1 << 30
 BYTES_PER_QUERY = 8  # 4 B float32 query read + 4 B int32 index written
+SPEC_HBM_GBS = 8000.0  # B200 nominal HBM3e bandwidth (secondary denominator)
 CPU_SAMPLE = 1 << 24
 
 
@@ -456,6 +457,7 @@ def main():
                 "frac": achieved / pk["hbm_gbs"],
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                 "peak_source": pk["source"],
+                "frac_of_spec": achieved / SPEC_HBM_GBS,  # the ~8 TB/s nominal peak the north star cites
                 "algorithmic_bytes_per_query": BYTES_PER_QUERY,
             },
             "bsearch": {
