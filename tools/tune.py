@@ -3,6 +3,11 @@ part of the product).  Times each variant with CUDA events over device-
 resident queries and prints one JSON line per variant.
 
     python tools/tune.py [--configs cfg3,cfg4] [--geometry] [--steps 10]
+
+Config specs: cfgN (BASELINE recipes), cfg5:<N+1>, cfg2:<seed>, cfg5u (the
+unfiltered cfg5 draw, bitset2 fall-back instance), big32:<N+1> (sorted f32
+U[0,1) knots).  Layout variants: direct-k (plain K), direct-rank (rank
+directory only), direct-hot (hot window), bitset2-flat (no subtree records).
 """
 
 from __future__ import annotations
@@ -93,7 +98,7 @@ def main():
         for algo in args.algos.split(","):
             try:
                 base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct",
-                        "bitset2-sorted": "bitset2"}.get(algo, algo)
+                        "bitset2-flat": "bitset2"}.get(algo, algo)
                 prep = fs.prepare(base, p)
                 if algo == "direct-k":  # plain K table instead of rank directory / records
                     prep.plan.rank = None
@@ -103,9 +108,8 @@ def main():
                     prep.plan.sparse = None
                 if algo == "direct-hot":
                     prep = fs.prepare("direct", p, hot_window=True)
-                if algo == "bitset2-sorted":  # bottom levels from the sorted padded array
-                    prep = fs.prepare("bitset2", p)
-                    prep.plan.aux = None
+                if algo == "bitset2-flat":  # global levels from the padded array (no subtree records)
+                    prep.plan.b2_deep = None
             except fs.InfeasibleError as e:
                 print(json.dumps({"config": spec, "algo": algo, "infeasible": type(e).__name__}), flush=True)
                 continue
