@@ -233,13 +233,23 @@ bool domain_clean_two_sided(const T* z, uint64_t m, uint64_t chunk, T x0, T xn, 
   return !bad.load();
 }
 
+// Processes sharing this host's cores: one per GPU under torchrun
+// (LOCAL_WORLD_SIZE), so N ranks do not oversubscribe the host N times over.
+inline unsigned host_procs() {
+  if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) {
+    const int n = std::atoi(e);
+    if (n > 1) return (unsigned)n;
+  }
+  return 1u;
+}
+
 inline int host_scan_threads() {
   if (const char* e = std::getenv("FSG_SCAN_THREADS")) {  // tuning override
     const int n = std::atoi(e);
     if (n > 0) return std::min(n, 64);
   }
   const unsigned hc = std::thread::hardware_concurrency();
-  return (int)std::max(1u, std::min(32u, hc ? hc : 4u));
+  return (int)std::max(1u, std::min(32u, (hc ? hc : 4u) / host_procs()));
 }
 
 inline int host_copy_threads() {
@@ -247,10 +257,11 @@ inline int host_copy_threads() {
     const int n = std::atoi(e);
     if (n > 0) return std::min(n, 64);
   }
-  // every hardware thread: staging is host-memory-bandwidth bound
-  // (tools/pageable_threads.py on the 16-core GPU host: 8 -> 4.7, 16 -> 5.2 G queries/s)
+  // every hardware thread (this process's share of them): staging is host-
+  // memory-bandwidth bound (tools/pageable_threads.py on the 16-core GPU
+  // host: 8 -> 4.7, 16 -> 5.2 G queries/s)
   const unsigned hc = std::thread::hardware_concurrency();
-  return (int)std::max(2u, std::min(32u, hc ? hc : 4u));
+  return (int)std::max(2u, std::min(32u, (hc ? hc : 4u) / host_procs()));
 }
 
 }  // namespace fsg
