@@ -45,3 +45,30 @@ def partitions(draw, max_size=96):
         x = np.array([0.0, 1.0], dtype=dtype)
     assert np.all(np.isfinite(x)) and np.all(np.diff(x) > 0)
     return x
+
+
+@st.composite
+def big_partitions(draw):
+    """Large strictly increasing knot arrays (2^12 .. 2^20 + 1 knots) that
+    reach the big-table device paths: subtree records below the smem top
+    (bitset2), the sparse two-level table and the L2 rank directory
+    (direct), bank-replicated levels with large batches."""
+    dtype = draw(st.sampled_from([np.float32, np.float64]))
+    n1 = draw(st.sampled_from([(1 << 12) + 1, 5000, (1 << 15) + 1, 70_000, (1 << 17) + 3, 300_000, (1 << 20) + 1]))
+    seed = draw(st.integers(min_value=0, max_value=2**32 - 1))
+    rng = np.random.default_rng(seed)
+    kind = draw(st.sampled_from(["uniform", "geometric", "clustered", "sorted_random", "offset"]))
+    if kind == "uniform":
+        gaps = rng.uniform(1.0, 5.0, n1 - 1)
+    elif kind == "geometric":
+        gaps = 1e-4 * 1.0001 ** np.arange(n1 - 1) * rng.uniform(0.9, 1.1, n1 - 1)
+    elif kind == "clustered":
+        gaps = np.where(rng.random(n1 - 1) < 0.3, 1e-3, 1.0) * rng.uniform(1, 2, n1 - 1)
+    elif kind == "sorted_random":
+        gaps = np.diff(np.sort(rng.uniform(0, 1, n1 + 1)))[: n1 - 1] + 1e-7
+    else:
+        gaps = rng.uniform(0.5, 1.5, n1 - 1)
+    origin = -2.0e4 if kind == "offset" else 0.0
+    x = np.unique((origin + np.concatenate([[0.0], np.cumsum(gaps)])).astype(dtype))
+    assert len(x) >= 2 and np.all(np.diff(x) > 0)
+    return x

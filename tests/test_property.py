@@ -17,7 +17,7 @@ from hypothesis import HealthCheck, given, settings
 from hypothesis import strategies as st
 
 from oracle import fs_oracle as orc
-from strategies import partitions
+from strategies import big_partitions, partitions
 
 REF = Path("/root/reference/pkg/src")
 
@@ -95,3 +95,28 @@ def test_gpu_equals_oracle(cuda, xs):
             continue
         got = fs.run_batch(prep, z)
         assert np.array_equal(got, want), algo
+
+
+@pytest.mark.gpu
+@settings(max_examples=24, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+                                                                  HealthCheck.function_scoped_fixture])
+@given(xs=big_partitions())
+def test_gpu_big_tables_equal_oracle(cuda, xs):
+    """Large partitions and batches (4M queries + knot neighbourhoods): the
+    big-table layouts of direct, direct-cache and bitset2 equal the oracle."""
+    import paper_1506_08620_b200 as fs
+
+    p = fs.validate_partition(xs)
+    rng = np.random.default_rng(len(xs))
+    pick = xs[rng.integers(0, len(xs) - 1, 20_000)]
+    t = xs.dtype.type
+    near = np.concatenate([pick, np.nextafter(pick, t(np.inf)), np.nextafter(pick, t(-np.inf))])
+    near = near[(near >= xs[0]) & (near < xs[-1])]
+    z = np.concatenate([orc.random_queries(xs, 1 << 22, seed=len(xs) + 1), near])
+    want = orc.rank_oracle(xs, z)
+    for algo in ("direct", "direct-cache", "bitset2"):
+        try:
+            prep = fs.prepare(algo, p)
+        except fs.InfeasibleError:
+            continue
+        assert np.array_equal(fs.run_batch(prep, z), want), (algo, prep.placement())
