@@ -99,9 +99,10 @@ typedef struct fs_plan {
   int32_t smem_policy;/* 0 auto, 1 force global (L2) gathers                      */
   int32_t tune;       /* launch-geometry override for tuning runs, 0 = auto:
                          bits 0-11 threads per CTA, bits 12-19 max CTAs per SM   */
-  const void* rank;   /* direct (gap 1) only, optional: rank directory of K
-                         (fs_build_rank); when set the kernel reads it instead
-                         of K.  NULL = read K.                                    */
+  const void* rank;   /* direct, optional: rank directory of K (gap 1:
+                         fs_build_rank, 8-B words; gap 2: fs_build_rank2, 16-B
+                         words); when set the kernel reads it instead of K.
+                         NULL = read K.                                           */
   const void* records;/* direct (gap 1) only, optional: fused (K[j], X[K[j]])
                          records (fs_build_fused); used, staged in shared
                          memory, when they fit there.  NULL = unused.            */
@@ -175,6 +176,18 @@ int fs_build_table(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint
  */
 int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
                   uint64_t* f_scratch_dev, void* dir_dev, void* stream);
+
+/*
+ * Rank directory of the gap-2 table (a device layout of build_index with
+ * q = 2, direct.py:498-541; no reference counterpart).  A gap-2 certificate
+ * allows at most two knots per bucket, so each 32-bucket word is 16 B
+ * {m1: buckets with a knot, m2: buckets with two, base = K-count before the
+ * word, 0}; the gap-2 kernel recovers K2[j] exactly and reads X only for
+ * buckets holding knots.  dir_dev holds (r >> 5) + 1 words; set it as
+ * fs_plan.rank of a FS_ALGO_DIRECT_GAP2 plan.
+ */
+int fs_build_rank2(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
+                   uint64_t* f_scratch_dev, void* dir_dev, void* stream);
 
 /*
  * Two-level sparse encoding of the gap-1 table, for R >> N.  Super-bucket J
@@ -276,7 +289,8 @@ int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* o
 /*
  * End-to-end host-buffer search: the whole batch_search contract
  * (batch.py:399-441) on host arrays.  Copies z_host -> z_dev in chunks on
- * `copy_stream` overlapped with the search kernel per chunk on `stream`;
+ * `copy_stream` (ordered after all work already queued on `stream`)
+ * overlapped with the search kernel per chunk on `stream`;
  * then reads the first-bad word and, only if every query is in domain,
  * copies the results to out_host (nothing is written on error, as
  * batch.py:404 promises).  z_dev/out_dev are device scratch of m elements.

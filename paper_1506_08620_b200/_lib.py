@@ -70,6 +70,7 @@ EXPORTED = (
     "fs_build_hot_window",
     "fs_build_fused",
     "fs_build_padded",
+    "fs_build_rank2",
     "fs_b2_deep_bytes",
     "fs_build_b2_deep",
     "fs_build_eytzinger",
@@ -142,6 +143,8 @@ def _declare(lib):
     lib.fs_build_table.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp, _vp]
     lib.fs_build_rank.restype = ctypes.c_int
     lib.fs_build_rank.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _vp, _vp, _vp]
+    lib.fs_build_rank2.restype = ctypes.c_int
+    lib.fs_build_rank2.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _vp, _vp, _vp]
     lib.fs_sparse_bytes.restype = ctypes.c_uint64
     lib.fs_sparse_bytes.argtypes = [_u64, _u64, _i32, _u64]
     lib.fs_plan_sparse.restype = ctypes.c_int

@@ -321,6 +321,16 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
         plan.algorithm = _lib.ALGO_CODES["direct"]
         plan.table = structure.k_dev.data_ptr()
         keep.append(structure.k_dev)
+    x_bytes = (len(p.values) * p.values.dtype.itemsize + 127) // 128 * 128
+    if (algorithm == "direct-gap2" and structure.q == 2
+            and x_bytes + (structure.r + 1) * 4 > SMEM_RECORDS_MAX and structure.r < (1 << 32)):
+        # K and X cannot both be staged: the 16-B-per-32-bucket directory (8x
+        # smaller than K, X read only for buckets holding knots) beats K via L2
+        # (cfg5 N+1 = 32769: 132 -> 216 G queries/s); when they fit, plain K
+        # in smem stays faster (cfg3: 612 vs 439)
+        rank2 = build_rank2_directory(p, structure)
+        plan.rank = rank2.data_ptr()
+        keep.append(rank2)
     if plan.algorithm == _lib.ALGO_CODES["direct"] and structure.q == 1:
         if (structure.r + 1) * rec_bytes <= SMEM_RECORDS_MAX:
             rec = _device.empty((structure.r + 1) * rec_bytes, np.uint8)
@@ -456,6 +466,21 @@ def build_rank_directory(p: SortedPartition, idx: DirectIndex):
     rc = _lib.load().fs_build_rank(fs_dtype(p.precision), x.data_ptr(), len(p.values), float(idx.h), idx.r,
                                    f.data_ptr(), d.data_ptr(), _device.stream_ptr())
     _lib.check(rc, what="fs_build_rank")
+    return d
+
+
+def build_rank2_directory(p: SortedPartition, idx: DirectIndex):
+    """Device rank directory of the gap-2 table (fs_build_rank2): 16-B words
+    {m1, m2, K-count base, 0} per 32 buckets (a gap-2 bucket holds at most
+    two knots).  The kernel recovers K2[j] exactly and reads X only for
+    buckets holding knots."""
+    x = p.device_values()
+    f = _device.empty(len(p.values), np.uint64)
+    words = (idx.r >> 5) + 1
+    d = _device.empty(4 * words, np.uint32)
+    rc = _lib.load().fs_build_rank2(fs_dtype(p.precision), x.data_ptr(), len(p.values), float(idx.h), idx.r,
+                                    f.data_ptr(), d.data_ptr(), _device.stream_ptr())
+    _lib.check(rc, what="fs_build_rank2")
     return d
 
 

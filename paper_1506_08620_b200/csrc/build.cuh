@@ -210,6 +210,28 @@ __global__ void fill_rank_kernel(const uint64_t* __restrict__ f, uint64_t n1, ui
   }
 }
 
+// Rank directory of the gap-2 table (fs_build_rank2).  A gap-2 certificate
+// allows at most two knots per bucket (f_{i+2} > f_i), so word w holds
+// m1 = buckets with >= 1 knot, m2 = buckets with 2 knots and base =
+// #{i : f_i < 32w}; then K2[j] = upper_bound(f, j) - 1 =
+// base + popc(m1 & le) + popc(m2 & le) - 1 with le = bits 0..j mod 32.
+__global__ void fill_rank2_kernel(const uint64_t* __restrict__ f, uint64_t n1, uint64_t r, uint4* __restrict__ dir) {
+  const uint64_t words = (r >> 5) + 1;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j0 = w << 5;
+    const uint64_t base = bound_search<false>(f, 0, n1, j0);
+    uint32_t m1 = 0, m2 = 0;
+    for (uint64_t i = base; i < n1; ++i) {
+      const uint64_t fi = __ldg(f + i);
+      if (fi >= j0 + 32) break;
+      const uint32_t bit = 1u << (uint32_t)(fi - j0);
+      if (m1 & bit) m2 |= bit;
+      else m1 |= bit;
+    }
+    dir[w] = make_uint4(m1, m2, (uint32_t)base, 0u);
+  }
+}
+
 // Two-level sparse encoding of the gap-1 table for R >> N: super-bucket J
 // (buckets J 2^s .. (J+1) 2^s - 1) stores C[J] = K[J 2^s] = lower_bound(f,
 // J 2^s); every knot i stores F[i] = f_i mod 2^s (16 bit).  The knots of

@@ -182,6 +182,9 @@ Placement place(const fs_plan* p) {
     }
   }
   const bool use_rank = p->algorithm == FS_ALGO_DIRECT && p->rank != nullptr && p->q == 1;
+  // gap 2 over its own directory (16-B words, fs_build_rank2)
+  const bool use_rank2 = p->algorithm == FS_ALGO_DIRECT_GAP2 && p->rank != nullptr && p->q == 2;
+  const bool use_dir = use_rank || use_rank2;
   // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
   if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->q == 1 && !force_global && p->r < (1ull << 32) &&
       p->sparse_shift >= 5 && p->sparse_shift <= 16) {
@@ -229,18 +232,18 @@ Placement place(const fs_plan* p) {
       return pl;
     }
   }
-  switch (use_rank ? -1 : p->algorithm) {
-    case -1:  // direct, gap 1, over the rank directory: X and/or directory in smem
+  switch (use_dir ? -1 : p->algorithm) {
+    case -1:  // direct (gap 1 / 2) over its rank directory: X and/or directory in smem
     case FS_ALGO_DIRECT:
     case FS_ALGO_DIRECT_GAP2:
     case FS_ALGO_DIRECT_GENERIC: {
       const uint64_t xb = p->n1 * es;
-      const uint64_t kb = use_rank ? ((p->r >> 5) + 1) * 8 : (p->r + 1) * 4;
-      const void* tab = use_rank ? p->rank : p->table;
+      const uint64_t kb = use_rank ? ((p->r >> 5) + 1) * 8 : use_rank2 ? ((p->r >> 5) + 1) * 16 : (p->r + 1) * 4;
+      const void* tab = use_dir ? p->rank : p->table;
       if (force_global || p->r >= (1ull << 32)) break;
       if (align128(xb) + kb <= budget) {
         pl.xs = pl.ks = true;
-      } else if (use_rank && kb <= budget) {
+      } else if (use_dir && kb <= budget) {
         pl.ks = true;  // every query reads the directory, few read X
       } else if (xb <= budget) {
         pl.xs = true;
@@ -571,6 +574,12 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       return dispatch_direct<T, OutT, uint32_t, 1>(d, pl, z, m, out, fb, base, st);
     case FS_ALGO_DIRECT_GAP2:
       if (wide) return launch_probe<T, OutT, DirectProbe<T, uint64_t, 2, false, false>>(d, pl, z, m, out, fb, base, st);
+      if (p->rank && p->q == 2) {
+        if (pl.xs && pl.ks) return launch_probe<T, OutT, Rank2Probe<T, true, true>>(d, pl, z, m, out, fb, base, st);
+        if (pl.xs) return launch_probe<T, OutT, Rank2Probe<T, true, false>>(d, pl, z, m, out, fb, base, st);
+        if (pl.ks) return launch_probe<T, OutT, Rank2Probe<T, false, true>>(d, pl, z, m, out, fb, base, st);
+        return launch_probe<T, OutT, Rank2Probe<T, false, false>>(d, pl, z, m, out, fb, base, st);
+      }
       return dispatch_direct<T, OutT, uint32_t, 2>(d, pl, z, m, out, fb, base, st);
     case FS_ALGO_DIRECT_GENERIC:
       if (wide) return launch_probe<T, OutT, DirectProbe<T, uint64_t, 3, false, false>>(d, pl, z, m, out, fb, base, st);
@@ -740,6 +749,19 @@ int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
   cudaStream_t s = as_stream(stream);
   const uint64_t words = (r >> 5) + 1;
   fill_rank_kernel<<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint2*>(dir_dev));
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_build_rank2(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t* f_scratch_dev,
+                   void* dir_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !dir_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  if (n1 - 1 >= (1ull << 32)) return fail(FS_INVALID_ARG, "table entries are 32-bit; partition is too large");
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  const uint64_t words = (r >> 5) + 1;
+  fill_rank2_kernel<<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint4*>(dir_dev));
   FS_CUDA(cudaGetLastError());
   return FS_OK;
 }
@@ -1039,6 +1061,18 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   if (rc) return rc;
   if (m && (!z_host || !out_host)) return fail(FS_INVALID_ARG, "host pointer is NULL");
   cudaStream_t s = as_stream(stream), cs = as_stream(copy_stream);
+  if (m && cs != s) {
+    // The uploads run on the copy stream into z_dev, memory the caller's
+    // allocator may have just recycled from buffers that work still queued
+    // on `stream` reads or writes (e.g. an index build's scratch).  Order the
+    // copy stream after everything already queued on `stream`.
+    cudaEvent_t entry;
+    FS_CUDA(cudaEventCreateWithFlags(&entry, cudaEventDisableTiming));
+    cudaError_t e = cudaEventRecord(entry, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, entry, 0);
+    cudaEventDestroy(entry);
+    if (e != cudaSuccess) return fail(FS_CUDA_ERROR, std::string("stream ordering: ") + cudaGetErrorString(e));
+  }
   // pageable buffers of any real size go through the library's own pinned staging
   if (m * (uint64_t)out_bytes >= (4ull << 20) && !(flags & FS_HOST_NO_STAGING) &&
       !(is_pinned(z_host) && is_pinned(out_host)))

@@ -173,6 +173,64 @@ struct RankProbe {
 #endif
 };
 
+// Direct search (gap 2) over the rank directory of its table (fill_rank2_
+// kernel): t = K2[j] recovered exactly; a bucket holding no knot needs no X
+// read (its last knot lies in an earlier bucket, so X[t] < z by the
+// monotone bucket function), one holding c knots needs the c reads of
+// batch.py:341-343 (t - (z < X[t]) - (z < X[t-1])).  Identical answers to
+// DirectProbe<GAP=2>.
+template <typename T, bool XS, bool DS>
+struct Rank2Probe {
+  const T* X;
+  const uint4* D;
+  T h, x0;
+  uint32_t r;
+  __device__ __forceinline__ Rank2Probe(const DevPlan<T>& p, unsigned char* smem) {
+    X = XS ? reinterpret_cast<const T*>(smem) : p.x;
+    D = DS ? reinterpret_cast<const uint4*>(smem + p.x_smem_bytes_aligned()) : reinterpret_cast<const uint4*>(p.rank);
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+  }
+  __device__ __forceinline__ int64_t resolve(T z, uint4 d, uint32_t b) const {
+    const uint32_t le = ((1u << b) << 1) - 1u;  // bits 0..b (b = 31: all)
+    const uint32_t t = d.z + __popc(d.x & le) + __popc(d.y & le) - 1u;
+    const uint32_t c = ((d.x >> b) & 1u) + ((d.y >> b) & 1u);
+    uint32_t miss = 0;
+    if (c >= 1) miss += z < tload<XS>(X, t) ? 1u : 0u;
+    if (c == 2) miss += z < tload<XS>(X, t - 1) ? 1u : 0u;
+    return (int64_t)t - (int64_t)miss;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
+    j = j < r ? j : r;
+    return resolve(z, tload<DS>(D, (uint64_t)(j >> 5)), j & 31u);
+  }
+  // every directory gather of the group in flight before the first is used
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    constexpr int G = N < FSG_RANK_GROUP ? N : FSG_RANK_GROUP;
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += G) {
+      uint4 d[G];
+      uint32_t b[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z[g0 + q], x0), h));
+        j = j < r ? j : r;
+        b[q] = j & 31u;
+        d[q] = tload<DS>(D, (uint64_t)(j >> 5));
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        o[g0 + q] = (R)resolve(z[g0 + q], d[q], b[q]);
+      }
+    }
+  }
+};
+
 // Direct search (gap 1) over the two-level sparse encoding of K (fill_sparse_
 // kernel), staged in shared memory: C (super-bucket ranks) and F (16-bit
 // knot offsets) after X when X fits (else X via L2 -- read only for buckets

@@ -60,8 +60,8 @@ def big_partitions(draw):
     kind = draw(st.sampled_from(["uniform", "geometric", "clustered", "sorted_random", "offset"]))
     if kind == "uniform":
         gaps = rng.uniform(1.0, 5.0, n1 - 1)
-    elif kind == "geometric":
-        gaps = 1e-4 * 1.0001 ** np.arange(n1 - 1) * rng.uniform(0.9, 1.1, n1 - 1)
+    elif kind == "geometric":  # growth capped so float32 stays finite at 2^20 knots
+        gaps = 1e-4 * 1.0001 ** (np.arange(n1 - 1) % 60_000) * rng.uniform(0.9, 1.1, n1 - 1)
     elif kind == "clustered":
         gaps = np.where(rng.random(n1 - 1) < 0.3, 1e-3, 1.0) * rng.uniform(1, 2, n1 - 1)
     elif kind == "sorted_random":

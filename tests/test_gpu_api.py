@@ -299,6 +299,55 @@ def test_direct_cache_with_records_too_large_for_smem(cuda):
     assert [fs.direct_search_cache(prep.structure, v) for v in z[:50]] == want[:50].tolist()
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_uploads_ordered_after_pending_work(cuda, pinned):
+    """Found by the large-table property test: the caller's allocator may hand
+    z_dev a block whose previous owner still has work queued on the current
+    stream (an index build's scratch).  The library uploads on its copy
+    stream, which must therefore wait for that work -- here a delayed fill
+    of the freed block with an out-of-domain value."""
+    import torch
+
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots("cfg3")
+    prep = fs.prepare("direct", p)
+    cfg = fs.LaneConfig(64, "direct", prep)
+    m = 3_000_000 if pinned else 6_000_000  # pageable >= 4 MB takes the staged path
+    zh = workloads.queries_host("cfg3", p, m, seed=23)
+    z = torch.from_numpy(zh).pin_memory().numpy() if pinned else zh
+    want = orc.rank_oracle(p.values, zh)
+    fs.batch_search(cfg, z, np.empty(m, np.int32))  # warm: library streams and slots exist
+    for _ in range(3):
+        victim = torch.empty(m, dtype=torch.float32, device=cuda)
+        torch.cuda._sleep(200_000_000)  # ~0.1 s of queued work on the current stream ...
+        victim.fill_(-5.0)              # ... then a write into the block
+        del victim                      # freed while the write is still queued
+        out = np.empty(m, np.int32)
+        fs.batch_search(cfg, z, out)    # z_dev may reuse the block
+        assert np.array_equal(out, want)
+
+
+@pytest.mark.parametrize("name,kw", [("cfg5", {"n1": 32_769}), ("cfg4", {})])
+def test_gap2_rank_directory(cuda, name, kw):
+    """direct-gap2 with K and X too large to stage reads the gap-2 rank
+    directory (fs_build_rank2: 16-B words, up to two knots per bucket).
+    The layout holds buckets with two knots; answers equal the oracle on
+    random queries, every knot and its neighbours."""
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    p = workloads.knots(name, **kw)
+    prep = fs.prepare("direct-gap2", p)
+    assert prep.plan.rank and prep.structure.q == 2
+    f = fs.knot_buckets(p, prep.structure.h)
+    assert np.any(f[1:] == f[:-1]), "no two-knot bucket: the case is not exercised"
+    xs = p.values
+    z = np.concatenate([workloads.queries_host(name, p, 2_000_000, seed=29), orc.boundary_probes(xs)])
+    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
+
+
 def test_batch_beyond_2_pow_32(cuda):
     """Positions and offsets are 64-bit: one batch of 2^32 + 9 queries (16 GiB
     in, 16 GiB out).  Every answer satisfies the bracket property, the tail

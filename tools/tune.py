@@ -7,7 +7,8 @@ resident queries and prints one JSON line per variant.
 Config specs: cfgN (BASELINE recipes), cfg5:<N+1>, cfg2:<seed>, cfg5u (the
 unfiltered cfg5 draw, bitset2 fall-back instance), big32:<N+1> (sorted f32
 U[0,1) knots).  Layout variants: direct-k (plain K), direct-rank (rank
-directory only), direct-hot (hot window), bitset2-flat (no subtree records).
+directory only), direct-hot (hot window), bitset2-flat (no subtree records),
+direct-gap2-k (gap 2 over plain K).
 """
 
 from __future__ import annotations
@@ -98,7 +99,7 @@ def main():
         for algo in args.algos.split(","):
             try:
                 base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct",
-                        "bitset2-flat": "bitset2"}.get(algo, algo)
+                        "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
                 prep = fs.prepare(base, p)
                 if algo == "direct-k":  # plain K table instead of rank directory / records
                     prep.plan.rank = None
@@ -110,6 +111,8 @@ def main():
                     prep = fs.prepare("direct", p, hot_window=True)
                 if algo == "bitset2-flat":  # global levels from the padded array (no subtree records)
                     prep.plan.b2_deep = None
+                if algo == "direct-gap2-k":  # gap-2 over its plain K table (no rank directory)
+                    prep.plan.rank = None
             except fs.InfeasibleError as e:
                 print(json.dumps({"config": spec, "algo": algo, "infeasible": type(e).__name__}), flush=True)
                 continue
