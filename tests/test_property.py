@@ -65,7 +65,7 @@ def test_oracle_build_equals_reference(reference, xs, q):
 
 
 @pytest.mark.gpu
-@settings(max_examples=400, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+@settings(max_examples=int(__import__("os").environ.get("FSG_SMALL_EXAMPLES", "400")), deadline=None, suppress_health_check=[HealthCheck.too_slow,
                                                                    HealthCheck.function_scoped_fixture])
 @given(xs=partitions())
 def test_gpu_equals_oracle(cuda, xs):
