@@ -348,6 +348,53 @@ def test_gap2_rank_directory(cuda, name, kw):
     assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
 
 
+def test_concurrent_big_tables_prepare_then_search(cuda):
+    """Soak: four threads on one stream each repeatedly build a large index
+    (sparse table, rank directory, subtree records, gap-2 directory) and
+    search immediately through the device, pageable and pinned paths, while
+    the others' builds are still queued -- the pattern behind the upload
+    ordering fix.  Every answer equals the oracle."""
+    import threading
+
+    import torch
+
+    fs = _fs()
+    from paper_1506_08620_b200 import workloads
+
+    specs = [("cfg5", {"n1": 32_769}, "direct"), ("cfg5", {"n1": 1025}, "direct"),
+             ("cfg4", {}, "direct-gap2"), ("cfg5", {"n1": 1_048_577, "filtered": False}, "bitset2")]
+    errors = []
+
+    def work(k):
+        try:
+            name, kw, algo = specs[k]
+            p = workloads.knots(name, **kw)
+            zh = workloads.queries_host(name, p, 5_000_011, seed=40 + k)
+            want = orc.rank_oracle(p.values, zh)
+            zp = torch.from_numpy(zh).pin_memory().numpy()
+            for it in range(3):
+                prep = fs.prepare(algo, p)
+                cfg = fs.LaneConfig(64, algo, prep)
+                out = np.empty(len(zh), np.int64)
+                fs.batch_search(cfg, zh, out)  # pageable, staged
+                assert np.array_equal(out, want), ("pageable", k, it)
+                out32 = np.empty(len(zh), np.int32)
+                fs.batch_search(cfg, zp, out32)  # pinned, two-sided check
+                assert np.array_equal(out32, want), ("pinned", k, it)
+                ot = torch.empty(len(zh), dtype=torch.int32, device=cuda)
+                fs.batch_search(cfg, torch.from_numpy(zh).to(cuda), ot)
+                assert np.array_equal(ot.cpu().numpy(), want), ("device", k, it)
+        except BaseException as ex:  # noqa: BLE001 -- reported by the main thread
+            errors.append((k, repr(ex)[:300]))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(specs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+
+
 def test_batch_beyond_2_pow_32(cuda):
     """Positions and offsets are 64-bit: one batch of 2^32 + 9 queries (16 GiB
     in, 16 GiB out).  Every answer satisfies the bracket property, the tail
