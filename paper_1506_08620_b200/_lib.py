@@ -54,6 +54,8 @@ PLACE_SMEM_K = 2
 PLACE_SMEM_TOP = 4
 PLACE_SMEM_HOT = 8
 PLACE_SMEM_SPARSE = 16
+SPARSE_TWO_LEVEL = 0
+SPARSE_RECORDS = 1
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (
@@ -67,6 +69,9 @@ EXPORTED = (
     "fs_sparse_bytes",
     "fs_plan_sparse",
     "fs_build_sparse",
+    "fs_sparse_rec_bytes",
+    "fs_plan_sparse_rec",
+    "fs_build_sparse_rec",
     "fs_build_hot_window",
     "fs_build_fused",
     "fs_build_padded",
@@ -113,6 +118,7 @@ class FsPlan(ctypes.Structure):
         ("b2_deep", ctypes.c_void_p),
         ("b2_deep_top", ctypes.c_int32),
         ("b2_deep_k", ctypes.c_int32),
+        ("sparse_format", ctypes.c_int32),
     ]
 
 
@@ -152,6 +158,13 @@ def _declare(lib):
                                    _vp]
     lib.fs_build_sparse.restype = ctypes.c_int
     lib.fs_build_sparse.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp]
+    lib.fs_sparse_rec_bytes.restype = ctypes.c_uint64
+    lib.fs_sparse_rec_bytes.argtypes = [_u64, _u64, _i32, _u64]
+    lib.fs_plan_sparse_rec.restype = ctypes.c_int
+    lib.fs_plan_sparse_rec.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _u64, _i32, _vp, _p_i32, _p_u64,
+                                       _p_u64, _p_u32, _vp]
+    lib.fs_build_sparse_rec.restype = ctypes.c_int
+    lib.fs_build_sparse_rec.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _u64, _vp, _vp, _vp]
     lib.fs_build_hot_window.restype = ctypes.c_int
     lib.fs_build_hot_window.argtypes = [_i32, _vp, _u64, _u64, _vp, _p_u64, _p_u64, _p_u64, _p_u64, _p_u64, _vp]
     lib.fs_build_fused.restype = ctypes.c_int

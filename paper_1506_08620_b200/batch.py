@@ -240,6 +240,8 @@ class PreparedKernel:
             "smem_top": bool(f & _lib.PLACE_SMEM_TOP),
             "smem_hot": bool(f & _lib.PLACE_SMEM_HOT),
             "smem_sparse": bool(f & _lib.PLACE_SMEM_SPARSE),
+            "sparse_format": ("records" if self.plan.sparse_format == _lib.SPARSE_RECORDS else "two-level")
+            if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
         }
 
@@ -354,6 +356,17 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
 #: the sparse two-level table is used when its dense (bitmask) super-buckets
 #: hold at most this fraction of the knots
 SPARSE_MAX_DENSE_KNOT_FRACTION = 0.25
+#: group records are used when at most this share of uniform queries (parts
+#: per million) falls past a sixth knot of its super-bucket (the slow path)
+SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = 20_000
+#: group records replace the two-level table when its super-buckets would
+#: hold at least this many knots on average (measured: cfg2 at 0.41 knots
+#: per super-bucket 342 -> 413 G queries/s with records, cfg5 N+1 = 32769 at
+#: 0.84: 336 -> 368; cfg5 N+1 = 1025 at 0.03 stays two-level, 484 vs 446)
+SPARSE_RECORDS_MIN_LOAD = 0.2
+#: sparse layouts allowed; a tuning run or test may narrow it to one
+#: (a leading "records" also skips the load rule)
+SPARSE_FORMATS = ("two-level", "records")
 
 #: hot-window staging budget: small enough that the L2-gather kernel keeps
 #: full occupancy (3-4 CTAs per SM) for the queries outside the window
@@ -410,34 +423,84 @@ def _set_b2_deep(plan, pp: PaddedPartition, keep: list) -> None:
     keep.append(buf)
 
 
+def _set_sparse_records(plan, p: SortedPartition, idx: DirectIndex, keep: list, f, budget: int) -> bool:
+    """Group records of K (fs_build_sparse_rec): one 16-B record per
+    super-bucket resolves K[j] with a single shared-memory load; used when
+    they fit and few queries fall past a sixth knot of a super-bucket."""
+    lib = _lib.load()
+    dt = fs_dtype(p.precision)
+    n1 = len(p.values)
+    x = p.device_values()
+    shift, novf, nbytes, ppm = ctypes.c_int32(-1), ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_uint32(0)
+    for with_x in (1, 0):  # X staged beside the records if possible, else X via L2
+        rc = lib.fs_plan_sparse_rec(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, with_x, f.data_ptr(),
+                                    ctypes.byref(shift), ctypes.byref(novf), ctypes.byref(nbytes), ctypes.byref(ppm),
+                                    _device.stream_ptr())
+        if rc == _lib.FS_OK:
+            break
+        if rc != _lib.FS_TOO_LARGE:
+            _lib.check(rc, what="fs_plan_sparse_rec")
+    else:
+        return False
+    if ppm.value > SPARSE_RECORDS_MAX_PAST_SIXTH_PPM:
+        return False
+    buf = _device.empty(int(nbytes.value), np.uint8)
+    rc = lib.fs_build_sparse_rec(dt, x.data_ptr(), n1, float(idx.h), idx.r, shift.value, novf.value, f.data_ptr(),
+                                 buf.data_ptr(), _device.stream_ptr())
+    _lib.check(rc, what="fs_build_sparse_rec")
+    plan.sparse = buf.data_ptr()
+    plan.sparse_shift = shift.value
+    plan.sparse_ndense = novf.value
+    plan.sparse_format = _lib.SPARSE_RECORDS
+    keep.append(buf)
+    return True
+
+
+def _plan_two_level(p: SortedPartition, idx: DirectIndex, f, budget: int):
+    """fs_plan_sparse with X staged if possible: (shift, ndense, bytes) or None."""
+    lib = _lib.load()
+    x = p.device_values()
+    shift, ndense, nbytes = ctypes.c_int32(-1), ctypes.c_uint64(0), ctypes.c_uint64(0)
+    for with_x in (1, 0):  # X staged beside the table if possible, else X via L2
+        rc = lib.fs_plan_sparse(fs_dtype(p.precision), x.data_ptr(), len(p.values), float(idx.h), idx.r, budget,
+                                with_x, f.data_ptr(), ctypes.byref(shift), ctypes.byref(ndense), ctypes.byref(nbytes),
+                                _device.stream_ptr())
+        if rc == _lib.FS_OK:
+            return shift.value, ndense.value, nbytes.value
+        if rc != _lib.FS_TOO_LARGE:
+            _lib.check(rc, what="fs_plan_sparse")
+    return None
+
+
 def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:
-    """For R >> N, the two-level sparse encoding of K (fs_build_sparse) fits
-    in shared memory where the rank directory does not; the kernel picks it
-    over L2 gathers when the directory (plus X) cannot be staged."""
+    """For R >> N, a sparse encoding of K fits in shared memory where the
+    rank directory does not; the kernel picks it over L2 gathers when the
+    directory (plus X) cannot be staged.  Two layouts: the two-level table
+    (fs_build_sparse; a short search per query, cheapest when super-buckets
+    are nearly empty) and group records (fs_build_sparse_rec; one record
+    load plus fixed arithmetic per query).  Group records are used when the
+    two-level table's super-buckets would hold SPARSE_RECORDS_MIN_LOAD knots
+    or more on average, or it does not fit."""
     if idx.r >= (1 << 32) or len(p.values) >= (1 << 31):
         return
     lib = _lib.load()
     budget = _smem_budget() - 512
-    dt = fs_dtype(p.precision)
     n1 = len(p.values)
-    x = p.device_values()
     f = _device.empty(n1, np.uint64)
-    shift, ndense, nbytes = ctypes.c_int32(-1), ctypes.c_uint64(0), ctypes.c_uint64(0)
-    for with_x in (1, 0):  # X staged beside the table if possible, else X via L2
-        rc = lib.fs_plan_sparse(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, with_x, f.data_ptr(),
-                                ctypes.byref(shift), ctypes.byref(ndense), ctypes.byref(nbytes),
-                                _device.stream_ptr())
-        if rc == _lib.FS_OK:
-            break
-        if rc != _lib.FS_TOO_LARGE:
-            _lib.check(rc, what="fs_plan_sparse")
-    else:
+    two = _plan_two_level(p, idx, f, budget) if "two-level" in SPARSE_FORMATS else None
+    load = n1 / ((idx.r >> two[0]) + 1) if two else None
+    if "records" in SPARSE_FORMATS and (load is None or load >= SPARSE_RECORDS_MIN_LOAD or SPARSE_FORMATS[0] == "records"):
+        if _set_sparse_records(plan, p, idx, keep, f, budget):
+            return
+    if two is None:
         return
-    buf = _device.empty(int(nbytes.value), np.uint8)
-    rc = lib.fs_build_sparse(dt, x.data_ptr(), n1, float(idx.h), idx.r, shift.value, f.data_ptr(), buf.data_ptr(),
-                             _device.stream_ptr())
+    shift, ndense, nbytes = two
+    x = p.device_values()
+    buf = _device.empty(int(nbytes), np.uint8)
+    rc = lib.fs_build_sparse(fs_dtype(p.precision), x.data_ptr(), n1, float(idx.h), idx.r, shift, f.data_ptr(),
+                             buf.data_ptr(), _device.stream_ptr())
     _lib.check(rc, what="fs_build_sparse")
-    if ndense.value:
+    if ndense:
         # queries in dense super-buckets still read X through L2 for almost
         # every bucket; when those regions hold many knots (cfg4's start:
         # 31%) the L2-gather kernel at full occupancy is faster (measured
@@ -445,13 +508,14 @@ def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) ->
         # layouts only
         import torch
 
-        c = buf[: 4 * ((idx.r >> shift.value) + 2)].view(torch.int32).long() & 0x7FFFFFFF
+        c = buf[: 4 * ((idx.r >> shift) + 2)].view(torch.int32).long() & 0x7FFFFFFF
         occ = c[1:] - c[:-1]
         if int(occ[occ > 64].sum().item()) > SPARSE_MAX_DENSE_KNOT_FRACTION * n1:
             return
     plan.sparse = buf.data_ptr()
-    plan.sparse_shift = shift.value
-    plan.sparse_ndense = ndense.value
+    plan.sparse_shift = shift
+    plan.sparse_ndense = ndense
+    plan.sparse_format = _lib.SPARSE_TWO_LEVEL
     keep.append(buf)
 
 

@@ -18,6 +18,12 @@ namespace fsg {
 constexpr uint32_t kDenseFlag = 0x80000000u;
 // Super-buckets holding more knots than this are stored densely.
 constexpr uint32_t kDenseOcc = 64;
+// Group records (fs_build_sparse_rec): knot offsets per 16-B record, the
+// value of an unused offset slot, and the largest super-bucket shift (its
+// offsets stay below the sentinel and the 15-bit SWAR compare of the probe).
+constexpr uint32_t kRecSlots = 6;
+constexpr uint32_t kRecSentinel = 0x7FFFu;
+constexpr int kRecMaxShift = 14;
 
 // ---------------------------------------------------------------------------
 // Exact arithmetic in the partition's precision

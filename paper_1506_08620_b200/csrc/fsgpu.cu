@@ -139,7 +139,10 @@ int validate_plan(const fs_plan* p) {
       if (p->hot_words && (p->hot_word0 > (p->r >> 5) + 1 || p->hot_words > (p->r >> 5) + 1 - p->hot_word0 ||
                            p->hot_knot0 > p->n1 || p->hot_knots > p->n1 - p->hot_knot0))
         return fail(FS_INVALID_ARG, "hot window outside the rank directory / knots");
-      if (p->sparse && (p->sparse_shift < 5 || p->sparse_shift > 16 ||
+      if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS))
+        return fail(FS_INVALID_ARG, "unknown sparse table format");
+      if (p->sparse && (p->sparse_shift < 5 ||
+                        p->sparse_shift > (p->sparse_format == FS_SPARSE_RECORDS ? kRecMaxShift : 16) ||
                         p->sparse_ndense > (p->r >> p->sparse_shift) + 2))
         return fail(FS_INVALID_ARG, "sparse table parameters out of range");
       break;
@@ -190,7 +193,9 @@ Placement place(const fs_plan* p) {
       p->sparse_shift >= 5 && p->sparse_shift <= 16) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
-    const uint64_t cfb = fs_sparse_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense);
+    const uint64_t cfb = p->sparse_format == FS_SPARSE_RECORDS
+                             ? fs_sparse_rec_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense)
+                             : fs_sparse_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense);
     const bool rank_fits = use_rank && align128(xb) + dir_b <= budget;
     if (!rank_fits && cfb <= budget) {
       pl.sparse = pl.ks = true;
@@ -368,6 +373,17 @@ Placement place_for_batch(const fs_plan* p, uint64_t m) {
 #ifndef FSG_UNROLL_F64
 #define FSG_UNROLL_F64 2  // f64: same bytes in flight, half the live registers
 #endif
+#ifndef FSG_UNROLL_F64_SMEM
+#define FSG_UNROLL_F64_SMEM 3
+#endif
+// group records: the default unroll and register budget measure best
+// (profiles/r01/tune_sparse_records.txt)
+#ifndef FSG_UNROLL_F64_REC
+#define FSG_UNROLL_F64_REC 2
+#endif
+#ifndef FSG_REC_BOUNDED
+#define FSG_REC_BOUNDED 0
+#endif
 template <typename T>
 constexpr int kUnroll = sizeof(T) == 8 ? FSG_UNROLL_F64 : FSG_UNROLL;
 // Per-probe override: f64 probes whose whole table sits in smem have short,
@@ -384,7 +400,11 @@ struct UnrollFor<double, CacheProbe<double, J, true>> {
 };
 template <bool DENSE>
 struct UnrollFor<double, SparseProbe<double, true, DENSE>> {
-  static constexpr int value = 3;
+  static constexpr int value = FSG_UNROLL_F64_SMEM;
+};
+template <bool XS, bool OVF>
+struct UnrollFor<double, SparseRecProbe<double, XS, OVF>> {
+  static constexpr int value = FSG_UNROLL_F64_REC;
 };
 // Probes launched through the 1024-thread-bounded entry point: the sparse
 // probe with X in smem exceeds 64 registers with int64 outputs and gains
@@ -398,6 +418,10 @@ struct BoundedFor {
 template <typename T, bool DENSE>
 struct BoundedFor<T, SparseProbe<T, true, DENSE>> {
   static constexpr bool value = true;
+};
+template <typename T, bool XS, bool OVF>
+struct BoundedFor<T, SparseRecProbe<T, XS, OVF>> {
+  static constexpr bool value = FSG_REC_BOUNDED;
 };
 
 
@@ -474,12 +498,14 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
   sh.m = m;
   sh.base = base;
   const uintptr_t za = reinterpret_cast<uintptr_t>(z);
-  uint64_t head = ((16 - (za & 15)) & 15) / sizeof(T);
+  constexpr uint32_t va = Vec4<T>::kAlign;  // query groups start va-aligned
+  uint64_t head = ((va - (za & (va - 1))) & (va - 1)) / sizeof(T);
   if (head > m) head = m;
   sh.head = head;
   sh.nvec = (m - head) / 4;
   DevPlan<T> d = dp;
-  d.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) + head * sizeof(OutT)) & 15) == 0;
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(out) + head * sizeof(OutT);
+  d.out_vec_ok = (oa & 15) ? 0 : (oa & 31) ? 1 : 2;
 
   const uint64_t full = (uint64_t)per_sm * sm_count();
   uint64_t want = (sh.nvec + (uint64_t)threads * kU - 1) / ((uint64_t)threads * kU);
@@ -555,6 +581,14 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
     case FS_ALGO_DIRECT:
       if (pl.records) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
+      if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS) {
+        if (p->sparse_ndense) {
+          if (pl.xs) return launch_probe<T, OutT, SparseRecProbe<T, true, true>>(d, pl, z, m, out, fb, base, st);
+          return launch_probe<T, OutT, SparseRecProbe<T, false, true>>(d, pl, z, m, out, fb, base, st);
+        }
+        if (pl.xs) return launch_probe<T, OutT, SparseRecProbe<T, true, false>>(d, pl, z, m, out, fb, base, st);
+        return launch_probe<T, OutT, SparseRecProbe<T, false, false>>(d, pl, z, m, out, fb, base, st);
+      }
       if (pl.sparse) {
         if (p->sparse_ndense) {
           if (pl.xs) return launch_probe<T, OutT, SparseProbe<T, true, true>>(d, pl, z, m, out, fb, base, st);
@@ -834,6 +868,85 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
   const int grid = (int)std::min<uint64_t>(dense_j.size(), (uint64_t)sm_count() * 8);
   fill_dense_kernel<<<grid, 128, 0, s>>>(C, F, reinterpret_cast<const uint32_t*>(f_scratch_dev), dense_j.size(), shift,
                                         dmask, dpre);
+  FS_CUDA(cudaGetLastError());
+  FS_CUDA(cudaStreamSynchronize(s));
+  return FS_OK;
+}
+
+uint64_t fs_sparse_rec_bytes(uint64_t n1, uint64_t r, int32_t shift, uint64_t novf) {
+  if (shift < 5 || shift > kRecMaxShift) return 0;
+  const uint64_t ng = (r >> shift) + 2;
+  return (16 * ng + (novf ? 2 * n1 : 0) + 15) & ~15ull;
+}
+
+int fs_plan_sparse_rec(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                       int32_t with_x, uint64_t* f_scratch_dev, int32_t* shift_out, uint64_t* novf_out,
+                       uint64_t* bytes_out, uint32_t* past_sixth_ppm_out, void* stream) {
+  if (!x_dev || !f_scratch_dev || n1 < 2 || !shift_out) return fail(FS_INVALID_ARG, "bad arguments");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "group records need R < 2^32, N < 2^31");
+  const uint64_t xb = with_x ? align128(n1 * (dtype == FS_F32 ? 4 : 8)) : 0;
+  if (xb + fs_sparse_rec_bytes(n1, r, kRecMaxShift, 0) > budget_bytes)
+    return fail(FS_TOO_LARGE, "no group-record layout fits the budget");
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
+  if (rc) return rc;
+  std::vector<uint64_t> f(n1);
+  FS_CUDA(cudaMemcpyAsync(f.data(), f_scratch_dev, n1 * 8, cudaMemcpyDeviceToHost, as_stream(stream)));
+  FS_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  // per shift: overflowing records and the buckets lying past a sixth knot
+  // (the only ones whose queries leave the record); f is sorted
+  struct Cand {
+    int s;
+    uint64_t novf, past;
+  };
+  std::vector<Cand> cands;
+  for (int s = 5; s <= kRecMaxShift; ++s) {
+    if (xb + fs_sparse_rec_bytes(n1, r, s, 0) > budget_bytes) continue;
+    uint64_t novf = 0, past = 0;
+    for (uint64_t i = 0; i < n1;) {
+      const uint64_t J = f[i] >> s;
+      uint64_t e = i;
+      while (e < n1 && (f[e] >> s) == J) ++e;
+      if (e - i > kRecSlots) {
+        ++novf;
+        const uint64_t end = std::min(((J + 1) << s) - 1, r);  // last bucket of the super-bucket
+        past += end - f[i + kRecSlots - 1];
+      }
+      i = e;
+    }
+    if (xb + fs_sparse_rec_bytes(n1, r, s, novf) <= budget_bytes) cands.push_back({s, novf, past});
+  }
+  // the fewest queries past a sixth knot; among shifts within 1e-3 of that,
+  // the largest (smallest table)
+  uint64_t min_past = ~0ull;
+  for (const Cand& c : cands) min_past = std::min(min_past, c.past);
+  int best = -1;
+  uint64_t best_novf = 0, best_past = 0;
+  for (const Cand& c : cands)
+    if ((double)(c.past - min_past) <= 1e-3 * (double)(r + 1) && c.s > best) {
+      best = c.s;
+      best_novf = c.novf;
+      best_past = c.past;
+    }
+  if (best < 0) return fail(FS_TOO_LARGE, "no group-record layout fits the budget");
+  *shift_out = best;
+  if (novf_out) *novf_out = best_novf;
+  if (bytes_out) *bytes_out = fs_sparse_rec_bytes(n1, r, best, best_novf);
+  if (past_sixth_ppm_out) *past_sixth_ppm_out = (uint32_t)(1e6 * (double)best_past / (double)(r + 1));
+  return FS_OK;
+}
+
+int fs_build_sparse_rec(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t shift,
+                        uint64_t novf, uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2 || shift < 5 || shift > kRecMaxShift)
+    return fail(FS_INVALID_ARG, "bad arguments");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "group records need R < 2^32, N < 2^31");
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  const uint64_t ng = (r >> shift) + 2;
+  uint4* G = static_cast<uint4*>(buf_dev);
+  uint16_t* F = novf ? reinterpret_cast<uint16_t*>(G + ng) : nullptr;
+  fill_sparse_rec_kernel<<<grid_1d(std::max(ng, n1), 256), 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
   FS_CUDA(cudaGetLastError());
   FS_CUDA(cudaStreamSynchronize(s));
   return FS_OK;

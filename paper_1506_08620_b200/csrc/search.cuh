@@ -32,6 +32,11 @@
 #define FSG_RANK_GROUP 8
 #endif
 
+// Queries per two-phase group in the group-record probe.
+#ifndef FSG_REC_GROUP
+#define FSG_REC_GROUP 4
+#endif
+
 namespace fsg {
 
 // Device image of fs_plan with typed scalars.
@@ -52,7 +57,7 @@ struct DevPlan {
   uint32_t off_f, off_s, off_j;  // offset search constants
   uint32_t x_smem_bytes;     // bytes of X (or padded / tree / top table) staged; 0 = global
   uint32_t table_smem_bytes; // bytes of K / records staged; 0 = global
-  int32_t out_vec_ok;        // output pointer co-aligned with the 16-B query groups
+  int32_t out_vec_ok;        // output groups 16-B aligned (1) / 32-B aligned (2) / neither (0)
   int32_t sparse_shift;      // sparse two-level table: super-bucket = 2^shift buckets
   uint32_t sparse_ndense;    // ... and its number of dense (bitmask) super-buckets
   uint32_t hot_w0, hot_nw;   // rank-directory hot window (words) staged in smem
@@ -289,6 +294,113 @@ struct SparseProbe {
     T xv = z;
     if (knot) xv = tload<XS>(X, t);
     return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
+  }
+};
+
+// Direct search (gap 1) over the group records of K (fill_sparse_rec_kernel),
+// staged in shared memory after X when X fits.  One 16-B LDS per query:
+// t = K[j] = base + #{record offsets < j mod 2^s}, counted branch-free with
+// a 15-bit SWAR compare of the six packed offsets (sentinels never count);
+// bucket j holds knot t iff offset slot t - base equals j mod 2^s.  Only a
+// query in an overflowing super-bucket (more than six knots) whose bucket
+// lies past the sixth knot continues with a lower_bound over F (OVF).
+// Identical answers to DirectProbe<GAP=1> (batch.py:315-317).
+template <typename T, bool XS, bool OVF>
+struct SparseRecProbe {
+  const T* X;
+  uint32_t xs;  // shared-window address of X (XS)
+  const uint4* G;
+  const uint16_t* F;
+  T h, x0;
+  uint32_t r, s, mask;
+  __device__ __forceinline__ SparseRecProbe(const DevPlan<T>& p, unsigned char* smem) {
+    X = XS ? reinterpret_cast<const T*>(smem) : p.x;
+    xs = (uint32_t)__cvta_generic_to_shared(smem);
+    unsigned char* g = smem + p.x_smem_bytes_aligned();
+    G = reinterpret_cast<const uint4*>(g);
+    F = reinterpret_cast<const uint16_t*>(g + 16 * (((uint64_t)p.r >> p.sparse_shift) + 2));
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+    s = (uint32_t)p.sparse_shift;
+    mask = (1u << s) - 1u;
+  }
+  __device__ __forceinline__ uint32_t bucket(T z) const {
+    uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
+    return j < r ? j : r;
+  }
+  // X[t]: a shared-window load (no generic-address rematerialisation per
+  // query) or an L2 gather
+  __device__ __forceinline__ T xat(uint32_t t) const {
+    if constexpr (XS) {
+      T v;
+      if constexpr (sizeof(T) == 4) asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xs + 4u * t));
+      else asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(xs + 8u * t));
+      return v;
+    } else {
+      return __ldg(X + t);
+    }
+  }
+  // (t, knot) of bucket j from its group record g
+  __device__ __forceinline__ void resolve(uint4 g, uint32_t j, uint32_t& t, bool& knot) const {
+    constexpr uint32_t H = 0x80008000u;
+    const uint32_t jl = j & mask;
+    // (w + hm) & H: bit 15 / 31 set iff the low / high offset >= jl
+    // (offsets and jl < 2^15: no borrow crosses a half)
+    const uint32_t hm = H - jl * 0x10001u;
+    const uint32_t ge = __popc((g.y + hm) & H) + __popc((g.z + hm) & H) + __popc((g.w + hm) & H);
+    const uint32_t lt = kRecSlots - ge;
+    t = (g.x & ~kDenseFlag) + lt;
+    const uint32_t w = lt < 2 ? g.y : (lt < 4 ? g.z : g.w);
+    knot = lt < kRecSlots && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
+    if constexpr (OVF) {
+      if ((g.x & kDenseFlag) && lt == kRecSlots) {  // past the sixth knot of an overflowing super-bucket
+        uint32_t lo = t, hi = G[(j >> s) + 1].x & ~kDenseFlag;
+        const uint32_t end = hi;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (F[mid] < jl) lo = mid + 1;
+          else hi = mid;
+        }
+        t = lo;
+        knot = lo < end && F[lo] == jl;
+      }
+    }
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    const uint32_t j = bucket(z);
+    uint32_t t;
+    bool knot;
+    resolve(G[j >> s], j, t, knot);
+    T xv = z;
+    if (knot) xv = xat(t);
+    return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
+  }
+  // every record load of a group issued before the first is resolved
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    constexpr int GR = N < FSG_REC_GROUP ? N : FSG_REC_GROUP;  // live-register bound (4 regs per record)
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += GR) {
+      uint4 g[GR];
+      uint32_t j[GR];
+#pragma unroll
+      for (int q = 0; q < GR; ++q) {
+        if (g0 + q >= N) break;
+        j[q] = bucket(z[g0 + q]);
+        g[q] = G[j[q] >> s];
+      }
+#pragma unroll
+      for (int q = 0; q < GR; ++q) {
+        if (g0 + q >= N) break;
+        uint32_t t;
+        bool knot;
+        resolve(g[q], j[q], t, knot);
+        T xv = z[g0 + q];
+        if (knot) xv = xat(t);
+        o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
+      }
+    }
   }
 };
 
@@ -756,22 +868,35 @@ struct CompareProbe {
 // ---------------------------------------------------------------------------
 template <typename T> struct Vec4;
 template <> struct Vec4<float> {
+  static constexpr uint32_t kAlign = 16;
   float v[4];
   __device__ __forceinline__ void load(const float* p) {
     float4 a = ld_stream(reinterpret_cast<const float4*>(p));
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
   }
 };
+// f64 groups are one 32-B load (LDG.E.256; the head peel aligns them to
+// 32 B): two 16-B halves per lane would touch twice the L1 lines per
+// instruction (16 wavefronts per warp's 1 KB instead of 8; ncu on cfg2).
+#ifndef FSG_F64_LD256
+#define FSG_F64_LD256 1
+#endif
 template <> struct Vec4<double> {
+  static constexpr uint32_t kAlign = FSG_F64_LD256 ? 32 : 16;
   double v[4];
   __device__ __forceinline__ void load(const double* p) {
+#if FSG_F64_LD256
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+#else
     double2 a = ld_stream(reinterpret_cast<const double2*>(p));
     double2 b = ld_stream(reinterpret_cast<const double2*>(p) + 1);
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+#endif
   }
 };
 
-__device__ __forceinline__ void store4(int32_t* p, const int32_t (&o)[4], bool vec) {
+__device__ __forceinline__ void store4(int32_t* p, const int32_t (&o)[4], int vec) {
   if (vec) {
     st_stream(reinterpret_cast<int4*>(p), make_int4(o[0], o[1], o[2], o[3]));
   } else {
@@ -779,7 +904,20 @@ __device__ __forceinline__ void store4(int32_t* p, const int32_t (&o)[4], bool v
     for (int e = 0; e < 4; ++e) st_stream(p + e, o[e]);
   }
 }
-__device__ __forceinline__ void store4(int64_t* p, const int64_t (&o)[4], bool vec) {
+// int64 groups: one 32-B streaming store when the output is 32-B aligned
+// (vec == 2; half the L1 lines per instruction of two 16-B halves), else two
+// 16-B stores (vec == 1) or scalars
+#ifndef FSG_I64_ST256
+#define FSG_I64_ST256 1
+#endif
+__device__ __forceinline__ void store4(int64_t* p, const int64_t (&o)[4], int vec) {
+#if FSG_I64_ST256
+  if (vec == 2) {
+    asm volatile("st.global.cs.v4.s64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(o[0]), "l"(o[1]), "l"(o[2]), "l"(o[3])
+                 : "memory");
+    return;
+  }
+#endif
   if (vec) {
     st_stream(reinterpret_cast<longlong2*>(p), make_longlong2(o[0], o[1]));
     st_stream(reinterpret_cast<longlong2*>(p) + 1, make_longlong2(o[2], o[3]));
@@ -854,7 +992,7 @@ __device__ __forceinline__ void search_body(const T* __restrict__ z, OutT* __res
     const uint64_t tail0 = sh.head + 4 * sh.nvec;
     if (tid < sh.head) one(tid);
     if (tid < sh.m - tail0) one(tail0 + tid);
-    const bool vec_out = plan.out_vec_ok != 0;
+    const int vec_out = plan.out_vec_ok;
     const T* zv = z + sh.head;
     OutT* ov = out + sh.head;
     for (uint64_t g0 = tid; g0 < sh.nvec; g0 += stride * UNROLL) {

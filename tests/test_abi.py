@@ -82,6 +82,16 @@ def test_argument_validation_without_gpu():
         plan.sparse_shift, plan.sparse_ndense = shift, ndense
         assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
         assert b"sparse" in lib.fs_last_error()
+    # group records: shifts 5..14 only; unknown formats rejected
+    plan.sparse_format = _lib.SPARSE_RECORDS
+    for shift, novf in ((4, 0), (15, 0), (5, 40)):
+        plan.sparse_shift, plan.sparse_ndense = shift, novf
+        assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
+        assert b"sparse" in lib.fs_last_error()
+    plan.sparse_format, plan.sparse_shift, plan.sparse_ndense = 7, 8, 0
+    assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
+    assert b"sparse" in lib.fs_last_error()
+    assert lib.fs_sparse_rec_bytes(4, 1000, 15, 0) == 0 and lib.fs_sparse_rec_bytes(4, 1000, 5, 0) == 16 * 33
 
 
 def test_status_codes_map_to_reference_exceptions():

@@ -557,8 +557,15 @@ def test_sparse_table_with_dense_super_buckets(cuda):
     cluster = 0.5 + 1e-7 * np.arange(1, 201)
     xs = np.unique(np.concatenate([base[(base < 0.5) | (base > 0.5 + 1e-4)], cluster, [0.0, 1.0]]))
     p = fs.validate_partition(xs)
-    prep = fs.prepare("direct", p)
-    assert prep.placement()["smem_sparse"] and prep.plan.sparse_ndense > 0
+    from paper_1506_08620_b200 import batch
+
+    old = batch.SPARSE_FORMATS
+    try:
+        batch.SPARSE_FORMATS = ("two-level",)  # group records are tested in test_gpu_sparse_records.py
+        prep = fs.prepare("direct", p)
+    finally:
+        batch.SPARSE_FORMATS = old
+    assert prep.placement()["sparse_format"] == "two-level" and prep.plan.sparse_ndense > 0
     z = np.concatenate([orc.random_queries(xs, 300_000, seed=2), orc.boundary_probes(xs),
                         np.random.default_rng(3).uniform(0.5, 0.5 + 2.1e-5, 100_000)])
     z = z[(z >= xs[0]) & (z < xs[-1])]

@@ -3,7 +3,7 @@
 set -e
 cd "$(dirname "$0")/.."
 cp paper_1506_08620_b200/libfsgpu.so /tmp/libfsgpu_main.so
-for v in tools/variants/*.so; do
+for v in ${VARIANTS_DIR:-tools/variants}/*.so; do
   cp "$v" paper_1506_08620_b200/libfsgpu.so
   echo "== $v"
   python tools/tune.py "$@" | sed "s|^|$(basename $v) |"
