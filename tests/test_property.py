@@ -124,3 +124,23 @@ def test_gpu_big_tables_equal_oracle(cuda, xs):
         bad = np.flatnonzero(got != want)
         assert len(bad) == 0, (algo, len(xs), xs.dtype.name, int(len(bad)), int(bad[0]), float(z[bad[0]]),
                                int(got[bad[0]]), int(want[bad[0]]), prep.placement(), int(getattr(prep.structure, "r", 0)))
+    # each sparse layout forced on its own (group records also past the
+    # planner's slow-path bound): the same answers whenever it fits
+    from paper_1506_08620_b200 import batch
+
+    keep = batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM
+    try:
+        for fmt in (("records",), ("two-level",)):
+            batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = fmt, 10**6
+            try:
+                prep = fs.prepare("direct", p)
+            except fs.InfeasibleError:
+                break
+            if prep.placement()["sparse_format"] != fmt[0]:
+                continue
+            got = fs.run_batch(prep, z)
+            bad = np.flatnonzero(got != want)
+            assert len(bad) == 0, (fmt, len(xs), xs.dtype.name, int(len(bad)), int(bad[0]), prep.placement(),
+                                   prep.plan.sparse_shift, prep.plan.sparse_ndense)
+    finally:
+        batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = keep
