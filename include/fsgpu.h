@@ -79,7 +79,8 @@ enum {
 /* ---- layouts of fs_plan.sparse ---- */
 enum {
   FS_SPARSE_TWO_LEVEL = 0, /* C | F (| dense masks): fs_build_sparse                */
-  FS_SPARSE_RECORDS = 1    /* 16-B group records (| F): fs_build_sparse_rec         */
+  FS_SPARSE_RECORDS = 1,   /* 16-B group records, six offsets (| F): fs_build_sparse_rec */
+  FS_SPARSE_RECORDS8 = 2   /* 8-B group records, two offsets (| F): fs_build_sparse_rec  */
 };
 
 /*
@@ -128,7 +129,8 @@ typedef struct fs_plan {
   int32_t b2_deep_top;  /* ... built for this many staged top levels             */
   int32_t b2_deep_k;    /* ... levels per record (3 for f32, 2 for f64)           */
   int32_t sparse_format;/* layout of `sparse`: FS_SPARSE_TWO_LEVEL (fs_build_sparse)
-                           or FS_SPARSE_RECORDS (fs_build_sparse_rec)             */
+                           or FS_SPARSE_RECORDS / FS_SPARSE_RECORDS8
+                           (fs_build_sparse_rec)                                  */
 } fs_plan;
 
 /* Library identification. */
@@ -225,32 +227,34 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
 /*
  * Group records of the gap-1 table (a device layout of build_index,
  * direct.py:498-541; no reference counterpart), for R >> N.  The
- * super-buckets of fs_build_sparse, each packed into one 16-B record
- * {base | overflow flag (bit 31), six uint16 knot offsets}: base =
- * K[J 2^shift], the offsets f_i mod 2^shift of the super-bucket's first
- * min(count, 6) knots in ascending order, unused slots 0x7FFF.  The kernel
- * resolves K[j] = base + #{offsets < j mod 2^shift} from one shared-memory
- * load, and bucket j holds knot K[j] iff that offset slot equals
- * j mod 2^shift.  A super-bucket with more than six knots sets bit 31; its
- * later knots are searched in F (f_i mod 2^shift, uint16 per knot), which
- * follows the (r >> shift) + 2 records only when some record overflows.
- *   fs_sparse_rec_bytes: buffer size for (shift, novf overflowing records).
+ * super-buckets of fs_build_sparse, each packed into one record {base |
+ * overflow flag (bit 31), S uint16 knot offsets}: FS_SPARSE_RECORDS is 16 B
+ * with S = 6, FS_SPARSE_RECORDS8 is 8 B with S = 2.  base = K[J 2^shift], the
+ * offsets f_i mod 2^shift of the super-bucket's first min(count, S) knots in
+ * ascending order, unused slots 0x7FFF.  The kernel resolves
+ * K[j] = base + #{offsets < j mod 2^shift} from one shared-memory load, and
+ * bucket j holds knot K[j] iff that offset slot equals j mod 2^shift.  A
+ * super-bucket with more than S knots sets bit 31; its later knots are
+ * searched in F (f_i mod 2^shift, uint16 per knot), which follows the
+ * (r >> shift) + 2 records only when some record overflows.
+ *   fs_sparse_rec_bytes: buffer size for (format, shift, novf overflowing
+ *     records); 0 for an invalid format or shift.
  *   fs_plan_sparse_rec: the shift (5..14) whose layout (plus X when with_x)
- *     fits in budget_bytes and sends the fewest queries past a sixth knot
- *     (uniform queries; among shifts within 1e-3 of the best, the smallest
- *     table) -> shift, novf, bytes, and that fraction in parts per million.
- *     FS_TOO_LARGE if none fits.  SYNC.
+ *     fits in budget_bytes and sends the fewest queries past a record's last
+ *     offset (uniform queries; among shifts within 1e-3 of the best, the
+ *     smallest table) -> shift, novf, bytes, and that fraction in parts per
+ *     million.  FS_TOO_LARGE if none fits.  SYNC.
  *   fs_build_sparse_rec: fill the buffer (F too when novf > 0).  SYNC.
  * Set fs_plan.sparse to the buffer, sparse_shift to the shift,
- * sparse_ndense to novf and sparse_format to FS_SPARSE_RECORDS.
+ * sparse_ndense to novf and sparse_format to the format.
  * f_scratch_dev: n1 uint64.
  */
-uint64_t fs_sparse_rec_bytes(uint64_t n1, uint64_t r, int32_t shift, uint64_t novf);
-int fs_plan_sparse_rec(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
-                       int32_t with_x, uint64_t* f_scratch_dev, int32_t* shift_out, uint64_t* novf_out,
-                       uint64_t* bytes_out, uint32_t* past_sixth_ppm_out, void* stream);
-int fs_build_sparse_rec(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t shift,
-                        uint64_t novf, uint64_t* f_scratch_dev, void* buf_dev, void* stream);
+uint64_t fs_sparse_rec_bytes(int32_t format, uint64_t n1, uint64_t r, int32_t shift, uint64_t novf);
+int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
+                       uint64_t budget_bytes, int32_t with_x, uint64_t* f_scratch_dev, int32_t* shift_out,
+                       uint64_t* novf_out, uint64_t* bytes_out, uint32_t* past_last_ppm_out, void* stream);
+int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
+                        int32_t shift, uint64_t novf, uint64_t* f_scratch_dev, void* buf_dev, void* stream);
 
 /*
  * Hot window of a rank directory for shared-memory staging: among all

@@ -56,6 +56,7 @@ PLACE_SMEM_HOT = 8
 PLACE_SMEM_SPARSE = 16
 SPARSE_TWO_LEVEL = 0
 SPARSE_RECORDS = 1
+SPARSE_RECORDS8 = 2
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (
@@ -159,12 +160,12 @@ def _declare(lib):
     lib.fs_build_sparse.restype = ctypes.c_int
     lib.fs_build_sparse.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp]
     lib.fs_sparse_rec_bytes.restype = ctypes.c_uint64
-    lib.fs_sparse_rec_bytes.argtypes = [_u64, _u64, _i32, _u64]
+    lib.fs_sparse_rec_bytes.argtypes = [_i32, _u64, _u64, _i32, _u64]
     lib.fs_plan_sparse_rec.restype = ctypes.c_int
-    lib.fs_plan_sparse_rec.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _u64, _i32, _vp, _p_i32, _p_u64,
-                                       _p_u64, _p_u32, _vp]
+    lib.fs_plan_sparse_rec.argtypes = [_i32, _i32, _vp, _u64, ctypes.c_double, _u64, _u64, _i32, _vp, _p_i32,
+                                       _p_u64, _p_u64, _p_u32, _vp]
     lib.fs_build_sparse_rec.restype = ctypes.c_int
-    lib.fs_build_sparse_rec.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _u64, _vp, _vp, _vp]
+    lib.fs_build_sparse_rec.argtypes = [_i32, _i32, _vp, _u64, ctypes.c_double, _u64, _i32, _u64, _vp, _vp, _vp]
     lib.fs_build_hot_window.restype = ctypes.c_int
     lib.fs_build_hot_window.argtypes = [_i32, _vp, _u64, _u64, _vp, _p_u64, _p_u64, _p_u64, _p_u64, _p_u64, _vp]
     lib.fs_build_fused.restype = ctypes.c_int

@@ -240,8 +240,8 @@ class PreparedKernel:
             "smem_top": bool(f & _lib.PLACE_SMEM_TOP),
             "smem_hot": bool(f & _lib.PLACE_SMEM_HOT),
             "smem_sparse": bool(f & _lib.PLACE_SMEM_SPARSE),
-            "sparse_format": ("records" if self.plan.sparse_format == _lib.SPARSE_RECORDS else "two-level")
-            if f & _lib.PLACE_SMEM_SPARSE else None,
+            "sparse_format": {_lib.SPARSE_RECORDS: "records", _lib.SPARSE_RECORDS8: "records8"}.get(
+                self.plan.sparse_format, "two-level") if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
         }
 
@@ -364,9 +364,12 @@ SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = 20_000
 #: per super-bucket 342 -> 413 G queries/s with records, cfg5 N+1 = 32769 at
 #: 0.84: 336 -> 368; cfg5 N+1 = 1025 at 0.03 stays two-level, 484 vs 446)
 SPARSE_RECORDS_MIN_LOAD = 0.2
+#: 8-B group records (two offsets) are used when at most this share of
+#: uniform queries (ppm) falls past a record's second knot
+SPARSE_RECORDS8_MAX_PAST_PPM = 5_000
 #: sparse layouts allowed; a tuning run or test may narrow it to one
-#: (a leading "records" also skips the load rule)
-SPARSE_FORMATS = ("two-level", "records")
+#: (a leading records format also skips the load rule)
+SPARSE_FORMATS = ("two-level", "records8", "records")
 
 #: hot-window staging budget: small enough that the L2-gather kernel keeps
 #: full occupancy (3-4 CTAs per SM) for the queries outside the window
@@ -423,37 +426,40 @@ def _set_b2_deep(plan, pp: PaddedPartition, keep: list) -> None:
     keep.append(buf)
 
 
-def _set_sparse_records(plan, p: SortedPartition, idx: DirectIndex, keep: list, f, budget: int) -> bool:
-    """Group records of K (fs_build_sparse_rec): one 16-B record per
-    super-bucket resolves K[j] with a single shared-memory load; used when
-    they fit and few queries fall past a sixth knot of a super-bucket."""
+def _set_sparse_records(plan, p: SortedPartition, idx: DirectIndex, keep: list, f, budget: int, name: str,
+                        with_x: tuple = (1, 0)) -> bool:
+    """Group records of K (fs_build_sparse_rec): one record per super-bucket
+    resolves K[j] with a single shared-memory load ("records8": 8 B, two knot
+    offsets; "records": 16 B, six).  Used when they fit and few uniform queries
+    fall past a record's last offset; X is staged beside them (with_x 1) or
+    read through L2 for the buckets holding a knot (with_x 0)."""
     lib = _lib.load()
     dt = fs_dtype(p.precision)
     n1 = len(p.values)
     x = p.device_values()
-    shift, novf, nbytes, ppm = ctypes.c_int32(-1), ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_uint32(0)
-    for with_x in (1, 0):  # X staged beside the records if possible, else X via L2
-        rc = lib.fs_plan_sparse_rec(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, with_x, f.data_ptr(),
+    fmt, max_ppm = {"records8": (_lib.SPARSE_RECORDS8, SPARSE_RECORDS8_MAX_PAST_PPM),
+                    "records": (_lib.SPARSE_RECORDS, SPARSE_RECORDS_MAX_PAST_SIXTH_PPM)}[name]
+    for wx in with_x:
+        shift, novf, nbytes, ppm = ctypes.c_int32(-1), ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_uint32(0)
+        rc = lib.fs_plan_sparse_rec(fmt, dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, wx, f.data_ptr(),
                                     ctypes.byref(shift), ctypes.byref(novf), ctypes.byref(nbytes), ctypes.byref(ppm),
                                     _device.stream_ptr())
-        if rc == _lib.FS_OK:
-            break
-        if rc != _lib.FS_TOO_LARGE:
-            _lib.check(rc, what="fs_plan_sparse_rec")
-    else:
-        return False
-    if ppm.value > SPARSE_RECORDS_MAX_PAST_SIXTH_PPM:
-        return False
-    buf = _device.empty(int(nbytes.value), np.uint8)
-    rc = lib.fs_build_sparse_rec(dt, x.data_ptr(), n1, float(idx.h), idx.r, shift.value, novf.value, f.data_ptr(),
-                                 buf.data_ptr(), _device.stream_ptr())
-    _lib.check(rc, what="fs_build_sparse_rec")
-    plan.sparse = buf.data_ptr()
-    plan.sparse_shift = shift.value
-    plan.sparse_ndense = novf.value
-    plan.sparse_format = _lib.SPARSE_RECORDS
-    keep.append(buf)
-    return True
+        if rc == _lib.FS_TOO_LARGE:
+            continue
+        _lib.check(rc, what="fs_plan_sparse_rec")
+        if ppm.value > max_ppm:
+            continue
+        buf = _device.empty(int(nbytes.value), np.uint8)
+        rc = lib.fs_build_sparse_rec(fmt, dt, x.data_ptr(), n1, float(idx.h), idx.r, shift.value, novf.value,
+                                     f.data_ptr(), buf.data_ptr(), _device.stream_ptr())
+        _lib.check(rc, what="fs_build_sparse_rec")
+        plan.sparse = buf.data_ptr()
+        plan.sparse_shift = shift.value
+        plan.sparse_ndense = novf.value
+        plan.sparse_format = fmt
+        keep.append(buf)
+        return True
+    return False
 
 
 def _plan_two_level(p: SortedPartition, idx: DirectIndex, f, budget: int):
@@ -477,20 +483,28 @@ def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) ->
     rank directory does not; the kernel picks it over L2 gathers when the
     directory (plus X) cannot be staged.  Two layouts: the two-level table
     (fs_build_sparse; a short search per query, cheapest when super-buckets
-    are nearly empty) and group records (fs_build_sparse_rec; one record
-    load plus fixed arithmetic per query).  Group records are used when the
-    two-level table's super-buckets would hold SPARSE_RECORDS_MIN_LOAD knots
-    or more on average, or it does not fit."""
+    are nearly empty) and group records (fs_build_sparse_rec; one 8-B or 16-B
+    record load plus fixed arithmetic per query).  Measured per config:
+    profiles/r01/tune_sparse_records.txt."""
     if idx.r >= (1 << 32) or len(p.values) >= (1 << 31):
         return
     lib = _lib.load()
     budget = _smem_budget() - 512
     n1 = len(p.values)
     f = _device.empty(n1, np.uint64)
+    # In order: 8-B records with X staged; the two-level table when its
+    # super-buckets are nearly empty; 16-B records with X; then 8-B and 16-B
+    # records with X read through L2 (fine for uniform queries, but streams
+    # with many exact-knot queries, like cfg2's 1%, lose: 433 -> 423).
+    def records(name, wx):
+        return name in SPARSE_FORMATS and _set_sparse_records(plan, p, idx, keep, f, budget, name, wx)
+
+    if records("records8", (1,)):
+        return
     two = _plan_two_level(p, idx, f, budget) if "two-level" in SPARSE_FORMATS else None
     load = n1 / ((idx.r >> two[0]) + 1) if two else None
-    if "records" in SPARSE_FORMATS and (load is None or load >= SPARSE_RECORDS_MIN_LOAD or SPARSE_FORMATS[0] == "records"):
-        if _set_sparse_records(plan, p, idx, keep, f, budget):
+    if load is None or load >= SPARSE_RECORDS_MIN_LOAD:
+        if records("records", (1,)) or records("records8", (0,)) or records("records", (0,)):
             return
     if two is None:
         return

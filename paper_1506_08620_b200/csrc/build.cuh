@@ -249,34 +249,39 @@ __global__ void fill_sparse_kernel(const uint64_t* __restrict__ f, uint64_t n1, 
 }
 
 // Group records of the gap-1 table (fs_build_sparse_rec): the same
-// super-buckets as fill_sparse_kernel, each packed into one 16-B record
-// {base | overflow flag, six 16-bit knot offsets} so that one shared-memory
-// load resolves K[j] for super-buckets holding up to six knots.  base =
-// lower_bound(f, J 2^s) = K[J 2^s]; offsets are f_i mod 2^s of the first
-// min(count, 6) knots, ascending, unused slots kRecSentinel (> any j mod
-// 2^s for s <= kRecMaxShift).  A super-bucket with more than six knots sets
-// bit 31 of base; its further knots are found in F (f_i mod 2^s, u16 per
-// knot, written when F != NULL).  ng = (r >> s) + 2 records, the last has
-// base = n1 (the probe reads record J + 1 as the end of J's knots).
+// super-buckets as fill_sparse_kernel, each packed into one record {base |
+// overflow flag, SLOTS 16-bit knot offsets} (16 B with six slots, 8 B with
+// two) so that one shared-memory load resolves K[j] for super-buckets
+// holding up to SLOTS knots.  base = lower_bound(f, J 2^s) = K[J 2^s];
+// offsets are f_i mod 2^s of the first min(count, SLOTS) knots, ascending,
+// unused slots kRecSentinel (> any j mod 2^s for s <= kRecMaxShift).  A
+// super-bucket with more knots sets bit 31 of base; its further knots are
+// found in F (f_i mod 2^s, u16 per knot, written when F != NULL).  ng =
+// (r >> s) + 2 records, the last has base = n1 (the probe reads record J + 1
+// as the end of J's knots).
+template <int SLOTS>
 __global__ void fill_sparse_rec_kernel(const uint64_t* __restrict__ f, uint64_t n1, uint64_t r, int s,
-                                       uint4* __restrict__ G, uint16_t* __restrict__ F) {
+                                       typename RecWord<SLOTS>::type* __restrict__ G, uint16_t* __restrict__ F) {
   const uint64_t ng = (r >> s) + 2;
   const uint64_t mask = (1ull << s) - 1;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ng || i < n1;
        i += (uint64_t)gridDim.x * blockDim.x) {
     if (i < ng) {
       const uint64_t lo = i == ng - 1 ? n1 : bound_search<false>(f, 0, n1, i << s);
-      uint32_t off[kRecSlots];
+      uint32_t off[SLOTS];
       uint64_t k = 0;
-      for (; k < kRecSlots && lo + k < n1; ++k) {
+      for (; k < SLOTS && lo + k < n1; ++k) {
         const uint64_t fi = __ldg(f + lo + k);
         if ((fi >> s) != i) break;
         off[k] = (uint32_t)(fi & mask);
       }
-      for (uint64_t e = k; e < kRecSlots; ++e) off[e] = kRecSentinel;
-      const bool ovf = k == kRecSlots && lo + k < n1 && (__ldg(f + lo + k) >> s) == i;
-      G[i] = make_uint4((uint32_t)lo | (ovf ? kDenseFlag : 0u), off[0] | (off[1] << 16), off[2] | (off[3] << 16),
-                        off[4] | (off[5] << 16));
+      for (uint64_t e = k; e < SLOTS; ++e) off[e] = kRecSentinel;
+      const bool ovf = k == SLOTS && lo + k < n1 && (__ldg(f + lo + k) >> s) == i;
+      const uint32_t b = (uint32_t)lo | (ovf ? kDenseFlag : 0u);
+      if constexpr (SLOTS == 6)
+        G[i] = make_uint4(b, off[0] | (off[1] << 16), off[2] | (off[3] << 16), off[4] | (off[5] << 16));
+      else
+        G[i] = make_uint2(b, off[0] | (off[1] << 16));
     }
     if (F && i < n1) F[i] = (uint16_t)(__ldg(f + i) & mask);
   }

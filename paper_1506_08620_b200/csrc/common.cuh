@@ -18,10 +18,13 @@ namespace fsg {
 constexpr uint32_t kDenseFlag = 0x80000000u;
 // Super-buckets holding more knots than this are stored densely.
 constexpr uint32_t kDenseOcc = 64;
-// Group records (fs_build_sparse_rec): knot offsets per 16-B record, the
-// value of an unused offset slot, and the largest super-bucket shift (its
-// offsets stay below the sentinel and the 15-bit SWAR compare of the probe).
-constexpr uint32_t kRecSlots = 6;
+// Group records (fs_build_sparse_rec): knot offsets per record (16-B
+// records hold six, 8-B records two), the value of an unused offset slot, and
+// the largest super-bucket shift (its offsets stay below the sentinel and the
+// 15-bit SWAR compare of the probe).
+template <int SLOTS> struct RecWord;
+template <> struct RecWord<6> { using type = uint4; };
+template <> struct RecWord<2> { using type = uint2; };
 constexpr uint32_t kRecSentinel = 0x7FFFu;
 constexpr int kRecMaxShift = 14;
 

@@ -139,10 +139,11 @@ int validate_plan(const fs_plan* p) {
       if (p->hot_words && (p->hot_word0 > (p->r >> 5) + 1 || p->hot_words > (p->r >> 5) + 1 - p->hot_word0 ||
                            p->hot_knot0 > p->n1 || p->hot_knots > p->n1 - p->hot_knot0))
         return fail(FS_INVALID_ARG, "hot window outside the rank directory / knots");
-      if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS))
+      if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS &&
+                        p->sparse_format != FS_SPARSE_RECORDS8))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
       if (p->sparse && (p->sparse_shift < 5 ||
-                        p->sparse_shift > (p->sparse_format == FS_SPARSE_RECORDS ? kRecMaxShift : 16) ||
+                        p->sparse_shift > (p->sparse_format != FS_SPARSE_TWO_LEVEL ? kRecMaxShift : 16) ||
                         p->sparse_ndense > (p->r >> p->sparse_shift) + 2))
         return fail(FS_INVALID_ARG, "sparse table parameters out of range");
       break;
@@ -193,8 +194,8 @@ Placement place(const fs_plan* p) {
       p->sparse_shift >= 5 && p->sparse_shift <= 16) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
-    const uint64_t cfb = p->sparse_format == FS_SPARSE_RECORDS
-                             ? fs_sparse_rec_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense)
+    const uint64_t cfb = p->sparse_format != FS_SPARSE_TWO_LEVEL
+                             ? fs_sparse_rec_bytes(p->sparse_format, p->n1, p->r, p->sparse_shift, p->sparse_ndense)
                              : fs_sparse_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense);
     const bool rank_fits = use_rank && align128(xb) + dir_b <= budget;
     if (!rank_fits && cfb <= budget) {
@@ -402,8 +403,8 @@ template <bool DENSE>
 struct UnrollFor<double, SparseProbe<double, true, DENSE>> {
   static constexpr int value = FSG_UNROLL_F64_SMEM;
 };
-template <bool XS, bool OVF>
-struct UnrollFor<double, SparseRecProbe<double, XS, OVF>> {
+template <int SLOTS, bool XS, bool OVF>
+struct UnrollFor<double, SparseRecProbe<double, SLOTS, XS, OVF>> {
   static constexpr int value = FSG_UNROLL_F64_REC;
 };
 // Probes launched through the 1024-thread-bounded entry point: the sparse
@@ -419,8 +420,8 @@ template <typename T, bool DENSE>
 struct BoundedFor<T, SparseProbe<T, true, DENSE>> {
   static constexpr bool value = true;
 };
-template <typename T, bool XS, bool OVF>
-struct BoundedFor<T, SparseRecProbe<T, XS, OVF>> {
+template <typename T, int SLOTS, bool XS, bool OVF>
+struct BoundedFor<T, SparseRecProbe<T, SLOTS, XS, OVF>> {
   static constexpr bool value = FSG_REC_BOUNDED;
 };
 
@@ -565,6 +566,17 @@ int dispatch_direct(const DevPlan<T>& d, const Placement& pl, const T* z, uint64
   return launch_probe<T, OutT, DirectProbe<T, J, GAP, false, false>>(d, pl, z, m, out, fb, base, st);
 }
 
+template <typename T, typename OutT, int SLOTS>
+int dispatch_records(const DevPlan<T>& d, const Placement& pl, bool ovf, const T* z, uint64_t m, OutT* out,
+                     unsigned long long* fb, uint64_t base, cudaStream_t st) {
+  if (ovf) {
+    if (pl.xs) return launch_probe<T, OutT, SparseRecProbe<T, SLOTS, true, true>>(d, pl, z, m, out, fb, base, st);
+    return launch_probe<T, OutT, SparseRecProbe<T, SLOTS, false, true>>(d, pl, z, m, out, fb, base, st);
+  }
+  if (pl.xs) return launch_probe<T, OutT, SparseRecProbe<T, SLOTS, true, false>>(d, pl, z, m, out, fb, base, st);
+  return launch_probe<T, OutT, SparseRecProbe<T, SLOTS, false, false>>(d, pl, z, m, out, fb, base, st);
+}
+
 template <typename T, typename OutT, int ALGO>
 int dispatch_compare(const DevPlan<T>& d, const Placement& pl, const T* z, uint64_t m, OutT* out,
                      unsigned long long* fb, uint64_t base, cudaStream_t st) {
@@ -581,14 +593,10 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
     case FS_ALGO_DIRECT:
       if (pl.records) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
-      if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS) {
-        if (p->sparse_ndense) {
-          if (pl.xs) return launch_probe<T, OutT, SparseRecProbe<T, true, true>>(d, pl, z, m, out, fb, base, st);
-          return launch_probe<T, OutT, SparseRecProbe<T, false, true>>(d, pl, z, m, out, fb, base, st);
-        }
-        if (pl.xs) return launch_probe<T, OutT, SparseRecProbe<T, true, false>>(d, pl, z, m, out, fb, base, st);
-        return launch_probe<T, OutT, SparseRecProbe<T, false, false>>(d, pl, z, m, out, fb, base, st);
-      }
+      if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS)
+        return dispatch_records<T, OutT, 6>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
+      if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS8)
+        return dispatch_records<T, OutT, 2>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
       if (pl.sparse) {
         if (p->sparse_ndense) {
           if (pl.xs) return launch_probe<T, OutT, SparseProbe<T, true, true>>(d, pl, z, m, out, fb, base, st);
@@ -873,50 +881,53 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
   return FS_OK;
 }
 
-uint64_t fs_sparse_rec_bytes(uint64_t n1, uint64_t r, int32_t shift, uint64_t novf) {
+uint64_t fs_sparse_rec_bytes(int32_t format, uint64_t n1, uint64_t r, int32_t shift, uint64_t novf) {
   if (shift < 5 || shift > kRecMaxShift) return 0;
+  if (format != FS_SPARSE_RECORDS && format != FS_SPARSE_RECORDS8) return 0;
   const uint64_t ng = (r >> shift) + 2;
-  return (16 * ng + (novf ? 2 * n1 : 0) + 15) & ~15ull;
+  return ((format == FS_SPARSE_RECORDS ? 16 : 8) * ng + (novf ? 2 * n1 : 0) + 15) & ~15ull;
 }
 
-int fs_plan_sparse_rec(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
-                       int32_t with_x, uint64_t* f_scratch_dev, int32_t* shift_out, uint64_t* novf_out,
-                       uint64_t* bytes_out, uint32_t* past_sixth_ppm_out, void* stream) {
+int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
+                       uint64_t budget_bytes, int32_t with_x, uint64_t* f_scratch_dev, int32_t* shift_out,
+                       uint64_t* novf_out, uint64_t* bytes_out, uint32_t* past_last_ppm_out, void* stream) {
   if (!x_dev || !f_scratch_dev || n1 < 2 || !shift_out) return fail(FS_INVALID_ARG, "bad arguments");
+  if (format != FS_SPARSE_RECORDS && format != FS_SPARSE_RECORDS8) return fail(FS_INVALID_ARG, "not a record format");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "group records need R < 2^32, N < 2^31");
+  const uint64_t slots = format == FS_SPARSE_RECORDS ? 6 : 2;
   const uint64_t xb = with_x ? align128(n1 * (dtype == FS_F32 ? 4 : 8)) : 0;
-  if (xb + fs_sparse_rec_bytes(n1, r, kRecMaxShift, 0) > budget_bytes)
+  if (xb + fs_sparse_rec_bytes(format, n1, r, kRecMaxShift, 0) > budget_bytes)
     return fail(FS_TOO_LARGE, "no group-record layout fits the budget");
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
   if (rc) return rc;
   std::vector<uint64_t> f(n1);
   FS_CUDA(cudaMemcpyAsync(f.data(), f_scratch_dev, n1 * 8, cudaMemcpyDeviceToHost, as_stream(stream)));
   FS_CUDA(cudaStreamSynchronize(as_stream(stream)));
-  // per shift: overflowing records and the buckets lying past a sixth knot
-  // (the only ones whose queries leave the record); f is sorted
+  // per shift: overflowing records and the buckets lying past their last
+  // recorded knot (the only ones whose queries leave the record); f is sorted
   struct Cand {
     int s;
     uint64_t novf, past;
   };
   std::vector<Cand> cands;
   for (int s = 5; s <= kRecMaxShift; ++s) {
-    if (xb + fs_sparse_rec_bytes(n1, r, s, 0) > budget_bytes) continue;
+    if (xb + fs_sparse_rec_bytes(format, n1, r, s, 0) > budget_bytes) continue;
     uint64_t novf = 0, past = 0;
     for (uint64_t i = 0; i < n1;) {
       const uint64_t J = f[i] >> s;
       uint64_t e = i;
       while (e < n1 && (f[e] >> s) == J) ++e;
-      if (e - i > kRecSlots) {
+      if (e - i > slots) {
         ++novf;
         const uint64_t end = std::min(((J + 1) << s) - 1, r);  // last bucket of the super-bucket
-        past += end - f[i + kRecSlots - 1];
+        past += end - f[i + slots - 1];
       }
       i = e;
     }
-    if (xb + fs_sparse_rec_bytes(n1, r, s, novf) <= budget_bytes) cands.push_back({s, novf, past});
+    if (xb + fs_sparse_rec_bytes(format, n1, r, s, novf) <= budget_bytes) cands.push_back({s, novf, past});
   }
-  // the fewest queries past a sixth knot; among shifts within 1e-3 of that,
-  // the largest (smallest table)
+  // the fewest queries past a last recorded knot; among shifts within 1e-3
+  // of that, the largest (smallest table)
   uint64_t min_past = ~0ull;
   for (const Cand& c : cands) min_past = std::min(min_past, c.past);
   int best = -1;
@@ -930,23 +941,31 @@ int fs_plan_sparse_rec(int32_t dtype, const void* x_dev, uint64_t n1, double h, 
   if (best < 0) return fail(FS_TOO_LARGE, "no group-record layout fits the budget");
   *shift_out = best;
   if (novf_out) *novf_out = best_novf;
-  if (bytes_out) *bytes_out = fs_sparse_rec_bytes(n1, r, best, best_novf);
-  if (past_sixth_ppm_out) *past_sixth_ppm_out = (uint32_t)(1e6 * (double)best_past / (double)(r + 1));
+  if (bytes_out) *bytes_out = fs_sparse_rec_bytes(format, n1, r, best, best_novf);
+  if (past_last_ppm_out) *past_last_ppm_out = (uint32_t)(1e6 * (double)best_past / (double)(r + 1));
   return FS_OK;
 }
 
-int fs_build_sparse_rec(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t shift,
-                        uint64_t novf, uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
+int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
+                        int32_t shift, uint64_t novf, uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
   if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2 || shift < 5 || shift > kRecMaxShift)
     return fail(FS_INVALID_ARG, "bad arguments");
+  if (format != FS_SPARSE_RECORDS && format != FS_SPARSE_RECORDS8) return fail(FS_INVALID_ARG, "not a record format");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "group records need R < 2^32, N < 2^31");
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
   if (rc) return rc;
   cudaStream_t s = as_stream(stream);
   const uint64_t ng = (r >> shift) + 2;
-  uint4* G = static_cast<uint4*>(buf_dev);
-  uint16_t* F = novf ? reinterpret_cast<uint16_t*>(G + ng) : nullptr;
-  fill_sparse_rec_kernel<<<grid_1d(std::max(ng, n1), 256), 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
+  const int grid = grid_1d(std::max(ng, n1), 256);
+  if (format == FS_SPARSE_RECORDS) {
+    uint4* G = static_cast<uint4*>(buf_dev);
+    uint16_t* F = novf ? reinterpret_cast<uint16_t*>(G + ng) : nullptr;
+    fill_sparse_rec_kernel<6><<<grid, 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
+  } else {
+    uint2* G = static_cast<uint2*>(buf_dev);
+    uint16_t* F = novf ? reinterpret_cast<uint16_t*>(G + ng) : nullptr;
+    fill_sparse_rec_kernel<2><<<grid, 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
+  }
   FS_CUDA(cudaGetLastError());
   FS_CUDA(cudaStreamSynchronize(s));
   return FS_OK;

@@ -298,18 +298,20 @@ struct SparseProbe {
 };
 
 // Direct search (gap 1) over the group records of K (fill_sparse_rec_kernel),
-// staged in shared memory after X when X fits.  One 16-B LDS per query:
+// staged in shared memory after X when X fits.  One LDS per query (16-B
+// records with six offsets, or 8-B records with two):
 // t = K[j] = base + #{record offsets < j mod 2^s}, counted branch-free with
-// a 15-bit SWAR compare of the six packed offsets (sentinels never count);
+// a 15-bit SWAR compare of the packed offsets (sentinels never count);
 // bucket j holds knot t iff offset slot t - base equals j mod 2^s.  Only a
-// query in an overflowing super-bucket (more than six knots) whose bucket
-// lies past the sixth knot continues with a lower_bound over F (OVF).
+// query in an overflowing super-bucket (more than SLOTS knots) whose bucket
+// lies past its last recorded knot continues with a lower_bound over F (OVF).
 // Identical answers to DirectProbe<GAP=1> (batch.py:315-317).
-template <typename T, bool XS, bool OVF>
+template <typename T, int SLOTS, bool XS, bool OVF>
 struct SparseRecProbe {
+  using Rec = typename RecWord<SLOTS>::type;
   const T* X;
   uint32_t xs;  // shared-window address of X (XS)
-  const uint4* G;
+  const Rec* G;
   const uint16_t* F;
   T h, x0;
   uint32_t r, s, mask;
@@ -317,8 +319,8 @@ struct SparseRecProbe {
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
     xs = (uint32_t)__cvta_generic_to_shared(smem);
     unsigned char* g = smem + p.x_smem_bytes_aligned();
-    G = reinterpret_cast<const uint4*>(g);
-    F = reinterpret_cast<const uint16_t*>(g + 16 * (((uint64_t)p.r >> p.sparse_shift) + 2));
+    G = reinterpret_cast<const Rec*>(g);
+    F = reinterpret_cast<const uint16_t*>(g + sizeof(Rec) * (((uint64_t)p.r >> p.sparse_shift) + 2));
     h = p.h;
     x0 = p.x0;
     r = (uint32_t)p.r;
@@ -342,19 +344,26 @@ struct SparseRecProbe {
     }
   }
   // (t, knot) of bucket j from its group record g
-  __device__ __forceinline__ void resolve(uint4 g, uint32_t j, uint32_t& t, bool& knot) const {
+  __device__ __forceinline__ void resolve(Rec g, uint32_t j, uint32_t& t, bool& knot) const {
     constexpr uint32_t H = 0x80008000u;
     const uint32_t jl = j & mask;
     // (w + hm) & H: bit 15 / 31 set iff the low / high offset >= jl
     // (offsets and jl < 2^15: no borrow crosses a half)
     const uint32_t hm = H - jl * 0x10001u;
-    const uint32_t ge = __popc((g.y + hm) & H) + __popc((g.z + hm) & H) + __popc((g.w + hm) & H);
-    const uint32_t lt = kRecSlots - ge;
+    uint32_t ge, w;
+    if constexpr (SLOTS == 6) {
+      ge = __popc((g.y + hm) & H) + __popc((g.z + hm) & H) + __popc((g.w + hm) & H);
+      const uint32_t lt = SLOTS - ge;
+      w = lt < 2 ? g.y : (lt < 4 ? g.z : g.w);
+    } else {
+      ge = __popc((g.y + hm) & H);
+      w = g.y;
+    }
+    const uint32_t lt = SLOTS - ge;
     t = (g.x & ~kDenseFlag) + lt;
-    const uint32_t w = lt < 2 ? g.y : (lt < 4 ? g.z : g.w);
-    knot = lt < kRecSlots && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
+    knot = lt < SLOTS && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
     if constexpr (OVF) {
-      if ((g.x & kDenseFlag) && lt == kRecSlots) {  // past the sixth knot of an overflowing super-bucket
+      if ((g.x & kDenseFlag) && lt == SLOTS) {  // past the last recorded knot of an overflowing super-bucket
         uint32_t lo = t, hi = G[(j >> s) + 1].x & ~kDenseFlag;
         const uint32_t end = hi;
         while (lo < hi) {
@@ -379,10 +388,10 @@ struct SparseRecProbe {
   // every record load of a group issued before the first is resolved
   template <int N, typename R>
   __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
-    constexpr int GR = N < FSG_REC_GROUP ? N : FSG_REC_GROUP;  // live-register bound (4 regs per record)
+    constexpr int GR = N < FSG_REC_GROUP ? N : FSG_REC_GROUP;  // live-register bound (2-4 regs per record)
 #pragma unroll
     for (int g0 = 0; g0 < N; g0 += GR) {
-      uint4 g[GR];
+      Rec g[GR];
       uint32_t j[GR];
 #pragma unroll
       for (int q = 0; q < GR; ++q) {

@@ -91,7 +91,11 @@ def test_argument_validation_without_gpu():
     plan.sparse_format, plan.sparse_shift, plan.sparse_ndense = 7, 8, 0
     assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
     assert b"sparse" in lib.fs_last_error()
-    assert lib.fs_sparse_rec_bytes(4, 1000, 15, 0) == 0 and lib.fs_sparse_rec_bytes(4, 1000, 5, 0) == 16 * 33
+    rb = lib.fs_sparse_rec_bytes
+    assert rb(_lib.SPARSE_RECORDS, 4, 1000, 15, 0) == 0 and rb(_lib.SPARSE_RECORDS, 4, 1000, 5, 0) == 16 * 33
+    assert rb(_lib.SPARSE_RECORDS8, 4, 1000, 5, 0) == (8 * 33 + 15) // 16 * 16
+    assert rb(_lib.SPARSE_RECORDS8, 4, 1000, 5, 2) == (8 * 33 + 2 * 4 + 15) // 16 * 16
+    assert rb(_lib.SPARSE_TWO_LEVEL, 4, 1000, 5, 0) == 0 and rb(3, 4, 1000, 5, 0) == 0
 
 
 def test_status_codes_map_to_reference_exceptions():

@@ -15,8 +15,8 @@ from oracle import fs_oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-SLOTS = 6
 SENTINEL = 0x7FFF
+FORMATS = {"records": 6, "records8": 2}  # offset slots per record
 
 
 def _fs():
@@ -25,22 +25,27 @@ def _fs():
     return fs
 
 
-def expected_records(xs, h, r, s):
-    """uint32 (ng, 4): {base | overflow << 31, off0 | off1 << 16, ...}."""
+def _fmt_code(name):
+    from paper_1506_08620_b200 import _lib
+
+    return {"records": _lib.SPARSE_RECORDS, "records8": _lib.SPARSE_RECORDS8}[name]
+
+
+def expected_records(xs, h, r, s, slots=6):
+    """uint32 (ng, 1 + slots / 2): {base | overflow << 31, off0 | off1 << 16, ...}."""
     f = orc.knot_buckets(xs, h).astype(np.uint64)
     ng = (r >> s) + 2
     base = np.searchsorted(f, np.arange(ng, dtype=np.uint64) << np.uint64(s), side="left").astype(np.int64)
-    rec = np.zeros((ng, 4), dtype=np.uint32)
+    rec = np.zeros((ng, 1 + slots // 2), dtype=np.uint32)
     mask = (1 << s) - 1
     for J in range(ng):
         lo = int(base[J])
         hi = int(base[J + 1]) if J + 1 < ng else lo
-        offs = [int(f[i]) & mask for i in range(lo, min(hi, lo + SLOTS))]
-        offs += [SENTINEL] * (SLOTS - len(offs))
-        rec[J, 0] = lo | ((hi - lo > SLOTS) << 31)
-        rec[J, 1] = offs[0] | (offs[1] << 16)
-        rec[J, 2] = offs[2] | (offs[3] << 16)
-        rec[J, 3] = offs[4] | (offs[5] << 16)
+        offs = [int(f[i]) & mask for i in range(lo, min(hi, lo + slots))]
+        offs += [SENTINEL] * (slots - len(offs))
+        rec[J, 0] = lo | ((hi - lo > slots) << 31)
+        for w in range(slots // 2):
+            rec[J, 1 + w] = offs[2 * w] | (offs[2 * w + 1] << 16)
     return rec, f & np.uint64(mask)
 
 
@@ -48,28 +53,30 @@ def _buffer_of(prep, ptr):
     return next(b for b in prep.buffers if b.data_ptr() == ptr)
 
 
-def with_records(fs, p, prep, s):
-    """Rebuild prep's sparse table as group records with super-bucket shift s
-    (the caller keeps the returned buffer alive while the plan uses it)."""
+def with_records(fs, p, prep, s, fmt="records"):
+    """Rebuild prep's sparse table as group records (format fmt) with
+    super-bucket shift s (the caller keeps the returned buffer alive while the
+    plan uses it)."""
     from paper_1506_08620_b200 import _device, _lib
 
     idx = prep.structure
-    rec, _ = expected_records(p.values, idx.h, idx.r, s)
+    rec, _ = expected_records(p.values, idx.h, idx.r, s, FORMATS[fmt])
     novf = int(np.count_nonzero(rec[:, 0] >> 31))
     lib = _lib.load()
-    nbytes = int(lib.fs_sparse_rec_bytes(len(p.values), idx.r, s, novf))
+    code = _fmt_code(fmt)
+    nbytes = int(lib.fs_sparse_rec_bytes(code, len(p.values), idx.r, s, novf))
     buf = _device.empty(nbytes, np.uint8)
     f = _device.empty(len(p.values), np.uint64)
-    rc = lib.fs_build_sparse_rec(_lib.FS_F32 if p.precision == "single" else _lib.FS_F64, p.device_values().data_ptr(),
-                                 len(p.values), float(idx.h), idx.r, s, novf, f.data_ptr(), buf.data_ptr(),
-                                 _device.stream_ptr())
+    rc = lib.fs_build_sparse_rec(code, _lib.FS_F32 if p.precision == "single" else _lib.FS_F64,
+                                 p.device_values().data_ptr(), len(p.values), float(idx.h), idx.r, s, novf,
+                                 f.data_ptr(), buf.data_ptr(), _device.stream_ptr())
     _lib.check(rc)
     prep.plan.records = None
     prep.plan.rank = None  # records are used whenever they fit (a fitting directory would win otherwise)
     prep.plan.sparse = buf.data_ptr()
     prep.plan.sparse_shift = s
     prep.plan.sparse_ndense = novf
-    prep.plan.sparse_format = _lib.SPARSE_RECORDS
+    prep.plan.sparse_format = code
     return buf, rec, novf
 
 
@@ -95,37 +102,38 @@ def clustered_partition(seed, dtype=np.float64):
     return xs
 
 
-def _records_forced(fs, p):
+def _records_forced(fs, p, fmt="records"):
     from paper_1506_08620_b200 import batch
 
-    old = batch.SPARSE_FORMATS
+    old = batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, batch.SPARSE_RECORDS8_MAX_PAST_PPM
     try:
-        batch.SPARSE_FORMATS = ("records",)
+        batch.SPARSE_FORMATS = (fmt,)
+        batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = batch.SPARSE_RECORDS8_MAX_PAST_PPM = 10**6
         return fs.prepare("direct", p)
     finally:
-        batch.SPARSE_FORMATS = old
+        batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, batch.SPARSE_RECORDS8_MAX_PAST_PPM = old
 
 
 def test_records_chosen_for_sparse_configs(cuda):
-    """cfg2 (R = 24.8 M, N = 10^4; X staged too) and cfg5 N+1 = 32769 (X via
-    L2, overflowing records): group records chosen, the buffer equals the
-    numpy construction, answers equal the oracle; cfg5 N+1 = 1025 (0.03 knots
-    per super-bucket) keeps the two-level table."""
+    """The planner's picks (profiles/r01/tune_sparse_records.txt): cfg2 seed 0
+    16-B records with X staged; cfg2 seed 1 (R = 398.6 M) 8-B records, X via
+    L2; cfg5 N+1 = 1025 8-B records with X; cfg5 N+1 = 32769 overflowing 16-B
+    records, X via L2.  The buffer equals the numpy construction, answers
+    equal the oracle."""
     fs = _fs()
     from paper_1506_08620_b200 import workloads
 
-    p = workloads.knots("cfg5", n1=1025)
-    assert fs.prepare("direct", p).placement()["sparse_format"] == "two-level"
-    for name, kw in (("cfg2", {}), ("cfg5", {"n1": 32769})):
+    for name, kw, fmt, sx in (("cfg2", {}, "records", True), ("cfg2", {"seed": 1}, "records8", False),
+                              ("cfg5", {"n1": 1025}, "records8", True), ("cfg5", {"n1": 32769}, "records", False)):
         p = workloads.knots(name, **kw)
         prep = fs.prepare("direct", p)
         pl = prep.placement()
-        assert pl["smem_sparse"] and pl["sparse_format"] == "records", (name, pl)
+        assert pl["smem_sparse"] and pl["sparse_format"] == fmt and pl["smem_x"] == sx, (name, kw, pl)
         idx = prep.structure
         s = prep.plan.sparse_shift
-        rec, fmod = expected_records(p.values, idx.h, idx.r, s)
+        rec, fmod = expected_records(p.values, idx.h, idx.r, s, FORMATS[fmt])
         buf = _buffer_of(prep, prep.plan.sparse).cpu().numpy()
-        assert np.array_equal(buf[: rec.nbytes].view(np.uint32).reshape(-1, 4), rec), name
+        assert np.array_equal(buf[: rec.nbytes].view(np.uint32).reshape(rec.shape), rec), name
         novf = int(np.count_nonzero(rec[:, 0] >> 31))
         assert prep.plan.sparse_ndense == novf
         if novf:
@@ -133,16 +141,18 @@ def test_records_chosen_for_sparse_configs(cuda):
         z = np.concatenate([_probe_set(p.values, idx.h, idx.r, 400_000, seed=3),
                             workloads.queries_host(name, p, 200_000, seed=5)])
         want = orc.rank_oracle(p.values, z)
-        assert np.array_equal(fs.run_batch(prep, z), want), name
+        assert np.array_equal(fs.run_batch(prep, z), want), (name, kw)
         out32 = np.empty(len(z), dtype=np.int32)
         fs.batch_search(fs.LaneConfig(1, "direct", prep), z, out32)
-        assert np.array_equal(out32, want), name
+        assert np.array_equal(out32, want), (name, kw)
+        del prep
 
 
+@pytest.mark.parametrize("fmt", sorted(FORMATS))
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_records_every_shift_with_overflow(cuda, dtype):
-    """Clusters of 1..12 knots: records with 0..6 knots and overflowing
-    records at every shift 5..14; buffer bit-exact, answers exact."""
+def test_records_every_shift_with_overflow(cuda, dtype, fmt):
+    """Clusters of 1..12 knots: records holding 0..slots knots and
+    overflowing records at every shift 5..14; buffer bit-exact, answers exact."""
     fs = _fs()
     xs = clustered_partition(7, dtype)
     p = fs.validate_partition(xs)
@@ -154,22 +164,22 @@ def test_records_every_shift_with_overflow(cuda, dtype):
                            (xs[:-1] + (xs[1:] - xs[:-1]) * 0.5).astype(xs.dtype)])
     z = np.concatenate([z, near[(near >= xs[0]) & (near < xs[-1])]]).astype(xs.dtype)
     want = orc.rank_oracle(xs, z)
-    seen_ovf = False
     assert idx.r < 230_000
+    seen_ovf = False
     for s in range(5, 15):
-        buf, rec, novf = with_records(fs, p, prep, s)
+        buf, rec, novf = with_records(fs, p, prep, s, fmt)
         seen_ovf |= novf > 0
-        got = buf.cpu().numpy()[: rec.nbytes].view(np.uint32).reshape(-1, 4)
+        got = buf.cpu().numpy()[: rec.nbytes].view(np.uint32).reshape(rec.shape)
         assert np.array_equal(got, rec), s
-        assert prep.placement()["sparse_format"] == "records"
+        assert prep.placement()["sparse_format"] == fmt
         assert np.array_equal(fs.run_batch(prep, z), want), s
     assert seen_ovf
 
 
 def test_records_overflow_chosen_by_planner(cuda):
-    """A tight 200-knot cluster in a sparse layout: group records (forced;
-    few queries fall past a sixth knot) with overflowing records, and the
-    two-level table the planner picks gives the same answers."""
+    """A tight 200-knot cluster in a sparse layout: group records of either
+    width (forced) with overflowing records, and the layout the planner picks,
+    give the oracle's answers."""
     fs = _fs()
 
     rng = np.random.default_rng(17)
@@ -178,19 +188,21 @@ def test_records_overflow_chosen_by_planner(cuda):
     cluster = 0.5 + 1e-7 * np.arange(1, 201)
     xs = np.unique(np.concatenate([base[(base < 0.5) | (base > 0.5 + 1e-4)], cluster, [0.0, 1.0]]))
     p = fs.validate_partition(xs)
-    prep = _records_forced(fs, p)
-    assert prep.placement()["sparse_format"] == "records" and prep.plan.sparse_ndense > 0
     z = np.concatenate([orc.random_queries(xs, 300_000, seed=2), orc.boundary_probes(xs),
                         np.random.default_rng(3).uniform(0.5, 0.5 + 2.1e-5, 100_000)])
     z = z[(z >= xs[0]) & (z < xs[-1])]
     want = orc.rank_oracle(xs, z)
-    assert np.array_equal(fs.run_batch(prep, z), want)
+    for fmt in FORMATS:
+        prep = _records_forced(fs, p, fmt)
+        assert prep.placement()["sparse_format"] == fmt and prep.plan.sparse_ndense > 0
+        assert np.array_equal(fs.run_batch(prep, z), want), fmt
     prep2 = fs.prepare("direct", p)
-    assert prep2.placement()["sparse_format"] == "two-level"
+    assert prep2.placement()["smem_sparse"]
     assert np.array_equal(fs.run_batch(prep2, z), want)
 
 
-def test_records_out_of_domain_and_last_bucket(cuda):
+@pytest.mark.parametrize("fmt", sorted(FORMATS))
+def test_records_out_of_domain_and_last_bucket(cuda, fmt):
     """Out-of-domain lanes (NaN, +-inf, below X0, at XN) clamp inside the
     records; the first bad position is reported; the last bucket R (the
     sentinel record after it is read by the overflow path) answers N-1."""
@@ -198,8 +210,8 @@ def test_records_out_of_domain_and_last_bucket(cuda):
     from paper_1506_08620_b200 import workloads
 
     p = workloads.knots("cfg5", n1=1025)
-    prep = _records_forced(fs, p)
-    assert prep.placement()["sparse_format"] == "records"
+    prep = _records_forced(fs, p, fmt)
+    assert prep.placement()["sparse_format"] == fmt
     xs = p.values
     top = np.nextafter(xs[-1], -np.inf)
     z = np.array([xs[0], top, xs[-2], np.nextafter(xs[-2], -np.inf)], dtype=xs.dtype)
@@ -221,7 +233,7 @@ def test_records_abi_validation(cuda):
     p = workloads.knots("cfg5", n1=1025)
     prep = _records_forced(fs, p)
     z = orc.random_queries(p.values, 1000, seed=1)
-    for fmt, shift in ((2, prep.plan.sparse_shift), (_lib.SPARSE_RECORDS, 15)):
+    for fmt, shift in ((3, prep.plan.sparse_shift), (_lib.SPARSE_RECORDS, 15)):
         keep = (prep.plan.sparse_format, prep.plan.sparse_shift)
         prep.plan.sparse_format, prep.plan.sparse_shift = fmt, shift
         with pytest.raises(ValueError):
@@ -229,6 +241,8 @@ def test_records_abi_validation(cuda):
         prep.plan.sparse_format, prep.plan.sparse_shift = keep
     assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(p.values, z))
     lib = _lib.load()
-    assert lib.fs_sparse_rec_bytes(1025, 1 << 20, 15, 0) == 0
-    assert lib.fs_sparse_rec_bytes(1025, 1 << 20, 10, 0) == 16 * ((1 << 10) + 2)
-    assert lib.fs_sparse_rec_bytes(1025, 1 << 20, 10, 3) == (16 * ((1 << 10) + 2) + 2 * 1025 + 15) // 16 * 16
+    rb = lib.fs_sparse_rec_bytes
+    assert rb(_lib.SPARSE_RECORDS, 1025, 1 << 20, 15, 0) == 0
+    assert rb(_lib.SPARSE_RECORDS, 1025, 1 << 20, 10, 0) == 16 * ((1 << 10) + 2)
+    assert rb(_lib.SPARSE_RECORDS, 1025, 1 << 20, 10, 3) == (16 * ((1 << 10) + 2) + 2 * 1025 + 15) // 16 * 16
+    assert rb(_lib.SPARSE_RECORDS8, 1025, 1 << 20, 10, 3) == (8 * ((1 << 10) + 2) + 2 * 1025 + 15) // 16 * 16

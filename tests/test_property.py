@@ -128,10 +128,11 @@ def test_gpu_big_tables_equal_oracle(cuda, xs):
     # planner's slow-path bound): the same answers whenever it fits
     from paper_1506_08620_b200 import batch
 
-    keep = batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM
+    keep = batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, batch.SPARSE_RECORDS8_MAX_PAST_PPM
     try:
-        for fmt in (("records",), ("two-level",)):
-            batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = fmt, 10**6
+        for fmt in (("records",), ("records8",), ("two-level",)):
+            batch.SPARSE_FORMATS = fmt
+            batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = batch.SPARSE_RECORDS8_MAX_PAST_PPM = 10**6
             try:
                 prep = fs.prepare("direct", p)
             except fs.InfeasibleError:
@@ -143,4 +144,4 @@ def test_gpu_big_tables_equal_oracle(cuda, xs):
             assert len(bad) == 0, (fmt, len(xs), xs.dtype.name, int(len(bad)), int(bad[0]), prep.placement(),
                                    prep.plan.sparse_shift, prep.plan.sparse_ndense)
     finally:
-        batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = keep
+        batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, batch.SPARSE_RECORDS8_MAX_PAST_PPM = keep

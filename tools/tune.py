@@ -7,8 +7,8 @@ resident queries and prints one JSON line per variant.
 Config specs: cfgN (BASELINE recipes), cfg5:<N+1>, cfg2:<seed>, cfg5u (the
 unfiltered cfg5 draw, bitset2 fall-back instance), big32:<N+1> (sorted f32
 U[0,1) knots).  Layout variants: direct-k (plain K), direct-rank (rank
-directory only), direct-hot (hot window), direct-sparse2 / direct-rec (two-level sparse table / group records
-forced), bitset2-flat (no subtree records),
+directory only), direct-hot (hot window), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
+records forced), bitset2-flat (no subtree records),
 direct-gap2-k (gap 2 over plain K).
 """
 
@@ -101,17 +101,18 @@ def main():
             try:
                 base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct",
                         "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
-                if algo in ("direct-sparse2", "direct-rec"):  # force one sparse-table format
+                if algo in ("direct-sparse2", "direct-rec", "direct-rec8"):  # force one sparse-table format
                     from paper_1506_08620_b200 import batch as _b
 
-                    keep_fmt = _b.SPARSE_FORMATS
-                    _b.SPARSE_FORMATS = ("two-level",) if algo == "direct-sparse2" else ("records",)
-                    _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, keep_ppm = 10**6, _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM
+                    keep = (_b.SPARSE_FORMATS, _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, _b.SPARSE_RECORDS8_MAX_PAST_PPM)
+                    _b.SPARSE_FORMATS = {"direct-sparse2": ("two-level",), "direct-rec": ("records",),
+                                         "direct-rec8": ("records8",)}[algo]
+                    _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = _b.SPARSE_RECORDS8_MAX_PAST_PPM = 10**6
                     try:
                         prep = fs.prepare("direct", p)
                     finally:
-                        _b.SPARSE_FORMATS = keep_fmt
-                        _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = keep_ppm
+                        (_b.SPARSE_FORMATS, _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM,
+                         _b.SPARSE_RECORDS8_MAX_PAST_PPM) = keep
                 else:
                     prep = fs.prepare(base, p)
                 if algo == "direct-k":  # plain K table instead of rank directory / records
