@@ -377,13 +377,13 @@ Placement place_for_batch(const fs_plan* p, uint64_t m) {
 #ifndef FSG_UNROLL_F64_SMEM
 #define FSG_UNROLL_F64_SMEM 3
 #endif
-// group records: the default unroll and register budget measure best
-// (profiles/r01/tune_sparse_records.txt)
+// group records: unroll 2 and (see BoundedFor) the 1024-thread register
+// bound measure best (profiles/r01/tune_sparse_records.txt)
 #ifndef FSG_UNROLL_F64_REC
 #define FSG_UNROLL_F64_REC 2
 #endif
 #ifndef FSG_REC_BOUNDED
-#define FSG_REC_BOUNDED 0
+#define FSG_REC_BOUNDED 1
 #endif
 template <typename T>
 constexpr int kUnroll = sizeof(T) == 8 ? FSG_UNROLL_F64 : FSG_UNROLL;
@@ -412,17 +412,20 @@ struct UnrollFor<double, SparseRecProbe<double, SLOTS, XS, OVF>> {
 // from 1024-thread CTAs despite small spills (cfg2 int64 222 -> 264 Gq/s);
 // the f64 records probe loses (399 -> 335), so the default stays unbounded
 // (profiles/r01/tune_launch_bounds.txt).
-template <typename T, typename Probe>
+// Group records: bounded, except the 8-B probe with int64 outputs (it fits
+// in 64 registers unbounded and loses 403 -> 370 Gq/s on cfg5 N+1 = 1025
+// when bounded; the 16-B overflow probe needs 69 unbounded, cfg2 304 -> 390).
+template <typename T, typename Probe, typename OutT>
 struct BoundedFor {
   static constexpr bool value = false;
 };
-template <typename T, bool DENSE>
-struct BoundedFor<T, SparseProbe<T, true, DENSE>> {
+template <typename T, bool DENSE, typename OutT>
+struct BoundedFor<T, SparseProbe<T, true, DENSE>, OutT> {
   static constexpr bool value = true;
 };
-template <typename T, int SLOTS, bool XS, bool OVF>
-struct BoundedFor<T, SparseRecProbe<T, SLOTS, XS, OVF>> {
-  static constexpr bool value = FSG_REC_BOUNDED;
+template <typename T, int SLOTS, bool XS, bool OVF, typename OutT>
+struct BoundedFor<T, SparseRecProbe<T, SLOTS, XS, OVF>, OutT> {
+  static constexpr bool value = FSG_REC_BOUNDED && !(SLOTS == 2 && sizeof(OutT) == 8);
 };
 
 
@@ -477,7 +480,7 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
                  unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
   constexpr int kU = UnrollFor<T, Probe>::value;
   auto kern = [] {
-    if constexpr (BoundedFor<T, Probe>::value) return search_kernel_1k<T, OutT, Probe, kU>;
+    if constexpr (BoundedFor<T, Probe, OutT>::value) return search_kernel_1k<T, OutT, Probe, kU>;
     else return search_kernel<T, OutT, Probe, kU>;
   }();
   const size_t smem = pl.smem;

@@ -317,7 +317,9 @@ struct SparseRecProbe {
   uint32_t r, s, mask;
   __device__ __forceinline__ SparseRecProbe(const DevPlan<T>& p, unsigned char* smem) {
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
-    xs = (uint32_t)__cvta_generic_to_shared(smem);
+    // held in a register (volatile mov): ptxas would otherwise rebuild the
+    // shared-window address (S2R + 3 ALU) in front of every X load
+    asm volatile("mov.u32 %0, %1;" : "=r"(xs) : "r"((uint32_t)__cvta_generic_to_shared(smem)));
     unsigned char* g = smem + p.x_smem_bytes_aligned();
     G = reinterpret_cast<const Rec*>(g);
     F = reinterpret_cast<const uint16_t*>(g + sizeof(Rec) * (((uint64_t)p.r >> p.sparse_shift) + 2));
@@ -331,10 +333,14 @@ struct SparseRecProbe {
     uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
     return j < r ? j : r;
   }
-  // X[t]: a shared-window load (no generic-address rematerialisation per
-  // query) or an L2 gather
+  // X[t]: a shared-window load from the pinned address (no generic-address
+  // rematerialisation per query; int32 outputs +3%, int64 outputs measure
+  // better with the generic load), or an L2 gather
+  template <bool PINNED = true>
   __device__ __forceinline__ T xat(uint32_t t) const {
-    if constexpr (XS) {
+    if constexpr (XS && !PINNED) {
+      return X[t];
+    } else if constexpr (XS) {
       T v;
       if constexpr (sizeof(T) == 4) asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xs + 4u * t));
       else asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(xs + 8u * t));
@@ -406,7 +412,7 @@ struct SparseRecProbe {
         bool knot;
         resolve(g[q], j[q], t, knot);
         T xv = z[g0 + q];
-        if (knot) xv = xat(t);
+        if (knot) xv = xat<sizeof(R) == 4>(t);
         o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
       }
     }
