@@ -109,12 +109,16 @@ class ClockSampler:
                 self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
             except Exception:
                 pass
-            time.sleep(0.005)
+            self._first.set()
+            time.sleep(0.002)
 
     def __enter__(self):
         if self._nv is not None:
+            self._first = threading.Event()
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+            self._first.wait(5.0)  # the region starts once the sampler is running
+            self.samples.clear()  # (that first sample predates the region)
         return self
 
     def __exit__(self, *exc):
