@@ -391,6 +391,34 @@ constexpr int kUnroll = sizeof(T) == 8 ? FSG_UNROLL_F64 : FSG_UNROLL;
 // latency-light chains and take one more 4-query group in flight
 // (profiles/r01/tune_unroll_f64.txt: records +2.6%, sparse with X in smem
 // +3.6%; the L2-gathering and bitset2 probes lose with it).
+// Queries per vector group: 8 for f32 queries with int32 outputs (one 32-B
+// load and one 32-B store per group) when FSG_F32_VW8, else 4.
+#ifndef FSG_F32_VW8
+#define FSG_F32_VW8 1
+#endif
+template <typename T, typename OutT, typename Probe>
+struct VecWidthFor {
+  static constexpr int value = (FSG_F32_VW8 && sizeof(T) == 4 && sizeof(OutT) == 4) ? 8 : 4;
+};
+// 8-query groups in flight per thread: one for the smem-resident probes
+// (cfg3 direct 797 -> 832 Gq/s, the torch copy ceiling; two groups: 720),
+// two for the L2-gather rank directory and bitset2 (cfg4 347 -> 373,
+// bitset2 cfg3 364 -> 382); profiles/r01/tune_vw8.txt.
+#ifndef FSG_UNROLL_VW8
+#define FSG_UNROLL_VW8 1
+#endif
+template <typename Probe>
+struct UnrollVW8For {
+  static constexpr int value = FSG_UNROLL_VW8;
+};
+template <typename J, bool XS, bool DS>
+struct UnrollVW8For<RankProbe<float, J, XS, DS>> {
+  static constexpr int value = 2;
+};
+template <bool TOP, bool DEEP>
+struct UnrollVW8For<Bitset2Probe<float, TOP, DEEP>> {
+  static constexpr int value = 2;
+};
 template <typename T, typename Probe>
 struct UnrollFor {
   static constexpr int value = kUnroll<T>;
@@ -478,10 +506,11 @@ int launch_geometry(const void* fn, size_t smem, int mode, int* threads_out, int
 template <typename T, typename OutT, typename Probe>
 int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t m, OutT* out,
                  unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
-  constexpr int kU = UnrollFor<T, Probe>::value;
+  constexpr int VW = VecWidthFor<T, OutT, Probe>::value;
+  constexpr int kU = VW == 8 ? UnrollVW8For<Probe>::value : UnrollFor<T, Probe>::value;
   auto kern = [] {
-    if constexpr (BoundedFor<T, Probe, OutT>::value) return search_kernel_1k<T, OutT, Probe, kU>;
-    else return search_kernel<T, OutT, Probe, kU>;
+    if constexpr (BoundedFor<T, Probe, OutT>::value) return search_kernel_1k<T, OutT, Probe, kU, VW>;
+    else return search_kernel<T, OutT, Probe, kU, VW>;
   }();
   const size_t smem = pl.smem;
   // Kernels that stage tables in shared memory run best with ~1024 threads
@@ -502,17 +531,20 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
   sh.m = m;
   sh.base = base;
   const uintptr_t za = reinterpret_cast<uintptr_t>(z);
-  constexpr uint32_t va = Vec4<T>::kAlign;  // query groups start va-aligned
+  constexpr uint32_t va = VecLoad<T, VW>::kAlign;  // query groups start va-aligned
   uint64_t head = ((va - (za & (va - 1))) & (va - 1)) / sizeof(T);
   if (head > m) head = m;
   sh.head = head;
-  sh.nvec = (m - head) / 4;
+  sh.nvec = (m - head) / VW;
   DevPlan<T> d = dp;
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out) + head * sizeof(OutT);
   d.out_vec_ok = (oa & 15) ? 0 : (oa & 31) ? 1 : 2;
 
   const uint64_t full = (uint64_t)per_sm * sm_count();
-  uint64_t want = (sh.nvec + (uint64_t)threads * kU - 1) / ((uint64_t)threads * kU);
+  // one group per thread at least: a small batch spreads over every SM
+  // instead of filling a few CTAs kU groups deep (cfg1 bitset2 80 -> see
+  // profiles/r01/tune_vw8.txt)
+  uint64_t want = (sh.nvec + (uint64_t)threads - 1) / (uint64_t)threads;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(full, want));
 
   StageSeg s0{nullptr, pl.seg0_src, pl.seg0_bytes};

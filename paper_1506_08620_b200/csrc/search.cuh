@@ -881,13 +881,25 @@ struct CompareProbe {
 // ---------------------------------------------------------------------------
 // Streaming driver
 // ---------------------------------------------------------------------------
-template <typename T> struct Vec4;
-template <> struct Vec4<float> {
+// Query groups: VW consecutive queries per vector access.  VW = 4 (16-B f32
+// / 32-B f64 loads) everywhere; f32 queries with int32 outputs may use VW = 8
+// (one 32-B load and one 32-B store per group; FSG_F32_VW8).
+template <typename T, int VW> struct VecLoad;
+template <> struct VecLoad<float, 4> {
   static constexpr uint32_t kAlign = 16;
   float v[4];
   __device__ __forceinline__ void load(const float* p) {
     float4 a = ld_stream(reinterpret_cast<const float4*>(p));
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+};
+template <> struct VecLoad<float, 8> {
+  static constexpr uint32_t kAlign = 32;
+  float v[8];
+  __device__ __forceinline__ void load(const float* p) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
   }
 };
 // f64 groups are one 32-B load (LDG.E.256; the head peel aligns them to
@@ -896,7 +908,7 @@ template <> struct Vec4<float> {
 #ifndef FSG_F64_LD256
 #define FSG_F64_LD256 1
 #endif
-template <> struct Vec4<double> {
+template <> struct VecLoad<double, 4> {
   static constexpr uint32_t kAlign = FSG_F64_LD256 ? 32 : 16;
   double v[4];
   __device__ __forceinline__ void load(const double* p) {
@@ -911,12 +923,25 @@ template <> struct Vec4<double> {
   }
 };
 
-__device__ __forceinline__ void store4(int32_t* p, const int32_t (&o)[4], int vec) {
+// Output groups: vec = 2 when the group is 32-B aligned, 1 when 16-B
+// aligned, 0 otherwise (scalar stores).
+template <int VW>
+__device__ __forceinline__ void store_group(int32_t* p, const int32_t (&o)[VW], int vec) {
+  if constexpr (VW == 8) {
+    if (vec == 2) {
+      asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(o[0]), "r"(o[1]), "r"(o[2]),
+                   "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+                   : "memory");
+      return;
+    }
+  }
   if (vec) {
-    st_stream(reinterpret_cast<int4*>(p), make_int4(o[0], o[1], o[2], o[3]));
+#pragma unroll
+    for (int h = 0; h < VW; h += 4)
+      st_stream(reinterpret_cast<int4*>(p + h), make_int4(o[h], o[h + 1], o[h + 2], o[h + 3]));
   } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) st_stream(p + e, o[e]);
+    for (int e = 0; e < VW; ++e) st_stream(p + e, o[e]);
   }
 }
 // int64 groups: one 32-B streaming store when the output is 32-B aligned
@@ -925,7 +950,9 @@ __device__ __forceinline__ void store4(int32_t* p, const int32_t (&o)[4], int ve
 #ifndef FSG_I64_ST256
 #define FSG_I64_ST256 1
 #endif
-__device__ __forceinline__ void store4(int64_t* p, const int64_t (&o)[4], int vec) {
+template <int VW>
+__device__ __forceinline__ void store_group(int64_t* p, const int64_t (&o)[VW], int vec) {
+  static_assert(VW == 4, "int64 groups are 4 wide");
 #if FSG_I64_ST256
   if (vec == 2) {
     asm volatile("st.global.cs.v4.s64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(o[0]), "l"(o[1]), "l"(o[2]), "l"(o[3])
@@ -971,12 +998,12 @@ __device__ __forceinline__ void probe_batch(const P& p, const T (&z)[N], R (&o)[
 
 struct StreamShape {
   uint64_t m;      // total queries
-  uint64_t head;   // scalar queries before the first 16-B aligned group
-  uint64_t nvec;   // groups of 4 (vector path)
+  uint64_t head;   // scalar queries before the first aligned group
+  uint64_t nvec;   // groups of VW (vector path)
   uint64_t base;   // global position of z[0] (for first-bad reporting)
 };
 
-template <typename T, typename OutT, typename Probe, int UNROLL>
+template <typename T, typename OutT, typename Probe, int UNROLL, int VW>
 __device__ __forceinline__ void search_body(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh,
                                             DevPlan<T> plan, unsigned long long* __restrict__ status, int merge,
                                             StageSeg seg0, StageSeg seg1, int nseg) {
@@ -1003,46 +1030,52 @@ __device__ __forceinline__ void search_body(const T* __restrict__ z, OutT* __res
   };
 
   {
-    // scalar head (< 4 queries) and tail (< 4 queries)
-    const uint64_t tail0 = sh.head + 4 * sh.nvec;
+    // scalar head (< VW queries) and tail (< VW queries)
+    const uint64_t tail0 = sh.head + VW * sh.nvec;
     if (tid < sh.head) one(tid);
     if (tid < sh.m - tail0) one(tail0 + tid);
     const int vec_out = plan.out_vec_ok;
     const T* zv = z + sh.head;
     OutT* ov = out + sh.head;
     for (uint64_t g0 = tid; g0 < sh.nvec; g0 += stride * UNROLL) {
-      T zz[UNROLL * 4];
+      T zz[UNROLL * VW];
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const uint64_t g = g0 + u * stride;
-        Vec4<T> b;
-        if (g < sh.nvec) b.load(zv + 4 * g);
-        else b.v[0] = b.v[1] = b.v[2] = b.v[3] = x0;
+        VecLoad<T, VW> b;
+        if (g < sh.nvec) {
+          b.load(zv + VW * g);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) zz[4 * u + e] = b.v[e];
+          for (int e = 0; e < VW; ++e) b.v[e] = x0;
+        }
+#pragma unroll
+        for (int e = 0; e < VW; ++e) zz[VW * u + e] = b.v[e];
       }
       // results in the output's width: int32 halves the live registers
       using R = std::conditional_t<sizeof(OutT) == 4, int32_t, int64_t>;
-      R o[UNROLL * 4];
-      probe_batch<Probe, T, R, UNROLL * 4>(probe, zz, o);
+      R o[UNROLL * VW];
+      probe_batch<Probe, T, R, UNROLL * VW>(probe, zz, o);
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const uint64_t g = g0 + u * stride;
         if (g < sh.nvec) {
-          // domain check: a 4-bit mask per group; the position is formed and
+          // domain check: a VW-bit mask per group; the position is formed and
           // min-merged only for a group holding a bad query (rare)
           uint32_t badmask = 0;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const T v = zz[4 * u + e];
+          for (int e = 0; e < VW; ++e) {
+            const T v = zz[VW * u + e];
             badmask |= (uint32_t)!(v >= x0 && v < xn) << e;
           }
           if (badmask) {
-            const uint64_t pos = sh.head + 4 * g + (uint32_t)__ffs(badmask) - 1;
+            const uint64_t pos = sh.head + VW * g + (uint32_t)__ffs(badmask) - 1;
             if (pos < mybad) mybad = pos;
           }
-          const R ou[4] = {o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]};
-          store4(ov + 4 * g, ou, vec_out);
+          R ou[VW];
+#pragma unroll
+          for (int e = 0; e < VW; ++e) ou[e] = o[VW * u + e];
+          store_group<VW>(ov + VW * g, ou, vec_out);
         }
       }
     }
@@ -1054,17 +1087,17 @@ __device__ __forceinline__ void search_body(const T* __restrict__ z, OutT* __res
 // above 64 registers then runs 512-thread CTAs), or bounded so that one
 // 1024-thread CTA fits per SM (at most 64 registers, small spills allowed);
 // which one a probe uses is measured (BoundedFor, fsgpu.cu).
-template <typename T, typename OutT, typename Probe, int UNROLL>
+template <typename T, typename OutT, typename Probe, int UNROLL, int VW>
 __global__ void search_kernel(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh, DevPlan<T> plan,
                               unsigned long long* __restrict__ status, int merge, StageSeg seg0, StageSeg seg1,
                               int nseg) {
-  search_body<T, OutT, Probe, UNROLL>(z, out, sh, plan, status, merge, seg0, seg1, nseg);
+  search_body<T, OutT, Probe, UNROLL, VW>(z, out, sh, plan, status, merge, seg0, seg1, nseg);
 }
-template <typename T, typename OutT, typename Probe, int UNROLL>
+template <typename T, typename OutT, typename Probe, int UNROLL, int VW>
 __global__ void __launch_bounds__(1024, 1)
     search_kernel_1k(const T* __restrict__ z, OutT* __restrict__ out, StreamShape sh, DevPlan<T> plan,
                      unsigned long long* __restrict__ status, int merge, StageSeg seg0, StageSeg seg1, int nseg) {
-  search_body<T, OutT, Probe, UNROLL>(z, out, sh, plan, status, merge, seg0, seg1, nseg);
+  search_body<T, OutT, Probe, UNROLL, VW>(z, out, sh, plan, status, merge, seg0, seg1, nseg);
 }
 
 }  // namespace fsg
