@@ -396,9 +396,13 @@ constexpr int kUnroll = sizeof(T) == 8 ? FSG_UNROLL_F64 : FSG_UNROLL;
 #ifndef FSG_F32_VW8
 #define FSG_F32_VW8 1
 #endif
+#ifndef FSG_F32_I64_VW8
+#define FSG_F32_I64_VW8 0
+#endif
 template <typename T, typename OutT, typename Probe>
 struct VecWidthFor {
-  static constexpr int value = (FSG_F32_VW8 && sizeof(T) == 4 && sizeof(OutT) == 4) ? 8 : 4;
+  static constexpr int value =
+      (FSG_F32_VW8 && sizeof(T) == 4 && (sizeof(OutT) == 4 || FSG_F32_I64_VW8)) ? 8 : 4;
 };
 // 8-query groups in flight per thread: one for the smem-resident probes
 // (cfg3 direct 797 -> 832 Gq/s, the torch copy ceiling; two groups: 720),

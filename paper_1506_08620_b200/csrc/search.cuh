@@ -952,20 +952,22 @@ __device__ __forceinline__ void store_group(int32_t* p, const int32_t (&o)[VW], 
 #endif
 template <int VW>
 __device__ __forceinline__ void store_group(int64_t* p, const int64_t (&o)[VW], int vec) {
-  static_assert(VW == 4, "int64 groups are 4 wide");
 #if FSG_I64_ST256
   if (vec == 2) {
-    asm volatile("st.global.cs.v4.s64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(o[0]), "l"(o[1]), "l"(o[2]), "l"(o[3])
-                 : "memory");
+#pragma unroll
+    for (int h = 0; h < VW; h += 4)
+      asm volatile("st.global.cs.v4.s64 [%0], {%1,%2,%3,%4};" ::"l"(p + h), "l"(o[h]), "l"(o[h + 1]), "l"(o[h + 2]),
+                   "l"(o[h + 3])
+                   : "memory");
     return;
   }
 #endif
   if (vec) {
-    st_stream(reinterpret_cast<longlong2*>(p), make_longlong2(o[0], o[1]));
-    st_stream(reinterpret_cast<longlong2*>(p) + 1, make_longlong2(o[2], o[3]));
+#pragma unroll
+    for (int h = 0; h < VW; h += 2) st_stream(reinterpret_cast<longlong2*>(p + h), make_longlong2(o[h], o[h + 1]));
   } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) st_stream(p + e, o[e]);
+    for (int e = 0; e < VW; ++e) st_stream(p + e, o[e]);
   }
 }
 
