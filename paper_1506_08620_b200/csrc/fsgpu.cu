@@ -415,9 +415,12 @@ template <typename Probe>
 struct UnrollVW8For {
   static constexpr int value = FSG_UNROLL_VW8;
 };
+#ifndef FSG_UNROLL_VW8_RANK
+#define FSG_UNROLL_VW8_RANK 2
+#endif
 template <typename J, bool XS, bool DS>
 struct UnrollVW8For<RankProbe<float, J, XS, DS>> {
-  static constexpr int value = 2;
+  static constexpr int value = FSG_UNROLL_VW8_RANK;
 };
 template <bool TOP, bool DEEP>
 struct UnrollVW8For<Bitset2Probe<float, TOP, DEEP>> {
