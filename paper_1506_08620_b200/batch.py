@@ -286,14 +286,16 @@ def _make_callables(plan, p: SortedPartition):
     return scalar, lanes
 
 
-def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: bool = False) -> PreparedKernel:
+def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: bool = True) -> PreparedKernel:
     """Build the device search structure for ``algorithm`` (batch.py:156-255).
 
     Direct-family preparation propagates NotDistinguishable/Overflow from
-    index construction, as the reference does.  ``hot_window`` (direct only,
-    opt-in) stages the knot-densest slice of a directory too large for
-    shared memory (fs_build_hot_window); measured neutral on cfg4, whose
-    dense queries already share L1 lines, so it is off by default.
+    index construction, as the reference does.  ``hot_window`` (direct
+    only) stages the knot-densest slice of a directory too large for shared
+    memory (fs_build_hot_window) when the table is skewed enough
+    (HOT_WINDOW_MIN_DENSITY_RATIO); cfg4 373 -> 390 G queries/s with
+    8-query groups (profiles/r01/tune_hot_window_vw8.txt).  False keeps the
+    whole directory in L2.
     """
     n = p.n_intervals
     if algorithm == "classic":

@@ -422,6 +422,10 @@ template <typename J, bool XS, bool DS>
 struct UnrollVW8For<RankProbe<float, J, XS, DS>> {
   static constexpr int value = FSG_UNROLL_VW8_RANK;
 };
+template <>
+struct UnrollVW8For<HotRankProbe<float>> {
+  static constexpr int value = FSG_UNROLL_VW8_RANK;
+};
 template <bool TOP, bool DEEP>
 struct UnrollVW8For<Bitset2Probe<float, TOP, DEEP>> {
   static constexpr int value = 2;

@@ -457,6 +457,36 @@ struct HotRankProbe {
     if (knot) xv = tl < nt ? Xs[tl] : __ldg(X + t);
     return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
   }
+  // Two phases over groups of queries, as RankProbe::batch: every directory
+  // word of the group (window or L2) in flight before the first is used.
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    constexpr int G = N < FSG_RANK_GROUP ? N : FSG_RANK_GROUP;
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += G) {
+      uint2 d[G];
+      uint32_t b[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z[g0 + q], x0), h));
+        j = j < r ? j : r;
+        const uint32_t w = j >> 5, wl = w - w0;
+        b[q] = j & 31u;
+        d[q] = wl < nw ? Ds[wl] : __ldg(D + w);
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        const uint32_t t = d[q].y + __popc(d[q].x & ((1u << b[q]) - 1u));
+        const bool knot = (d[q].x >> b[q]) & 1u;
+        const uint32_t tl = t - t0;
+        T xv = z[g0 + q];
+        if (knot) xv = tl < nt ? Xs[tl] : __ldg(X + t);
+        o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
+      }
+    }
+  }
 };
 
 // Cache-fused records: {u32 idx, f32 val} (8 B) / {u32 idx, u32 pad, f64 val}

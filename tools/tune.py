@@ -7,7 +7,7 @@ resident queries and prints one JSON line per variant.
 Config specs: cfgN (BASELINE recipes), cfg5:<N+1>, cfg2:<seed>, cfg5u (the
 unfiltered cfg5 draw, bitset2 fall-back instance), big32:<N+1> (sorted f32
 U[0,1) knots).  Layout variants: direct-k (plain K), direct-rank (rank
-directory only), direct-hot (hot window), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
+directory only), direct-hot / direct-hot:<KB> / direct-nohot (hot window on, of a given size, off), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
 records forced), bitset2-flat (no subtree records),
 direct-gap2-k (gap 2 over plain K).
 """
@@ -99,8 +99,10 @@ def main():
                               "gbs": qbytes * m / t / 1e9, "frac": qbytes * m / t / 1e9 / PEAK}), flush=True)
         for algo in args.algos.split(","):
             try:
-                base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct",
+                base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct", "direct-nohot": "direct",
                         "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
+                if algo.startswith("direct-hot:"):  # hot window of the given size in KB
+                    base = "direct"
                 if algo in ("direct-sparse2", "direct-rec", "direct-rec8"):  # force one sparse-table format
                     from paper_1506_08620_b200 import batch as _b
 
@@ -123,6 +125,17 @@ def main():
                     prep.plan.sparse = None
                 if algo == "direct-hot":
                     prep = fs.prepare("direct", p, hot_window=True)
+                if algo == "direct-nohot":
+                    prep = fs.prepare("direct", p, hot_window=False)
+                if algo.startswith("direct-hot:"):
+                    from paper_1506_08620_b200 import batch as _b
+
+                    keep_hw = _b.HOT_WINDOW_BYTES
+                    _b.HOT_WINDOW_BYTES = int(algo.split(":")[1]) * 1024
+                    try:
+                        prep = fs.prepare("direct", p, hot_window=True)
+                    finally:
+                        _b.HOT_WINDOW_BYTES = keep_hw
                 if algo == "bitset2-flat":  # global levels from the padded array (no subtree records)
                     prep.plan.b2_deep = None
                 if algo == "direct-gap2-k":  # gap-2 over its plain K table (no rank directory)
