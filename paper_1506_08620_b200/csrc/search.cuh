@@ -32,6 +32,11 @@
 #define FSG_RANK_GROUP 8
 #endif
 
+// bitset2: subtree-record gathers in flight per group.
+#ifndef FSG_B2_DEEP_GROUP
+#define FSG_B2_DEEP_GROUP 4
+#endif
+
 // Queries per two-phase group in the group-record probe.
 #ifndef FSG_REC_GROUP
 #define FSG_REC_GROUP 4
@@ -737,7 +742,7 @@ struct Bitset2Probe {
         for (; pbits - lvl >= 2; ) {
           const int kc = pbits - lvl < deep_k ? pbits - lvl : deep_k;
           const int sh = pbits - lvl;
-          constexpr int G = N < 4 ? N : 4;  // records in flight per group (32 B each)
+          constexpr int G = N < FSG_B2_DEEP_GROUP ? N : FSG_B2_DEEP_GROUP;  // records in flight per group (32 B each)
 #pragma unroll
           for (int g0 = 0; g0 < N; g0 += G) {
             Rec r[G];
