@@ -438,6 +438,12 @@ template <typename J>
 struct UnrollFor<double, CacheProbe<double, J, true>> {
   static constexpr int value = 3;
 };
+// f32 records with int64 outputs (the 4-query-group path): two groups
+// (cfg3 487 -> 500 Gq/s; profiles/r01/tune_i64_unroll.txt)
+template <typename J>
+struct UnrollFor<float, CacheProbe<float, J, true>> {
+  static constexpr int value = 2;
+};
 template <bool DENSE>
 struct UnrollFor<double, SparseProbe<double, true, DENSE>> {
   static constexpr int value = FSG_UNROLL_F64_SMEM;
