@@ -62,13 +62,29 @@ def test_misaligned_views_and_odd_sizes(cuda, sweep4095):
     want = orc.rank_oracle(xs, z)
     zt = torch.from_numpy(z).to(cuda)
     prep = fs.prepare("direct", p)
+    # f32 + int32 runs 8-query groups (32-B aligned: heads of 0..7 queries;
+    # outputs 32-B, 16-B or 4-B aligned relative to the group), with one
+    # (direct) or two (bitset2) groups in flight per thread
+    for algo, pr in (("direct", prep), ("bitset2", fs.prepare("bitset2", p))):
+        for a in range(0, 9):
+            for b in (len(z), len(z) - 1, len(z) - 3, len(z) - 7, a + 1, a + 9, a + 17):
+                for oshift in range(0, 8):
+                    out = torch.full((b - a + oshift,), -9, dtype=torch.int32, device=cuda)
+                    fs.batch_search(fs.LaneConfig(1, algo, pr), zt[a:b], out[oshift:])
+                    got = out[oshift:].cpu().numpy()
+                    assert np.array_equal(got, want[a:b]), (algo, a, b, oshift)
+                    assert (out[:oshift].cpu().numpy() == -9).all()
+    # f64 queries (32-B groups of 4) and int64 outputs (32-B stores)
+    z64 = zt.double()
+    p64 = fs.validate_partition(xs.astype(np.float64))
+    prep64 = fs.prepare("direct", p64)
     for a in range(0, 5):
-        for b in (len(z), len(z) - 1, len(z) - 3, a + 1, a + 7):
-            for oshift in (0, 1, 2, 3):
-                out = torch.full((b - a + oshift,), -9, dtype=torch.int32, device=cuda)
-                fs.batch_search(fs.LaneConfig(1, "direct", prep), zt[a:b], out[oshift:])
-                got = out[oshift:].cpu().numpy()
-                assert np.array_equal(got, want[a:b]), (a, b, oshift)
+        for oshift in range(0, 5):
+            for odt in (torch.int32, torch.int64):
+                b = len(z) - 1
+                out = torch.full((b - a + oshift,), -9, dtype=odt, device=cuda)
+                fs.batch_search(fs.LaneConfig(1, "direct", prep64), z64[a:b], out[oshift:])
+                assert np.array_equal(out[oshift:].cpu().numpy(), orc.rank_oracle(p64.values, z64[a:b].cpu().numpy()))
                 assert (out[:oshift].cpu().numpy() == -9).all()
     # host arrays: odd lengths, non-contiguous out, other integer dtypes
     for m in (1, 2, 3, 5, 4001):
