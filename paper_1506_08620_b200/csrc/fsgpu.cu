@@ -97,15 +97,22 @@ inline uint64_t b2_deep_total_bytes(int pbits, int top, int k) {
 inline int b2_top_bits(int pbits, size_t es) {
   return std::min(bit_length(smem_budget() / es + 1) - 1, pbits);
 }
-inline uint64_t b2_smem_bytes(int top, int l1, int l2, size_t es) {
-  return (((1ull << l1) - 1) + ((1ull << l2) - (1ull << l1)) * 32 + ((1ull << top) - (1ull << l2))) * es;
+// levels [0, l1) plain, [l1, l2) 32 copies, [l2, l3) 16 copies, [l3, top) plain
+inline uint64_t b2_smem_bytes(int top, int l1, int l2, int l3, size_t es) {
+  return (((1ull << l1) - 1) + ((1ull << l2) - (1ull << l1)) * 32 + ((1ull << l3) - (1ull << l2)) * 16 +
+          ((1ull << top) - (1ull << l3))) *
+         es;
 }
+#ifndef FSG_B2_HALF
+#define FSG_B2_HALF 1
+#endif
 
 struct Placement {
   uint32_t x_bytes = 0;      // bytes staged at smem offset 0 (X / padded / tree / top)
   uint32_t table_bytes = 0;  // bytes staged after align128(x_bytes) (K / records)
   int top_bits = 0;          // bitset2: levels staged in smem ...
   int b2_l1 = 0, b2_l2 = 0;  // ... of which [b2_l1, b2_l2) replicated per bank
+  int b2_l3 = 0;             // ... and [b2_l2, b2_l3) in 16 copies (lane pairs share one)
   bool xs = false, ks = false, top = false;
   int flags = FS_PLACE_GLOBAL;
   size_t smem = 0;
@@ -301,13 +308,22 @@ Placement place(const fs_plan* p) {
       const int tb = b2_top_bits(p->pbits, es);
       pl.top_bits = tb;
       pl.flags |= tb == p->pbits ? FS_PLACE_SMEM_X : FS_PLACE_SMEM_TOP;
-      pl.b2_l1 = pl.b2_l2 = std::min(kB2ConflictFree, tb);
+      pl.b2_l1 = pl.b2_l2 = pl.b2_l3 = std::min(kB2ConflictFree, tb);
       // (only when every level is in smem: with global levels below, the L1
       // the larger carve-out takes away costs more than the conflicts)
       while (kB2Replicate && tb == p->pbits && pl.b2_l2 < tb &&
-             b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2 + 1, es) <= budget)
+             b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2 + 1, pl.b2_l2 + 1, es) <= budget)
         ++pl.b2_l2;
-      pl.x_bytes = (uint32_t)b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2, es);
+      // f64: the next levels in 16 copies where the rest of the budget allows
+      // (a lane pair shares a copy: ~1.3 instead of ~3.5 wavefronts per level;
+      // cfg5 N+1 = 1025 281 -> 307, cfg2 158 -> 166 Gq/s).  f32 loses (cfg3
+      // 382 -> 364): its issue-bound loop pays more for the two region
+      // transitions than it saves (profiles/r01/tune_bitset2_half.txt)
+      pl.b2_l3 = pl.b2_l2;
+      while (FSG_B2_HALF && es == 8 && kB2Replicate && tb == p->pbits && pl.b2_l2 > pl.b2_l1 && pl.b2_l3 < tb &&
+             b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2, pl.b2_l3 + 1, es) <= budget)
+        ++pl.b2_l3;
+      pl.x_bytes = (uint32_t)b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2, pl.b2_l3, es);
       pl.smem = pl.x_bytes;
       break;
     }
@@ -346,8 +362,8 @@ Placement place_for_batch(const fs_plan* p, uint64_t m) {
     const size_t es = p->dtype == FS_F32 ? 4 : 8;
     const uint64_t query_bytes = m * (es + 4);
     if (query_bytes < (uint64_t)pl.smem * sm_count()) {
-      pl.b2_l2 = pl.b2_l1;
-      pl.x_bytes = (uint32_t)b2_smem_bytes(pl.top_bits, pl.b2_l1, pl.b2_l2, es);
+      pl.b2_l2 = pl.b2_l3 = pl.b2_l1;
+      pl.x_bytes = (uint32_t)b2_smem_bytes(pl.top_bits, pl.b2_l1, pl.b2_l2, pl.b2_l3, es);
       pl.smem = pl.x_bytes;
     }
     return pl;
@@ -468,6 +484,16 @@ template <typename T, bool DENSE, typename OutT>
 struct BoundedFor<T, SparseProbe<T, true, DENSE>, OutT> {
   static constexpr bool value = true;
 };
+// bitset2 with its top levels in smem runs one 1024-thread CTA per SM: the
+// 16-copy region's address arithmetic would otherwise take it past 64
+// registers (66-72) and halve the resident warps.
+#ifndef FSG_B2_BOUNDED
+#define FSG_B2_BOUNDED 1
+#endif
+template <typename T, bool DEEP, typename OutT>
+struct BoundedFor<T, Bitset2Probe<T, true, DEEP>, OutT> {
+  static constexpr bool value = FSG_B2_BOUNDED;
+};
 template <typename T, int SLOTS, bool XS, bool OVF, typename OutT>
 struct BoundedFor<T, SparseRecProbe<T, SLOTS, XS, OVF>, OutT> {
   static constexpr bool value = FSG_REC_BOUNDED && !(SLOTS == 2 && sizeof(OutT) == 8);
@@ -587,6 +613,7 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   d.top_bits = pl.top_bits;
   d.b2_l1 = pl.b2_l1;
   d.b2_l2 = pl.b2_l2;
+  d.b2_l3 = pl.b2_l3;
   // subtree records apply only to the staged-top split they were built for
   const bool deep = pl.top && p->b2_deep && p->b2_deep_top == pl.top_bits &&
                     p->b2_deep_k == b2_deep_k(p->dtype);

@@ -57,6 +57,7 @@ struct DevPlan {
   int32_t pbits;         // bitset / eytzinger depth
   int32_t top_bits;      // bitset2: levels served from smem
   int32_t b2_l1, b2_l2;  // bitset2: levels [b2_l1, b2_l2) replicated per bank in smem
+  int32_t b2_l3;         // bitset2: levels [b2_l2, b2_l3) in 16 copies (lane pairs share one)
   const void* b2_deep;   // bitset2: subtree records of the levels below top_bits, or NULL
   int32_t b2_deep_k;     // ... levels per record
   uint32_t off_f, off_s, off_j;  // offset search constants
@@ -565,7 +566,7 @@ struct Bitset2Probe {
   const T* top;
   const T* xpad;
   const char* deep;  // subtree records of the global levels (fs_build_b2_deep) or NULL
-  int pbits, top_bits, l1, l2, deep_k;
+  int pbits, top_bits, l1, l2, l3, deep_k;
   __device__ __forceinline__ Bitset2Probe(const DevPlan<T>& p, unsigned char* smem) {
     top = reinterpret_cast<const T*>(smem);
     xpad = static_cast<const T*>(p.table);
@@ -573,6 +574,7 @@ struct Bitset2Probe {
     top_bits = TOP ? p.top_bits : 0;
     l1 = TOP ? p.b2_l1 : 0;
     l2 = TOP ? p.b2_l2 : 0;
+    l3 = TOP ? p.b2_l3 : 0;
     deep = DEEP ? static_cast<const char*>(p.b2_deep) : nullptr;
     deep_k = DEEP ? p.b2_deep_k : 0;
   }
@@ -614,12 +616,15 @@ struct Bitset2Probe {
       const T* src = static_cast<const T*>(p.table);
       const uint32_t n1w = (1u << p.b2_l1) - 1;                                   // P1 words
       const uint32_t nrw = ((1u << p.b2_l2) - (1u << p.b2_l1)) * 32u;            // R words
-      const uint32_t total = n1w + nrw + ((1u << p.top_bits) - (1u << p.b2_l2));  // + P2 words
+      const uint32_t nhw = ((1u << p.b2_l3) - (1u << p.b2_l2)) * 16u;            // H words
+      const uint32_t total = n1w + nrw + nhw + ((1u << p.top_bits) - (1u << p.b2_l3));  // + P2 words
       for (uint32_t w = threadIdx.x; w < total; w += blockDim.x) {
-        // level-order node index of word w (P1 | R: 32 copies per node | P2)
-        const uint32_t node = w < n1w         ? w
-                              : w < n1w + nrw ? n1w + ((w - n1w) >> 5)
-                                              : (1u << p.b2_l2) - 1 + (w - n1w - nrw);
+        // level-order node index of word w (P1 | R: 32 copies per node |
+        // H: 16 copies per node | P2)
+        const uint32_t node = w < n1w               ? w
+                              : w < n1w + nrw       ? n1w + ((w - n1w) >> 5)
+                              : w < n1w + nrw + nhw ? (1u << p.b2_l2) - 1 + ((w - n1w - nrw) >> 4)
+                                                    : (1u << p.b2_l3) - 1 + (w - n1w - nrw - nhw);
         const int l = 31 - __clz(node + 1);
         const uint32_t m = node + 1 - (1u << l);
         const uint64_t r = ((uint64_t)m << (p.pbits - l)) | (1ull << (p.pbits - 1 - l));
@@ -707,14 +712,34 @@ struct Bitset2Probe {
         }
         if constexpr (N & 1) a[N - 1] = step<0>(a[N - 1], z[N - 1], c1, c2, two, one);
       }
-      b2 = rb + ((1u << l2) - (1u << l1)) * 32u * sz;  // B_l2: P2 starts here
+      b2 = rb + ((1u << l2) - (1u << l1)) * 32u * sz;  // B_l2: H (or P2) starts here
       s0 = (1u << l2) - 1;
+      if (l3 > l2) {  // H: a = B_l + m * 16sz + (lane & 15) * sz, B_l = b2 + (2^l - 2^l2) * 16sz
+        const uint32_t lh = lane & 15u;
 #pragma unroll
-      for (int q = 0; q < N; ++q) a[q] = b2 + (a[q] - b2 - lane * sz) / (32u * sz) * sz;
+        for (int q = 0; q < N; ++q) a[q] = b2 + (a[q] - b2 - lane * sz) / (32u * sz) * (16u * sz) + lh * sz;
+        const uint32_t h1 = (1u << l2) * 16u * sz - b2 - lh * sz, h2 = h1 + 16u * sz;
+        for (int l = l2; l < l3; ++l) {
+#pragma unroll
+          for (int q = 0; q + 1 < N; q += 2) {
+            a[q] = step<0>(a[q], z[q], h1, h2, two, one);
+            a[q + 1] = step<1>(a[q + 1], z[q + 1], h1, h2, two, one);
+          }
+          if constexpr (N & 1) a[N - 1] = step<0>(a[N - 1], z[N - 1], h1, h2, two, one);
+        }
+        const uint32_t b3 = b2 + ((1u << l3) - (1u << l2)) * 16u * sz;  // B_l3: P2 starts here
+#pragma unroll
+        for (int q = 0; q < N; ++q) a[q] = b3 + (a[q] - b3 - lh * sz) / (16u * sz) * sz;
+        b2 = b3;
+        s0 = (1u << l3) - 1;
+      } else {
+#pragma unroll
+        for (int q = 0; q < N; ++q) a[q] = b2 + (a[q] - b2 - lane * sz) / (32u * sz) * sz;
+      }
     }
     {  // P2 (or the rest of P1 when nothing is replicated)
       const uint32_t c1 = (s0 + 1) * sz - b2, c2 = c1 + sz;
-      for (int l = l2 > l1 ? l2 : l1; l < top_bits; ++l) {
+      for (int l = l2 > l1 ? (l3 > l2 ? l3 : l2) : l1; l < top_bits; ++l) {
 #pragma unroll
         for (int q = 0; q + 1 < N; q += 2) {
           a[q] = step<0>(a[q], z[q], c1, c2, two, one);
