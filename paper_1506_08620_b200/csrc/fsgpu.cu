@@ -560,9 +560,11 @@ int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t
   // per SM in one wide CTA (measured on cfg3: 1x1024 95% of HBM peak vs
   // 3x512 86%; fewer resident warps contend less for the smem crossbar the
   // table gathers share with the stream).  L2-gather kernels use 512-thread
-  // CTAs at full occupancy (geometry-insensitive within 1%).
+  // CTAs at full occupancy (geometry-insensitive within 1%); with a hot
+  // window, 1024-thread CTAs at full occupancy (cfg4 390 -> 405 Gq/s;
+  // profiles/r01/tune_tail_records_rejected.txt).
   const bool smem_resident = pl.smem > 0 && !pl.hot;  // a hot window still gathers through L2
-  const int mode = (pl.tune & 0xfff) ? (pl.tune & 0xfff) : (smem_resident ? -1 : -2);
+  const int mode = (pl.tune & 0xfff) ? (pl.tune & 0xfff) : (smem_resident || pl.hot ? -1 : -2);
   int threads = 0, per_sm = 0;
   int rc = launch_geometry(reinterpret_cast<const void*>(kern), smem, mode, &threads, &per_sm);
   if (rc) return rc;
