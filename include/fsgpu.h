@@ -80,7 +80,8 @@ enum {
 enum {
   FS_SPARSE_TWO_LEVEL = 0, /* C | F (| dense masks): fs_build_sparse                */
   FS_SPARSE_RECORDS = 1,   /* 16-B group records, six offsets (| F): fs_build_sparse_rec */
-  FS_SPARSE_RECORDS8 = 2   /* 8-B group records, two offsets (| F): fs_build_sparse_rec  */
+  FS_SPARSE_RECORDS8 = 2,  /* 8-B group records, two offsets (| F): fs_build_sparse_rec  */
+  FS_SPARSE_RECORDS12 = 3  /* 16-B group records, eight 12-bit offsets (shift <= 10)      */
 };
 
 /*
@@ -129,8 +130,8 @@ typedef struct fs_plan {
   int32_t b2_deep_top;  /* ... built for this many staged top levels             */
   int32_t b2_deep_k;    /* ... levels per record (3 for f32, 2 for f64)           */
   int32_t sparse_format;/* layout of `sparse`: FS_SPARSE_TWO_LEVEL (fs_build_sparse)
-                           or FS_SPARSE_RECORDS / FS_SPARSE_RECORDS8
-                           (fs_build_sparse_rec)                                  */
+                           or FS_SPARSE_RECORDS / FS_SPARSE_RECORDS8 /
+                           FS_SPARSE_RECORDS12 (fs_build_sparse_rec)              */
 } fs_plan;
 
 /* Library identification. */
@@ -229,7 +230,9 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
  * direct.py:498-541; no reference counterpart), for R >> N.  The
  * super-buckets of fs_build_sparse, each packed into one record {base |
  * overflow flag (bit 31), S uint16 knot offsets}: FS_SPARSE_RECORDS is 16 B
- * with S = 6, FS_SPARSE_RECORDS8 is 8 B with S = 2.  base = K[J 2^shift], the
+ * with S = 6, FS_SPARSE_RECORDS8 is 8 B with S = 2, FS_SPARSE_RECORDS12 is
+ * 16 B with S = 8 offsets in 12-bit fields (0x800 | offset at bit 12k of the
+ * 96 bits after base, unused 0xFFF; shift <= 10).  base = K[J 2^shift], the
  * offsets f_i mod 2^shift of the super-bucket's first min(count, S) knots in
  * ascending order, unused slots 0x7FFF.  The kernel resolves
  * K[j] = base + #{offsets < j mod 2^shift} from one shared-memory load, and

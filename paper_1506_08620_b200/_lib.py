@@ -57,6 +57,7 @@ PLACE_SMEM_SPARSE = 16
 SPARSE_TWO_LEVEL = 0
 SPARSE_RECORDS = 1
 SPARSE_RECORDS8 = 2
+SPARSE_RECORDS12 = 3
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (

@@ -275,13 +275,24 @@ __global__ void fill_sparse_rec_kernel(const uint64_t* __restrict__ f, uint64_t 
         if ((fi >> s) != i) break;
         off[k] = (uint32_t)(fi & mask);
       }
-      for (uint64_t e = k; e < SLOTS; ++e) off[e] = kRecSentinel;
+      for (uint64_t e = k; e < SLOTS; ++e) off[e] = SLOTS == 8 ? 0x7FFu : kRecSentinel;
       const bool ovf = k == SLOTS && lo + k < n1 && (__ldg(f + lo + k) >> s) == i;
       const uint32_t b = (uint32_t)lo | (ovf ? kDenseFlag : 0u);
-      if constexpr (SLOTS == 6)
+      if constexpr (SLOTS == 6) {
         G[i] = make_uint4(b, off[0] | (off[1] << 16), off[2] | (off[3] << 16), off[4] | (off[5] << 16));
-      else
+      } else if constexpr (SLOTS == 8) {
+        // 96 bits of fields 0x800 | offset at bit 12k (field 2 and 5 straddle words)
+        unsigned long long lo64 = 0, hi32 = 0;
+        for (int e = 0; e < 8; ++e) {
+          const unsigned long long v = 0x800ull | off[e];
+          if (e < 5) lo64 |= v << (12 * e);                                  // bits 0..59
+          if (e == 5) { lo64 |= v << 60; hi32 |= v >> 4; }                    // bits 60..71
+          if (e > 5) hi32 |= v << (12 * e - 64);                              // bits 72..95
+        }
+        G[i] = make_uint4(b, (uint32_t)lo64, (uint32_t)(lo64 >> 32), (uint32_t)hi32);
+      } else {
         G[i] = make_uint2(b, off[0] | (off[1] << 16));
+      }
     }
     if (F && i < n1) F[i] = (uint16_t)(__ldg(f + i) & mask);
   }

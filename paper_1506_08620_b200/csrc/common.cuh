@@ -25,8 +25,14 @@ constexpr uint32_t kDenseOcc = 64;
 template <int SLOTS> struct RecWord;
 template <> struct RecWord<6> { using type = uint4; };
 template <> struct RecWord<2> { using type = uint2; };
+template <> struct RecWord<8> { using type = uint4; };
 constexpr uint32_t kRecSentinel = 0x7FFFu;
 constexpr int kRecMaxShift = 14;
+// 16-B records with eight 12-bit offset fields (FS_SPARSE_RECORDS12): each
+// field stored as 0x800 | offset (guard bit preset, offsets < 2^10), unused
+// fields 0xFFF; shifts up to 10.
+constexpr int kRec12MaxShift = 10;
+template <int SLOTS> constexpr int rec_max_shift() { return SLOTS == 8 ? kRec12MaxShift : kRecMaxShift; }
 
 // ---------------------------------------------------------------------------
 // Exact arithmetic in the partition's precision

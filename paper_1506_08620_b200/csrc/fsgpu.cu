@@ -147,10 +147,12 @@ int validate_plan(const fs_plan* p) {
                            p->hot_knot0 > p->n1 || p->hot_knots > p->n1 - p->hot_knot0))
         return fail(FS_INVALID_ARG, "hot window outside the rank directory / knots");
       if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS &&
-                        p->sparse_format != FS_SPARSE_RECORDS8))
+                        p->sparse_format != FS_SPARSE_RECORDS8 && p->sparse_format != FS_SPARSE_RECORDS12))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
       if (p->sparse && (p->sparse_shift < 5 ||
-                        p->sparse_shift > (p->sparse_format != FS_SPARSE_TWO_LEVEL ? kRecMaxShift : 16) ||
+                        p->sparse_shift > (p->sparse_format == FS_SPARSE_TWO_LEVEL    ? 16
+                                           : p->sparse_format == FS_SPARSE_RECORDS12 ? kRec12MaxShift
+                                                                                     : kRecMaxShift) ||
                         p->sparse_ndense > (p->r >> p->sparse_shift) + 2))
         return fail(FS_INVALID_ARG, "sparse table parameters out of range");
       break;
@@ -676,6 +678,8 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS)
         return dispatch_records<T, OutT, 6>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
+      if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS12)
+        return dispatch_records<T, OutT, 8>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS8)
         return dispatch_records<T, OutT, 2>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
       if (pl.sparse) {
@@ -962,22 +966,29 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
   return FS_OK;
 }
 
+namespace {
+bool is_record_format(int32_t format) {
+  return format == FS_SPARSE_RECORDS || format == FS_SPARSE_RECORDS8 || format == FS_SPARSE_RECORDS12;
+}
+int record_max_shift(int32_t format) { return format == FS_SPARSE_RECORDS12 ? kRec12MaxShift : kRecMaxShift; }
+}  // namespace
+
 uint64_t fs_sparse_rec_bytes(int32_t format, uint64_t n1, uint64_t r, int32_t shift, uint64_t novf) {
-  if (shift < 5 || shift > kRecMaxShift) return 0;
-  if (format != FS_SPARSE_RECORDS && format != FS_SPARSE_RECORDS8) return 0;
+  if (!is_record_format(format) || shift < 5 || shift > record_max_shift(format)) return 0;
   const uint64_t ng = (r >> shift) + 2;
-  return ((format == FS_SPARSE_RECORDS ? 16 : 8) * ng + (novf ? 2 * n1 : 0) + 15) & ~15ull;
+  return ((format == FS_SPARSE_RECORDS8 ? 8 : 16) * ng + (novf ? 2 * n1 : 0) + 15) & ~15ull;
 }
 
 int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
                        uint64_t budget_bytes, int32_t with_x, uint64_t* f_scratch_dev, int32_t* shift_out,
                        uint64_t* novf_out, uint64_t* bytes_out, uint32_t* past_last_ppm_out, void* stream) {
   if (!x_dev || !f_scratch_dev || n1 < 2 || !shift_out) return fail(FS_INVALID_ARG, "bad arguments");
-  if (format != FS_SPARSE_RECORDS && format != FS_SPARSE_RECORDS8) return fail(FS_INVALID_ARG, "not a record format");
+  if (!is_record_format(format)) return fail(FS_INVALID_ARG, "not a record format");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "group records need R < 2^32, N < 2^31");
-  const uint64_t slots = format == FS_SPARSE_RECORDS ? 6 : 2;
+  const uint64_t slots = format == FS_SPARSE_RECORDS ? 6 : format == FS_SPARSE_RECORDS12 ? 8 : 2;
+  const int max_shift = record_max_shift(format);
   const uint64_t xb = with_x ? align128(n1 * (dtype == FS_F32 ? 4 : 8)) : 0;
-  if (xb + fs_sparse_rec_bytes(format, n1, r, kRecMaxShift, 0) > budget_bytes)
+  if (xb + fs_sparse_rec_bytes(format, n1, r, max_shift, 0) > budget_bytes)
     return fail(FS_TOO_LARGE, "no group-record layout fits the budget");
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
   if (rc) return rc;
@@ -991,7 +1002,7 @@ int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_
     uint64_t novf, past;
   };
   std::vector<Cand> cands;
-  for (int s = 5; s <= kRecMaxShift; ++s) {
+  for (int s = 5; s <= max_shift; ++s) {
     if (xb + fs_sparse_rec_bytes(format, n1, r, s, 0) > budget_bytes) continue;
     uint64_t novf = 0, past = 0;
     for (uint64_t i = 0; i < n1;) {
@@ -1029,19 +1040,20 @@ int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_
 
 int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
                         int32_t shift, uint64_t novf, uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
-  if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2 || shift < 5 || shift > kRecMaxShift)
+  if (!is_record_format(format)) return fail(FS_INVALID_ARG, "not a record format");
+  if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2 || shift < 5 || shift > record_max_shift(format))
     return fail(FS_INVALID_ARG, "bad arguments");
-  if (format != FS_SPARSE_RECORDS && format != FS_SPARSE_RECORDS8) return fail(FS_INVALID_ARG, "not a record format");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "group records need R < 2^32, N < 2^31");
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
   if (rc) return rc;
   cudaStream_t s = as_stream(stream);
   const uint64_t ng = (r >> shift) + 2;
   const int grid = grid_1d(std::max(ng, n1), 256);
-  if (format == FS_SPARSE_RECORDS) {
+  if (format == FS_SPARSE_RECORDS || format == FS_SPARSE_RECORDS12) {
     uint4* G = static_cast<uint4*>(buf_dev);
     uint16_t* F = novf ? reinterpret_cast<uint16_t*>(G + ng) : nullptr;
-    fill_sparse_rec_kernel<6><<<grid, 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
+    if (format == FS_SPARSE_RECORDS) fill_sparse_rec_kernel<6><<<grid, 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
+    else fill_sparse_rec_kernel<8><<<grid, 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
   } else {
     uint2* G = static_cast<uint2*>(buf_dev);
     uint16_t* F = novf ? reinterpret_cast<uint16_t*>(G + ng) : nullptr;

@@ -362,18 +362,40 @@ struct SparseRecProbe {
     // (w + hm) & H: bit 15 / 31 set iff the low / high offset >= jl
     // (offsets and jl < 2^15: no borrow crosses a half)
     const uint32_t hm = H - jl * 0x10001u;
-    uint32_t ge, w;
-    if constexpr (SLOTS == 6) {
-      ge = __popc((g.y + hm) & H) + __popc((g.z + hm) & H) + __popc((g.w + hm) & H);
-      const uint32_t lt = SLOTS - ge;
-      w = lt < 2 ? g.y : (lt < 4 ? g.z : g.w);
+    uint32_t ge, lt;
+    if constexpr (SLOTS == 8) {
+      // 96-bit SWAR: fields (0x800 | offset) - jl keep bit 11 iff offset >= jl
+      // (no borrow leaves a field); Y = jl in every 12-bit field
+      const uint32_t y0 = jl * 0x01001001u;
+      const uint32_t y1 = jl * 0x10010010u + (jl >> 8);
+      const uint32_t y2 = jl * 0x00100100u + (jl >> 4);
+      uint32_t d0, d1, d2;
+      asm("sub.cc.u32 %0, %3, %6;\n\tsubc.cc.u32 %1, %4, %7;\n\tsubc.u32 %2, %5, %8;"
+          : "=r"(d0), "=r"(d1), "=r"(d2)
+          : "r"(g.y), "r"(g.z), "r"(g.w), "r"(y0), "r"(y1), "r"(y2));
+      // guard bits at 11, 23, 35, 47, 59, 71, 83, 95: word0 bits 11, 23;
+      // word1 bits 3, 15, 27; word2 bits 7, 19, 31
+      ge = __popc(d0 & 0x00800800u) + __popc(d1 & 0x08008008u) + __popc(d2 & 0x80080080u);
+      lt = SLOTS - ge;
+      // field lt (bits 12 lt .. 12 lt + 11) through a funnel shift of its word pair
+      const uint32_t bit = 12u * lt, wi = bit >> 5, sh = bit & 31u;
+      const uint32_t a0 = wi == 0 ? g.y : (wi == 1 ? g.z : g.w);
+      const uint32_t a1 = wi == 0 ? g.z : g.w;
+      knot = lt < SLOTS && ((__funnelshift_r(a0, a1, sh) & 0x7FFu) == jl);
     } else {
-      ge = __popc((g.y + hm) & H);
-      w = g.y;
+      uint32_t w;
+      if constexpr (SLOTS == 6) {
+        ge = __popc((g.y + hm) & H) + __popc((g.z + hm) & H) + __popc((g.w + hm) & H);
+        const uint32_t l6 = SLOTS - ge;
+        w = l6 < 2 ? g.y : (l6 < 4 ? g.z : g.w);
+      } else {
+        ge = __popc((g.y + hm) & H);
+        w = g.y;
+      }
+      lt = SLOTS - ge;
+      knot = lt < SLOTS && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
     }
-    const uint32_t lt = SLOTS - ge;
     t = (g.x & ~kDenseFlag) + lt;
-    knot = lt < SLOTS && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
     if constexpr (OVF) {
       if ((g.x & kDenseFlag) && lt == SLOTS) {  // past the last recorded knot of an overflowing super-bucket
         uint32_t lo = t, hi = G[(j >> s) + 1].x & ~kDenseFlag;

@@ -16,7 +16,8 @@ from oracle import fs_oracle as orc
 pytestmark = pytest.mark.gpu
 
 SENTINEL = 0x7FFF
-FORMATS = {"records": 6, "records8": 2}  # offset slots per record
+FORMATS = {"records": 6, "records8": 2, "records12": 8}  # offset slots per record
+MAX_SHIFT = {"records": 14, "records8": 14, "records12": 10}
 
 
 def _fs():
@@ -28,24 +29,30 @@ def _fs():
 def _fmt_code(name):
     from paper_1506_08620_b200 import _lib
 
-    return {"records": _lib.SPARSE_RECORDS, "records8": _lib.SPARSE_RECORDS8}[name]
+    return {"records": _lib.SPARSE_RECORDS, "records8": _lib.SPARSE_RECORDS8, "records12": _lib.SPARSE_RECORDS12}[name]
 
 
 def expected_records(xs, h, r, s, slots=6):
-    """uint32 (ng, 1 + slots / 2): {base | overflow << 31, off0 | off1 << 16, ...}."""
+    """uint32 (ng, words): {base | overflow << 31, off0 | off1 << 16, ...};
+    for 8 slots, 96 bits of 12-bit fields 0x800 | offset (unused 0xFFF)."""
     f = orc.knot_buckets(xs, h).astype(np.uint64)
     ng = (r >> s) + 2
     base = np.searchsorted(f, np.arange(ng, dtype=np.uint64) << np.uint64(s), side="left").astype(np.int64)
-    rec = np.zeros((ng, 1 + slots // 2), dtype=np.uint32)
+    rec = np.zeros((ng, 4 if slots == 8 else 1 + slots // 2), dtype=np.uint32)
     mask = (1 << s) - 1
     for J in range(ng):
         lo = int(base[J])
         hi = int(base[J + 1]) if J + 1 < ng else lo
         offs = [int(f[i]) & mask for i in range(lo, min(hi, lo + slots))]
-        offs += [SENTINEL] * (slots - len(offs))
+        offs += [0x7FF if slots == 8 else SENTINEL] * (slots - len(offs))
         rec[J, 0] = lo | ((hi - lo > slots) << 31)
-        for w in range(slots // 2):
-            rec[J, 1 + w] = offs[2 * w] | (offs[2 * w + 1] << 16)
+        if slots == 8:
+            bits = sum((0x800 | o) << (12 * e) for e, o in enumerate(offs))
+            for w in range(3):
+                rec[J, 1 + w] = (bits >> (32 * w)) & 0xFFFFFFFF
+        else:
+            for w in range(slots // 2):
+                rec[J, 1 + w] = offs[2 * w] | (offs[2 * w + 1] << 16)
     return rec, f & np.uint64(mask)
 
 
@@ -123,12 +130,14 @@ def test_records_chosen_for_sparse_configs(cuda):
     fs = _fs()
     from paper_1506_08620_b200 import workloads
 
-    for name, kw, fmt, sx in (("cfg2", {}, "records", True), ("cfg2", {"seed": 1}, "records8", False),
-                              ("cfg5", {"n1": 1025}, "records8", True), ("cfg5", {"n1": 32769}, "records", False)):
+    for name, kw, fmts, sx in (("cfg2", {}, ("records",), True), ("cfg2", {"seed": 1}, ("records8",), False),
+                               ("cfg5", {"n1": 1025}, ("records8",), True),
+                               ("cfg5", {"n1": 32769}, ("records", "records12"), False)):
         p = workloads.knots(name, **kw)
         prep = fs.prepare("direct", p)
         pl = prep.placement()
-        assert pl["smem_sparse"] and pl["sparse_format"] == fmt and pl["smem_x"] == sx, (name, kw, pl)
+        fmt = pl["sparse_format"]
+        assert pl["smem_sparse"] and fmt in fmts and pl["smem_x"] == sx, (name, kw, pl)
         idx = prep.structure
         s = prep.plan.sparse_shift
         rec, fmod = expected_records(p.values, idx.h, idx.r, s, FORMATS[fmt])
@@ -166,7 +175,7 @@ def test_records_every_shift_with_overflow(cuda, dtype, fmt):
     want = orc.rank_oracle(xs, z)
     assert idx.r < 230_000
     seen_ovf = False
-    for s in range(5, 15):
+    for s in range(5, MAX_SHIFT[fmt] + 1):
         buf, rec, novf = with_records(fs, p, prep, s, fmt)
         seen_ovf |= novf > 0
         got = buf.cpu().numpy()[: rec.nbytes].view(np.uint32).reshape(rec.shape)
@@ -233,7 +242,7 @@ def test_records_abi_validation(cuda):
     p = workloads.knots("cfg5", n1=1025)
     prep = _records_forced(fs, p)
     z = orc.random_queries(p.values, 1000, seed=1)
-    for fmt, shift in ((3, prep.plan.sparse_shift), (_lib.SPARSE_RECORDS, 15)):
+    for fmt, shift in ((4, prep.plan.sparse_shift), (_lib.SPARSE_RECORDS, 15), (_lib.SPARSE_RECORDS12, 11)):
         keep = (prep.plan.sparse_format, prep.plan.sparse_shift)
         prep.plan.sparse_format, prep.plan.sparse_shift = fmt, shift
         with pytest.raises(ValueError):
