@@ -81,7 +81,8 @@ enum {
   FS_SPARSE_TWO_LEVEL = 0, /* C | F (| dense masks): fs_build_sparse                */
   FS_SPARSE_RECORDS = 1,   /* 16-B group records, six offsets (| F): fs_build_sparse_rec */
   FS_SPARSE_RECORDS8 = 2,  /* 8-B group records, two offsets (| F): fs_build_sparse_rec  */
-  FS_SPARSE_RECORDS12 = 3  /* 16-B group records, eight 12-bit offsets (shift <= 10)      */
+  FS_SPARSE_RECORDS12 = 3, /* 16-B group records, eight 12-bit offsets (shift <= 10)      */
+  FS_SPARSE_RECORDS8X3 = 4 /* 8-B group records, three 13-bit offsets (shift <= 11, N+1 <= 2^24) */
 };
 
 /*
@@ -131,7 +132,8 @@ typedef struct fs_plan {
   int32_t b2_deep_k;    /* ... levels per record (3 for f32, 2 for f64)           */
   int32_t sparse_format;/* layout of `sparse`: FS_SPARSE_TWO_LEVEL (fs_build_sparse)
                            or FS_SPARSE_RECORDS / FS_SPARSE_RECORDS8 /
-                           FS_SPARSE_RECORDS12 (fs_build_sparse_rec)              */
+                           FS_SPARSE_RECORDS12 / FS_SPARSE_RECORDS8X3
+                           (fs_build_sparse_rec)                                  */
 } fs_plan;
 
 /* Library identification. */
@@ -232,7 +234,10 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
  * overflow flag (bit 31), S uint16 knot offsets}: FS_SPARSE_RECORDS is 16 B
  * with S = 6, FS_SPARSE_RECORDS8 is 8 B with S = 2, FS_SPARSE_RECORDS12 is
  * 16 B with S = 8 offsets in 12-bit fields (0x800 | offset at bit 12k of the
- * 96 bits after base, unused 0xFFF; shift <= 10).  base = K[J 2^shift], the
+ * 96 bits after base, unused 0xFFF; shift <= 10), FS_SPARSE_RECORDS8X3 is 8 B
+ * with S = 3: the 64-bit word holds base (bits 0..23, so N+1 <= 2^24), the
+ * overflow flag (bit 24) and fields 0x1000 | offset at bits 25 + 13k (unused
+ * 0x1FFF; shift <= 11).  base = K[J 2^shift], the
  * offsets f_i mod 2^shift of the super-bucket's first min(count, S) knots in
  * ascending order, unused slots 0x7FFF.  The kernel resolves
  * K[j] = base + #{offsets < j mod 2^shift} from one shared-memory load, and

@@ -58,6 +58,7 @@ SPARSE_TWO_LEVEL = 0
 SPARSE_RECORDS = 1
 SPARSE_RECORDS8 = 2
 SPARSE_RECORDS12 = 3
+SPARSE_RECORDS8X3 = 4
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (

@@ -241,7 +241,7 @@ class PreparedKernel:
             "smem_hot": bool(f & _lib.PLACE_SMEM_HOT),
             "smem_sparse": bool(f & _lib.PLACE_SMEM_SPARSE),
             "sparse_format": {_lib.SPARSE_RECORDS: "records", _lib.SPARSE_RECORDS8: "records8",
-                              _lib.SPARSE_RECORDS12: "records12"}.get(
+                              _lib.SPARSE_RECORDS12: "records12", _lib.SPARSE_RECORDS8X3: "records8x3"}.get(
                 self.plan.sparse_format, "two-level") if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
         }
@@ -372,7 +372,7 @@ SPARSE_RECORDS_MIN_LOAD = 0.2
 SPARSE_RECORDS8_MAX_PAST_PPM = 5_000
 #: sparse layouts allowed; a tuning run or test may narrow it to one
 #: (a leading records format also skips the load rule)
-SPARSE_FORMATS = ("two-level", "records8", "records", "records12")
+SPARSE_FORMATS = ("two-level", "records8", "records8x3", "records", "records12")
 
 #: hot-window staging budget: small enough that the L2-gather kernel keeps
 #: full occupancy (3-4 CTAs per SM) for the queries outside the window
@@ -433,8 +433,9 @@ def _set_sparse_records(plan, p: SortedPartition, idx: DirectIndex, keep: list, 
                         with_x: tuple = (1, 0)) -> bool:
     """Group records of K (fs_build_sparse_rec): one record per super-bucket
     resolves K[j] with a single shared-memory load ("records8": 8 B, two knot
-    offsets; "records": 16 B, six; "records12": 16 B, eight 12-bit offsets,
-    super-buckets of at most 2^10 buckets).  Used when they fit and few uniform queries
+    offsets; "records8x3": 8 B, three 13-bit offsets, super-buckets of at
+    most 2^11 buckets; "records": 16 B, six; "records12": 16 B, eight 12-bit
+    offsets, super-buckets of at most 2^10 buckets).  Used when they fit and few uniform queries
     fall past a record's last offset; X is staged beside them (with_x 1) or
     read through L2 for the buckets holding a knot (with_x 0)."""
     lib = _lib.load()
@@ -443,7 +444,8 @@ def _set_sparse_records(plan, p: SortedPartition, idx: DirectIndex, keep: list, 
     x = p.device_values()
     fmt, max_ppm = {"records8": (_lib.SPARSE_RECORDS8, SPARSE_RECORDS8_MAX_PAST_PPM),
                     "records": (_lib.SPARSE_RECORDS, SPARSE_RECORDS_MAX_PAST_SIXTH_PPM),
-                    "records12": (_lib.SPARSE_RECORDS12, SPARSE_RECORDS_MAX_PAST_SIXTH_PPM)}[name]
+                    "records12": (_lib.SPARSE_RECORDS12, SPARSE_RECORDS_MAX_PAST_SIXTH_PPM),
+                    "records8x3": (_lib.SPARSE_RECORDS8X3, SPARSE_RECORDS8_MAX_PAST_PPM)}[name]
     for wx in with_x:
         shift, novf, nbytes, ppm = ctypes.c_int32(-1), ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_uint32(0)
         rc = lib.fs_plan_sparse_rec(fmt, dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, wx, f.data_ptr(),
@@ -511,7 +513,7 @@ def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) ->
     budget = _smem_budget() - 512
     n1 = len(p.values)
     f = _device.empty(n1, np.uint64)
-    # In order: 8-B records with X staged; the two-level table when its
+    # In order: 8-B records (two, then three offsets) with X staged; the two-level table when its
     # super-buckets are nearly empty; 16-B records with X (eight 12-bit
     # offsets when that sends fewer queries past the last offset, else six
     # 16-bit ones); then 8-B and 16-B records with X read through L2 (fine
@@ -532,12 +534,12 @@ def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) ->
                 names = ["records", "records12"]
         return any(records(n, (wx,)) for n in names)
 
-    if records("records8", (1,)):
+    if records("records8", (1,)) or records("records8x3", (1,)):
         return
     two = _plan_two_level(p, idx, f, budget) if "two-level" in SPARSE_FORMATS else None
     load = n1 / ((idx.r >> two[0]) + 1) if two else None
     if load is None or load >= SPARSE_RECORDS_MIN_LOAD:
-        if wide_records(1) or records("records8", (0,)) or wide_records(0):
+        if wide_records(1) or records("records8", (0,)) or records("records8x3", (0,)) or wide_records(0):
             return
     if two is None:
         return

@@ -275,7 +275,7 @@ __global__ void fill_sparse_rec_kernel(const uint64_t* __restrict__ f, uint64_t 
         if ((fi >> s) != i) break;
         off[k] = (uint32_t)(fi & mask);
       }
-      for (uint64_t e = k; e < SLOTS; ++e) off[e] = SLOTS == 8 ? 0x7FFu : kRecSentinel;
+      for (uint64_t e = k; e < SLOTS; ++e) off[e] = SLOTS == 8 ? 0x7FFu : SLOTS == 3 ? 0xFFFu : kRecSentinel;
       const bool ovf = k == SLOTS && lo + k < n1 && (__ldg(f + lo + k) >> s) == i;
       const uint32_t b = (uint32_t)lo | (ovf ? kDenseFlag : 0u);
       if constexpr (SLOTS == 6) {
@@ -290,6 +290,10 @@ __global__ void fill_sparse_rec_kernel(const uint64_t* __restrict__ f, uint64_t 
           if (e > 5) hi32 |= v << (12 * e - 64);                              // bits 72..95
         }
         G[i] = make_uint4(b, (uint32_t)lo64, (uint32_t)(lo64 >> 32), (uint32_t)hi32);
+      } else if constexpr (SLOTS == 3) {
+        unsigned long long w = (unsigned long long)lo | (ovf ? (1ull << 24) : 0ull);
+        for (int e = 0; e < 3; ++e) w |= (0x1000ull | off[e]) << (25 + 13 * e);
+        G[i] = make_uint2((uint32_t)w, (uint32_t)(w >> 32));
       } else {
         G[i] = make_uint2(b, off[0] | (off[1] << 16));
       }

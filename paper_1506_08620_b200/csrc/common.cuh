@@ -26,13 +26,18 @@ template <int SLOTS> struct RecWord;
 template <> struct RecWord<6> { using type = uint4; };
 template <> struct RecWord<2> { using type = uint2; };
 template <> struct RecWord<8> { using type = uint4; };
+template <> struct RecWord<3> { using type = uint2; };
 constexpr uint32_t kRecSentinel = 0x7FFFu;
 constexpr int kRecMaxShift = 14;
 // 16-B records with eight 12-bit offset fields (FS_SPARSE_RECORDS12): each
 // field stored as 0x800 | offset (guard bit preset, offsets < 2^10), unused
 // fields 0xFFF; shifts up to 10.
 constexpr int kRec12MaxShift = 10;
-template <int SLOTS> constexpr int rec_max_shift() { return SLOTS == 8 ? kRec12MaxShift : kRecMaxShift; }
+// 8-B records with three 13-bit offset fields (FS_SPARSE_RECORDS8X3): the
+// 64-bit word is base (bits 0..23, N + 1 <= 2^24) | overflow (bit 24) | fields
+// 0x1000 | offset at bits 25 + 13k (offsets < 2^11, unused 0x1FFF); shifts up
+// to 11.
+constexpr int kRec3MaxShift = 11;
 
 // ---------------------------------------------------------------------------
 // Exact arithmetic in the partition's precision

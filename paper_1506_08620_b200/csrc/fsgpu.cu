@@ -147,12 +147,16 @@ int validate_plan(const fs_plan* p) {
                            p->hot_knot0 > p->n1 || p->hot_knots > p->n1 - p->hot_knot0))
         return fail(FS_INVALID_ARG, "hot window outside the rank directory / knots");
       if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS &&
-                        p->sparse_format != FS_SPARSE_RECORDS8 && p->sparse_format != FS_SPARSE_RECORDS12))
+                        p->sparse_format != FS_SPARSE_RECORDS8 && p->sparse_format != FS_SPARSE_RECORDS12 &&
+                        p->sparse_format != FS_SPARSE_RECORDS8X3))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
+      if (p->sparse && p->sparse_format == FS_SPARSE_RECORDS8X3 && p->n1 > (1ull << 24))
+        return fail(FS_INVALID_ARG, "3-offset records need N+1 <= 2^24");
       if (p->sparse && (p->sparse_shift < 5 ||
                         p->sparse_shift > (p->sparse_format == FS_SPARSE_TWO_LEVEL    ? 16
                                            : p->sparse_format == FS_SPARSE_RECORDS12 ? kRec12MaxShift
-                                                                                     : kRecMaxShift) ||
+                                           : p->sparse_format == FS_SPARSE_RECORDS8X3 ? kRec3MaxShift
+                                                                                      : kRecMaxShift) ||
                         p->sparse_ndense > (p->r >> p->sparse_shift) + 2))
         return fail(FS_INVALID_ARG, "sparse table parameters out of range");
       break;
@@ -678,6 +682,8 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS)
         return dispatch_records<T, OutT, 6>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
+      if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS8X3)
+        return dispatch_records<T, OutT, 3>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS12)
         return dispatch_records<T, OutT, 8>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS8)
@@ -968,15 +974,22 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
 
 namespace {
 bool is_record_format(int32_t format) {
-  return format == FS_SPARSE_RECORDS || format == FS_SPARSE_RECORDS8 || format == FS_SPARSE_RECORDS12;
+  return format == FS_SPARSE_RECORDS || format == FS_SPARSE_RECORDS8 || format == FS_SPARSE_RECORDS12 ||
+         format == FS_SPARSE_RECORDS8X3;
 }
-int record_max_shift(int32_t format) { return format == FS_SPARSE_RECORDS12 ? kRec12MaxShift : kRecMaxShift; }
+int record_max_shift(int32_t format) {
+  return format == FS_SPARSE_RECORDS12 ? kRec12MaxShift : format == FS_SPARSE_RECORDS8X3 ? kRec3MaxShift : kRecMaxShift;
+}
+int record_bytes(int32_t format) { return format == FS_SPARSE_RECORDS8 || format == FS_SPARSE_RECORDS8X3 ? 8 : 16; }
+uint64_t record_slots(int32_t format) {
+  return format == FS_SPARSE_RECORDS ? 6 : format == FS_SPARSE_RECORDS12 ? 8 : format == FS_SPARSE_RECORDS8X3 ? 3 : 2;
+}
 }  // namespace
 
 uint64_t fs_sparse_rec_bytes(int32_t format, uint64_t n1, uint64_t r, int32_t shift, uint64_t novf) {
   if (!is_record_format(format) || shift < 5 || shift > record_max_shift(format)) return 0;
   const uint64_t ng = (r >> shift) + 2;
-  return ((format == FS_SPARSE_RECORDS8 ? 8 : 16) * ng + (novf ? 2 * n1 : 0) + 15) & ~15ull;
+  return (record_bytes(format) * ng + (novf ? 2 * n1 : 0) + 15) & ~15ull;
 }
 
 int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
@@ -985,7 +998,8 @@ int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_
   if (!x_dev || !f_scratch_dev || n1 < 2 || !shift_out) return fail(FS_INVALID_ARG, "bad arguments");
   if (!is_record_format(format)) return fail(FS_INVALID_ARG, "not a record format");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "group records need R < 2^32, N < 2^31");
-  const uint64_t slots = format == FS_SPARSE_RECORDS ? 6 : format == FS_SPARSE_RECORDS12 ? 8 : 2;
+  if (format == FS_SPARSE_RECORDS8X3 && n1 > (1ull << 24)) return fail(FS_TOO_LARGE, "3-offset records need N+1 <= 2^24");
+  const uint64_t slots = record_slots(format);
   const int max_shift = record_max_shift(format);
   const uint64_t xb = with_x ? align128(n1 * (dtype == FS_F32 ? 4 : 8)) : 0;
   if (xb + fs_sparse_rec_bytes(format, n1, r, max_shift, 0) > budget_bytes)
@@ -1043,6 +1057,7 @@ int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64
   if (!is_record_format(format)) return fail(FS_INVALID_ARG, "not a record format");
   if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2 || shift < 5 || shift > record_max_shift(format))
     return fail(FS_INVALID_ARG, "bad arguments");
+  if (format == FS_SPARSE_RECORDS8X3 && n1 > (1ull << 24)) return fail(FS_TOO_LARGE, "3-offset records need N+1 <= 2^24");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "group records need R < 2^32, N < 2^31");
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
   if (rc) return rc;
@@ -1057,7 +1072,8 @@ int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64
   } else {
     uint2* G = static_cast<uint2*>(buf_dev);
     uint16_t* F = novf ? reinterpret_cast<uint16_t*>(G + ng) : nullptr;
-    fill_sparse_rec_kernel<2><<<grid, 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
+    if (format == FS_SPARSE_RECORDS8) fill_sparse_rec_kernel<2><<<grid, 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
+    else fill_sparse_rec_kernel<3><<<grid, 256, 0, s>>>(f_scratch_dev, n1, r, shift, G, F);
   }
   FS_CUDA(cudaGetLastError());
   FS_CUDA(cudaStreamSynchronize(s));

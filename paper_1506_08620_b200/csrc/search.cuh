@@ -355,6 +355,16 @@ struct SparseRecProbe {
       return __ldg(X + t);
     }
   }
+  // a record's first knot index and overflow flag (8-B/3-offset records keep
+  // them in bits 0..23 and 24, the others in 31 bits and bit 31)
+  static __device__ __forceinline__ uint32_t base_of(Rec g) {
+    if constexpr (SLOTS == 3) return g.x & 0xFFFFFFu;
+    else return g.x & ~kDenseFlag;
+  }
+  static __device__ __forceinline__ bool overflows(Rec g) {
+    if constexpr (SLOTS == 3) return (g.x >> 24) & 1u;
+    else return (g.x & kDenseFlag) != 0;
+  }
   // (t, knot) of bucket j from its group record g
   __device__ __forceinline__ void resolve(Rec g, uint32_t j, uint32_t& t, bool& knot) const {
     constexpr uint32_t H = 0x80008000u;
@@ -363,7 +373,20 @@ struct SparseRecProbe {
     // (offsets and jl < 2^15: no borrow crosses a half)
     const uint32_t hm = H - jl * 0x10001u;
     uint32_t ge, lt;
-    if constexpr (SLOTS == 8) {
+    if constexpr (SLOTS == 3) {
+      // 64-bit SWAR: fields (0x1000 | offset) - jl at bits 25 + 13k keep their
+      // guard bit (37, 50, 63) iff offset >= jl; bits 0..24 are untouched
+      const uint32_t ylo = jl << 25, yhi = jl * 0x80040u + (jl >> 7);
+      uint32_t dlo, dhi;
+      asm("sub.cc.u32 %0, %2, %4;\n\tsubc.u32 %1, %3, %5;" : "=r"(dlo), "=r"(dhi) : "r"(g.x), "r"(g.y), "r"(ylo),
+          "r"(yhi));
+      (void)dlo;
+      ge = __popc(dhi & 0x80040020u);
+      lt = 3u - ge;
+      const unsigned long long w64 = ((unsigned long long)g.y << 32) | g.x;
+      const uint32_t fv = (uint32_t)(w64 >> (lt < 3u ? 25u + 13u * lt : 63u));  // field lt
+      knot = lt < 3u && (fv & 0xFFFu) == jl;
+    } else if constexpr (SLOTS == 8) {
       // 96-bit SWAR: fields (0x800 | offset) - jl keep bit 11 iff offset >= jl
       // (no borrow leaves a field); Y = jl in every 12-bit field
       const uint32_t y0 = jl * 0x01001001u;
@@ -395,10 +418,10 @@ struct SparseRecProbe {
       lt = SLOTS - ge;
       knot = lt < SLOTS && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
     }
-    t = (g.x & ~kDenseFlag) + lt;
+    t = base_of(g) + lt;
     if constexpr (OVF) {
-      if ((g.x & kDenseFlag) && lt == SLOTS) {  // past the last recorded knot of an overflowing super-bucket
-        uint32_t lo = t, hi = G[(j >> s) + 1].x & ~kDenseFlag;
+      if (overflows(g) && lt == SLOTS) {  // past the last recorded knot of an overflowing super-bucket
+        uint32_t lo = t, hi = base_of(G[(j >> s) + 1]);
         const uint32_t end = hi;
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;

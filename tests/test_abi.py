@@ -95,7 +95,8 @@ def test_argument_validation_without_gpu():
     assert rb(_lib.SPARSE_RECORDS, 4, 1000, 15, 0) == 0 and rb(_lib.SPARSE_RECORDS, 4, 1000, 5, 0) == 16 * 33
     assert rb(_lib.SPARSE_RECORDS8, 4, 1000, 5, 0) == (8 * 33 + 15) // 16 * 16
     assert rb(_lib.SPARSE_RECORDS8, 4, 1000, 5, 2) == (8 * 33 + 2 * 4 + 15) // 16 * 16
-    assert rb(_lib.SPARSE_TWO_LEVEL, 4, 1000, 5, 0) == 0 and rb(4, 4, 1000, 5, 0) == 0
+    assert rb(_lib.SPARSE_TWO_LEVEL, 4, 1000, 5, 0) == 0 and rb(5, 4, 1000, 5, 0) == 0
+    assert rb(_lib.SPARSE_RECORDS8X3, 4, 1000, 11, 0) == 16 and rb(_lib.SPARSE_RECORDS8X3, 4, 1000, 12, 0) == 0
     assert rb(_lib.SPARSE_RECORDS12, 4, 1000, 10, 0) == 16 * 2 and rb(_lib.SPARSE_RECORDS12, 4, 1000, 11, 0) == 0
 
 

@@ -16,8 +16,8 @@ from oracle import fs_oracle as orc
 pytestmark = pytest.mark.gpu
 
 SENTINEL = 0x7FFF
-FORMATS = {"records": 6, "records8": 2, "records12": 8}  # offset slots per record
-MAX_SHIFT = {"records": 14, "records8": 14, "records12": 10}
+FORMATS = {"records": 6, "records8": 2, "records12": 8, "records8x3": 3}  # offset slots per record
+MAX_SHIFT = {"records": 14, "records8": 14, "records12": 10, "records8x3": 11}
 
 
 def _fs():
@@ -29,7 +29,8 @@ def _fs():
 def _fmt_code(name):
     from paper_1506_08620_b200 import _lib
 
-    return {"records": _lib.SPARSE_RECORDS, "records8": _lib.SPARSE_RECORDS8, "records12": _lib.SPARSE_RECORDS12}[name]
+    return {"records": _lib.SPARSE_RECORDS, "records8": _lib.SPARSE_RECORDS8, "records12": _lib.SPARSE_RECORDS12,
+            "records8x3": _lib.SPARSE_RECORDS8X3}[name]
 
 
 def expected_records(xs, h, r, s, slots=6):
@@ -38,15 +39,19 @@ def expected_records(xs, h, r, s, slots=6):
     f = orc.knot_buckets(xs, h).astype(np.uint64)
     ng = (r >> s) + 2
     base = np.searchsorted(f, np.arange(ng, dtype=np.uint64) << np.uint64(s), side="left").astype(np.int64)
-    rec = np.zeros((ng, 4 if slots == 8 else 1 + slots // 2), dtype=np.uint32)
+    rec = np.zeros((ng, {8: 4, 3: 2}.get(slots, 1 + slots // 2)), dtype=np.uint32)
     mask = (1 << s) - 1
     for J in range(ng):
         lo = int(base[J])
         hi = int(base[J + 1]) if J + 1 < ng else lo
         offs = [int(f[i]) & mask for i in range(lo, min(hi, lo + slots))]
-        offs += [0x7FF if slots == 8 else SENTINEL] * (slots - len(offs))
+        offs += [{8: 0x7FF, 3: 0xFFF}.get(slots, SENTINEL)] * (slots - len(offs))
         rec[J, 0] = lo | ((hi - lo > slots) << 31)
-        if slots == 8:
+        if slots == 3:
+            w = lo | ((hi - lo > slots) << 24)
+            w |= sum((0x1000 | o) << (25 + 13 * e) for e, o in enumerate(offs))
+            rec[J, 0], rec[J, 1] = w & 0xFFFFFFFF, w >> 32
+        elif slots == 8:
             bits = sum((0x800 | o) << (12 * e) for e, o in enumerate(offs))
             for w in range(3):
                 rec[J, 1 + w] = (bits >> (32 * w)) & 0xFFFFFFFF
@@ -68,7 +73,7 @@ def with_records(fs, p, prep, s, fmt="records"):
 
     idx = prep.structure
     rec, _ = expected_records(p.values, idx.h, idx.r, s, FORMATS[fmt])
-    novf = int(np.count_nonzero(rec[:, 0] >> 31))
+    novf = int(np.count_nonzero((rec[:, 0] >> 24) & 1 if fmt == "records8x3" else rec[:, 0] >> 31))
     lib = _lib.load()
     code = _fmt_code(fmt)
     nbytes = int(lib.fs_sparse_rec_bytes(code, len(p.values), idx.r, s, novf))
@@ -130,7 +135,7 @@ def test_records_chosen_for_sparse_configs(cuda):
     fs = _fs()
     from paper_1506_08620_b200 import workloads
 
-    for name, kw, fmts, sx in (("cfg2", {}, ("records",), True), ("cfg2", {"seed": 1}, ("records8",), False),
+    for name, kw, fmts, sx in (("cfg2", {}, ("records", "records8x3"), True), ("cfg2", {"seed": 1}, ("records8",), False),
                                ("cfg5", {"n1": 1025}, ("records8",), True),
                                ("cfg5", {"n1": 32769}, ("records", "records12"), False)):
         p = workloads.knots(name, **kw)
@@ -143,7 +148,7 @@ def test_records_chosen_for_sparse_configs(cuda):
         rec, fmod = expected_records(p.values, idx.h, idx.r, s, FORMATS[fmt])
         buf = _buffer_of(prep, prep.plan.sparse).cpu().numpy()
         assert np.array_equal(buf[: rec.nbytes].view(np.uint32).reshape(rec.shape), rec), name
-        novf = int(np.count_nonzero(rec[:, 0] >> 31))
+        novf = int(np.count_nonzero((rec[:, 0] >> 24) & 1 if fmt == "records8x3" else rec[:, 0] >> 31))
         assert prep.plan.sparse_ndense == novf
         if novf:
             assert np.array_equal(buf[rec.nbytes: rec.nbytes + 2 * len(fmod)].view(np.uint16), fmod.astype(np.uint16))
@@ -242,7 +247,8 @@ def test_records_abi_validation(cuda):
     p = workloads.knots("cfg5", n1=1025)
     prep = _records_forced(fs, p)
     z = orc.random_queries(p.values, 1000, seed=1)
-    for fmt, shift in ((4, prep.plan.sparse_shift), (_lib.SPARSE_RECORDS, 15), (_lib.SPARSE_RECORDS12, 11)):
+    for fmt, shift in ((5, prep.plan.sparse_shift), (_lib.SPARSE_RECORDS, 15), (_lib.SPARSE_RECORDS12, 11),
+                       (_lib.SPARSE_RECORDS8X3, 12)):
         keep = (prep.plan.sparse_format, prep.plan.sparse_shift)
         prep.plan.sparse_format, prep.plan.sparse_shift = fmt, shift
         with pytest.raises(ValueError):

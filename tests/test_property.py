@@ -130,7 +130,7 @@ def test_gpu_big_tables_equal_oracle(cuda, xs):
 
     keep = batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, batch.SPARSE_RECORDS8_MAX_PAST_PPM
     try:
-        for fmt in (("records",), ("records8",), ("records12",), ("two-level",)):
+        for fmt in (("records",), ("records8",), ("records12",), ("records8x3",), ("two-level",)):
             batch.SPARSE_FORMATS = fmt
             batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = batch.SPARSE_RECORDS8_MAX_PAST_PPM = 10**6
             try:

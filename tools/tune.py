@@ -103,12 +103,13 @@ def main():
                         "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
                 if algo.startswith("direct-hot:"):  # hot window of the given size in KB
                     base = "direct"
-                if algo in ("direct-sparse2", "direct-rec", "direct-rec8", "direct-rec12"):  # force one sparse format
+                if algo in ("direct-sparse2", "direct-rec", "direct-rec8", "direct-rec12", "direct-rec8x3"):
                     from paper_1506_08620_b200 import batch as _b
 
                     keep = (_b.SPARSE_FORMATS, _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, _b.SPARSE_RECORDS8_MAX_PAST_PPM)
                     _b.SPARSE_FORMATS = {"direct-sparse2": ("two-level",), "direct-rec": ("records",),
-                                         "direct-rec8": ("records8",), "direct-rec12": ("records12",)}[algo]
+                                         "direct-rec8": ("records8",), "direct-rec12": ("records12",),
+                                         "direct-rec8x3": ("records8x3",)}[algo]
                     _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = _b.SPARSE_RECORDS8_MAX_PAST_PPM = 10**6
                     try:
                         prep = fs.prepare("direct", p)
