@@ -474,6 +474,17 @@ template <int SLOTS, bool XS, bool OVF>
 struct UnrollFor<double, SparseRecProbe<double, SLOTS, XS, OVF>> {
   static constexpr int value = FSG_UNROLL_F64_REC;
 };
+// The light three-offset probe takes a third group with int32 outputs (cfg2
+// 459 -> 470 Gq/s; int64 outputs 370 -> 355 and the other probes lose with
+// it: profiles/r01/tune_sparse_records.txt).
+template <typename T, typename Probe, typename OutT>
+struct UnrollOutFor {
+  static constexpr int value = UnrollFor<T, Probe>::value;
+};
+template <bool XS, bool OVF>
+struct UnrollOutFor<double, SparseRecProbe<double, 3, XS, OVF>, int32_t> {
+  static constexpr int value = 3;
+};
 // Probes launched through the 1024-thread-bounded entry point: the sparse
 // probe with X in smem exceeds 64 registers with int64 outputs and gains
 // from 1024-thread CTAs despite small spills (cfg2 int64 222 -> 264 Gq/s);
@@ -556,7 +567,7 @@ template <typename T, typename OutT, typename Probe>
 int launch_probe(const DevPlan<T>& dp, const Placement& pl, const T* z, uint64_t m, OutT* out,
                  unsigned long long* first_bad, uint64_t base, cudaStream_t st) {
   constexpr int VW = VecWidthFor<T, OutT, Probe>::value;
-  constexpr int kU = VW == 8 ? UnrollVW8For<Probe>::value : UnrollFor<T, Probe>::value;
+  constexpr int kU = VW == 8 ? UnrollVW8For<Probe>::value : UnrollOutFor<T, Probe, OutT>::value;
   auto kern = [] {
     if constexpr (BoundedFor<T, Probe, OutT>::value) return search_kernel_1k<T, OutT, Probe, kU, VW>;
     else return search_kernel<T, OutT, Probe, kU, VW>;
