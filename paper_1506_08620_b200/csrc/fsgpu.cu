@@ -1015,6 +1015,11 @@ int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_
   const uint64_t xb = with_x ? align128(n1 * (dtype == FS_F32 ? 4 : 8)) : 0;
   if (xb + fs_sparse_rec_bytes(format, n1, r, max_shift, 0) > budget_bytes)
     return fail(FS_TOO_LARGE, "no group-record layout fits the budget");
+  // every layout holds each knot in a record slot or in F: at least
+  // min(n1 / slots records, 2 n1 bytes of F) -- skip the scan when even that
+  // exceeds the budget (large N: the directory stays in L2)
+  if (xb + std::min<uint64_t>((n1 / slots) * (uint64_t)record_bytes(format), 2 * n1) > budget_bytes)
+    return fail(FS_TOO_LARGE, "no group-record layout fits the budget");
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
   if (rc) return rc;
   std::vector<uint64_t> f(n1);
