@@ -1338,7 +1338,7 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   const bool overlap = (flags & FS_HOST_OVERLAP) != 0;
   const size_t es = plan->dtype == FS_F32 ? 4 : 8;
   if (chunk_elems == 0) chunk_elems = (64ull << 20) / es;
-  chunk_elems = (chunk_elems + 3) & ~3ull;  // keep every chunk 16-B aligned on device
+  chunk_elems = (chunk_elems + 7) & ~7ull;  // keep every chunk 32-B aligned on device (8-query groups)
   Placement pl = place_for_batch(plan, m);
   pl.merge = 1;  // every chunk min-merges into status[0]
   // atomic mode over several chunks: host threads check the domain while the
