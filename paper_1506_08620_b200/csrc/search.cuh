@@ -304,11 +304,12 @@ struct SparseProbe {
 };
 
 // Direct search (gap 1) over the group records of K (fill_sparse_rec_kernel),
-// staged in shared memory after X when X fits.  One LDS per query (16-B
-// records with six offsets, or 8-B records with two):
+// staged in shared memory after X when X fits.  One LDS per query; SLOTS
+// selects the layout: 6 (16 B, 16-bit offsets), 2 (8 B, 16-bit offsets),
+// 8 (16 B, 12-bit fields), 3 (8 B, 13-bit fields beside a 24-bit base).
 // t = K[j] = base + #{record offsets < j mod 2^s}, counted branch-free with
-// a 15-bit SWAR compare of the packed offsets (sentinels never count);
-// bucket j holds knot t iff offset slot t - base equals j mod 2^s.  Only a
+// a SWAR compare of the packed offsets (guard bit per field; sentinels never
+// count); bucket j holds knot t iff offset slot t - base equals j mod 2^s.  Only a
 // query in an overflowing super-bucket (more than SLOTS knots) whose bucket
 // lies past its last recorded knot continues with a lower_bound over F (OVF).
 // Identical answers to DirectProbe<GAP=1> (batch.py:315-317).
