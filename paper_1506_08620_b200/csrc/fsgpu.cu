@@ -481,9 +481,19 @@ template <typename T, typename Probe, typename OutT>
 struct UnrollOutFor {
   static constexpr int value = UnrollFor<T, Probe>::value;
 };
+#ifndef FSG_UNROLL_REC3
+#define FSG_UNROLL_REC3 3
+#endif
+#ifndef FSG_UNROLL_REC12
+#define FSG_UNROLL_REC12 FSG_UNROLL_F64_REC
+#endif
 template <bool XS, bool OVF>
 struct UnrollOutFor<double, SparseRecProbe<double, 3, XS, OVF>, int32_t> {
-  static constexpr int value = 3;
+  static constexpr int value = FSG_UNROLL_REC3;
+};
+template <bool XS, bool OVF>
+struct UnrollOutFor<double, SparseRecProbe<double, 8, XS, OVF>, int32_t> {
+  static constexpr int value = FSG_UNROLL_REC12;
 };
 // Probes launched through the 1024-thread-bounded entry point: the sparse
 // probe with X in smem exceeds 64 registers with int64 outputs and gains
