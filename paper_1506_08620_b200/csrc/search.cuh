@@ -449,7 +449,10 @@ struct SparseRecProbe {
     // live-register bound (2-4 regs per record); the wide-field layouts (3
     // and 8 offsets) measure best two at a time (cfg2 470 -> 496, cfg5 N+1 =
     // 32769 403 -> 410 Gq/s; profiles/r01/tune_sparse_records.txt)
-    constexpr int GW = (SLOTS == 3 || SLOTS == 8) ? 2 : FSG_REC_GROUP;
+#ifndef FSG_REC_GROUP_WIDE
+#define FSG_REC_GROUP_WIDE 2
+#endif
+    constexpr int GW = (SLOTS == 3 || SLOTS == 8) ? FSG_REC_GROUP_WIDE : FSG_REC_GROUP;
     constexpr int GR = N < GW ? N : GW;
 #pragma unroll
     for (int g0 = 0; g0 < N; g0 += GR) {
