@@ -144,11 +144,11 @@ const char* fs_last_error(void);
 size_t fs_workspace_bytes(void);
 
 /* ---------------------------------------------------------------------------
- * Index construction (direct.py:433-561)
+ * Index construction (direct.py:135-263)
  * ------------------------------------------------------------------------ */
 
 /*
- * Certified scale factor.  Replaces direct.compute_h_r (direct.py:433-489):
+ * Certified scale factor.  Replaces direct.compute_h_r (direct.py:135-191):
  * D = RN(X - X0); collision of D[i+q] == D[i] -> FS_NOT_DISTINGUISHABLE with
  * *pos_out = first i+q; h = RN(1 / min RN(D[i+b] - D[i])), b = min(q, N);
  * FS_OVERFLOW unless RN(h * D_N) < 2^qbits; growth loop with doubling ulp
@@ -162,14 +162,14 @@ int fs_certify(int32_t dtype, const void* x_dev, uint64_t n1, int32_t qbits, int
 
 /*
  * Knot buckets f_i = floor(RN(h * RN(X_i - X0))) as uint64.  Replaces
- * direct.knot_buckets (direct.py:492-495).
+ * direct.knot_buckets (direct.py:194-197).
  */
 int fs_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t* f_dev,
                     void* stream);
 
 /*
- * Bucket table K.  Replaces direct.build_index (direct.py:498-541) and
- * knot_buckets (direct.py:492-495): f_i = floor(RN(h * RN(X_i - X0)));
+ * Bucket table K.  Replaces direct.build_index (direct.py:200-243) and
+ * knot_buckets (direct.py:194-197): f_i = floor(RN(h * RN(X_i - X0)));
  * FS_INCONSISTENT unless f_N == r; q == 1: K[j] = i for f_{i-1} < j <= f_i,
  * K[0] = 0; q > 1: K[j] = max{i : f_i <= j}.  k_dev holds r+1 uint32.
  * f_scratch_dev holds n1 uint64.  SYNC (reads back the consistency flag).
@@ -193,7 +193,7 @@ int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
 
 /*
  * Rank directory of the gap-2 table (a device layout of build_index with
- * q = 2, direct.py:498-541; no reference counterpart).  A gap-2 certificate
+ * q = 2, direct.py:200-243; no reference counterpart).  A gap-2 certificate
  * allows at most two knots per bucket, so each 32-bucket word is 16 B
  * {m1: buckets with a knot, m2: buckets with two, base = K-count before the
  * word, 0}; the gap-2 kernel recovers K2[j] exactly and reads X only for
@@ -229,7 +229,7 @@ int fs_build_sparse(int32_t dtype, const void* x_dev, uint64_t n1, double h, uin
 
 /*
  * Group records of the gap-1 table (a device layout of build_index,
- * direct.py:498-541; no reference counterpart), for R >> N.  The
+ * direct.py:200-243; no reference counterpart), for R >> N.  The
  * super-buckets of fs_build_sparse, each packed into one record {base |
  * overflow flag (bit 31), S uint16 knot offsets}: FS_SPARSE_RECORDS is 16 B
  * with S = 6, FS_SPARSE_RECORDS8 is 8 B with S = 2, FS_SPARSE_RECORDS12 is
@@ -280,7 +280,7 @@ int fs_build_hot_window(int32_t dtype, const void* dir_dev, uint64_t r, uint64_t
 
 /*
  * Cache-fused (idx, val) records.  Replaces direct.with_fused
- * (direct.py:553-561): rec[j] = {K[j], X[K[j]]}; 8 B records for f32,
+ * (direct.py:255-263): rec[j] = {K[j], X[K[j]]}; 8 B records for f32,
  * 16 B {u32 idx, u32 pad = 0, f64 val} for f64.
  */
 int fs_build_fused(int32_t dtype, const void* x_dev, uint64_t n1, const uint32_t* k_dev,

@@ -146,7 +146,7 @@ def pad_right_pow2(xs: np.ndarray):
 
 
 def compute_h_r(xs: np.ndarray, qbits: int = 32, q: int = 1):
-    """direct.py:433-489, op for op in the array's precision.
+    """direct.py:135-191, op for op in the array's precision.
 
     Returns (h, r, increments, h_start) or raises OracleError.
     """
@@ -181,12 +181,12 @@ def compute_h_r(xs: np.ndarray, qbits: int = 32, q: int = 1):
 
 
 def knot_buckets(xs: np.ndarray, h) -> np.ndarray:
-    """direct.py:492-495."""
+    """direct.py:194-197."""
     return np.floor(h * (xs - xs[0])).astype(np.int64)
 
 
 def build_table(xs: np.ndarray, h, r: int, q: int = 1) -> np.ndarray:
-    """direct.py:498-527: K as np.repeat of knot indices over bucket runs."""
+    """direct.py:200-229: K as np.repeat of knot indices over bucket runs."""
     n = len(xs) - 1
     f = knot_buckets(xs, h)
     if f[-1] != r:
@@ -207,7 +207,7 @@ FUSED_DTYPES = {
 
 
 def fused_records(xs: np.ndarray, k: np.ndarray) -> np.ndarray:
-    """direct.py:553-561."""
+    """direct.py:255-263."""
     rec = np.zeros(len(k), dtype=FUSED_DTYPES[xs.dtype])
     rec["idx"] = k
     rec["val"] = xs[k]
@@ -233,7 +233,7 @@ def gap2_lanes(xs, h, k, z):
 
 
 def generic_lanes(xs, h, k, q, z):
-    """direct.py:592-598 vectorised."""
+    """direct.py:294-300 vectorised."""
     t = k[(h * (z - xs[0])).astype(np.int64)].astype(np.int64)
     hits = np.zeros_like(t)
     for m in range(q):

@@ -81,6 +81,7 @@ def _plan_for(algorithm: str, structure, p: SortedPartition):
     plan.n1 = len(p.values)
     x = p.device_values()
     plan.x = x.data_ptr()
+    plan.device_index = x.get_device()  # (Python-side only: the device the tables live on)
     plan.x0 = float(p.values[0])
     plan.xn = float(p.values[-1])
     plan.q = 1
@@ -189,7 +190,32 @@ def first_bad_of(status):
     return None if bad == -1 else bad
 
 
+def _check_device_batch(plan, z, out) -> None:
+    """Device batches the C-ABI can take as they are: query dtype = the
+    partition's (a narrower or wider buffer would be read with the wrong
+    element size), int32/int64 ``out``, both contiguous and on the
+    partition's device (the kernel writes ``out.numel()`` consecutive
+    elements from its base address)."""
+    import torch
+
+    want = torch.float32 if plan.dtype == _lib.FS_F32 else torch.float64
+    if z.dtype != want:
+        raise ValueError(f"query dtype {z.dtype} does not match the partition's {want}")
+    if out.dtype not in (torch.int32, torch.int64):
+        raise ValueError("out must be int32 or int64")
+    if not (z.is_cuda and out.is_cuda):
+        raise ValueError("device-resident batches need CUDA tensors for both queries and out")
+    if z.device != out.device or z.get_device() != plan.device_index:
+        raise ValueError(f"queries ({z.device}), out ({out.device}) and the prepared structure "
+                         f"(cuda:{plan.device_index}) must be on one device")
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous (search into a contiguous tensor and copy_ it)")
+    if out.numel() < z.numel():
+        raise ValueError("output array is smaller than the query batch")
+
+
 def _search_device_tensor(plan, z, out) -> None:
+    _check_device_batch(plan, z, out)
     st = _cached_status(z.device, _device.stream_ptr())
     _launch_device(plan, z, out, st)
     bad = first_bad_of(st)
@@ -224,7 +250,9 @@ class PreparedKernel:
         receives the first out-of-domain position (UINT64_MAX when clean;
         read it with ``first_bad_of``).  ``out`` is unspecified for
         out-of-domain queries.  No host synchronisation; capturable in a
-        CUDA graph."""
+        CUDA graph.  Raises ValueError for a dtype, device or layout the
+        kernel cannot take as is (``_check_device_batch``)."""
+        _check_device_batch(self.plan, z, out)
         _launch_device(self.plan, z, out, status)
 
     def placement(self) -> dict:
@@ -650,7 +678,13 @@ def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None, *, a
             raise ValueError(f"query dtype {z.dtype} does not match the partition's {p.values.dtype}")
         if out.dtype not in (torch.int32, torch.int64):
             raise ValueError("out must be int32 or int64")
-        _search_device_tensor(kern.plan, z.contiguous(), out[:m])
+        o = out[:m]
+        if o.is_contiguous():
+            _search_device_tensor(kern.plan, z.contiguous(), o)
+        else:  # any writable view, as the reference's slice assignment allows (batch.py:423)
+            tmp = torch.empty(m, dtype=out.dtype, device=out.device)
+            _search_device_tensor(kern.plan, z.contiguous(), tmp)
+            o.copy_(tmp)
         return m
     zz = coerce_queries(z, p.values.dtype)
     if isinstance(out, np.ndarray):

@@ -1,15 +1,15 @@
 // build.cuh — index construction kernels.
 //
 //   certify_prep / certify_finalize / certify_check / certify_grow
-//       restate direct.compute_h_r (direct.py:433-489) op for op
+//       restate direct.compute_h_r (direct.py:135-191) op for op
 //   knot_buckets_kernel  direct.knot_buckets + the f[-1] == r check
-//                        (direct.py:492-495, 513-515)
-//   fill_table_kernel    the np.repeat of build_index (direct.py:516-524),
+//                        (direct.py:194-197, 215-217)
+//   fill_table_kernel    the np.repeat of build_index (direct.py:218-226),
 //                        restated as K[j] = lower_bound(f, j) (gap 1) or
 //                        upper_bound(f, j) - 1 (gap > 1): bucket-parallel,
 //                        coalesced writes, O(R log(range)) instead of a
 //                        per-knot scatter whose run lengths vary by 10^4x
-//   fill_fused_kernel    direct.with_fused (direct.py:553-561)
+//   fill_fused_kernel    direct.with_fused (direct.py:255-263)
 //   pad_right_kernel     partition.pad_right_pow2 (partition.py:163-171)
 //   eytzinger_kernel     eytzinger.build_layout (eytzinger.py:45-63)
 #pragma once
@@ -57,7 +57,7 @@ __device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v
 }
 
 // K1: collisions of the rounded offsets and the smallest gap-b difference.
-// direct.py:454-464.
+// direct.py:156-166.
 template <typename T, int NT>
 __global__ void __launch_bounds__(NT) certify_prep(const T* __restrict__ x, uint64_t n1, uint64_t q,
                                                    uint64_t basis, CertStatus* st) {
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(NT) certify_prep(const T* __restrict__ x, uint
   }
 }
 
-// Initial guess, overflow test and first increment.  direct.py:456-471.
+// Initial guess, overflow test and first increment.  direct.py:158-173.
 template <typename T>
 __global__ void certify_finalize(const T* __restrict__ x, uint64_t n1, int qbits, CertStatus* st) {
   if (st->collide_pos != ~0ull) {
@@ -103,7 +103,7 @@ __global__ void certify_finalize(const T* __restrict__ x, uint64_t n1, int qbits
   st->growth = (double)sub_rn(next_up(h), h);
 }
 
-// K2: certify every gap-q pair at the current H.  direct.py:474-476, 483.
+// K2: certify every gap-q pair at the current H.  direct.py:176-178, 185.
 template <typename T, int NT>
 __global__ void __launch_bounds__(NT) certify_check(const T* __restrict__ x, uint64_t n1, uint64_t q,
                                                     CertStatus* st) {
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(NT) certify_check(const T* __restrict__ x, uin
 }
 
 // One growth step: h += growth; overflow test; growth doubles.
-// direct.py:477-481.
+// direct.py:179-183.
 template <typename T>
 __global__ void certify_grow(const T* __restrict__ x, uint64_t n1, int qbits, CertStatus* st) {
   const T span = sub_rn(x[n1 - 1], x[0]);
@@ -139,7 +139,7 @@ __global__ void certify_grow(const T* __restrict__ x, uint64_t n1, int qbits, Ce
   st->growth = (double)add_rn(g, g);
 }
 
-// f_i = floor(RN(h * RN(X_i - X0))) as an integer.  direct.py:492-495.
+// f_i = floor(RN(h * RN(X_i - X0))) as an integer.  direct.py:194-197.
 template <typename T>
 __global__ void knot_buckets_kernel(const T* __restrict__ x, uint64_t n1, T h, uint64_t r,
                                     uint64_t* __restrict__ f, CertStatus* st) {
@@ -381,7 +381,7 @@ __global__ void hot_window_finish(const uint2* __restrict__ dir, uint64_t words,
   out[2] = dir[lo].y;
 }
 
-// Fused (idx, val) records.  direct.py:553-561.
+// Fused (idx, val) records.  direct.py:255-263.
 __global__ void fill_fused_f32(const float* __restrict__ x, const uint32_t* __restrict__ K, uint64_t r,
                                uint2* __restrict__ rec) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= r; j += (uint64_t)gridDim.x * blockDim.x) {

@@ -11,10 +11,10 @@
 // (finalize_first_bad, common.cuh).
 //
 // Probes (each cites the reference kernel it restates):
-//   Direct<gap 1>     batch.py:315-317 / direct.py:570-574
-//   Direct<gap 2>     batch.py:341-343 / direct.py:577-589
-//   Direct<generic q> direct.py:592-598
-//   DirectCache       batch.py:368-371 / direct.py:601-610
+//   Direct<gap 1>     batch.py:315-317 / direct.py:272-276
+//   Direct<gap 2>     batch.py:341-343 / direct.py:279-291
+//   Direct<generic q> direct.py:294-300
+//   DirectCache       batch.py:368-371 / direct.py:303-312
 //   Bitset2           batch.py:193-200 / binsearch.py:72-86
 //   Bitset1 / Bitset3 batch.py:176-185, 208-216 / binsearch.py:60-69, 89-99
 //   Offset            batch.py:224-234 / binsearch.py:102-114
@@ -549,7 +549,7 @@ struct HotRankProbe {
 };
 
 // Cache-fused records: {u32 idx, f32 val} (8 B) / {u32 idx, u32 pad, f64 val}
-// (16 B), direct.py:337-342.  One gather resolves the query.
+// (16 B), direct.py:39-44.  One gather resolves the query.
 template <typename T, typename J, bool RS>
 struct CacheProbe;
 

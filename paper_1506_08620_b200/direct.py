@@ -3,10 +3,10 @@
 Drop-in for ``fastsearch/direct.py`` (direct.py:1-329).  Construction runs on
 the device through the C-ABI:
 
-  compute_h_r   -> fs_certify      (direct.py:433-489; K1/K2 kernels)
-  knot_buckets  -> fs_knot_buckets (direct.py:492-495)
-  build_index   -> fs_build_table  (direct.py:498-541; K3 bucket-parallel fill)
-  with_fused    -> fs_build_fused  (direct.py:553-561; K4)
+  compute_h_r   -> fs_certify      (direct.py:135-191; K1/K2 kernels)
+  knot_buckets  -> fs_knot_buckets (direct.py:194-197)
+  build_index   -> fs_build_table  (direct.py:200-243; K3 bucket-parallel fill)
+  with_fused    -> fs_build_fused  (direct.py:255-263; K4)
 
 and every arithmetic step is the reference's in the partition's own
 precision (see csrc/build.cuh), so h, r, the growth statistics and K are
@@ -36,7 +36,7 @@ K_DTYPE = np.uint32
 
 _FUSED_DTYPES = {
     # (knot index, knot value): 8 bytes single, 16 double with 4 zero pad
-    # bytes keeping the value aligned (direct.py:337-342).
+    # bytes keeping the value aligned (direct.py:39-44).
     "single": np.dtype([("idx", "<u4"), ("val", "<f4")]),
     "double": np.dtype([("idx", "<u4"), ("pad", "<u4"), ("val", "<f8")]),
 }
@@ -44,7 +44,7 @@ _FUSED_DTYPES = {
 
 @dataclass(frozen=True)
 class HGrowthStats:
-    """How often and how far the scale factor grew (direct.py:345-351)."""
+    """How often and how far the scale factor grew (direct.py:47-53)."""
 
     increments: int
     final_h: float
@@ -53,7 +53,7 @@ class HGrowthStats:
 
 @dataclass(frozen=True)
 class FeasibilityReport:
-    """direct.py:354-359."""
+    """direct.py:56-61."""
 
     feasible: bool
     margin: float
@@ -63,7 +63,7 @@ class FeasibilityReport:
 
 @dataclass(frozen=True)
 class DirectIndex:
-    """Immutable bucket index (direct.py:362-381), device resident.
+    """Immutable bucket index (direct.py:64-83), device resident.
 
     ``k_dev`` (uint32, r+1) and ``fused_dev`` (records) are the device
     tables the kernels read; ``k`` / ``fused`` are host views.
@@ -104,7 +104,7 @@ class DirectIndex:
 
 
 def feasibility_threshold(precision: str, qbits: int) -> float:
-    """direct.py:384-399."""
+    """direct.py:86-101."""
     table = {
         ("single", 32): 2.0 ** -23,
         ("double", 32): 2.0 ** -32,
@@ -117,7 +117,7 @@ def feasibility_threshold(precision: str, qbits: int) -> float:
 
 
 def feasibility_estimate(p: SortedPartition, qbits: int = 32, q: int = 1) -> FeasibilityReport:
-    """Advisory: smallest gap-q spacing against the span (direct.py:402-418)."""
+    """Advisory: smallest gap-q spacing against the span (direct.py:104-120)."""
     xs = p.values.astype(np.float64)
     ratio = float((xs[q:] - xs[:-q]).min() / (xs[-1] - xs[0]))
     threshold = feasibility_threshold(p.precision, qbits)
@@ -127,7 +127,7 @@ def feasibility_estimate(p: SortedPartition, qbits: int = 32, q: int = 1) -> Fea
 
 def closed_form_h_r(p: SortedPartition, q: int = 1) -> tuple[float, int]:
     """Rounding-naive sizing R = 1 + ceil(span / min gap), H = R / span
-    (direct.py:421-430)."""
+    (direct.py:123-132)."""
     xs = p.values.astype(np.float64)
     span = float(xs[-1] - xs[0])
     r = 1 + ceil(span / float((xs[q:] - xs[:-q]).min()))
@@ -135,7 +135,7 @@ def closed_form_h_r(p: SortedPartition, q: int = 1) -> tuple[float, int]:
 
 
 def compute_h_r(p: SortedPartition, qbits: int = 32, q: int = 1):
-    """Certified scale factor and bucket count, on the GPU (direct.py:433-489).
+    """Certified scale factor and bucket count, on the GPU (direct.py:135-191).
 
     Returns ``(h, r, HGrowthStats)`` with ``h`` a numpy scalar of the
     partition's dtype.  Raises NotDistinguishable(position) / Overflow
@@ -174,7 +174,7 @@ def compute_h_r(p: SortedPartition, qbits: int = 32, q: int = 1):
 
 def knot_buckets(p: SortedPartition, h) -> np.ndarray:
     """f evaluated at every knot, as int64, in the partition's precision
-    (direct.py:492-495), computed on the device."""
+    (direct.py:194-197), computed on the device."""
     x = p.device_values()
     f = _device.empty(len(p.values), np.uint64)
     rc = _lib.load().fs_knot_buckets(fs_dtype(p.precision), x.data_ptr(), len(p.values), float(h), f.data_ptr(),
@@ -184,7 +184,7 @@ def knot_buckets(p: SortedPartition, h) -> np.ndarray:
 
 
 def build_index(p: SortedPartition, h, r: int, q: int = 1, qbits: int = 32, fused: bool = False) -> DirectIndex:
-    """Materialise the bucket table K on the device (direct.py:498-541).
+    """Materialise the bucket table K on the device (direct.py:200-243).
 
     gap 1: K_j = i exactly when f(X_{i-1}) < j <= f(X_i), K_0 = 0;
     gap > 1: K_j = max{i : f(X_i) <= j}.  O(N + R) work, R+1 coalesced writes.
@@ -214,13 +214,13 @@ def build_index(p: SortedPartition, h, r: int, q: int = 1, qbits: int = 32, fuse
 
 def build(p: SortedPartition, qbits: int = 32, q: int = 1, fused: bool = False):
     """compute_h_r then build_index; returns (DirectIndex, HGrowthStats)
-    (direct.py:544-550)."""
+    (direct.py:246-252)."""
     h, r, stats = compute_h_r(p, qbits=qbits, q=q)
     return build_index(p, h, r, q=q, qbits=qbits, fused=fused), stats
 
 
 def with_fused(idx: DirectIndex, p: SortedPartition) -> DirectIndex:
-    """Attach cache-fused (index, value) records; gap-1 only (direct.py:553-561)."""
+    """Attach cache-fused (index, value) records; gap-1 only (direct.py:255-263)."""
     if idx.q != 1:
         raise ValueError("fused records pair with the gap-1 kernel")
     rec_bytes = _FUSED_DTYPES[idx.precision].itemsize
@@ -251,20 +251,20 @@ def _run_single(algorithm: str, structure, p: SortedPartition, z) -> int:
 
 
 def bucket_of(idx: DirectIndex, z) -> int:
-    """f(z) = floor(H * (z - X_0)) in the index's precision (direct.py:564-567).
+    """f(z) = floor(H * (z - X_0)) in the index's precision (direct.py:266-269).
     A scalar helper; the batch kernels fuse it."""
     t = idx.h.dtype.type
     return int(idx.h * (t(z) - idx.x0))
 
 
 def direct_search(idx: DirectIndex, p: SortedPartition, z) -> int:
-    """Gap-1 kernel, one query on the device (direct.py:570-574)."""
+    """Gap-1 kernel, one query on the device (direct.py:272-276)."""
     check_domain(p, z)
     return _run_single("direct", idx, p, z)
 
 
 def direct_search_gap2(idx: DirectIndex, p: SortedPartition, z) -> int:
-    """Gap-2 kernel, one query on the device (direct.py:577-589)."""
+    """Gap-2 kernel, one query on the device (direct.py:279-291)."""
     if idx.q != 2:
         raise ValueError("index was not built with gap 2")
     check_domain(p, z)
@@ -272,13 +272,13 @@ def direct_search_gap2(idx: DirectIndex, p: SortedPartition, z) -> int:
 
 
 def direct_search_generic(idx: DirectIndex, p: SortedPartition, z) -> int:
-    """Gap-q kernel, one query on the device (direct.py:592-598)."""
+    """Gap-q kernel, one query on the device (direct.py:294-300)."""
     check_domain(p, z)
     return _run_single("direct-generic", idx, p, z)
 
 
 def direct_search_cache(idx: DirectIndex, z, p: SortedPartition | None = None) -> int:
-    """Gap-1 kernel over fused records (direct.py:601-610).
+    """Gap-1 kernel over fused records (direct.py:303-312).
 
     The reference signature has no partition; the records carry X_N as
     the value of bucket R, which is the domain's upper end.
@@ -317,7 +317,7 @@ def _partition_of_index(idx: DirectIndex) -> SortedPartition:
 
 
 def minimal_index_bytes(n: int) -> int:
-    """Smallest power-of-two byte width covering index n (direct.py:613-618)."""
+    """Smallest power-of-two byte width covering index n (direct.py:315-320)."""
     for b in (1, 2, 4, 8):
         if 2 ** (8 * b) >= n:
             return b
@@ -325,7 +325,7 @@ def minimal_index_bytes(n: int) -> int:
 
 
 def memory_cost_estimate(p: SortedPartition, b: int | None = None) -> int:
-    """Estimated gap-1 table footprint (direct.py:621-627)."""
+    """Estimated gap-1 table footprint (direct.py:323-329)."""
     if b is None:
         b = minimal_index_bytes(p.n_intervals)
     xs = p.values.astype(np.float64)

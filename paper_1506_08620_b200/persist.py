@@ -1,7 +1,8 @@
 """Bit-exact FBSIDX1 index files, loaded straight into device memory.
 
 Same file format, return values and exceptions as the reference
-(``fastsearch/bench/persist.py:1-112``): 48-byte little-endian header
+(``fastsearch/bench/persist.py:1-112``; the index-file half of the
+reference's bench package, the only part on the hot path's data format): 48-byte little-endian header
 (magic ``FBSIDX1\\0``, version 1, precision, qbits, gap, N, R, raw binary64
 bits of H and X0), the u32 K payload, and the zlib CRC-32 of the payload.
 Files written here are byte-identical to the reference's and vice versa.
@@ -100,15 +101,29 @@ def load_index(path) -> DirectIndex:
                        n=hd["n"], precision=hd["precision"], left_pad=left_pad)
 
 
-def prepare_loaded(idx: DirectIndex, p, algorithm: str = "direct"):
+#: the search kernel that serves a loaded index of each gap (direct.py:272-300)
+LOADED_ALGORITHM = {1: "direct", 2: "direct-gap2"}
+
+
+def prepare_loaded(idx: DirectIndex, p, algorithm: str | None = None):
     """A PreparedKernel over a loaded index and its partition (the search
-    kernels of batch.prepare, without rebuilding the table)."""
+    kernels of batch.prepare, without rebuilding the table).  The kernel
+    follows the index's gap q: "direct" for q = 1, "direct-gap2" for q = 2,
+    "direct-generic" otherwise (the reference's direct_search_generic,
+    direct.py:294-300); an explicit ``algorithm`` that does not match q
+    raises ValueError, since a gap-1 probe over a gap-q table (or the
+    reverse) returns wrong answers."""
     from .batch import PreparedKernel, _make_callables, _plan_for, build_rank_directory
 
-    if algorithm not in ("direct", "direct-gap2"):
-        raise ValueError("loaded indices serve the direct and direct-gap2 kernels")
+    want = LOADED_ALGORITHM.get(idx.q, "direct-generic")
+    if algorithm is None:
+        algorithm = want
+    if algorithm not in ("direct", "direct-gap2", "direct-generic"):
+        raise ValueError("loaded indices serve the direct, direct-gap2 and direct-generic kernels")
+    if algorithm != want:
+        raise ValueError(f"an index of gap q={idx.q} is searched by {want!r}, not {algorithm!r}")
     plan, keep = _plan_for(algorithm, idx, p)
-    if algorithm == "direct" and idx.q == 1:
+    if algorithm == "direct":
         rank = build_rank_directory(p, idx)
         plan.rank = rank.data_ptr()
         keep.append(rank)

@@ -52,6 +52,47 @@ def test_device_tensor_path(cuda, sweep4095):
         gd.check_answers(case, prep.lanes(zt).cpu().numpy())
 
 
+def test_device_path_rejects_what_the_kernel_cannot_take(cuda, sweep4095):
+    """Strided outputs land in the right slots (searched into a contiguous
+    temporary); a query dtype other than the partition's is refused by
+    batch_search, lanes and launch alike, before any kernel reads it."""
+    import torch
+
+    fs = _fs()
+    case, xs, z = sweep4095
+    p = fs.validate_partition(xs)
+    zt = torch.from_numpy(z).to(cuda)
+    prep = fs.prepare("direct", p)
+    cfg = fs.LaneConfig(8, "direct", prep)
+    for odt in (torch.int32, torch.int64):
+        buf = torch.full((2 * len(z),), -7, dtype=odt, device=cuda)
+        assert fs.batch_search(cfg, zt, buf[::2]) == len(z)
+        gd.check_answers(case, buf[::2].cpu().numpy())
+        assert bool((buf[1::2] == -7).all())
+        col = torch.full((len(z), 3), -7, dtype=odt, device=cuda)
+        fs.batch_search(cfg, zt, col[:, 1])
+        gd.check_answers(case, col[:, 1].cpu().numpy())
+        assert bool((col[:, 0] == -7).all() and (col[:, 2] == -7).all())
+    wrong = zt.double() if zt.dtype == torch.float32 else zt.float()
+    out = torch.empty(len(z), dtype=torch.int64, device=cuda)
+    st = fs.new_status(cuda)
+    with pytest.raises(ValueError):
+        fs.batch_search(cfg, wrong, out)
+    with pytest.raises(ValueError):
+        prep.lanes(wrong)
+    with pytest.raises(ValueError):
+        prep.launch(wrong, out, st)
+    with pytest.raises(ValueError):
+        prep.launch(zt, out[::2], st)
+    with pytest.raises(ValueError):
+        prep.launch(zt, out.float(), st)
+    with pytest.raises(ValueError):
+        prep.launch(zt, out[: len(z) - 1], st)
+    prep.launch(zt, out, st)
+    assert fs.first_bad_of(st) is None
+    gd.check_answers(case, out.cpu().numpy())
+
+
 def test_misaligned_views_and_odd_sizes(cuda, sweep4095):
     """Every head/tail peel and the non-vector store path."""
     import torch
@@ -299,7 +340,7 @@ def test_first_bad_across_tail_and_vector_body(cuda, algo):
 def test_direct_cache_with_records_too_large_for_smem(cuda):
     """prepare("direct-cache") keeps the reference structure (fused records,
     host view, scalar cache lane) but, when the records cannot be staged,
-    searches through direct's device layouts: same answers (direct.py:601-610
+    searches through direct's device layouts: same answers (direct.py:303-312
     equals 570-574 by construction), no 16-B L2 record gathers."""
     fs = _fs()
     from paper_1506_08620_b200 import workloads

@@ -170,6 +170,29 @@ class TestCoercion:
         exact = np.searchsorted(xs.astype(np.float64), z64, side="right") - 1
         assert np.array_equal(orc.rank_oracle(xs, zc), exact)
 
+    def test_longdouble_and_large_integers_round_down(self):
+        """Inputs more precise than the partition (longdouble, integers above
+        2^53) round toward -inf too: a value just above a knot's predecessor
+        never rounds up across the knot (exact answers, no false
+        OutOfDomain just below X_N)."""
+        one = np.longdouble(1)
+        eps = np.longdouble(2) ** -60
+        z = np.array([one - eps, one + eps, np.longdouble(2) - eps], dtype=np.longdouble)
+        zc = coerce_queries(z, np.dtype(np.float64))
+        assert zc[0] < 1.0 and zc[1] == 1.0 and zc[2] < 2.0
+        xs = np.array([0.0, 1.0, 2.0])
+        assert orc.first_bad(xs, zc) is None
+        assert orc.rank_oracle(xs, zc).tolist() == [0, 1, 1]
+        big = np.array([2**53 + 1, 2**62 + 1, -(2**53) - 1, 7], dtype=np.int64)
+        zb = coerce_queries(big, np.dtype(np.float64))
+        assert [int(v) for v in zb] == [2**53, 2**62, -(2**53) - 2, 7]
+        z32 = coerce_queries(np.array([16777217, 3], dtype=np.int64), np.dtype(np.float32))
+        assert z32.tolist() == [16777216.0, 3.0]
+
+    def test_narrower_float_is_exact(self):
+        z = np.array([0.5, 65504.0], dtype=np.float16)
+        assert coerce_queries(z, np.dtype(np.float32)).tolist() == [0.5, 65504.0]
+
     def test_domain_preserved(self):
         xs = np.array([0.0, 1.0, 2.0], dtype=np.float32)
         z = np.array([np.nextafter(2.0, -np.inf), 2.0, -1e-300, np.nan])

@@ -74,15 +74,21 @@ def test_gpu_round_trip_search_identical(cuda, tmp_path):
     import paper_1506_08620_b200 as fs
 
     p = fs.gen_uniform_gap_partition(100, 1, 5, seed=31, precision="double")
-    for q, algo in ((1, "direct"), (2, "direct-gap2")):
+    z = np.concatenate([orc.random_queries(p.values, 20_000, seed=4), orc.boundary_probes(p.values)])
+    want = orc.rank_oracle(p.values, z)
+    for q, algo in ((1, "direct"), (2, "direct-gap2"), (3, "direct-generic"), (5, "direct-generic")):
         idx, _ = fs.build(p, q=q)
         path = tmp_path / f"t{q}.idx"
         persist.save_index(idx, path)
         back = persist.load_index(path)
-        assert back.h == idx.h and back.h.dtype == idx.h.dtype and back.x0 == idx.x0
-        z = orc.random_queries(p.values, 20_000, seed=4)
-        got = fs.run_batch(persist.prepare_loaded(back, p, algo), z)
-        assert np.array_equal(got, orc.rank_oracle(p.values, z))
+        assert back.h == idx.h and back.h.dtype == idx.h.dtype and back.x0 == idx.x0 and back.q == q
+        # the kernel follows the file's gap (default), and an explicit name must agree with it
+        assert persist.prepare_loaded(back, p).algorithm == algo
+        assert np.array_equal(fs.run_batch(persist.prepare_loaded(back, p), z), want), q
+        assert np.array_equal(fs.run_batch(persist.prepare_loaded(back, p, algo), z), want), q
+        for wrong in {"direct", "direct-gap2", "direct-generic"} - {algo}:
+            with pytest.raises(ValueError):
+                persist.prepare_loaded(back, p, wrong)
 
 
 @pytest.mark.gpu
