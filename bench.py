@@ -3,33 +3,43 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One JSON line on rank 0.  Workload (BASELINE.json configs[2], "cfg3", the
+One JSON line on rank 0.  Workload: BASELINE.json configs[2] ("cfg3"), the
 streaming config the >=70%-of-roofline target and the 1/2/4/8-GPU sharding
-are quoted on): float32 knots X, N+1 = 4,097, spacing 0.5 + U[0,1) summed
-from 0 (seed 0); 2^30 float32 queries Uniform[X0, XN) PER GPU (weak
-scaling: each rank owns a 2^30-query shard of an N x 2^30 global stream,
-X and J built locally on every GPU, no per-query communication).
+are quoted on -- float32 knots X, N+1 = 4,097, spacing 0.5 + U[0,1) summed
+from 0 (seed 0); ONE global stream of 2^30 float32 queries Uniform[X0, XN),
+rank r of N owning the contiguous shard dist.shard_span(2^30, r, N) (strong
+scaling, as configs[2] is written; X and J built locally on every GPU).
 
-A step = one batch search over the rank's 2^30 queries with the direct
-search kernel (one launch).  ``value`` = queries/s with queries resident in
-HBM (CUDA events on the launching stream, max over ranks); ``e2e`` = the
-same metric through the public drop-in API (``batch_search`` on pinned host
-numpy arrays: H2D copies, kernel and D2H inside every step); ``bsearch`` =
-the branchless binary search (Alg 3, bitset2) timed identically -- the
-"direct vs binary search" half of the metric.  Inputs are 4 GiB + 4 GiB of
-output per GPU, far larger than the 126 MB L2, so no flush is needed; the
-``per_config`` sweep flushes L2 before every launch of a stream that fits in
-it (cfg1).
+A step = one ``dist.sharded_batch_search`` over the rank's shard (the
+product call: one search kernel, the shard's first out-of-domain position
+made global on the device, one MIN all-reduce across ranks, one host read
+that raises OutOfDomain if needed).  ``value`` = 2^30 / (max over ranks of
+the device time per step) with the queries resident in HBM.  Also reported:
+``kernel_only`` (back-to-back launches, no per-step host read -- the
+roofline's kernel time), ``weak`` (every rank a full 2^30 stream of its own,
+the round-1 line), ``bsearch`` (bitset2, Alg 3, the "direct vs binary
+search" half of the metric), ``e2e`` (the same metric through the public
+drop-in API: ``batch_search`` on pinned host numpy arrays, H2D + kernel +
+D2H inside every step; pageable arrays and the multi-device split beside
+it) and ``per_config`` (every BASELINE config, each one global stream
+sharded over the ranks, direct or its fall-back vs bitset2).  Inputs are
+4 GiB + 4 GiB of output >> the 126 MB L2, so no flush is needed; the
+per-config sweep flushes L2 before every launch of a stream that fits in it.
 
-``--impl reference`` times the reference's CPU path (its numpy lane kernel
-and thread-span driver, restated in oracle/fs_oracle.py -- the reference
-itself is Python and cannot travel to the GPU box) on all host cores, on a
-bounded sample of the same workload.
+``--impl reference`` runs the UNMODIFIED reference (``fastsearch``, pip-
+installed into baseline/_ref) through its own public API:
+``batch_search(LaneConfig(65536, "direct", prepare("direct", p)), z,
+out_int32, threads=os.cpu_count())`` on a 2^26-query slice of the same
+workload per step, on every host core.  If baseline/_ref is missing it
+falls back to the oracle's restatement of that path (kind "port").
+``--plan-only`` (CPU, any backend) prints the sharding plan the GPU arm
+would time -- the spans and global query count -- for the torchrun tests.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -44,10 +54,12 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "queries/sec and achieved HBM GB/s (fraction of roofline), direct vs binary search"
 UNIT = "queries/s"
-M_PER_GPU = 1 << 30
+M_GLOBAL = 1 << 30  # configs[2]: 2^30 queries, sharded 2^30/g over g GPUs
 BYTES_PER_QUERY = 8  # 4 B float32 query read + 4 B int32 index written
 SPEC_HBM_GBS = 8000.0  # B200 nominal HBM3e bandwidth (secondary denominator)
-CPU_SAMPLE = 1 << 24
+CPU_SAMPLE = 1 << 26  # reference arm / cpu_baseline: a 2^26 slice of the stream
+WORKLOAD = "cfg3: f32 X N+1=4097, dX=0.5+U[0,1) (seed 0); 2^30 f32 queries U[X0,XN), one global stream"
+REF_DIR = ROOT / "baseline" / "_ref"
 
 
 def peaks() -> dict:
@@ -58,16 +70,35 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def ncu_traffic() -> dict | None:
-    """DRAM bytes per launch of the direct kernel from the committed ncu
-    capture (profiles/ncu_direct_cfg3.json), if one exists."""
-    p = ROOT / "profiles" / "ncu_direct_cfg3.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text())
-        except Exception:
-            return None
-    return None
+def lib_sha16() -> str | None:
+    lib = ROOT / "paper_1506_08620_b200" / "libfsgpu.so"
+    return hashlib.sha256(lib.read_bytes()).hexdigest()[:16] if lib.exists() else None
+
+
+def ncu_traffic(name: str) -> dict | None:
+    """DRAM bytes per launch (and L2 sectors per query) of a config's search
+    kernel from the committed ncu capture profiles/traffic/<name>.json, with
+    whether that capture was taken of this very build (lib_sha16)."""
+    p = ROOT / "profiles" / "traffic" / f"{name}.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+    except Exception:
+        return None
+    d["profile"] = str(p.relative_to(ROOT))
+    d["same_build"] = d.get("lib_sha16") == lib_sha16()
+    return d
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -143,59 +174,95 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_reference_rate(xs: np.ndarray, z: np.ndarray, algo: str, steps: int, warmup: int, min_time: float):
-    """Reference CPU lane path (restated) over all host cores: queries/s."""
-    from oracle import fs_oracle as orc
+# ---------------------------------------------------------------------------
+# The reference's CPU path (reference arm and cpu_baseline)
+# ---------------------------------------------------------------------------
+def cfg3_host_stream(n: int, seed: int = 1):
+    """cfg3 knots (the reference's own generator recipe, partition.py:126-147)
+    and n host queries of the workload (gen_queries recipe, partition.py:
+    150-160), as plain numpy arrays."""
+    rng = np.random.default_rng(0)
+    gaps = rng.uniform(0.5, 1.5, size=4096)
+    xs = np.concatenate([[0.0], np.cumsum(gaps)]).astype(np.float32)
+    r = np.random.default_rng(seed)
+    z = r.uniform(float(xs[0]), float(xs[-1]), size=n).astype(np.float32)
+    z[z >= xs[-1]] = np.nextafter(xs[-1], np.float32(-np.inf))
+    return xs, z
 
+
+def reference_runner(xs: np.ndarray):
+    """(kind, run(z, out), version): the unmodified reference's batch_search
+    over every host core when baseline/_ref holds it, else the oracle's
+    restatement of the same lane path."""
     threads = os.cpu_count() or 1
-    prep = orc.PreparedPort(algo, xs)
+    if (REF_DIR / "fastsearch" / "__init__.py").exists():
+        sys.path.insert(0, str(REF_DIR))
+        try:
+            import fastsearch as fsr
+
+            if Path(fsr.__file__).resolve().is_relative_to(REF_DIR.resolve()):
+                p = fsr.validate_partition(xs)
+                cfg = fsr.LaneConfig(d=65536, kernel="direct", structure=fsr.prepare("direct", p))
+
+                def run(z, out):
+                    fsr.batch_search(cfg, z, out, threads=threads)
+
+                return "reference", run, threads, f"fastsearch {getattr(fsr, '__version__', '?')} (baseline/_ref)"
+        finally:
+            sys.path.remove(str(REF_DIR))
+    from oracle import fs_oracle as orc  # the restated lane path (reference unavailable)
+
+    prep = orc.PreparedPort("direct", xs)
+
+    def run(z, out):
+        orc.batch_search_port(prep, z, out, d=65536, threads=threads)
+
+    return "port", run, threads, "oracle/fs_oracle.py restatement of batch.py:399-441"
+
+
+def time_reference(run, z, steps: int, warmup: int, min_time: float = 0.0):
     out = np.empty(len(z), dtype=np.int32)
     for _ in range(max(1, warmup)):
-        orc.batch_search_port(prep, z, out, d=65536, threads=threads)
+        run(z, out)
     times = []
     t_total = 0.0
     while len(times) < steps or t_total < min_time:
         t0 = time.perf_counter()
-        orc.batch_search_port(prep, z, out, d=65536, threads=threads)
+        run(z, out)
         dt = time.perf_counter() - t0
         times.append(dt)
         t_total += dt
-        if len(times) >= 10 * max(steps, 1) and t_total >= 0.5 * min_time:
-            break
-    rate = len(z) / float(np.median(times))
-    return rate, threads, len(times), out
+    return len(z) / float(np.median(times)), len(times), out
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1506_08620_b200 import workloads
-
-    p = workloads.knots("cfg3", seed=0)
     n = args.ref_sample
-    z = workloads.queries_host("cfg3", p, n, seed=1)
-    rate, threads, reps, _ = cpu_reference_rate(p.values, z, "direct", args.steps, args.warmup,
-                                                min_time=args.ref_min_time)
-    sample = (f"cfg3 direct lane path (batch.py:315-317 via oracle/fs_oracle.py), {n} queries "
-              f"per step, d=65536, {threads} threads, median of {reps} passes")
+    xs, z = cfg3_host_stream(n)
+    kind, run, threads, version = reference_runner(xs)
+    rate, reps, _ = time_reference(run, z, args.steps, args.warmup, args.ref_min_time)
+    sample = (f"{version}: batch_search(LaneConfig(d=65536, 'direct'), {n} cfg3 f32 queries, int32 out, "
+              f"threads={threads}) per step; median of {reps} steps; CPU {cpu_model()}")
     line = {
         "impl": "reference",
         "metric": METRIC,
-        "value": rate * 1.0,
+        "value": rate,
         "unit": UNIT,
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": 1e3 * n / rate,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded cfg3 recipe)",
-        "config": {"workload": "cfg3: f32 N+1=4097 gaps 0.5+U[0,1); uniform queries", "queries_per_step": n,
-                   "algorithm": "direct"},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "config": {"workload": WORKLOAD, "queries_per_step": n, "algorithm": "direct",
+                   "sample": f"a {n}-query slice of the 2^30-query stream per step"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -203,16 +270,51 @@ def run_reference(args):
     return 0
 
 
-def time_device(prep, z, out, fb, steps: int, warmup: int, barrier, flush=None):
-    """Warm up, then time exactly ``steps`` launches with CUDA events on the
-    launching stream, bracketed by barrier + synchronize.  With ``flush`` (a
-    device buffer larger than L2), every launch is preceded by an untimed
-    write of that buffer and timed by its own event pair, so a stream that
-    fits in L2 is read cold each time."""
+# ---------------------------------------------------------------------------
+# Sharding plan (also printed on CPU by --plan-only for the torchrun tests)
+# ---------------------------------------------------------------------------
+def shard_plan(m: int, world: int) -> list:
+    from paper_1506_08620_b200 import dist as fsdist
+
+    return [fsdist.shard_span(m, r, world, granularity=8) for r in range(world)]
+
+
+def run_plan_only(args):
+    import torch.distributed as dist
+
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    spans = shard_plan(args.m, world)
+    mine = spans[rank]
+    gathered = [None] * world
+    if world > 1:
+        dist.all_gather_object(gathered, list(mine))
+    else:
+        gathered = [list(mine)]
+    if rank == 0:
+        print(json.dumps({"plan_only": True, "n_gpus": world, "scaling": "strong",
+                          "config": {"workload": WORKLOAD, "global_queries": args.m,
+                                     "shards": gathered, "queries_per_gpu": [b - a for a, b in gathered]}}),
+              flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def time_steps(step, steps: int, warmup: int, barrier, flush=None):
+    """Warm up, then time exactly ``steps`` calls of ``step`` with CUDA events
+    on the current stream, bracketed by barrier + synchronize.  With
+    ``flush`` (a device buffer larger than L2), every call is preceded by an
+    untimed write of that buffer and timed by its own event pair."""
     import torch
 
     for _ in range(warmup):
-        prep.launch(z, out, fb)
+        step()
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -222,7 +324,7 @@ def time_device(prep, z, out, fb, steps: int, warmup: int, barrier, flush=None):
         for a, b in pairs:
             flush.zero_()
             a.record(s)
-            prep.launch(z, out, fb)
+            step()
             b.record(s)
         torch.cuda.synchronize()
         barrier()
@@ -232,34 +334,51 @@ def time_device(prep, z, out, fb, steps: int, warmup: int, barrier, flush=None):
     stop = torch.cuda.Event(enable_timing=True)
     start.record(s)
     for _ in range(steps):
-        prep.launch(z, out, fb)
+        step()
     stop.record(s)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    return start.elapsed_time(stop) / 1e3  # seconds for `steps` launches
+    return start.elapsed_time(stop) / 1e3  # seconds for `steps` calls
 
 
 L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2
 
-
 PER_CONFIG = (
-    # (label, config, knot-recipe kwargs, queries per GPU): BASELINE.json configs[0..4]
+    # (label, config, knot-recipe kwargs, global queries): BASELINE.json configs[0..4]
     ("cfg1", "cfg1", {"seed": 0}, 1_000_000),
     ("cfg2_s0", "cfg2", {"seed": 0}, 100_000_000),
+    ("cfg2_s1", "cfg2", {"seed": 1}, 100_000_000),
+    ("cfg2_s2", "cfg2", {"seed": 2}, 100_000_000),
     ("cfg3", "cfg3", {"seed": 0}, 1 << 30),
     ("cfg4", "cfg4", {}, 1 << 28),
     ("cfg5_33", "cfg5", {"n1": 33}, 1 << 28),
     ("cfg5_1025", "cfg5", {"n1": 1025}, 1 << 28),
     ("cfg5_32769", "cfg5", {"n1": 32_769}, 1 << 28),
     ("cfg5_1048577", "cfg5", {"n1": 1_048_577}, 1 << 28),
+    ("cfg5u_1048577", "cfg5", {"n1": 1_048_577, "filtered": False}, 1 << 28),  # the Overflow instance
 )
 
 
-def per_config(steps: int, barrier, world: int):
-    """Every BASELINE config on this GPU: direct (or its fall-back) vs
-    bitset2, device-resident, CUDA events, answers verified by the bracket
-    property.  Returns {label: {...}} with per-rank times max-reduced."""
+def local_stream(cfg: str, p, m_global: int, rank: int, world: int, seed: int):
+    """Rank's contiguous shard of the config's ONE global stream (the whole
+    stream is drawn on the device with a fixed seed, then sliced)."""
+    from paper_1506_08620_b200 import workloads
+
+    a, b = shard_plan(m_global, world)[rank]
+    z = workloads.queries_device(cfg, p, m_global, seed=seed)
+    if world == 1:
+        return z, a, b
+    zl = z[a:b].clone()
+    del z
+    return zl, a, b
+
+
+def per_config(steps: int, barrier, world: int, rank: int):
+    """Every BASELINE config: each one global stream sharded over the ranks,
+    direct (or its fall-back) vs bitset2, device-resident, CUDA events,
+    answers verified by the bracket property.  Returns {label: {...}} with
+    per-rank times max-reduced; gqs = global queries / max time."""
     import torch
     import torch.distributed as dist
 
@@ -270,33 +389,45 @@ def per_config(steps: int, barrier, world: int):
     res = {}
     for label, cfg, kw, m in PER_CONFIG:
         p = workloads.knots(cfg, **kw)
-        z = workloads.queries_device(cfg, p, m, seed=11)
-        out = torch.empty(m, dtype=torch.int32, device=z.device)
+        z, a, b = local_stream(cfg, p, m, rank, world, seed=11)
+        ml = b - a
+        out = torch.empty(ml, dtype=torch.int32, device=z.device)
         fb = fs.new_status(z.device)
         qb = z.element_size() + 4
-        row = {"queries_per_gpu": m, "dtype": "f32" if p.precision == "single" else "f64", "bytes_per_query": qb}
-        # streams that fit in L2 are read cold: the L2 is flushed before every launch
-        flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=z.device) if qb * m < L2_FLUSH_BYTES else None
+        row = {"global_queries": m, "queries_per_gpu": ml, "dtype": "f32" if p.precision == "single" else "f64",
+               "bytes_per_query": qb}
+        flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=z.device) if qb * ml < L2_FLUSH_BYTES else None
         row["l2"] = "flushed before each launch" if flush is not None else "stream > L2, no flush"
         for name in ("direct", "bitset2"):
+            t_prep = time.perf_counter()
             prep = fs.prepare_with_fallback(p) if name == "direct" else fs.prepare("bitset2", p)
-            n = steps * (1 if m >= (1 << 30) else 4) * (1 if m >= (1 << 26) else 10)
-            t = time_device(prep, z, out, fb, n, 3, barrier, flush) / n
+            torch.cuda.synchronize()
+            t_prep = time.perf_counter() - t_prep
+            n = steps * (1 if ml >= (1 << 29) else 4) * (1 if ml >= (1 << 26) else 10)
+            t = time_steps(lambda: prep.launch(z, out, fb), n, 3, barrier, flush) / n
             ok = fs.first_bad_of(fb) is None and verify_bracket(p, z, out)
             tt = torch.tensor([t, 0.0 if ok else 1.0], dtype=torch.float64, device=z.device)
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t, bad = tt.tolist()
-            row[name] = {
+            ent = {
                 "algorithm": prep.algorithm,
-                "gqs": world * m / t / 1e9,
+                "gqs": m / t / 1e9,
                 "ms": 1e3 * t,
-                "roofline_frac": qb * m / t / 1e9 / pk,
+                "roofline_frac": qb * ml / t / 1e9 / pk,
                 "placement": prep.placement(),
+                "prepare_ms": 1e3 * t_prep,
                 "verified": bad == 0,
+                "launches_per_step": prep.launches_per_batch(ml),
             }
             if name == "direct" and prep.algorithm.startswith("direct"):
-                row["R"] = prep.structure.r
+                ent["R"] = int(prep.structure.r)
+                ent["table_bytes"] = {"K": 4 * (int(prep.structure.r) + 1), "X": int(p.values.nbytes)}
+            tr = ncu_traffic(f"{label}_{'direct' if name == 'direct' else 'bitset2'}")
+            if tr:
+                ent["traffic"] = {k: tr.get(k) for k in ("dram_bytes_per_launch", "l2_sectors_per_query",
+                                                         "l1tex_pct", "profile", "same_build") if k in tr}
+            row[name] = ent
         res[label] = row
         del z, out, flush
         torch.cuda.empty_cache()
@@ -306,8 +437,6 @@ def per_config(steps: int, barrier, world: int):
 def verify_bracket(p, z, out) -> bool:
     """X[out] <= z < X[out+1] for every query (unique answer => equals the
     oracle's max{i : X_i <= z}); exact float compares on the device."""
-    import torch
-
     x = p.device_values()
     o = out.long()
     ok = (o >= 0) & (o < p.n_intervals)
@@ -324,14 +453,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--m", type=int, default=M_PER_GPU, help="queries per GPU")
+    ap.add_argument("--m", type=int, default=M_GLOBAL, help="global queries (sharded over the ranks)")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config sweep (cfg1..cfg5)")
-    ap.add_argument("--ref-sample", type=int, default=CPU_SAMPLE, help="--impl reference: queries per step")
-    ap.add_argument("--ref-min-time", type=float, default=10.0, help="--impl reference: minimum seconds sampled")
+    ap.add_argument("--ref-sample", type=int, default=CPU_SAMPLE, help="reference arm: queries per step")
+    ap.add_argument("--ref-min-time", type=float, default=0.0, help="reference arm: minimum seconds sampled")
+    ap.add_argument("--plan-only", action="store_true", help="print the sharding plan (CPU, no GPU work)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
+    if args.plan_only:
+        return run_plan_only(args)
 
     import torch
     import torch.distributed as dist
@@ -348,6 +480,7 @@ def main():
             pass
 
     import paper_1506_08620_b200 as fs
+    from paper_1506_08620_b200 import dist as fsdist
     from paper_1506_08620_b200 import workloads
 
     m = args.m
@@ -357,29 +490,46 @@ def main():
     torch.cuda.synchronize()
     build_ms = 1e3 * (time.perf_counter() - t0)
     prep_b = fs.prepare("bitset2", p)
-    z = workloads.queries_device("cfg3", p, m, seed=1 + rank)
-    out = torch.empty(m, dtype=torch.int32, device=z.device)
+    z, a, b = local_stream("cfg3", p, m, rank, world, seed=1)
+    ml = b - a
+    out = torch.empty(ml, dtype=torch.int32, device=z.device)
     fb = fs.new_status(z.device)
 
+    # the product call, strong scaling: value
     with ClockSampler(local) as clk:
-        t_dir = time_device(prep, z, out, fb, args.steps, args.warmup, barrier)
+        t_step = time_steps(lambda: fsdist.sharded_batch_search(prep, z, out, a, status=fb), args.steps,
+                            args.warmup, barrier)
     clocks = clk.summary()
-    bad = -1 if fs.first_bad_of(fb) is None else 0
-    verified = bad == -1 and verify_bracket(p, z, out)
-    t_bs = time_device(prep_b, z, out, fb, max(3, args.steps // 5), 3, barrier)
+    verified = fs.first_bad_of(fb) is None and verify_bracket(p, z, out)
+    # the kernel alone (roofline): back-to-back launches on the same stream
+    t_kern = time_steps(lambda: prep.launch(z, out, fb), args.steps, 3, barrier)
+    verified &= fs.first_bad_of(fb) is None and verify_bracket(p, z, out)
+    t_bs = time_steps(lambda: prep_b.launch(z, out, fb), max(3, args.steps // 5), 3, barrier)
     verified &= verify_bracket(p, z, out)
+    del z
+    # weak scaling (round-1 line): every rank its own full 2^30 stream
+    t_weak = None
+    if world > 1:
+        torch.cuda.empty_cache()
+        zw = workloads.queries_device("cfg3", p, m, seed=1 + rank)
+        ow = torch.empty(m, dtype=torch.int32, device=zw.device)
+        t_weak = time_steps(lambda: prep.launch(zw, ow, fb), args.steps, 3, barrier)
+        verified &= fs.first_bad_of(fb) is None and verify_bracket(p, zw, ow)
+        del zw, ow
 
-    # end-to-end through the public API on pinned host buffers (per rank: the
-    # full 2^30 shard at N=1; 2^28 at N>1 so N ranks' host buffers stay bounded)
+    # end to end through the public API on host arrays: the rank's shard of the
+    # global stream (at N>1 capped at 2^28 per rank so N host copies stay bounded)
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
-    me = m if world == 1 else min(m, 1 << 28)
+    me = ml if world == 1 else min(ml, 1 << 28)
+    zl, _, _ = local_stream("cfg3", p, m, rank, world, seed=1)
     zh_t = torch.empty(me, dtype=torch.float32, pin_memory=True)
-    zh_t.copy_(z[:me])
+    zh_t.copy_(zl[:me])
     oh_t = torch.empty(me, dtype=torch.int32, pin_memory=True)
     zh, oh = zh_t.numpy(), oh_t.numpy()
     cfg = fs.LaneConfig(d=65536, kernel="direct", structure=prep)
-    del z, out
+    del out
     torch.cuda.empty_cache()
+
     def timed_calls(call, n):
         """Median seconds of n synchronous public-API calls, each bracketed by
         CUDA events on the current stream (device clock; the call returns only
@@ -389,69 +539,92 @@ def main():
         ts = []
         for _ in range(n):
             torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record()
             call()
-            b.record()
-            b.synchronize()
-            ts.append(a.elapsed_time(b) / 1e3)
+            eb.record()
+            eb.synchronize()
+            ts.append(ea.elapsed_time(eb) / 1e3)
         barrier()
         return float(np.median(ts))
 
     t_e2e = timed_calls(lambda: fs.batch_search(cfg, zh, oh), e2e_steps)
+    e2e_launches = prep.host_launches(zh, oh)
+    e2e_ok = verify_bracket(p, zl[:me], torch.from_numpy(oh).to(zl.device))
+    del zl
+    torch.cuda.empty_cache()
     # opt-in speculative write-back (atomic=False): both PCIe directions overlap
     t_e2e_ov = timed_calls(lambda: fs.batch_search(cfg, zh, oh, atomic=False), e2e_steps)
     # what a drop-in numpy user passes: ordinary pageable arrays (staged by the library)
     zpg = zh.copy()
     opg = np.empty_like(oh)
     t_e2e_pg = timed_calls(lambda: fs.batch_search(cfg, zpg, opg), 3)
+    pg_launches = prep.host_launches(zpg, opg)
+    e2e_ok &= bool(np.array_equal(opg, oh))
     del zpg, opg
+    # in-process multi-device split of the same host batch (single process, every visible GPU)
+    ndev = torch.cuda.device_count()
+    t_e2e_md = None
+    if world == 1 and ndev > 1:
+        t_e2e_md = timed_calls(lambda: fs.batch_search(cfg, zh, oh, devices="all"), e2e_steps)
 
-    times = torch.tensor([t_dir, t_bs, t_e2e, t_e2e_ov, t_e2e_pg], dtype=torch.float64, device="cuda")
+    times = torch.tensor([t_step, t_kern, t_bs, t_weak or 0.0, t_e2e, t_e2e_ov, t_e2e_pg], dtype=torch.float64,
+                         device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
-        v = torch.tensor([1 if verified else 0], device="cuda")
+        v = torch.tensor([1 if (verified and e2e_ok) else 0], device="cuda")
         dist.all_reduce(v, op=dist.ReduceOp.MIN)
         verified = bool(v.item())
-    t_dir, t_bs, t_e2e, t_e2e_ov, t_e2e_pg = times.tolist()
-    z_cpu, o_cpu = zh[:CPU_SAMPLE].copy(), oh[:CPU_SAMPLE].copy()
+    else:
+        verified = verified and e2e_ok
+    t_step, t_kern, t_bs, t_weak, t_e2e, t_e2e_ov, t_e2e_pg = times.tolist()
+    z_cpu = zh[: min(CPU_SAMPLE, me)].copy()
+    o_cpu = oh[: min(CPU_SAMPLE, me)].copy()
     del zh_t, oh_t, zh, oh
     torch.cuda.empty_cache()
-    configs = None if args.no_configs else per_config(max(3, min(args.steps, 10)), barrier, world)
+    configs = None if args.no_configs else per_config(max(3, min(args.steps, 10)), barrier, world, rank)
 
     if rank == 0:
-        total = m * world
-        step = t_dir / args.steps
-        value = total / step
+        step = t_step / args.steps
+        kstep = t_kern / args.steps
         bs_steps = max(3, args.steps // 5)
         pk = peaks()
-        achieved = BYTES_PER_QUERY * m / step / 1e9  # per GPU GB/s
-        traffic = ncu_traffic()
+        achieved = BYTES_PER_QUERY * ml / kstep / 1e9  # per GPU GB/s, the kernel's own launch time
+        traffic = ncu_traffic("cfg3_direct")
         line = {
             "metric": METRIC,
-            "value": value,
+            "value": m / step,
             "unit": UNIT,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": 1e3 * step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (seeded cfg3 recipe; queries generated on device, Philox)",
             "config": {
-                "workload": "cfg3: f32 X N+1=4097, dX=0.5+U[0,1) (seed 0); 2^30 f32 queries U[X0,XN) per GPU",
-                "queries_per_gpu": m,
-                "global_queries": total,
-                "algorithm": "direct (gap 1, X+J staged in smem)",
+                "workload": WORKLOAD,
+                "global_queries": m,
+                "queries_per_gpu": ml,
+                "shards": shard_plan(m, world),
+                "step": "dist.sharded_batch_search: 1 search kernel + device-side global first-bad + MIN "
+                        "all-reduce (N>1) + 1 host read",
+                "algorithm": "direct (gap 1)",
                 "placement": prep.placement(),
                 "R": prep.structure.r,
                 "h": float(prep.structure.h),
                 "index_build_ms": build_ms,
-                "l2": "inputs 4 GiB + outputs 4 GiB per GPU >> 126 MB L2; no flush needed",
-                "parallelism": f"query shards x{world}, X/J replicated (built locally)",
+                "l2": "inputs 4 GiB + outputs 4 GiB >> 126 MB L2; no flush needed",
+                "parallelism": f"query shards x{world} of one global stream, X/J replicated (built locally)",
                 "verified": verified,
+                "lib_sha16": lib_sha16(),
+            },
+            "kernel_only": {
+                "value": m / kstep,
+                "ms_per_step": 1e3 * kstep,
+                "what": "PreparedKernel.launch back to back (no per-step host read or all-reduce)",
             },
             "roofline": {
                 "bound": "hbm",
@@ -459,58 +632,73 @@ def main():
                 "peak": pk["hbm_gbs"],
                 "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"],
-                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                "traffic": (traffic or {}).get("dram_bytes_per_launch") if world == 1 else None,
+                "traffic_source": None if not traffic else {
+                    k: traffic.get(k) for k in ("profile", "kernel", "lib_sha16", "same_build", "queries")},
                 "peak_source": pk["source"],
                 "frac_of_spec": achieved / SPEC_HBM_GBS,  # the ~8 TB/s nominal peak the north star cites
                 "algorithmic_bytes_per_query": BYTES_PER_QUERY,
+                "algorithmic_bytes_per_launch": BYTES_PER_QUERY * ml,
             },
             "bsearch": {
                 "algorithm": "bitset2 (Alg 3, padded, smem)",
-                "value": total / (t_bs / bs_steps),
+                "value": m / (t_bs / bs_steps),
                 "ms_per_step": 1e3 * t_bs / bs_steps,
-                "roofline_frac": BYTES_PER_QUERY * m / (t_bs / bs_steps) / 1e9 / pk["hbm_gbs"],
-                "direct_speedup": (t_bs / bs_steps) / step,
+                "roofline_frac": BYTES_PER_QUERY * ml / (t_bs / bs_steps) / 1e9 / pk["hbm_gbs"],
+                "direct_speedup": (t_bs / bs_steps) / kstep,
             },
             "e2e": {
                 "value": me * world / t_e2e,
                 "unit": UNIT,
-                "h2d_bytes_per_step": 4 * me,
-                "d2h_bytes_per_step": 4 * me,
+                "h2d_bytes_per_step": 4 * me * world,
+                "d2h_bytes_per_step": 4 * me * world,
                 "queries_per_gpu": me,
-                "api": "paper_1506_08620_b200.batch_search(LaneConfig(d=65536,'direct'), pinned numpy z, pinned numpy int32 out)",
+                "api": "paper_1506_08620_b200.batch_search(LaneConfig(d=65536,'direct'), pinned numpy z, "
+                       "pinned numpy int32 out)",
                 "ms_per_step": 1e3 * t_e2e,
+                "gpu_launches_per_step": e2e_launches,
                 "contract": "reference batch_search guarantee kept: nothing written to out on OutOfDomain "
                             "(host threads check the domain while chunks upload; write-back starts once "
                             "no query is bad, overlapping the remaining uploads)",
                 "pageable": {
                     "value": me * world / t_e2e_pg,
                     "ms_per_step": 1e3 * t_e2e_pg,
-                    "api": "batch_search on ordinary (pageable) numpy arrays: library pinned staging ring",
+                    "gpu_launches_per_step": pg_launches,
+                    "api": "batch_search on ordinary (pageable) numpy arrays: library pinned staging ring, "
+                           "persistent host pool",
                 },
                 "overlapped": {
                     "value": me * world / t_e2e_ov,
                     "ms_per_step": 1e3 * t_e2e_ov,
                     "api": "batch_search(..., atomic=False): chunk results written back while later chunks upload",
                 },
+                "multi_device": (
+                    {"value": me / t_e2e_md, "devices": ndev, "ms_per_step": 1e3 * t_e2e_md,
+                     "api": "batch_search(..., devices='all'): one process, contiguous spans per GPU, gated"}
+                    if t_e2e_md else {"skipped": f"{ndev} visible GPU(s) in one process" if world == 1
+                                      else "one process per GPU (torchrun)"}),
             },
-            "gpu_launches": args.steps * prep.launches_per_batch(m),
+            "gpu_launches": args.steps * prep.launches_per_batch(ml),
             "clocks": clocks,
         }
+        if world > 1:
+            line["weak"] = {"value": world * m / (t_weak / args.steps), "queries_per_gpu": m,
+                            "ms_per_step": 1e3 * t_weak / args.steps,
+                            "what": "every rank its own 2^30-query stream (weak scaling), kernel launches"}
         if configs is not None:
             line["per_config"] = configs
         if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
-            from oracle import fs_oracle as orc  # noqa: F401  (cpu_baseline leg only)
-
-            zs = z_cpu
-            rate, threads, reps, outc = cpu_reference_rate(p.values, zs, "direct", 3, 1, min_time=10.0)
+            xs, _ = cfg3_host_stream(1)
+            kind, run, threads, version = reference_runner(xs)
+            rate, reps, outc = time_reference(run, z_cpu, 3, 1)
             line["cpu_baseline"] = {
                 "value": rate,
                 "unit": UNIT,
                 "cores": threads,
-                "kind": "port",
-                "sample": f"first {CPU_SAMPLE} queries of rank 0's stream, reference direct lane path "
-                          f"(batch.py:315-317, restated in oracle/fs_oracle.py), d=65536, {threads} threads, "
-                          f"median of {reps} passes",
+                "kind": kind,
+                "cpu_model": cpu_model(),
+                "sample": f"{version}: batch_search(LaneConfig(d=65536, 'direct')) over the first {len(z_cpu)} "
+                          f"queries of the stream, int32 out, threads={threads}, median of {reps} passes",
             }
             line["config"]["cpu_sample_matches_gpu"] = bool(np.array_equal(outc, o_cpu))
         print(json.dumps(line), flush=True)

@@ -46,7 +46,9 @@ typedef enum fs_status {
   FS_CUDA_ERROR = 5,          /* CUDA runtime failure; see fs_last_error()    */
   FS_INCONSISTENT = 6,        /* build_index: "(h, r) pair is inconsistent";
                                  fs_search_host: host/device checks disagree */
-  FS_TOO_LARGE = 7            /* table/workspace does not fit the device path */
+  FS_TOO_LARGE = 7,           /* table/workspace does not fit the device path */
+  FS_ABORTED = 8              /* fs_search_host_gated: another span of the same
+                                 batch is out of domain; nothing written      */
 } fs_status;
 
 /* ---- element types ---- */
@@ -379,6 +381,30 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
                    unsigned long long* status_dev, uint64_t chunk_elems,
                    int64_t* pos_out, void* stream, void* copy_stream, int32_t flags);
 
+/*
+ * One host batch split into contiguous spans searched concurrently -- one
+ * fs_search_host_gated call per span, e.g. one per GPU, each with its own
+ * plan, scratch and streams on its device (the reference's thread spans,
+ * batch.py:385-396 and 428-440, with devices for threads).  The calls share
+ * a gate created for `parties` spans: a call writes results back only once
+ * every span is known to be in domain, so the batch keeps batch.py:404's
+ * "nothing written on OutOfDomain" as a whole.  A span with a bad query
+ * returns FS_OUT_OF_DOMAIN with its span-local position (the caller
+ * min-merges span offset + position); the others return FS_ABORTED and
+ * write nothing.  A caller that cannot make its call must fs_gate_abort()
+ * the gate, or the other calls wait for it.  FS_HOST_OVERLAP calls ignore
+ * the gate.  Destroy the gate after every call has returned.
+ */
+typedef struct fs_gate fs_gate;
+fs_gate* fs_gate_create(int32_t parties);
+void fs_gate_abort(fs_gate* gate);
+void fs_gate_destroy(fs_gate* gate);
+int fs_search_host_gated(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host,
+                         int32_t out_bytes, void* z_dev, void* out_dev,
+                         unsigned long long* status_dev, uint64_t chunk_elems,
+                         int64_t* pos_out, void* stream, void* copy_stream, int32_t flags,
+                         fs_gate* gate);
+
 /* ---------------------------------------------------------------------------
  * Index persistence (bench/persist.py:1-112)
  * ------------------------------------------------------------------------ */
@@ -396,9 +422,15 @@ int fs_crc32(const void* data_dev, uint64_t bytes, void* ws_dev, uint32_t* crc_o
  * plus the dynamic shared memory bytes per CTA it stages. */
 int fs_plan_placement(const fs_plan* plan, int32_t* placement_out, uint64_t* smem_bytes_out);
 
-/* Number of kernel launches fs_search_device issues for this plan (for the
- * bench's gpu_launches accounting). */
+/* Number of kernel launches fs_search_device issues for this plan and batch
+ * (1, or 0 for an empty batch; -1 for an invalid plan). */
 int fs_search_launches(const fs_plan* plan, uint64_t m);
+
+/* Number of search kernels fs_search_host issues for the same arguments: one
+ * per chunk -- 16 MB of queries per staging slot for pageable buffers, else
+ * chunk_elems (default 64 MB of queries).  -1 for an invalid plan. */
+int64_t fs_search_host_launches(const fs_plan* plan, const void* z_host, uint64_t m, const void* out_host,
+                                int32_t out_bytes, uint64_t chunk_elems, int32_t flags);
 
 #ifdef __cplusplus
 }

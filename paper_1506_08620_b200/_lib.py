@@ -14,7 +14,7 @@ import os
 import threading
 from pathlib import Path
 
-from .errors import DeviceError, NotDistinguishable, OutOfDomain, Overflow
+from .errors import DeviceError, NotDistinguishable, OutOfDomain, Overflow, SpanAborted
 
 LIB_NAME = "libfsgpu.so"
 LIB_PATH = Path(__file__).with_name(LIB_NAME)
@@ -28,6 +28,7 @@ FS_INVALID_ARG = 4
 FS_CUDA_ERROR = 5
 FS_INCONSISTENT = 6
 FS_TOO_LARGE = 7
+FS_ABORTED = 8
 
 FS_F32 = 0
 FS_F64 = 1
@@ -85,10 +86,15 @@ EXPORTED = (
     "fs_search_ws_words",
     "fs_search_device",
     "fs_search_host",
+    "fs_search_host_gated",
+    "fs_gate_create",
+    "fs_gate_abort",
+    "fs_gate_destroy",
     "fs_crc32_ws_bytes",
     "fs_crc32",
     "fs_plan_placement",
     "fs_search_launches",
+    "fs_search_host_launches",
 )
 
 
@@ -188,6 +194,16 @@ def _declare(lib):
     lib.fs_search_host.argtypes = [
         ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp, _vp, _u64, _p_i64, _vp, _vp, _i32,
     ]
+    lib.fs_search_host_gated.restype = ctypes.c_int
+    lib.fs_search_host_gated.argtypes = [
+        ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp, _vp, _u64, _p_i64, _vp, _vp, _i32, _vp,
+    ]
+    lib.fs_gate_create.restype = _vp
+    lib.fs_gate_create.argtypes = [_i32]
+    lib.fs_gate_abort.restype = None
+    lib.fs_gate_abort.argtypes = [_vp]
+    lib.fs_gate_destroy.restype = None
+    lib.fs_gate_destroy.argtypes = [_vp]
     lib.fs_crc32_ws_bytes.restype = ctypes.c_size_t
     lib.fs_crc32_ws_bytes.argtypes = [_u64]
     lib.fs_crc32.restype = ctypes.c_int
@@ -196,6 +212,8 @@ def _declare(lib):
     lib.fs_plan_placement.argtypes = [ctypes.POINTER(FsPlan), _p_i32, _p_u64]
     lib.fs_search_launches.restype = ctypes.c_int
     lib.fs_search_launches.argtypes = [ctypes.POINTER(FsPlan), _u64]
+    lib.fs_search_host_launches.restype = ctypes.c_int64
+    lib.fs_search_host_launches.argtypes = [ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _u64, _i32]
 
 
 def load(path: str | os.PathLike | None = None):
@@ -233,4 +251,6 @@ def check(rc: int, pos: int | None = None, what: str = ""):
         raise OutOfDomain(position=None if pos is None else int(pos))
     if rc in (FS_INVALID_ARG, FS_INCONSISTENT, FS_TOO_LARGE):
         raise ValueError(msg or what)
+    if rc == FS_ABORTED:
+        raise SpanAborted(msg or what)
     raise DeviceError(f"{what}: {msg}" if what else msg)

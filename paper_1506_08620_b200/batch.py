@@ -113,28 +113,34 @@ def _plan_for(algorithm: str, structure, p: SortedPartition):
 
 
 def _search_host_array(plan, z: np.ndarray, out: np.ndarray, chunk_bytes: int = HOST_CHUNK_BYTES,
-                       overlap: bool = False, precheck: bool = True) -> None:
+                       overlap: bool = False, precheck: bool = True, gate=None) -> None:
     """End-to-end search of host queries into host ``out[:m]`` (fs_search_host).
     ``overlap`` = speculative per-chunk write-back (FS_HOST_OVERLAP);
     ``precheck=False`` = wait for the device's domain check before any
-    write-back (FS_HOST_NO_PRECHECK)."""
+    write-back (FS_HOST_NO_PRECHECK); ``gate`` = this call is one span of a
+    batch split over devices (fs_search_host_gated)."""
     m = len(z)
     if m == 0:
         return
-    _device.require_cuda()
-    z = np.ascontiguousarray(z)
-    direct_out = out.dtype in (np.int32, np.int64) and out.flags.c_contiguous and out.flags.writeable
-    target = out[:m] if direct_out else np.empty(m, dtype=np.int64)
-    ob = target.dtype.itemsize
-    z_dev = _device.empty(m, z.dtype)
-    o_dev = _device.empty(m, target.dtype)
-    fb = _cached_status(z_dev.device, _device.stream_ptr())
+    try:
+        _device.require_cuda()
+        z = np.ascontiguousarray(z)
+        direct_out = out.dtype in (np.int32, np.int64) and out.flags.c_contiguous and out.flags.writeable
+        target = out[:m] if direct_out else np.empty(m, dtype=np.int64)
+        ob = target.dtype.itemsize
+        z_dev = _device.empty(m, z.dtype)
+        o_dev = _device.empty(m, target.dtype)
+        fb = _cached_status(z_dev.device, _device.stream_ptr())
+    except BaseException:
+        if gate is not None:  # this span cannot make its call: release the others
+            _lib.load().fs_gate_abort(gate)
+        raise
     pos = ctypes.c_int64(-1)
-    rc = _lib.load().fs_search_host(
+    rc = _lib.load().fs_search_host_gated(
         ctypes.byref(plan), z.ctypes.data, m, target.ctypes.data, ob, z_dev.data_ptr(), o_dev.data_ptr(),
         fb.data_ptr(), max(4, chunk_bytes // z.dtype.itemsize), ctypes.byref(pos), _device.stream_ptr(),
         _device.stream_ptr(_copy_stream()),
-        (_lib.FS_HOST_OVERLAP if overlap else 0) | (0 if precheck else _lib.FS_HOST_NO_PRECHECK),
+        (_lib.FS_HOST_OVERLAP if overlap else 0) | (0 if precheck else _lib.FS_HOST_NO_PRECHECK), gate,
     )
     _lib.check(rc, pos=pos.value, what="fs_search_host")
     if not direct_out:
@@ -241,6 +247,34 @@ class PreparedKernel:
     lanes: Callable | None
     plan: object = field(default=None, repr=False, compare=False)
     buffers: tuple = field(default=(), repr=False, compare=False)
+    replicas: dict = field(default_factory=dict, repr=False, compare=False)
+
+    @property
+    def device_index(self) -> int:
+        return self.plan.device_index
+
+    def on_device(self, device: int) -> "PreparedKernel":
+        """This kernel's structure built on another CUDA device (once, then
+        cached): the build is deterministic, so every replica is
+        bit-identical."""
+        import torch
+
+        device = int(device)
+        if device == self.plan.device_index:
+            return self
+        rep = self.replicas.get(device)
+        if rep is None:
+            with torch.cuda.device(device):
+                qbits = getattr(self.structure, "qbits", 32)
+                if self.algorithm == "direct-generic":  # only prepare_loaded serves gap q >= 3
+                    from .persist import prepare_loaded
+
+                    idx, _ = build(self.partition, qbits=qbits, q=self.structure.q)
+                    rep = prepare_loaded(idx, self.partition)
+                else:
+                    rep = prepare(self.algorithm, self.partition, qbits)
+            self.replicas[device] = rep
+        return rep
 
     # -- device-level API (no host copies, no synchronisation) -------------
     def launch(self, z, out, status) -> None:
@@ -275,7 +309,17 @@ class PreparedKernel:
         }
 
     def launches_per_batch(self, m: int) -> int:
+        """Kernels one device-resident search of m queries launches (1)."""
         return int(_lib.load().fs_search_launches(ctypes.byref(self.plan), m))
+
+    def host_launches(self, z: np.ndarray, out: np.ndarray) -> int:
+        """Kernels ``batch_search`` launches for these host arrays: one per
+        chunk (fs_search_host_launches, the same chunking fs_search_host
+        applies; pageable buffers go through 16 MB staging slots)."""
+        z = np.ascontiguousarray(z)
+        return int(_lib.load().fs_search_host_launches(
+            ctypes.byref(self.plan), z.ctypes.data, len(z), out.ctypes.data, out.dtype.itemsize,
+            max(4, HOST_CHUNK_BYTES // z.dtype.itemsize), 0))
 
 
 @dataclass(frozen=True)
@@ -646,7 +690,8 @@ def resolve_threads(threads: int | None) -> int:
     return max(1, int(env)) if env else 1
 
 
-def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None, *, atomic: bool = True) -> int:
+def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None, *, atomic: bool = True,
+                 devices=None) -> int:
     """Resolve every query into ``out``; returns the number resolved
     (batch.py:399-441).
 
@@ -656,6 +701,14 @@ def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None, *, a
     are written back chunk by chunk while later chunks are still uploading,
     overlapping the two PCIe directions (~2x end to end); the exception and
     its position are unchanged.
+
+    ``devices`` (not in the reference; host arrays only): CUDA device
+    indices to split the batch over -- contiguous spans, one per entry, as
+    the reference splits spans over threads (batch.py:385-396, 428-440).
+    Each device searches its span with its own replica of the structure and
+    its own PCIe link; the spans share a gate, so an OutOfDomain anywhere
+    still leaves all of ``out`` untouched (atomic mode) and reports the
+    batch's first bad position.  ``"all"`` = every visible device.
     """
     kern = cfg.structure
     resolve_threads(threads)
@@ -687,6 +740,21 @@ def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None, *, a
             o.copy_(tmp)
         return m
     zz = coerce_queries(z, p.values.dtype)
+    if devices is not None:
+        devs = _resolve_devices(devices)
+        if len(devs) > 1 and m > 0:
+            if isinstance(out, np.ndarray):
+                _search_host_spans(kern, zz, out, devs, overlap=not atomic)
+            else:
+                tmp = np.empty(m, dtype=np.int64)
+                _search_host_spans(kern, zz, tmp, devs, overlap=not atomic)
+                out[:m] = tmp.tolist()
+            return m
+        import torch
+
+        with torch.cuda.device(devs[0]):
+            return batch_search(LaneConfig(cfg.d, cfg.kernel, kern.on_device(devs[0])), zz, out, threads,
+                                atomic=atomic)
     if isinstance(out, np.ndarray):
         _search_host_array(kern.plan, zz, out, overlap=not atomic)
     else:  # any mutable sequence, as the reference's slice assignment allows (batch.py:423)
@@ -694,6 +762,89 @@ def batch_search(cfg: LaneConfig, queries, out, threads: int | None = None, *, a
         _search_host_array(kern.plan, zz, tmp)
         out[:m] = tmp.tolist()
     return m
+
+
+def _resolve_devices(devices) -> list:
+    import torch
+
+    if isinstance(devices, str):
+        if devices != "all":
+            raise ValueError('devices must be a sequence of CUDA device indices or "all"')
+        devs = list(range(torch.cuda.device_count()))
+    else:
+        devs = [int(getattr(d, "index", d) if not isinstance(d, int) else d) for d in devices]
+    if not devs:
+        raise ValueError("devices is empty")
+    n = torch.cuda.device_count()
+    for d in devs:
+        if not 0 <= d < n:
+            raise ValueError(f"no CUDA device {d} (visible: {n})")
+    return devs
+
+
+_span_pool = None
+_span_pool_lock = threading.Lock()
+
+
+def _span_executor(n: int):
+    """Persistent threads that drive one span each (the native call of a span
+    releases the GIL and blocks until its span is done)."""
+    global _span_pool
+    from concurrent.futures import ThreadPoolExecutor
+
+    with _span_pool_lock:
+        if _span_pool is None or _span_pool._max_workers < n:
+            _span_pool = ThreadPoolExecutor(max_workers=max(n, 8), thread_name_prefix="fs-span")
+        return _span_pool
+
+
+def _search_host_spans(kern: PreparedKernel, z: np.ndarray, out: np.ndarray, devices: list, overlap: bool) -> None:
+    """One host batch over several devices: contiguous spans (8-query
+    granularity, dist.shard_span), one gated fs_search_host call per span on
+    its device, concurrently.  Raises OutOfDomain(first bad position of the
+    whole batch); in atomic mode nothing is written then (fs_gate)."""
+    import torch
+
+    from .dist import shard_span
+    from .errors import SpanAborted
+
+    m = len(z)
+    lib = _lib.load()
+    devices = devices[: max(1, min(len(devices), m // 8))]  # no empty spans: every party makes its call
+    n = len(devices)
+    spans = [shard_span(m, i, n, granularity=8) for i in range(n)]
+    reps = {d: kern.on_device(d) for d in set(devices)}  # built before any span starts (no gate held)
+    gate = lib.fs_gate_create(n)
+    if not gate:
+        raise MemoryError("fs_gate_create failed")
+
+    def run(i):
+        a, b = spans[i]
+        called = False
+        try:
+            torch.cuda.set_device(devices[i])
+            called = True  # from here on the native call arrives at the gate on every path
+            _search_host_array(reps[devices[i]].plan, z[a:b], out[a:b], overlap=overlap, gate=gate)
+            return None
+        except OutOfDomain as e:
+            return ("bad", a + int(e.position))
+        except SpanAborted:
+            return ("aborted", None)
+        except BaseException as e:  # noqa: BLE001 -- reported after every span returned
+            if not called:
+                lib.fs_gate_abort(gate)
+            return ("error", e)
+
+    try:
+        results = list(_span_executor(n).map(run, range(n)))
+    finally:
+        lib.fs_gate_destroy(gate)
+    errors = [r[1] for r in results if r and r[0] == "error"]
+    if errors:
+        raise errors[0]
+    bad = [r[1] for r in results if r and r[0] == "bad"]
+    if bad:
+        raise OutOfDomain(position=min(bad))
 
 
 def run_batch(prepared: PreparedKernel, queries, d: int = 1, threads: int | None = None):

@@ -1237,6 +1237,78 @@ size_t fs_search_ws_words(void) { return FS_SEARCH_WS_WORDS; }
 
 namespace {
 
+}  // namespace
+
+// One batch split into spans searched concurrently (one call per span, e.g.
+// one per GPU): every span's call arrives here once its own span is known
+// clean or bad, and no call writes results back until every span is clean
+// -- the "nothing written on OutOfDomain" promise of batch.py:404 over the
+// whole batch.  Single use.
+struct fs_gate {
+  std::mutex mu;
+  std::condition_variable cv;
+  int parties = 1, arrived = 0;
+  bool bad = false;
+  // true iff every party arrived with a clean span (a bad party returns at once)
+  bool arrive_and_wait(bool clean) {
+    std::unique_lock<std::mutex> lk(mu);
+    ++arrived;
+    if (!clean) bad = true;
+    cv.notify_all();
+    if (!clean) return false;
+    cv.wait(lk, [&] { return bad || arrived >= parties; });
+    return !bad;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    bad = true;
+    cv.notify_all();
+  }
+};
+
+namespace {
+
+// A call's single arrival at its gate; a call that leaves early (CUDA error,
+// bad argument) arrives as "bad" on the way out so no other span waits forever.
+struct GateArrival {
+  fs_gate* g;
+  bool done = false;
+  explicit GateArrival(fs_gate* gate) : g(gate) {}
+  bool arrive(bool clean) {
+    if (done) return clean;
+    done = true;
+    return g ? g->arrive_and_wait(clean) : clean;
+  }
+  ~GateArrival() {
+    if (g && !done) g->arrive_and_wait(false);
+  }
+};
+
+// Queries per staging slot of the pageable path (16 MB).
+uint64_t staged_chunk_elems(size_t es) { return ((16ull << 20) / es + 3) & ~3ull; }
+
+// How fs_search_host splits a batch: through the library's pinned staging
+// (pageable buffers of any real size) or straight from page-locked memory,
+// and the queries per chunk (one search kernel per chunk).
+struct HostChunking {
+  bool staged;
+  uint64_t chunk;
+};
+HostChunking host_chunking(const fs_plan* plan, const void* z_host, uint64_t m, const void* out_host, int out_bytes,
+                           uint64_t chunk_elems, int flags) {
+  const size_t es = plan->dtype == FS_F32 ? 4 : 8;
+  HostChunking hc;
+  hc.staged = m * (uint64_t)out_bytes >= (4ull << 20) && !(flags & FS_HOST_NO_STAGING) &&
+              !(is_pinned(z_host) && is_pinned(out_host));
+  if (hc.staged) {
+    hc.chunk = staged_chunk_elems(es);
+  } else {
+    if (chunk_elems == 0) chunk_elems = (64ull << 20) / es;
+    hc.chunk = (chunk_elems + 7) & ~7ull;  // keep every chunk 32-B aligned on device (8-query groups)
+  }
+  return hc;
+}
+
 // End-to-end search of PAGEABLE host buffers through pinned staging slots:
 // phase 1 streams queries pageable -> pinned slot (host threads) -> device
 // (copy engine) with the search kernel of each chunk queued behind its
@@ -1244,10 +1316,10 @@ namespace {
 // 2 drains results device -> pinned slot -> pageable out the same way.
 int search_host_staged(const fs_plan* plan, Placement pl, const void* z_host, uint64_t m, void* out_host, int ob,
                        void* z_dev, void* out_dev, unsigned long long* fb, int64_t* pos_out, cudaStream_t s,
-                       cudaStream_t cs) {
+                       cudaStream_t cs, GateArrival& gate) {
   constexpr int kSlots = 3;
   const size_t es = plan->dtype == FS_F32 ? 4 : 8;
-  const uint64_t chunk = ((16ull << 20) / es + 3) & ~3ull;  // 16 MB of queries per slot
+  const uint64_t chunk = staged_chunk_elems(es);  // 16 MB of queries per slot
   const size_t slot_bytes = chunk * std::max<size_t>(es, (size_t)ob);
   void* slot[kSlots] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev[kSlots] = {nullptr, nullptr, nullptr};
@@ -1258,7 +1330,7 @@ int search_host_staged(const fs_plan* plan, Placement pl, const void* z_host, ui
     else if (cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess)
       status = fail(FS_CUDA_ERROR, "event creation failed");
   }
-  CopyPool pool(host_copy_threads());
+  const int copy_threads = host_copy_threads();
   pl.merge = 1;
   if (status == FS_OK && cudaMemsetAsync(fb, 0xff, sizeof(unsigned long long), s) != cudaSuccess)
     status = fail(FS_CUDA_ERROR, "status reset failed");
@@ -1271,7 +1343,7 @@ int search_host_staged(const fs_plan* plan, Placement pl, const void* z_host, ui
       status = fail(FS_CUDA_ERROR, "staging slot wait failed");
       break;
     }
-    pool.copy(slot[k], static_cast<const char*>(z_host) + off * es, n * es);
+    host_copy(slot[k], static_cast<const char*>(z_host) + off * es, n * es, copy_threads);
     char* dst = static_cast<char*>(z_dev) + off * es;
     cudaError_t e = cudaMemcpyAsync(dst, slot[k], n * es, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaEventRecord(ev[k], cs);
@@ -1290,8 +1362,10 @@ int search_host_staged(const fs_plan* plan, Placement pl, const void* z_host, ui
   }
   if (status == FS_OK && bad != ~0ull) {
     if (pos_out) *pos_out = (int64_t)bad;
+    gate.arrive(false);
     status = fail(FS_OUT_OF_DOMAIN, "query outside [X0, XN)");
   }
+  if (status == FS_OK && !gate.arrive(true)) status = fail(FS_ABORTED, "another span of the batch is out of domain");
   // phase 2: download (only for a clean batch)
   if (status == FS_OK) {
     const uint64_t nch = (m + chunk - 1) / chunk;
@@ -1307,7 +1381,7 @@ int search_host_staged(const fs_plan* plan, Placement pl, const void* z_host, ui
         const uint64_t off = (i - 1) * chunk, n = std::min(chunk, m - off);
         const int k = (int)((i - 1) % kSlots);
         if (cudaEventSynchronize(ev[k]) != cudaSuccess) status = fail(FS_CUDA_ERROR, "staging slot wait failed");
-        else pool.copy(static_cast<char*>(out_host) + off * ob, slot[k], n * ob);
+        else host_copy(static_cast<char*>(out_host) + off * ob, slot[k], n * ob, copy_threads);
       }
     }
   }
@@ -1321,9 +1395,31 @@ int search_host_staged(const fs_plan* plan, Placement pl, const void* z_host, ui
 
 }  // namespace
 
+fs_gate* fs_gate_create(int32_t parties) {
+  if (parties < 1) return nullptr;
+  fs_gate* g = new (std::nothrow) fs_gate();
+  if (g) g->parties = parties;
+  return g;
+}
+
+void fs_gate_abort(fs_gate* gate) {
+  if (gate) gate->abort();
+}
+
+void fs_gate_destroy(fs_gate* gate) { delete gate; }
+
 int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host, int32_t out_bytes, void* z_dev,
                    void* out_dev, unsigned long long* first_bad_dev, uint64_t chunk_elems, int64_t* pos_out,
                    void* stream, void* copy_stream, int32_t flags) {
+  return fs_search_host_gated(plan, z_host, m, out_host, out_bytes, z_dev, out_dev, first_bad_dev, chunk_elems,
+                              pos_out, stream, copy_stream, flags, nullptr);
+}
+
+int fs_search_host_gated(const fs_plan* plan, const void* z_host, uint64_t m, void* out_host, int32_t out_bytes,
+                         void* z_dev, void* out_dev, unsigned long long* first_bad_dev, uint64_t chunk_elems,
+                         int64_t* pos_out, void* stream, void* copy_stream, int32_t flags, fs_gate* gate_ptr) {
+  // the speculative mode promises nothing about other spans: no gate
+  GateArrival gate((flags & FS_HOST_OVERLAP) ? nullptr : gate_ptr);
   int rc = check_search_args(plan, z_dev, m, out_dev, out_bytes, first_bad_dev);
   if (rc) return rc;
   if (m && (!z_host || !out_host)) return fail(FS_INVALID_ARG, "host pointer is NULL");
@@ -1341,14 +1437,13 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
     if (e != cudaSuccess) return fail(FS_CUDA_ERROR, std::string("stream ordering: ") + cudaGetErrorString(e));
   }
   // pageable buffers of any real size go through the library's own pinned staging
-  if (m * (uint64_t)out_bytes >= (4ull << 20) && !(flags & FS_HOST_NO_STAGING) &&
-      !(is_pinned(z_host) && is_pinned(out_host)))
+  const HostChunking hc = host_chunking(plan, z_host, m, out_host, out_bytes, chunk_elems, flags);
+  if (hc.staged)
     return search_host_staged(plan, place_for_batch(plan, m), z_host, m, out_host, out_bytes, z_dev, out_dev,
-                              first_bad_dev, pos_out, s, cs);
+                              first_bad_dev, pos_out, s, cs, gate);
   const bool overlap = (flags & FS_HOST_OVERLAP) != 0;
   const size_t es = plan->dtype == FS_F32 ? 4 : 8;
-  if (chunk_elems == 0) chunk_elems = (64ull << 20) / es;
-  chunk_elems = (chunk_elems + 7) & ~7ull;  // keep every chunk 32-B aligned on device (8-query groups)
+  chunk_elems = hc.chunk;
   Placement pl = place_for_batch(plan, m);
   pl.merge = 1;  // every chunk min-merges into status[0]
   // atomic mode over several chunks: host threads check the domain while the
@@ -1387,7 +1482,7 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   std::vector<cudaEvent_t>& done = st.done;
   unsigned long long* prefix_bad = st.prefix_bad;
   int status = FS_OK;
-  bool wrote = false;
+  bool wrote = false, aborted = false;
   for (uint64_t off = 0; off < m && status == FS_OK; off += chunk_elems) {
     const uint64_t n = std::min(chunk_elems, m - off);
     const char* src = static_cast<const char*>(z_host) + off * es;
@@ -1427,12 +1522,15 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   // ends meanwhile, then queue each chunk's write-back behind its kernel
   if (status == FS_OK && precheck) {
     const int64_t nd = (int64_t)done.size();
-    const bool clean =
+    bool clean =
         plan->dtype == FS_F32
             ? domain_clean_two_sided<float>(static_cast<const float*>(z_host), m, chunk_elems, (float)plan->x0,
                                             (float)plan->xn, host_scan_threads(), done.data(), prefix_bad, nd)
             : domain_clean_two_sided<double>(static_cast<const double*>(z_host), m, chunk_elems, plan->x0, plan->xn,
                                              host_scan_threads(), done.data(), prefix_bad, nd);
+    // every other span of a gated batch must be clean too before any write-back
+    aborted = !gate.arrive(clean) && clean;
+    clean = clean && !aborted;
     for (uint64_t c = 0; clean && c < done.size() && status == FS_OK; ++c) {
       const uint64_t off = c * chunk_elems, n = std::min(chunk_elems, m - off);
       cudaError_t e = cudaStreamWaitEvent(ds, done[c], 0);
@@ -1454,9 +1552,11 @@ int fs_search_host(const fs_plan* plan, const void* z_host, uint64_t m, void* ou
   if (status != FS_OK) return status;
   if (bad != ~0ull) {
     if (pos_out) *pos_out = (int64_t)bad;
+    gate.arrive(false);
     if (wrote) return fail(FS_INCONSISTENT, "host and device domain checks disagree (queries modified during the call?)");
     return fail(FS_OUT_OF_DOMAIN, "query outside [X0, XN)");
   }
+  if (aborted || !gate.arrive(true)) return fail(FS_ABORTED, "another span of the batch is out of domain");
   if (m && !overlap && !wrote) {
     FS_CUDA(cudaMemcpyAsync(out_host, out_dev, m * (uint64_t)out_bytes, cudaMemcpyDeviceToHost, s));
     FS_CUDA(cudaStreamSynchronize(s));
@@ -1501,8 +1601,16 @@ int fs_plan_placement(const fs_plan* plan, int32_t* placement_out, uint64_t* sme
 }
 
 int fs_search_launches(const fs_plan* plan, uint64_t m) {
-  (void)plan;
-  return m ? 1 : 0;
+  if (validate_plan(plan)) return -1;
+  return m ? 1 : 0;  // launch_search: exactly one kernel; an empty batch only resets the status word
+}
+
+int64_t fs_search_host_launches(const fs_plan* plan, const void* z_host, uint64_t m, const void* out_host,
+                                int32_t out_bytes, uint64_t chunk_elems, int32_t flags) {
+  if (validate_plan(plan) || (out_bytes != 4 && out_bytes != 8)) return -1;
+  if (m == 0) return 0;
+  const HostChunking hc = host_chunking(plan, z_host, m, out_host, out_bytes, chunk_elems, flags);
+  return (int64_t)((m + hc.chunk - 1) / hc.chunk);  // one search kernel per chunk (staged or pinned)
 }
 
 }  // extern "C"

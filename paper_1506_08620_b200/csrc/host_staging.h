@@ -5,8 +5,8 @@
 // buffer at ~14 GB/s here (measured: 1.7 G queries/s end to end on cfg3
 // versus 6.9 with pinned arrays).  A numpy array handed to batch_search is
 // pageable, so the library stages it itself: a small ring of pinned slots
-// (cached process-wide, reused across calls) filled / drained by a pool of
-// host threads doing parallel memcpy, overlapped with the DMA of the
+// (cached process-wide, reused across calls) filled / drained by the
+// process-wide host pool doing parallel memcpy, overlapped with the DMA of the
 // previous slot on the copy engine.
 #pragma once
 
@@ -19,84 +19,153 @@
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <functional>
+#include <unistd.h>
 #include <mutex>
 #include <thread>
 #include <vector>
 
 namespace fsg {
 
-// Parallel memcpy by n threads (the caller is thread 0); workers live for
-// the lifetime of the pool.
-class CopyPool {
+// Process-wide pool of host worker threads, created once per process on first
+// use and kept for its lifetime (re-created in a forked child, whose copy of
+// the parent's pool has no threads).  Every host-side parallel step of the
+// end-to-end path -- the parallel memcpy of pageable staging and the host
+// half of the two-sided domain check -- runs as a job on it, so no call
+// spawns or joins threads (that cost hundreds of microseconds per call,
+// against ~0.1 ms of PCIe for a 4 MB batch).  Jobs from concurrent callers
+// queue and run in order; a caller may help run its own job's tasks.
+class HostPool {
  public:
-  explicit CopyPool(int n) : n_(std::max(1, n)) {
-    for (int i = 1; i < n_; ++i) threads_.emplace_back([this, i] { worker(i); });
-  }
-  ~CopyPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-      ++gen_;
-    }
-    cv_.notify_all();
-    for (auto& t : threads_) t.join();
-  }
-  CopyPool(const CopyPool&) = delete;
-  CopyPool& operator=(const CopyPool&) = delete;
+  struct Job {
+    std::function<void(int)> fn;
+    int n = 0;
+    int next = 0, finished = 0;  // guarded by the pool mutex
+    std::condition_variable cv;
+  };
 
-  void copy(void* dst, const void* src, size_t bytes) {
-    if (n_ == 1 || bytes < (1u << 20)) {
-      std::memcpy(dst, src, bytes);
-      return;
-    }
+  static HostPool& get();
+  int size() const { return (int)threads_.size(); }
+
+  std::shared_ptr<Job> submit(int n, std::function<void(int)> fn) {
+    auto job = std::make_shared<Job>();
+    job->fn = std::move(fn);
+    job->n = n;
+    if (n <= 0) return job;
     {
       std::lock_guard<std::mutex> lk(mu_);
-      dst_ = static_cast<char*>(dst);
-      src_ = static_cast<const char*>(src);
-      bytes_ = bytes;
-      pending_ = n_ - 1;
-      ++gen_;
+      q_.push_back(job);
     }
     cv_.notify_all();
-    slice(0, dst_, src_, bytes_);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_.wait(lk, [this] { return pending_ == 0; });
+    return job;
   }
+  // Wait for every task of `job`; with `help` the caller runs unclaimed tasks itself.
+  void wait(const std::shared_ptr<Job>& job, bool help) {
+    std::unique_lock<std::mutex> lk(mu_);
+    while (help && job->next < job->n) {
+      const int i = job->next++;
+      lk.unlock();
+      job->fn(i);
+      lk.lock();
+      ++job->finished;
+    }
+    job->cv.wait(lk, [&] { return job->finished == job->n; });
+    // a fully claimed job may still sit in the queue; workers drop it lazily
+  }
+  void run(int n, std::function<void(int)> fn) { wait(submit(n, std::move(fn)), true); }
 
  private:
-  void slice(int i, char* dst, const char* src, size_t bytes) const {
-    const size_t per = ((bytes + n_ - 1) / n_ + 63) & ~size_t(63);
-    const size_t a = std::min(bytes, per * i), b = std::min(bytes, a + per);
-    if (b > a) std::memcpy(dst + a, src + a, b - a);
+  explicit HostPool(int n) {
+    for (int i = 0; i < n; ++i) threads_.emplace_back([this] { worker(); });
   }
-  void worker(int i) {
-    unsigned long long seen = 0;
+  void worker() {
     std::unique_lock<std::mutex> lk(mu_);
     for (;;) {
-      cv_.wait(lk, [&] { return gen_ != seen; });
-      seen = gen_;
-      if (stop_) return;
-      char* d = dst_;
-      const char* s = src_;
-      const size_t b = bytes_;
+      cv_.wait(lk, [&] { return !q_.empty(); });
+      std::shared_ptr<Job> job = q_.front();
+      if (job->next >= job->n) {
+        q_.pop_front();
+        continue;
+      }
+      const int i = job->next++;
+      if (job->next >= job->n) q_.pop_front();
       lk.unlock();
-      slice(i, d, s, b);
+      job->fn(i);
       lk.lock();
-      if (--pending_ == 0) done_.notify_one();
+      if (++job->finished == job->n) job->cv.notify_all();
     }
   }
-
-  int n_;
-  std::vector<std::thread> threads_;
+  std::vector<std::thread> threads_;  // detached at exit: the pool lives as long as the process
   std::mutex mu_;
-  std::condition_variable cv_, done_;
-  unsigned long long gen_ = 0;
-  bool stop_ = false;
-  char* dst_ = nullptr;
-  const char* src_ = nullptr;
-  size_t bytes_ = 0;
-  int pending_ = 0;
+  std::condition_variable cv_;
+  std::deque<std::shared_ptr<Job>> q_;
 };
+
+// Processes sharing this host's cores: one per GPU under torchrun
+// (LOCAL_WORLD_SIZE), so N ranks do not oversubscribe the host N times over.
+inline unsigned host_procs() {
+  if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) {
+    const int n = std::atoi(e);
+    if (n > 1) return (unsigned)n;
+  }
+  return 1u;
+}
+
+inline int env_threads(const char* name) {
+  if (const char* e = std::getenv(name)) {  // tuning override
+    const int n = std::atoi(e);
+    if (n > 0) return std::min(n, 64);
+  }
+  return 0;
+}
+
+inline int host_share() {
+  const unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(32u, (hc ? hc : 4u) / host_procs()));
+}
+
+inline int host_scan_threads() {
+  const int n = env_threads("FSG_SCAN_THREADS");
+  return n ? n : host_share();
+}
+
+inline int host_copy_threads() {
+  // every hardware thread (this process's share of them): staging is host-
+  // memory-bandwidth bound (tools/pageable_threads.py on the 16-core GPU
+  // host: 8 -> 4.7, 16 -> 5.2 G queries/s)
+  const int n = env_threads("FSG_COPY_THREADS");
+  return n ? n : std::max(2, host_share());
+}
+
+inline HostPool& HostPool::get() {
+  static std::mutex mu;
+  static HostPool* pool = nullptr;
+  static pid_t owner = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pool || owner != getpid()) {  // first use, or a forked child
+    pool = new HostPool(std::max(host_copy_threads(), host_scan_threads()));
+    for (auto& t : pool->threads_) t.detach();
+    owner = getpid();
+  }
+  return *pool;
+}
+
+// Parallel memcpy over `n` slices on the host pool (the caller runs slices too).
+inline void host_copy(void* dst, const void* src, size_t bytes, int n) {
+  n = std::max(1, std::min(n, HostPool::get().size() + 1));
+  if (n == 1 || bytes < (1u << 20)) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+  const size_t per = ((bytes + n - 1) / n + 63) & ~size_t(63);
+  HostPool::get().run(n, [=](int i) {
+    const size_t a = std::min(bytes, per * i), b = std::min(bytes, a + per);
+    if (b > a) std::memcpy(d + a, s + a, b - a);
+  });
+}
 
 // Process-wide cache of pinned staging slots (allocation pins pages and is
 // slow; a slot is reused by later calls once released).
@@ -212,8 +281,8 @@ bool domain_clean_two_sided(const T* z, uint64_t m, uint64_t chunk, T x0, T xn, 
       clean[c].store(1);
     }
   };
-  std::vector<std::thread> th;
-  for (int i = 0; i < std::max(1, nthreads); ++i) th.emplace_back(worker);
+  auto job = HostPool::get().submit(std::max(1, std::min(nthreads, HostPool::get().size())),
+                                    [&](int) { worker(); });
   int64_t g = -1;  // chunks [0, g] verified by the device
   while (!bad.load()) {
     while (g + 1 < nch && cudaEventQuery(done[g + 1]) == cudaSuccess) {
@@ -229,39 +298,8 @@ bool domain_clean_two_sided(const T* z, uint64_t m, uint64_t chunk, T x0, T xn, 
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
   stop.store(true);
-  for (auto& t : th) t.join();
+  HostPool::get().wait(job, false);  // tasks not yet started return at once
   return !bad.load();
-}
-
-// Processes sharing this host's cores: one per GPU under torchrun
-// (LOCAL_WORLD_SIZE), so N ranks do not oversubscribe the host N times over.
-inline unsigned host_procs() {
-  if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) {
-    const int n = std::atoi(e);
-    if (n > 1) return (unsigned)n;
-  }
-  return 1u;
-}
-
-inline int host_scan_threads() {
-  if (const char* e = std::getenv("FSG_SCAN_THREADS")) {  // tuning override
-    const int n = std::atoi(e);
-    if (n > 0) return std::min(n, 64);
-  }
-  const unsigned hc = std::thread::hardware_concurrency();
-  return (int)std::max(1u, std::min(32u, (hc ? hc : 4u) / host_procs()));
-}
-
-inline int host_copy_threads() {
-  if (const char* e = std::getenv("FSG_COPY_THREADS")) {  // tuning override
-    const int n = std::atoi(e);
-    if (n > 0) return std::min(n, 64);
-  }
-  // every hardware thread (this process's share of them): staging is host-
-  // memory-bandwidth bound (tools/pageable_threads.py on the 16-core GPU
-  // host: 8 -> 4.7, 16 -> 5.2 G queries/s)
-  const unsigned hc = std::thread::hardware_concurrency();
-  return (int)std::max(2u, std::min(32u, (hc ? hc : 4u) / host_procs()));
 }
 
 }  // namespace fsg

@@ -50,17 +50,24 @@ def global_first_bad(local_first_bad: int | None, offset: int, group=None, devic
     return None if val == NO_BAD else val
 
 
-def sharded_batch_search(prepared, z_local, out_local, offset: int, group=None) -> int:
+def sharded_batch_search(prepared, z_local, out_local, offset: int, group=None, status=None) -> int:
     """Search this rank's span on its GPU, then agree on OutOfDomain.
 
     ``z_local``/``out_local`` are CUDA tensors holding queries
-    [offset, offset + len) of the global batch.  Raises OutOfDomain with the
-    global first position on every rank if any rank saw a bad query.
+    [offset, offset + len) of the global batch; ``status`` an optional
+    reusable workspace (new_status()).  One search kernel, then the span's
+    first bad position -- made global (offset added, "clean" mapped to the
+    int64 maximum) on the device -- goes through one MIN all-reduce, and a
+    single host read decides: OutOfDomain with the global first position
+    on every rank if any rank saw a bad query.  Returns the span's length.
     """
-    fb = new_status(z_local.device)
+    fb = status if status is not None else new_status(z_local.device)
     prepared.launch(z_local, out_local, fb)
-    local = first_bad_of(fb)
-    first = global_first_bad(local, offset, group=group, device=z_local.device)
-    if first is not None:
+    st = fb[:1].view(torch.int64)  # UINT64_MAX (clean) reads as -1
+    val = torch.where(st < 0, torch.full_like(st, NO_BAD), st + int(offset))
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(val, op=dist.ReduceOp.MIN, group=group)
+    first = int(val.item())
+    if first != NO_BAD:
         raise OutOfDomain(position=first)
     return z_local.numel()

@@ -18,7 +18,7 @@ HEADER = ROOT / "include" / "fsgpu.h"
 def declared_functions():
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:const\s+char\s*\*|int|size_t|uint64_t)\s+(fs_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+char\s*\*|int|int64_t|size_t|uint64_t|void|fs_gate\s*\*)\s*(fs_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_and_binding_agree():

@@ -707,3 +707,120 @@ def test_full_size_configs(cuda, name, kw, m):
     idx = torch.randint(0, m, (1_000_000,), device=cuda)
     zs = z[idx].cpu().numpy()
     assert np.array_equal(outs[0][idx].cpu().numpy(), orc.rank_oracle(p.values, zs))
+
+
+def test_launch_counts_match_the_kernels_launched(cuda):
+    """launches_per_batch / host_launches (fs_search_launches /
+    fs_search_host_launches) equal the search kernels CUPTI sees for the
+    device path, the chunked pinned path and the staged pageable path."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    fs = _fs()
+    p = fs.gen_uniform_gap_partition(4097, 0.5, 1.5, seed=0, precision="single")
+    prep = fs.prepare("direct", p)
+    cfg = fs.LaneConfig(8, "direct", prep)
+
+    def count(fn):
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        return sum(1 for e in prof.events() if "search_kernel" in e.name and e.device_type.name == "CUDA")
+
+    m = 3 * (16 << 20) // 4 + 12345  # four 16-MB staging slots / two 64-MB pinned chunks
+    z = orc.random_queries(p.values, m, seed=3)
+    zt = torch.from_numpy(z).cuda()
+    out_t = torch.empty(m, dtype=torch.int32, device=cuda)
+    assert count(lambda: fs.batch_search(cfg, zt, out_t)) == prep.launches_per_batch(m) == 1
+    out = np.empty(m, dtype=np.int32)
+    n_pageable = prep.host_launches(z, out)
+    assert n_pageable == 4
+    assert count(lambda: fs.batch_search(cfg, z, out)) == n_pageable
+    zp = torch.from_numpy(z).pin_memory()
+    op = torch.empty(m, dtype=torch.int32).pin_memory()
+    n_pinned = prep.host_launches(zp.numpy(), op.numpy())
+    assert n_pinned == 1  # 50 MB of queries < one 64-MB chunk
+    assert count(lambda: fs.batch_search(cfg, zp.numpy(), op.numpy())) == n_pinned
+    assert prep.launches_per_batch(0) == 0 and prep.host_launches(z[:0], out[:0]) == 0
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("nspan", [2, 3])
+def test_multi_device_spans_on_one_device(cuda, pinned, nspan):
+    """batch_search(..., devices=[0]*k): the batch split into k contiguous
+    spans, each a gated native call of its own (the multi-GPU host path,
+    exercised with every span on cuda:0).  Answers bit-identical to the
+    single call; an out-of-domain query in any span leaves ALL of out
+    untouched and reports the batch's first bad position; atomic=False
+    reports the same position."""
+    import torch
+
+    fs = _fs()
+    for prec, odt in (("single", np.int32), ("double", np.int64)):
+        p = fs.gen_uniform_gap_partition(4097, 0.5, 1.5, seed=2, precision=prec)
+        m = 3_000_011  # odd size: ragged last span, chunked per span
+        z = orc.random_queries(p.values, m, seed=5)
+        want = orc.rank_oracle(p.values, z)
+        prep = fs.prepare("direct", p)
+        cfg = fs.LaneConfig(8, "direct", prep)
+        if pinned:
+            zt = torch.from_numpy(z).pin_memory()
+            ot = torch.empty(m, dtype=torch.int32 if odt == np.int32 else torch.int64).pin_memory()
+            zz, out = zt.numpy(), ot.numpy()
+        else:
+            zz, out = z.copy(), np.empty(m, dtype=odt)
+        assert fs.batch_search(cfg, zz, out, devices=[0] * nspan) == m
+        assert np.array_equal(out, want)
+        for bad_at in (m - 1, m // 2 + 3, 5):
+            zb = zz.copy()
+            zb[bad_at] = np.nan
+            zb[min(m - 1, bad_at + 1000)] = p.values[-1]  # a later bad one in the same or next span
+            out[:] = -9
+            with pytest.raises(fs.OutOfDomain) as ei:
+                fs.batch_search(cfg, zb, out, devices=[0] * nspan)
+            assert ei.value.position == bad_at
+            assert bool((out == -9).all()), "atomic: nothing written when any span is bad"
+            with pytest.raises(fs.OutOfDomain) as ei:
+                fs.batch_search(cfg, zb, out, devices=[0] * nspan, atomic=False)
+            assert ei.value.position == bad_at
+        # a tiny batch uses fewer spans; one device entry = the plain path
+        assert np.array_equal(fs.run_batch(prep, z[:13]), want[:13])
+        small = np.empty(13, dtype=np.int64)
+        fs.batch_search(cfg, z[:13], small, devices=[0] * nspan)
+        assert np.array_equal(small, want[:13])
+        one = np.empty(1000, dtype=np.int64)
+        fs.batch_search(cfg, z[:1000], one, devices=[0])
+        assert np.array_equal(one, want[:1000])
+    with pytest.raises(ValueError):
+        fs.batch_search(cfg, z, np.empty(m, dtype=np.int64), devices=[99])
+
+
+def test_sharded_batch_search_spans_on_one_device(cuda):
+    """dist.sharded_batch_search, the call bench.py times per rank, driven
+    over k spans of one stream on cuda:0 (no process group: the all-reduce
+    is the identity): answers equal the oracle, out-of-domain positions are
+    global (span offset added on the device)."""
+    import torch
+
+    from paper_1506_08620_b200 import dist as fsdist
+
+    fs = _fs()
+    p = fs.gen_uniform_gap_partition(4097, 0.5, 1.5, seed=0, precision="single")
+    prep = fs.prepare("direct", p)
+    m = 1_000_003
+    z = orc.random_queries(p.values, m, seed=9)
+    want = orc.rank_oracle(p.values, z)
+    zt = torch.from_numpy(z).to(cuda)
+    out = torch.empty(m, dtype=torch.int32, device=cuda)
+    st = fs.new_status(cuda)
+    for k in (1, 2, 5):
+        for r in range(k):
+            a, b = fsdist.shard_span(m, r, k, granularity=8)
+            assert fsdist.sharded_batch_search(prep, zt[a:b], out[a:b], a, status=st) == b - a
+        assert np.array_equal(out.cpu().numpy(), want)
+    zt[777_777] = float("nan")
+    a, b = fsdist.shard_span(m, 1, 2, granularity=8)
+    with pytest.raises(fs.OutOfDomain) as ei:
+        fsdist.sharded_batch_search(prep, zt[a:b], out[a:b], a)
+    assert ei.value.position == 777_777
