@@ -111,7 +111,8 @@ typedef struct fs_plan {
   int32_t tune;       /* launch-geometry override for tuning runs, 0 = auto:
                          bits 0-11 threads per CTA, bits 12-19 max CTAs per SM   */
   const void* rank;   /* direct, optional: rank directory of K (gap 1:
-                         fs_build_rank, 8-B words; gap 2: fs_build_rank2, 16-B
+                         fs_build_rank, 8-B words; generic gap q:
+                         fs_build_countdir, 8-B words; gap 2: fs_build_rank2, 16-B
                          words); when set the kernel reads it instead of K.
                          NULL = read K.                                           */
   const void* records;/* direct (gap 1) only, optional: fused (K[j], X[K[j]])
@@ -202,6 +203,23 @@ int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
  * buckets holding knots.  dir_dev holds (r >> 5) + 1 words; set it as
  * fs_plan.rank of a FS_ALGO_DIRECT_GAP2 plan.
  */
+/*
+ * Count directory of a gap-q table, q = 2..15 (a device layout of
+ * build_index with q > 1, direct.py:200-243, searched as
+ * direct_search_generic, direct.py:294-300; no reference counterpart).  A
+ * gap-q certificate allows at most q knots per bucket, so a bucket's count
+ * fits 2 bits (q <= 3; 16 buckets per word) or 4 bits (q <= 15; 8 per word):
+ * 8-B words {counts, base = #knots before the word}.  The kernel recovers
+ * K_q[j] exactly and compares z only with the knots of its own bucket.
+ * This is what makes a larger gap a practical answer to an infeasible gap-1
+ * layout (the minimal q that meets a memory budget).
+ * dir_dev holds fs_countdir_bytes(q, r) bytes; set it as fs_plan.rank of a
+ * FS_ALGO_DIRECT_GENERIC plan with the same q.
+ */
+uint64_t fs_countdir_bytes(int32_t q, uint64_t r);
+int fs_build_countdir(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t q,
+                      uint64_t* f_scratch_dev, void* dir_dev, void* stream);
+
 int fs_build_rank2(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
                    uint64_t* f_scratch_dev, void* dir_dev, void* stream);
 
@@ -338,6 +356,17 @@ size_t fs_search_ws_words(void);
  */
 int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* out_dev,
                      int32_t out_bytes, unsigned long long* status_dev, void* stream);
+
+/*
+ * fs_search_device over queries base .. base + m - 1 of a larger batch (a
+ * shard): status word 0 receives base + the first bad offset (UINT64_MAX when
+ * clean) and word 3 the same value XOR 2^63 -- ordered as a SIGNED int64,
+ * "clean" = INT64_MAX -- so shards agree on the batch's first bad position
+ * with one MIN all-reduce of word 3 (dist.sharded_batch_search).  ASYNC:
+ * exactly one kernel launch (m > 0).
+ */
+int fs_search_device_at(const fs_plan* plan, const void* z_dev, uint64_t m, void* out_dev,
+                        int32_t out_bytes, unsigned long long* status_dev, uint64_t base, void* stream);
 
 /*
  * End-to-end host-buffer search: the whole batch_search contract

@@ -80,11 +80,14 @@ EXPORTED = (
     "fs_build_fused",
     "fs_build_padded",
     "fs_build_rank2",
+    "fs_countdir_bytes",
+    "fs_build_countdir",
     "fs_b2_deep_bytes",
     "fs_build_b2_deep",
     "fs_build_eytzinger",
     "fs_search_ws_words",
     "fs_search_device",
+    "fs_search_device_at",
     "fs_search_host",
     "fs_search_host_gated",
     "fs_gate_create",
@@ -190,6 +193,8 @@ def _declare(lib):
     lib.fs_search_ws_words.argtypes = []
     lib.fs_search_device.restype = ctypes.c_int
     lib.fs_search_device.argtypes = [ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp]
+    lib.fs_search_device_at.restype = ctypes.c_int
+    lib.fs_search_device_at.argtypes = [ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _u64, _vp]
     lib.fs_search_host.restype = ctypes.c_int
     lib.fs_search_host.argtypes = [
         ctypes.POINTER(FsPlan), _vp, _u64, _vp, _i32, _vp, _vp, _vp, _u64, _p_i64, _vp, _vp, _i32,
@@ -204,6 +209,10 @@ def _declare(lib):
     lib.fs_gate_abort.argtypes = [_vp]
     lib.fs_gate_destroy.restype = None
     lib.fs_gate_destroy.argtypes = [_vp]
+    lib.fs_countdir_bytes.restype = _u64
+    lib.fs_countdir_bytes.argtypes = [_i32, _u64]
+    lib.fs_build_countdir.restype = ctypes.c_int
+    lib.fs_build_countdir.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp]
     lib.fs_crc32_ws_bytes.restype = ctypes.c_size_t
     lib.fs_crc32_ws_bytes.argtypes = [_u64]
     lib.fs_crc32.restype = ctypes.c_int

@@ -177,12 +177,13 @@ def _cached_status(device, stream_ptr: int):
     return s
 
 
-def _launch_device(plan, z, out, status) -> None:
-    """Asynchronous device search (fs_search_device): exactly one kernel;
-    status[0] receives the first out-of-domain position."""
+def _launch_device(plan, z, out, status, base: int = 0) -> None:
+    """Asynchronous device search (fs_search_device_at): exactly one kernel;
+    status[0] receives base + the first out-of-domain position, status[3]
+    the same XOR 2^63 (signed order, clean = INT64_MAX)."""
     lib = _lib._lib or _lib.load()
-    rc = lib.fs_search_device(ctypes.byref(plan), z.data_ptr(), z.numel(), out.data_ptr(), out.element_size(),
-                              status.data_ptr(), _device.stream_ptr(device_index=z.get_device()))
+    rc = lib.fs_search_device_at(ctypes.byref(plan), z.data_ptr(), z.numel(), out.data_ptr(), out.element_size(),
+                                 status.data_ptr(), int(base), _device.stream_ptr(device_index=z.get_device()))
     if rc:
         _lib.check(rc, what="fs_search_device")
 
@@ -266,7 +267,7 @@ class PreparedKernel:
         if rep is None:
             with torch.cuda.device(device):
                 qbits = getattr(self.structure, "qbits", 32)
-                if self.algorithm == "direct-generic":  # only prepare_loaded serves gap q >= 3
+                if self.algorithm == "direct-generic":  # gap q >= 3 (prepare_direct_gap / prepare_loaded)
                     from .persist import prepare_loaded
 
                     idx, _ = build(self.partition, qbits=qbits, q=self.structure.q)
@@ -277,7 +278,7 @@ class PreparedKernel:
         return rep
 
     # -- device-level API (no host copies, no synchronisation) -------------
-    def launch(self, z, out, status) -> None:
+    def launch(self, z, out, status, base: int = 0) -> None:
         """Enqueue exactly one search kernel on the current stream.  ``z``:
         CUDA tensor of the partition's dtype; ``out``: int32/int64 CUDA
         tensor; ``status``: a workspace from ``new_status()`` whose word 0
@@ -285,9 +286,12 @@ class PreparedKernel:
         read it with ``first_bad_of``).  ``out`` is unspecified for
         out-of-domain queries.  No host synchronisation; capturable in a
         CUDA graph.  Raises ValueError for a dtype, device or layout the
-        kernel cannot take as is (``_check_device_batch``)."""
+        kernel cannot take as is (``_check_device_batch``).  ``base``: the
+        global position of z[0] when z is a shard of a larger batch (status
+        positions are then global; word 3 = word 0 XOR 2^63 orders them as
+        signed int64 for a MIN all-reduce)."""
         _check_device_batch(self.plan, z, out)
-        _launch_device(self.plan, z, out, status)
+        _launch_device(self.plan, z, out, status, base)
 
     def placement(self) -> dict:
         """Where the kernel keeps its tables: {'smem_x', 'smem_table',
@@ -669,15 +673,81 @@ def build_rank2_directory(p: SortedPartition, idx: DirectIndex):
     return d
 
 
+def build_count_directory(p: SortedPartition, idx: DirectIndex):
+    """Device count directory of a gap-q table, q = 2..15 (fs_build_countdir):
+    8-B words {2- or 4-bit knot counts of 16 / 8 buckets, knots before the
+    word}.  The kernel recovers K_q[j] exactly and compares z only with the
+    knots of its own bucket (direct.py:294-300)."""
+    lib = _lib.load()
+    x = p.device_values()
+    f = _device.empty(len(p.values), np.uint64)
+    nbytes = int(lib.fs_countdir_bytes(idx.q, idx.r))
+    d = _device.empty(nbytes // 4, np.uint32)
+    rc = lib.fs_build_countdir(fs_dtype(p.precision), x.data_ptr(), len(p.values), float(idx.h), idx.r, idx.q,
+                               f.data_ptr(), d.data_ptr(), _device.stream_ptr())
+    _lib.check(rc, what="fs_build_countdir")
+    return d
+
+
+def prepare_direct_gap(p: SortedPartition, q: int, qbits: int = 32, idx: DirectIndex | None = None) -> PreparedKernel:
+    """Direct search with gap q >= 2 over its count directory -- the
+    reference's direct_search_generic (direct.py:294-300) as a batch kernel
+    ("direct-generic"; the reference has no lane kernel for q > 2).  Raises
+    the index build's InfeasibleError like ``prepare``."""
+    if not 2 <= q <= 15:
+        raise ValueError("count directories serve gaps 2..15")
+    if idx is None:
+        idx, _ = build(p, qbits=qbits, q=q)
+    plan, keep = _plan_for("direct-generic", idx, p)
+    if idx.r < (1 << 32):
+        d = build_count_directory(p, idx)
+        plan.rank = d.data_ptr()
+        keep.append(d)
+    scalar, lanes = _make_callables(plan, p)
+    return PreparedKernel("direct-generic", p, idx, scalar, lanes, plan=plan, buffers=tuple(keep))
+
+
+#: gap-q fall-back: largest count directory accepted (it should stay L2-resident)
+GAP_FALLBACK_MAX_DIR_BYTES = 64 << 20
+#: gap-q fall-back: largest gap tried (4-bit counts)
+GAP_FALLBACK_MAX_Q = 15
+
+
 def prepare_with_fallback(p: SortedPartition, qbits: int = 32, algorithm: str = "direct",
-                          fallback: str = "bitset2") -> PreparedKernel:
-    """Direct search when its index is feasible, else the padded bit-set
-    binary search -- the fall-back the paper describes and
-    the reference leaves to its harness (bench/harness.py:153-159)."""
+                          fallback: str = "bitset2", gap_fallback: bool = True) -> PreparedKernel:
+    """Direct search when its index is feasible, else a fall-back -- the
+    paper's policy (the reference leaves it to its harness,
+    bench/harness.py:153-159).
+
+    The fall-back, in order: when the padded array fits in shared memory,
+    the padded bit-set binary search (fast there); otherwise the direct
+    search with the smallest gap q in 2..15 whose certified layout is
+    feasible and whose count directory stays L2-resident
+    (GAP_FALLBACK_MAX_DIR_BYTES) -- the paper's generalisation to gap q
+    "deriving the minimal number of q which achieves a given memory budget"
+     -- and else ``fallback`` (bitset2).  Every path returns
+    the same unique answers."""
     try:
         return prepare(algorithm, p, qbits)
     except InfeasibleError:
-        return prepare(fallback, p, qbits)
+        pass
+    es = p.values.dtype.itemsize
+    pad_bytes = (1 << p.n_intervals.bit_length()) * es
+    if gap_fallback and pad_bytes > _smem_budget():
+        from .direct import compute_h_r
+
+        lib = _lib.load()
+        for q in range(2, min(GAP_FALLBACK_MAX_Q, p.n_intervals) + 1):
+            try:
+                h, r, _ = compute_h_r(p, qbits=qbits, q=q)
+            except InfeasibleError:
+                continue
+            if r >= (1 << 32) or int(lib.fs_countdir_bytes(q, r)) > GAP_FALLBACK_MAX_DIR_BYTES:
+                continue
+            from .direct import build_index
+
+            return prepare_direct_gap(p, q, qbits, idx=build_index(p, h, r, q=q, qbits=qbits))
+    return prepare(fallback, p, qbits)
 
 
 def resolve_threads(threads: int | None) -> int:

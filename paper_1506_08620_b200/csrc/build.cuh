@@ -232,6 +232,29 @@ __global__ void fill_rank2_kernel(const uint64_t* __restrict__ f, uint64_t n1, u
   }
 }
 
+// Count directory of a gap-q table (fs_build_countdir): a gap-q certificate
+// (f_{i+q} > f_i, direct.py:176-178) allows at most q knots per bucket, so
+// each bucket's knot count fits B bits (B = 2 for q <= 3, 4 for q <= 15).
+// Word w = {B-bit counts of buckets w 32/B .. (w+1) 32/B - 1, base =
+// #{i : f_i < w 32/B}}; then K_q[j] = upper_bound(f, j) - 1 = base + (sum of
+// the counts of buckets <= j in the word) - 1 (direct.py:215-228).
+template <int B>
+__global__ void fill_countdir_kernel(const uint64_t* __restrict__ f, uint64_t n1, uint64_t r, uint2* __restrict__ dir) {
+  constexpr int LG = B == 2 ? 4 : 3;  // buckets per word: 16 / 8
+  const uint64_t words = (r >> LG) + 1;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j0 = w << LG;
+    const uint64_t base = bound_search<false>(f, 0, n1, j0);
+    uint32_t counts = 0;
+    for (uint64_t i = base; i < n1; ++i) {
+      const uint64_t fi = __ldg(f + i);
+      if (fi >= j0 + (1u << LG)) break;
+      counts += 1u << (B * (uint32_t)(fi - j0));  // certified: a field never exceeds q < 2^B
+    }
+    dir[w] = make_uint2(counts, (uint32_t)base);
+  }
+}
+
 // Two-level sparse encoding of the gap-1 table for R >> N: super-bucket J
 // (buckets J 2^s .. (J+1) 2^s - 1) stores C[J] = K[J 2^s] = lower_bound(f,
 // J 2^s); every knot i stores F[i] = f_i mod 2^s (16 bit).  The knots of

@@ -244,6 +244,9 @@ constexpr int kStatusHeader = 3;
 // so the zero-initialised word means "none"); every CTA takes a ticket and
 // the last one turns status[2] into the result (merge != 0: min with the
 // current value, for several launches over one batch) and rewinds [1], [2].
+// A single launch (merge == 0) also writes status[3] = status[0] ^ 2^63:
+// the same order under a SIGNED comparison, "none" the int64 maximum -- the
+// word a MIN all-reduce over shards takes as is (dist.sharded_batch_search).
 __device__ __forceinline__ void finalize_first_bad(unsigned long long mine, unsigned long long* status, int merge) {
   __shared__ int s_last;
   if (__any_sync(0xffffffffu, mine != ~0ull)) {
@@ -258,8 +261,12 @@ __device__ __forceinline__ void finalize_first_bad(unsigned long long mine, unsi
     if (s_last) {
       __threadfence();
       const unsigned long long first = ~__ldcg(status + 2);
-      if (merge) atomicMin(status, first);
-      else status[0] = first;
+      if (merge) {
+        atomicMin(status, first);
+      } else {
+        status[0] = first;
+        status[3] = first ^ (1ull << 63);
+      }
       status[2] = 0;
       *reinterpret_cast<volatile unsigned int*>(status + 1) = 0u;
     }

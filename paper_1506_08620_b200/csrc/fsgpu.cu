@@ -107,6 +107,9 @@ inline uint64_t b2_smem_bytes(int top, int l1, int l2, int l3, size_t es) {
 #define FSG_B2_HALF 1
 #endif
 
+// count directory of a gap-q table: log2 of the buckets per 8-B word
+inline int countdir_lg(int q) { return q <= 3 ? 4 : 3; }
+
 struct Placement {
   uint32_t x_bytes = 0;      // bytes staged at smem offset 0 (X / padded / tree / top)
   uint32_t table_bytes = 0;  // bytes staged after align128(x_bytes) (K / records)
@@ -201,7 +204,9 @@ Placement place(const fs_plan* p) {
   const bool use_rank = p->algorithm == FS_ALGO_DIRECT && p->rank != nullptr && p->q == 1;
   // gap 2 over its own directory (16-B words, fs_build_rank2)
   const bool use_rank2 = p->algorithm == FS_ALGO_DIRECT_GAP2 && p->rank != nullptr && p->q == 2;
-  const bool use_dir = use_rank || use_rank2;
+  // gap q >= 3 over its count directory (8-B words of 16 / 8 buckets, fs_build_countdir)
+  const bool use_count = p->algorithm == FS_ALGO_DIRECT_GENERIC && p->rank != nullptr && p->q >= 2 && p->q <= 15;
+  const bool use_dir = use_rank || use_rank2 || use_count;
   // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
   if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->q == 1 && !force_global && p->r < (1ull << 32) &&
       p->sparse_shift >= 5 && p->sparse_shift <= 16) {
@@ -257,14 +262,17 @@ Placement place(const fs_plan* p) {
     case FS_ALGO_DIRECT_GAP2:
     case FS_ALGO_DIRECT_GENERIC: {
       const uint64_t xb = p->n1 * es;
-      const uint64_t kb = use_rank ? ((p->r >> 5) + 1) * 8 : use_rank2 ? ((p->r >> 5) + 1) * 16 : (p->r + 1) * 4;
+      const uint64_t kb = use_rank    ? ((p->r >> 5) + 1) * 8
+                          : use_rank2 ? ((p->r >> 5) + 1) * 16
+                          : use_count ? ((p->r >> countdir_lg(p->q)) + 1) * 8
+                                      : (p->r + 1) * 4;
       const void* tab = use_dir ? p->rank : p->table;
       if (force_global || p->r >= (1ull << 32)) break;
       if (align128(xb) + kb <= budget) {
         pl.xs = pl.ks = true;
       } else if (use_dir && kb <= budget) {
         pl.ks = true;  // every query reads the directory, few read X
-      } else if (xb <= budget) {
+      } else if (xb <= budget && !use_count) {
         pl.xs = true;
       } else if (kb <= budget) {
         pl.ks = true;
@@ -674,6 +682,15 @@ int dispatch_direct(const DevPlan<T>& d, const Placement& pl, const T* z, uint64
   return launch_probe<T, OutT, DirectProbe<T, J, GAP, false, false>>(d, pl, z, m, out, fb, base, st);
 }
 
+// gap-q count directory (B bits per bucket); X staged only beside a staged directory
+template <typename T, typename OutT, int B>
+int dispatch_countdir(const DevPlan<T>& d, const Placement& pl, const T* z, uint64_t m, OutT* out,
+                      unsigned long long* fb, uint64_t base, cudaStream_t st) {
+  if (pl.xs && pl.ks) return launch_probe<T, OutT, CountDirProbe<T, B, true, true>>(d, pl, z, m, out, fb, base, st);
+  if (pl.ks) return launch_probe<T, OutT, CountDirProbe<T, B, false, true>>(d, pl, z, m, out, fb, base, st);
+  return launch_probe<T, OutT, CountDirProbe<T, B, false, false>>(d, pl, z, m, out, fb, base, st);
+}
+
 template <typename T, typename OutT, int SLOTS>
 int dispatch_records(const DevPlan<T>& d, const Placement& pl, bool ovf, const T* z, uint64_t m, OutT* out,
                      unsigned long long* fb, uint64_t base, cudaStream_t st) {
@@ -737,6 +754,8 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       return dispatch_direct<T, OutT, uint32_t, 2>(d, pl, z, m, out, fb, base, st);
     case FS_ALGO_DIRECT_GENERIC:
       if (wide) return launch_probe<T, OutT, DirectProbe<T, uint64_t, 3, false, false>>(d, pl, z, m, out, fb, base, st);
+      if (p->rank && p->q >= 2 && p->q <= 3) return dispatch_countdir<T, OutT, 2>(d, pl, z, m, out, fb, base, st);
+      if (p->rank && p->q >= 4 && p->q <= 15) return dispatch_countdir<T, OutT, 4>(d, pl, z, m, out, fb, base, st);
       return dispatch_direct<T, OutT, uint32_t, 3>(d, pl, z, m, out, fb, base, st);
     case FS_ALGO_DIRECT_CACHE:
       if (wide) return launch_probe<T, OutT, CacheProbe<T, uint64_t, false>>(d, pl, z, m, out, fb, base, st);
@@ -916,6 +935,28 @@ int fs_build_rank2(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint
   cudaStream_t s = as_stream(stream);
   const uint64_t words = (r >> 5) + 1;
   fill_rank2_kernel<<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint4*>(dir_dev));
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+uint64_t fs_countdir_bytes(int32_t q, uint64_t r) {
+  if (q < 2 || q > 15) return 0;
+  return ((r >> countdir_lg(q)) + 1) * 8;
+}
+
+int fs_build_countdir(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t q,
+                      uint64_t* f_scratch_dev, void* dir_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !dir_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  if (q < 2 || q > 15) return fail(FS_INVALID_ARG, "count directories serve gaps 2..15");
+  if (n1 - 1 >= (1ull << 32) || r >= (1ull << 32)) return fail(FS_INVALID_ARG, "table entries are 32-bit");
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  const uint64_t words = (r >> countdir_lg(q)) + 1;
+  if (q <= 3)
+    fill_countdir_kernel<2><<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint2*>(dir_dev));
+  else
+    fill_countdir_kernel<4><<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint2*>(dir_dev));
   FS_CUDA(cudaGetLastError());
   return FS_OK;
 }
@@ -1225,12 +1266,22 @@ int fs_build_b2_deep(int32_t dtype, const void* xpad_dev, int32_t pbits, int32_t
 
 int fs_search_device(const fs_plan* plan, const void* z_dev, uint64_t m, void* out_dev, int32_t out_bytes,
                      unsigned long long* first_bad_dev, void* stream) {
+  return fs_search_device_at(plan, z_dev, m, out_dev, out_bytes, first_bad_dev, 0, stream);
+}
+
+int fs_search_device_at(const fs_plan* plan, const void* z_dev, uint64_t m, void* out_dev, int32_t out_bytes,
+                        unsigned long long* first_bad_dev, uint64_t base, void* stream) {
   int rc = check_search_args(plan, z_dev, m, out_dev, out_bytes, first_bad_dev);
   if (rc) return rc;
   cudaStream_t s = as_stream(stream);
-  // the kernel's last CTA writes status[0]; only an empty batch needs a write here
-  if (m == 0) FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
-  return launch_search(plan, place_for_batch(plan, m), z_dev, m, out_dev, out_bytes, first_bad_dev, 0, s);
+  // the kernel's last CTA writes status[0] and [3]; only an empty batch needs writes here
+  if (m == 0) {
+    FS_CUDA(cudaMemsetAsync(first_bad_dev, 0xff, sizeof(unsigned long long), s));
+    FS_CUDA(cudaMemsetAsync(first_bad_dev + 3, 0xff, sizeof(unsigned long long), s));
+    FS_CUDA(cudaMemsetAsync(reinterpret_cast<unsigned char*>(first_bad_dev + 3) + 7, 0x7f, 1, s));
+    return FS_OK;
+  }
+  return launch_search(plan, place_for_batch(plan, m), z_dev, m, out_dev, out_bytes, first_bad_dev, base, s);
 }
 
 size_t fs_search_ws_words(void) { return FS_SEARCH_WS_WORDS; }

@@ -242,6 +242,78 @@ struct Rank2Probe {
   }
 };
 
+// Direct search (gap q >= 2) over the count directory of its table
+// (fill_countdir_kernel): t = K_q[j] recovered exactly from one 8-B word;
+// the knots of bucket j are X[t - c + 1 .. t] (c = its count <= q), every
+// earlier knot lies in an earlier bucket and so below z (monotone bucket
+// function), hence the reference's q clamped comparisons t - #{m < q : z <
+// X[t - m]} (direct.py:294-300, batch.py:341-343) reduce to the c reads of
+// the bucket's own knots -- usually none.  Identical answers to
+// DirectProbe<GAP=q>.
+template <typename T, int B, bool XS, bool DS>
+struct CountDirProbe {
+  static constexpr int LG = B == 2 ? 4 : 3;  // buckets per word: 16 / 8
+  const T* X;
+  const uint2* D;
+  T h, x0;
+  uint32_t r;
+  __device__ __forceinline__ CountDirProbe(const DevPlan<T>& p, unsigned char* smem) {
+    X = XS ? reinterpret_cast<const T*>(smem) : p.x;
+    D = DS ? reinterpret_cast<const uint2*>(smem + p.x_smem_bytes_aligned()) : p.rank;
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+  }
+  // (sum of the counts of fields 0..b, count of field b) of a counts word
+  static __device__ __forceinline__ void sums(uint32_t c, uint32_t b, uint32_t& s, uint32_t& cb) {
+    const uint32_t hi = B * (b + 1);
+    const uint32_t v = hi >= 32 ? c : c & ((1u << hi) - 1u);
+    if constexpr (B == 2) {
+      s = __popc(v & 0x55555555u) + 2u * __popc(v & 0xAAAAAAAAu);
+    } else {
+      const uint32_t bytes = (v & 0x0F0F0F0Fu) + ((v >> 4) & 0x0F0F0F0Fu);
+      s = (bytes * 0x01010101u) >> 24;
+    }
+    cb = (c >> (B * b)) & ((1u << B) - 1u);
+  }
+  __device__ __forceinline__ int64_t resolve(T z, uint2 d, uint32_t b) const {
+    uint32_t s, c;
+    sums(d.x, b, s, c);
+    const uint32_t t = d.y + s - 1u;
+    uint32_t miss = 0;
+    for (uint32_t k = 0; k < c; ++k) miss += z < tload<XS>(X, t - k) ? 1u : 0u;
+    return (int64_t)t - (int64_t)miss;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
+    j = j < r ? j : r;
+    return resolve(z, tload<DS>(D, (uint64_t)(j >> LG)), j & ((1u << LG) - 1u));
+  }
+  // every directory gather of the group in flight before the first is used
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    constexpr int G = N < FSG_RANK_GROUP ? N : FSG_RANK_GROUP;
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += G) {
+      uint2 d[G];
+      uint32_t b[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z[g0 + q], x0), h));
+        j = j < r ? j : r;
+        b[q] = j & ((1u << LG) - 1u);
+        d[q] = tload<DS>(D, (uint64_t)(j >> LG));
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        o[g0 + q] = (R)resolve(z[g0 + q], d[q], b[q]);
+      }
+    }
+  }
+};
+
 // Direct search (gap 1) over the two-level sparse encoding of K (fill_sparse_
 // kernel), staged in shared memory: C (super-bucket ranks) and F (16-bit
 // knot offsets) after X when X fits (else X via L2 -- read only for buckets

@@ -55,19 +55,19 @@ def sharded_batch_search(prepared, z_local, out_local, offset: int, group=None, 
 
     ``z_local``/``out_local`` are CUDA tensors holding queries
     [offset, offset + len) of the global batch; ``status`` an optional
-    reusable workspace (new_status()).  One search kernel, then the span's
-    first bad position -- made global (offset added, "clean" mapped to the
-    int64 maximum) on the device -- goes through one MIN all-reduce, and a
-    single host read decides: OutOfDomain with the global first position
-    on every rank if any rank saw a bad query.  Returns the span's length.
+    reusable workspace (new_status()).  One search kernel that reports
+    global positions (fs_search_device_at: status word 3 = first bad
+    position XOR 2^63, a signed-int64 key with "clean" = INT64_MAX), one MIN
+    all-reduce of that word in place, and a single host read decides:
+    OutOfDomain with the global first position on every rank if any rank
+    saw a bad query.  Returns the span's length.
     """
     fb = status if status is not None else new_status(z_local.device)
-    prepared.launch(z_local, out_local, fb)
-    st = fb[:1].view(torch.int64)  # UINT64_MAX (clean) reads as -1
-    val = torch.where(st < 0, torch.full_like(st, NO_BAD), st + int(offset))
+    prepared.launch(z_local, out_local, fb, base=int(offset))
+    key = fb[3:4].view(torch.int64)
     if dist.is_available() and dist.is_initialized():
-        dist.all_reduce(val, op=dist.ReduceOp.MIN, group=group)
-    first = int(val.item())
-    if first != NO_BAD:
-        raise OutOfDomain(position=first)
+        dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+    k = int(key.item())
+    if k != NO_BAD:
+        raise OutOfDomain(position=k + (1 << 63))
     return z_local.numel()

@@ -122,6 +122,10 @@ def prepare_loaded(idx: DirectIndex, p, algorithm: str | None = None):
         raise ValueError("loaded indices serve the direct, direct-gap2 and direct-generic kernels")
     if algorithm != want:
         raise ValueError(f"an index of gap q={idx.q} is searched by {want!r}, not {algorithm!r}")
+    if algorithm == "direct-generic" and idx.q <= 15:
+        from .batch import prepare_direct_gap
+
+        return prepare_direct_gap(p, idx.q, idx.qbits, idx=idx)  # over its count directory
     plan, keep = _plan_for(algorithm, idx, p)
     if algorithm == "direct":
         rank = build_rank_directory(p, idx)

@@ -55,10 +55,12 @@ class _CpuLaunch:
     def __init__(self, xs):
         self.xs = xs
 
-    def launch(self, z, out, status):
+    def launch(self, z, out, status, base=0):
         zn = z.numpy()
         bad = orc.first_bad(self.xs, zn)
-        status[:1].view(torch.int64)[0] = -1 if bad is None else bad  # UINT64_MAX = clean
+        w = status.view(torch.int64)
+        w[0] = -1 if bad is None else base + bad  # UINT64_MAX = clean
+        w[3] = (1 << 63) - 1 if bad is None else base + bad - (1 << 63)  # word 0 XOR 2^63, as int64
         if bad is None:
             out.copy_(torch.from_numpy(orc.rank_oracle(self.xs, zn).astype(np.int32)))
 

@@ -568,17 +568,19 @@ def test_pageable_staged_host_path(cuda, prec, odt):
 
 
 def test_fallback_policy(cuda):
-    """infeasible direct layouts fall back to bitset2."""
+    """PAPER.md:877 / 754-762: infeasible direct layouts fall back to a larger
+    gap (its count directory) or to bitset2."""
     fs = _fs()
     from paper_1506_08620_b200 import workloads
 
     p = workloads.knots("cfg5", n1=1_048_577, filtered=False)
     with pytest.raises(fs.Overflow):
         fs.prepare("direct", p)
-    prep = fs.prepare_with_fallback(p)
-    assert prep.algorithm == "bitset2"
     z = workloads.queries_host("cfg5", p, 300_001, seed=9)
-    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(p.values, z))
+    for prep, algo in ((fs.prepare_with_fallback(p), "direct-generic"),
+                       (fs.prepare_with_fallback(p, gap_fallback=False), "bitset2")):
+        assert prep.algorithm == algo
+        assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(p.values, z))
     collide = fs.validate_partition(np.array([-1e9, 0.0, 1.0], dtype=np.float32))
     assert fs.prepare_with_fallback(collide).algorithm == "bitset2"
     assert fs.prepare_with_fallback(collide, algorithm="direct-gap2").algorithm == "direct-gap2"
