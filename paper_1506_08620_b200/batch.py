@@ -405,13 +405,20 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
     x_bytes = (len(p.values) * p.values.dtype.itemsize + 127) // 128 * 128
     if (algorithm == "direct-gap2" and structure.q == 2
             and x_bytes + (structure.r + 1) * 4 > SMEM_RECORDS_MAX and structure.r < (1 << 32)):
-        # K and X cannot both be staged: the 16-B-per-32-bucket directory (8x
-        # smaller than K, X read only for buckets holding knots) beats K via L2
-        # (cfg5 N+1 = 32769: 132 -> 216 G queries/s); when they fit, plain K
-        # in smem stays faster (cfg3: 612 vs 439)
-        rank2 = build_rank2_directory(p, structure)
-        plan.rank = rank2.data_ptr()
-        keep.append(rank2)
+        # K and X cannot both be staged: a directory 8x smaller than K, X read
+        # only for the knots of the query's own bucket, beats K via L2 -- the
+        # count directory (8-B words of 16 buckets, 2-bit counts) over the
+        # rank2 one (16-B words of 32): cfg5 N+1 = 32769 132 (K) -> 220
+        # (rank2) -> 232 G queries/s, N+1 = 2^20+1 147 -> 181 (8-B gathers
+        # cost fewer L1 cycles than 16-B ones; profiles/r02/tune_countdir.txt).
+        # When K and X fit, plain K in smem stays faster (cfg3: 686 vs 305).
+        if GAP2_DIRECTORY == "countdir":
+            d = build_count_directory(p, structure)
+            plan.algorithm = _lib.ALGO_CODES["direct-generic"]  # same answers (direct.py:279-300)
+        else:
+            d = build_rank2_directory(p, structure)
+        plan.rank = d.data_ptr()
+        keep.append(d)
     if plan.algorithm == _lib.ALGO_CODES["direct"] and structure.q == 1:
         if (structure.r + 1) * rec_bytes <= SMEM_RECORDS_MAX:
             rec = _device.empty((structure.r + 1) * rec_bytes, np.uint8)
@@ -707,6 +714,8 @@ def prepare_direct_gap(p: SortedPartition, q: int, qbits: int = 32, idx: DirectI
     return PreparedKernel("direct-generic", p, idx, scalar, lanes, plan=plan, buffers=tuple(keep))
 
 
+#: directory of a gap-2 table that cannot be staged: "countdir" or "rank2"
+GAP2_DIRECTORY = "countdir"
 #: gap-q fall-back: largest count directory accepted (it should stay L2-resident)
 GAP_FALLBACK_MAX_DIR_BYTES = 64 << 20
 #: gap-q fall-back: largest gap tried (4-bit counts)

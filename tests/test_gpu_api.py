@@ -388,21 +388,31 @@ def test_host_uploads_ordered_after_pending_work(cuda, pinned):
 
 @pytest.mark.parametrize("name,kw", [("cfg5", {"n1": 32_769}), ("cfg4", {})])
 def test_gap2_rank_directory(cuda, name, kw):
-    """direct-gap2 with K and X too large to stage reads the gap-2 rank
-    directory (fs_build_rank2: 16-B words, up to two knots per bucket).
+    """direct-gap2 with K and X too large to stage reads a gap-2 directory:
+    the count directory (fs_build_countdir, the default) or the rank2 one
+    (fs_build_rank2: 16-B words, up to two knots per bucket).
     The layout holds buckets with two knots; answers equal the oracle on
     random queries, every knot and its neighbours."""
     fs = _fs()
     from paper_1506_08620_b200 import workloads
 
+    from paper_1506_08620_b200 import batch as fsb
+
     p = workloads.knots(name, **kw)
-    prep = fs.prepare("direct-gap2", p)
-    assert prep.plan.rank and prep.structure.q == 2
-    f = fs.knot_buckets(p, prep.structure.h)
-    assert np.any(f[1:] == f[:-1]), "no two-knot bucket: the case is not exercised"
     xs = p.values
     z = np.concatenate([workloads.queries_host(name, p, 2_000_000, seed=29), orc.boundary_probes(xs)])
-    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
+    want = orc.rank_oracle(xs, z)
+    keep = fsb.GAP2_DIRECTORY
+    try:
+        for layout in ("countdir", "rank2"):  # the default, and the 16-B rank2 words
+            fsb.GAP2_DIRECTORY = layout
+            prep = fs.prepare("direct-gap2", p)
+            assert prep.plan.rank and prep.structure.q == 2 and prep.algorithm == "direct-gap2"
+            f = fs.knot_buckets(p, prep.structure.h)
+            assert np.any(f[1:] == f[:-1]), "no two-knot bucket: the case is not exercised"
+            assert np.array_equal(fs.run_batch(prep, z), want), layout
+    finally:
+        fsb.GAP2_DIRECTORY = keep
 
 
 def test_concurrent_big_tables_prepare_then_search(cuda):

@@ -9,7 +9,8 @@ unfiltered cfg5 draw, bitset2 fall-back instance), big32:<N+1> (sorted f32
 U[0,1) knots).  Layout variants: direct-k (plain K), direct-rank (rank
 directory only), direct-hot / direct-hot:<KB> / direct-nohot (hot window on, of a given size, off), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
 records forced), bitset2-flat (no subtree records),
-direct-gap2-k (gap 2 over plain K).
+direct-gap2-k (gap 2 over plain K), fallback (prepare_with_fallback), gap:<q>
+(direct with gap q over its count directory).
 """
 
 from __future__ import annotations
@@ -116,6 +117,10 @@ def main():
                     finally:
                         (_b.SPARSE_FORMATS, _b.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM,
                          _b.SPARSE_RECORDS8_MAX_PAST_PPM) = keep
+                elif algo == "fallback":  # prepare_with_fallback: direct, else gap-q count directory, else bitset2
+                    prep = fs.prepare_with_fallback(p)
+                elif algo.startswith("gap:"):  # direct with gap q over its count directory
+                    prep = fs.prepare_direct_gap(p, int(algo.split(":")[1]))
                 else:
                     prep = fs.prepare(base, p)
                 if algo == "direct-k":  # plain K table instead of rank directory / records
@@ -160,7 +165,8 @@ def main():
                     "config": spec, "algo": algo, "threads": tune & 0xfff, "cap": tune >> 12, "m": m,
                     "ms": round(t * 1e3, 4), "gqs": round(m / t / 1e9, 2), "gbs": round(gbs, 1),
                     "frac": round(gbs / PEAK, 4), "ok": ok, "placement": prep.placement(),
-                    "r": getattr(prep.structure, "r", None),
+                    "r": getattr(prep.structure, "r", None), "algorithm": prep.algorithm,
+                    "q": getattr(prep.structure, "q", None),
                 }), flush=True)
             prep.plan.tune = 0
         del z, out
