@@ -84,7 +84,8 @@ enum {
   FS_SPARSE_RECORDS = 1,   /* 16-B group records, six offsets (| F): fs_build_sparse_rec */
   FS_SPARSE_RECORDS8 = 2,  /* 8-B group records, two offsets (| F): fs_build_sparse_rec  */
   FS_SPARSE_RECORDS12 = 3, /* 16-B group records, eight 12-bit offsets (shift <= 10)      */
-  FS_SPARSE_RECORDS8X3 = 4 /* 8-B group records, three 13-bit offsets (shift <= 11, N+1 <= 2^24) */
+  FS_SPARSE_RECORDS8X3 = 4,/* 8-B group records, three 13-bit offsets (shift <= 11, N+1 <= 2^24) */
+  FS_SPARSE_ZONED = 5      /* zone descriptors | 16-B records, per-zone form: fs_build_zoned */
 };
 
 /*
@@ -125,9 +126,11 @@ typedef struct fs_plan {
   const void* sparse; /* direct (gap 1) only, optional: two-level sparse table
                          (fs_build_sparse); staged in shared memory when the
                          rank directory does not fit there.  NULL = unused.      */
-  int32_t sparse_shift;/* super-bucket = 2^sparse_shift buckets (5..16)           */
+  int32_t sparse_shift;/* super-bucket = 2^sparse_shift buckets (5..16);
+                          zoned: zone = 2^sparse_shift buckets (10..31)         */
   uint32_t sparse_ndense; /* two-level: dense (bitmask) super-buckets in `sparse`;
-                             records: overflowing records (> 0: F follows)     */
+                             records: overflowing records (> 0: F follows);
+                             zoned: number of 16-B records                      */
   const void* b2_deep;  /* bitset2 only, optional: subtree records of the levels
                            below the shared-memory top (fs_build_b2_deep); one
                            32-B gather resolves b2_deep_k levels.  NULL = unused. */
@@ -283,6 +286,34 @@ int fs_plan_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_
                        uint64_t* novf_out, uint64_t* bytes_out, uint32_t* past_last_ppm_out, void* stream);
 int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
                         int32_t shift, uint64_t novf, uint64_t* f_scratch_dev, void* buf_dev, void* stream);
+
+/*
+ * Zoned records of the gap-1 table (FS_SPARSE_ZONED; a device layout of K,
+ * no reference counterpart).  The buckets [0, R] are cut into nz = (R >>
+ * zs) + 1 <= 64 zones of 2^zs buckets, and each zone takes the 16-B record
+ * form its own knot density needs: slot records {K[j0], six 16-bit
+ * offsets f_i - j0} per 2^s buckets (s = 7..min(14, zs), the largest whose
+ * records hold at most six knots; unused offsets 0x7FFF), else rank records
+ * {K[j0], 64-bit mask of the buckets holding a knot, 0} per 64 buckets.
+ * Buffer: nz u32 descriptors (first record << 5 | 16 if rank | s), padded to
+ * a multiple of four, then the records.  The kernel resolves K[j] from one
+ * descriptor and one record load, both in shared memory, and reads X only for
+ * a bucket holding a knot -- from a staged window X[t0, t0 + nt) or L2.
+ *   fs_plan_zoned: the zone shift (the fewest zones, 32 or 64, whose table
+ *     fits budget_bytes) -> zs, records, table bytes, and the window of X
+ *     (the densest nt consecutive knots, nt = as many as the rest of the
+ *     budget holds).  FS_TOO_LARGE if no zoning fits.  SYNC.
+ *   fs_build_zoned: fill the buffer for that zs.  SYNC.
+ * Set fs_plan.sparse to the buffer, sparse_format = FS_SPARSE_ZONED,
+ * sparse_shift = zs, sparse_ndense = records, hot_knot0 = t0, hot_knots = nt
+ * (hot_words = 0).  f_scratch_dev: n1 uint64.
+ */
+uint64_t fs_zoned_bytes(uint64_t r, int32_t zs, uint64_t nrec);
+int fs_plan_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                  uint64_t* f_scratch_dev, int32_t* zs_out, uint64_t* nrec_out, uint64_t* bytes_out,
+                  uint64_t* t0_out, uint64_t* nt_out, void* stream);
+int fs_build_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t zs,
+                   uint64_t* f_scratch_dev, void* buf_dev, void* stream);
 
 /*
  * Hot window of a rank directory for shared-memory staging: among all

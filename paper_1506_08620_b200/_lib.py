@@ -60,6 +60,7 @@ SPARSE_RECORDS = 1
 SPARSE_RECORDS8 = 2
 SPARSE_RECORDS12 = 3
 SPARSE_RECORDS8X3 = 4
+SPARSE_ZONED = 5
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (
@@ -77,6 +78,9 @@ EXPORTED = (
     "fs_plan_sparse_rec",
     "fs_build_sparse_rec",
     "fs_build_hot_window",
+    "fs_zoned_bytes",
+    "fs_plan_zoned",
+    "fs_build_zoned",
     "fs_build_fused",
     "fs_build_padded",
     "fs_build_rank2",
@@ -177,6 +181,13 @@ def _declare(lib):
                                        _p_u64, _p_u64, _p_u32, _vp]
     lib.fs_build_sparse_rec.restype = ctypes.c_int
     lib.fs_build_sparse_rec.argtypes = [_i32, _i32, _vp, _u64, ctypes.c_double, _u64, _i32, _u64, _vp, _vp, _vp]
+    lib.fs_zoned_bytes.restype = ctypes.c_uint64
+    lib.fs_zoned_bytes.argtypes = [_u64, _i32, _u64]
+    lib.fs_plan_zoned.restype = ctypes.c_int
+    lib.fs_plan_zoned.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _u64, _vp, _p_i32, _p_u64, _p_u64,
+                                  _p_u64, _p_u64, _vp]
+    lib.fs_build_zoned.restype = ctypes.c_int
+    lib.fs_build_zoned.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp]
     lib.fs_build_hot_window.restype = ctypes.c_int
     lib.fs_build_hot_window.argtypes = [_i32, _vp, _u64, _u64, _vp, _p_u64, _p_u64, _p_u64, _p_u64, _p_u64, _vp]
     lib.fs_build_fused.restype = ctypes.c_int

@@ -307,7 +307,8 @@ class PreparedKernel:
             "smem_hot": bool(f & _lib.PLACE_SMEM_HOT),
             "smem_sparse": bool(f & _lib.PLACE_SMEM_SPARSE),
             "sparse_format": {_lib.SPARSE_RECORDS: "records", _lib.SPARSE_RECORDS8: "records8",
-                              _lib.SPARSE_RECORDS12: "records12", _lib.SPARSE_RECORDS8X3: "records8x3"}.get(
+                              _lib.SPARSE_RECORDS12: "records12", _lib.SPARSE_RECORDS8X3: "records8x3",
+                              _lib.SPARSE_ZONED: "zoned"}.get(
                 self.plan.sparse_format, "two-level") if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
         }
@@ -433,8 +434,12 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
         keep.append(rank)
         if not plan.records:
             _set_sparse_table(plan, p, structure, keep)
-        if hot_window:
+        if ZONED == "first" and not plan.records and not plan.sparse:
+            _set_zoned(plan, p, structure, keep)
+        if hot_window and not plan.sparse:
             _set_hot_window(plan, p, structure, rank)
+        if ZONED is True and not plan.records and not plan.sparse and not plan.hot_words:
+            _set_zoned(plan, p, structure, keep)
     scalar, lanes = _make_callables(plan, p)
     return PreparedKernel(algorithm, p, structure, scalar, lanes, plan=plan, buffers=tuple(keep))
 
@@ -465,6 +470,15 @@ HOT_WINDOW_BYTES = 48 * 1024
 HOT_WINDOW_MIN_DENSITY_RATIO = 4.0
 
 
+#: zoned records (fs_build_zoned) are tried when neither the rank directory,
+#: a sparse layout nor a hot window is staged (True); "first" tries them
+#: before the hot window, False never (tuning, tests).  cfg4's query mix
+#: measures the hot window first: 405 vs 377 G queries/s -- zoned records
+#: win its uniform half (378 vs 242) and lose its clustered half (370 vs
+#: 510; profiles/r02/zoned_cfg4.txt)
+ZONED: bool | str = True
+
+
 def _smem_budget() -> int:
     import torch
 
@@ -490,6 +504,45 @@ def _set_hot_window(plan, p: SortedPartition, idx: DirectIndex, rank) -> None:
     density_ratio = (inside / HOT_WINDOW_BYTES) / (p.n_intervals / table_bytes)
     if nw and density_ratio >= HOT_WINDOW_MIN_DENSITY_RATIO:
         plan.hot_word0, plan.hot_words, plan.hot_knot0, plan.hot_knots = w0, nw, t0, nt
+
+
+def _set_zoned(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:
+    """Zoned records of K (fs_build_zoned): the buckets cut into at most 64
+    zones, each zone in the 16-B record form its knot density needs (slot
+    records of 2^7..2^10 buckets holding at most eight knots, or 64-bucket
+    rank records), plus a window of the densest knots.  For tables whose
+    density varies by orders of magnitude (cfg4's geometric knots: one
+    record shift for the whole table overflows at its dense end and exceeds
+    shared memory at its sparse end) the whole directory then fits in shared
+    memory.  Used when the rank directory cannot be staged."""
+    dir_bytes = ((idx.r >> 5) + 1) * 8
+    x_bytes = len(p.values) * p.values.dtype.itemsize
+    budget = _smem_budget() - 512
+    if idx.r >= (1 << 32) or len(p.values) >= (1 << 31) or dir_bytes + x_bytes <= budget:
+        return
+    lib = _lib.load()
+    dt = fs_dtype(p.precision)
+    n1 = len(p.values)
+    x = p.device_values()
+    f = _device.empty(n1, np.uint64)
+    zs, nrec, nbytes, t0, nt = ctypes.c_int32(-1), *(ctypes.c_uint64(0) for _ in range(4))
+    rc = lib.fs_plan_zoned(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, f.data_ptr(), ctypes.byref(zs),
+                           ctypes.byref(nrec), ctypes.byref(nbytes), ctypes.byref(t0), ctypes.byref(nt),
+                           _device.stream_ptr())
+    if rc == _lib.FS_TOO_LARGE:
+        return
+    _lib.check(rc, what="fs_plan_zoned")
+    buf = _device.empty(int(nbytes.value), np.uint8)
+    rc = lib.fs_build_zoned(dt, x.data_ptr(), n1, float(idx.h), idx.r, zs.value, f.data_ptr(), buf.data_ptr(),
+                            _device.stream_ptr())
+    _lib.check(rc, what="fs_build_zoned")
+    plan.sparse = buf.data_ptr()
+    plan.sparse_format = _lib.SPARSE_ZONED
+    plan.sparse_shift = zs.value
+    plan.sparse_ndense = nrec.value
+    plan.hot_word0, plan.hot_words = 0, 0
+    plan.hot_knot0, plan.hot_knots = t0.value, nt.value
+    keep.append(buf)
 
 
 def _set_b2_deep(plan, pp: PaddedPartition, keep: list) -> None:

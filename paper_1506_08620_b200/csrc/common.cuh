@@ -38,6 +38,17 @@ constexpr int kRec12MaxShift = 10;
 // 0x1000 | offset at bits 25 + 13k (offsets < 2^11, unused 0x1FFF); shifts up
 // to 11.
 constexpr int kRec3MaxShift = 11;
+// Zoned records (FS_SPARSE_ZONED): at most this many zones, so a warp's
+// zone-descriptor loads touch at most two words per bank; slot records hold
+// up to kZonedSlots 16-bit offsets and use shifts kZonedMinShift..
+// kZonedMaxShift (below that a zone takes 64-bucket rank records, which cost
+// the same 16 B per 64 buckets and decode faster).
+constexpr uint32_t kZonedMaxZones = 64;
+constexpr int kZonedSlots = 6;
+constexpr int kZonedMinShift = 7;
+constexpr int kZonedMaxShift = 14;
+constexpr int kZonedMinZoneShift = 10;
+constexpr uint32_t kZonedRankFlag = 16u;
 
 // ---------------------------------------------------------------------------
 // Exact arithmetic in the partition's precision

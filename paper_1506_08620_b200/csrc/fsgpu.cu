@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -127,6 +128,7 @@ struct Placement {
   bool records = false;  // direct served from fused records in smem
   bool hot = false;      // direct over the rank directory with a smem hot window
   bool sparse = false;   // direct over the two-level sparse table in smem
+  bool zoned = false;    // ... the zoned records (with a window of X)
   int merge = 0;         // status[0] = min(status[0], result) (chunked host path)
 };
 
@@ -151,11 +153,17 @@ int validate_plan(const fs_plan* p) {
         return fail(FS_INVALID_ARG, "hot window outside the rank directory / knots");
       if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS &&
                         p->sparse_format != FS_SPARSE_RECORDS8 && p->sparse_format != FS_SPARSE_RECORDS12 &&
-                        p->sparse_format != FS_SPARSE_RECORDS8X3))
+                        p->sparse_format != FS_SPARSE_RECORDS8X3 && p->sparse_format != FS_SPARSE_ZONED))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
+      if (p->sparse && p->sparse_format == FS_SPARSE_ZONED) {
+        if (fs_zoned_bytes(p->r, p->sparse_shift, p->sparse_ndense) == 0 || p->r >= (1ull << 32))
+          return fail(FS_INVALID_ARG, "zoned table parameters out of range");
+        if (p->hot_knot0 > p->n1 || p->hot_knots > p->n1 - p->hot_knot0)
+          return fail(FS_INVALID_ARG, "knot window outside the knots");
+      }
       if (p->sparse && p->sparse_format == FS_SPARSE_RECORDS8X3 && p->n1 > (1ull << 24))
         return fail(FS_INVALID_ARG, "3-offset records need N+1 <= 2^24");
-      if (p->sparse && (p->sparse_shift < 5 ||
+      if (p->sparse && p->sparse_format != FS_SPARSE_ZONED && (p->sparse_shift < 5 ||
                         p->sparse_shift > (p->sparse_format == FS_SPARSE_TWO_LEVEL    ? 16
                                            : p->sparse_format == FS_SPARSE_RECORDS12 ? kRec12MaxShift
                                            : p->sparse_format == FS_SPARSE_RECORDS8X3 ? kRec3MaxShift
@@ -207,9 +215,37 @@ Placement place(const fs_plan* p) {
   // gap q >= 3 over its count directory (8-B words of 16 / 8 buckets, fs_build_countdir)
   const bool use_count = p->algorithm == FS_ALGO_DIRECT_GENERIC && p->rank != nullptr && p->q >= 2 && p->q <= 15;
   const bool use_dir = use_rank || use_rank2 || use_count;
+  // zoned records + a window of X (prepare sets them only when the rank
+  // directory cannot be staged)
+  if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->sparse_format == FS_SPARSE_ZONED && p->q == 1 &&
+      !force_global && p->r < (1ull << 32)) {
+    const uint64_t tb = fs_zoned_bytes(p->r, p->sparse_shift, p->sparse_ndense);
+    const uint64_t xb = p->hot_knots * es;
+    if (tb && align128(xb) + tb <= budget) {
+      pl.sparse = pl.zoned = pl.ks = true;
+      pl.xs = xb > 0;
+      pl.x_bytes = (uint32_t)xb;
+      pl.table_bytes = (uint32_t)tb;
+      if (pl.xs) {
+        pl.seg0_src = static_cast<const char*>(p->x) + p->hot_knot0 * es;
+        pl.seg0_bytes = (uint32_t)xb;
+        pl.seg1_src = p->sparse;
+        pl.seg1_bytes = (uint32_t)tb;
+        pl.nseg = 2;
+        pl.smem = align128(xb) + tb;
+      } else {
+        pl.seg0_src = p->sparse;
+        pl.seg0_bytes = (uint32_t)tb;
+        pl.nseg = 1;
+        pl.smem = tb;
+      }
+      pl.flags |= FS_PLACE_SMEM_SPARSE | (pl.xs ? FS_PLACE_SMEM_X : 0);
+      return pl;
+    }
+  }
   // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
-  if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->q == 1 && !force_global && p->r < (1ull << 32) &&
-      p->sparse_shift >= 5 && p->sparse_shift <= 16) {
+  if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->sparse_format != FS_SPARSE_ZONED && p->q == 1 &&
+      !force_global && p->r < (1ull << 32) && p->sparse_shift >= 5 && p->sparse_shift <= 16) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
     const uint64_t cfb = p->sparse_format != FS_SPARSE_TWO_LEVEL
@@ -529,6 +565,13 @@ template <typename T, bool DEEP, typename OutT>
 struct BoundedFor<T, Bitset2Probe<T, true, DEEP>, OutT> {
   static constexpr bool value = FSG_B2_BOUNDED;
 };
+#ifndef FSG_ZONED_BOUNDED
+#define FSG_ZONED_BOUNDED 1
+#endif
+template <typename T, typename OutT>
+struct BoundedFor<T, ZonedProbe<T>, OutT> {
+  static constexpr bool value = FSG_ZONED_BOUNDED;
+};
 template <typename T, int SLOTS, bool XS, bool OVF, typename OutT>
 struct BoundedFor<T, SparseRecProbe<T, SLOTS, XS, OVF>, OutT> {
   static constexpr bool value = FSG_REC_BOUNDED && !(SLOTS == 2 && sizeof(OutT) == 8);
@@ -665,7 +708,7 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   d.hot_w0 = (uint32_t)p->hot_word0;
   d.hot_nw = pl.hot ? (uint32_t)p->hot_words : 0;
   d.hot_t0 = (uint32_t)p->hot_knot0;
-  d.hot_nt = pl.hot ? (uint32_t)p->hot_knots : 0;
+  d.hot_nt = pl.hot || pl.zoned ? (uint32_t)p->hot_knots : 0;
   d.x_smem_bytes = pl.xs || pl.top ? pl.x_bytes : 0;
   d.table_smem_bytes = pl.ks ? pl.table_bytes : 0;
   // With only K staged it sits at offset 0.
@@ -718,6 +761,7 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
     case FS_ALGO_DIRECT:
       if (pl.records) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
+      if (pl.zoned) return launch_probe<T, OutT, ZonedProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS)
         return dispatch_records<T, OutT, 6>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS8X3)
@@ -1144,6 +1188,147 @@ int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64
   }
   FS_CUDA(cudaGetLastError());
   FS_CUDA(cudaStreamSynchronize(s));
+  return FS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Zoned records (FS_SPARSE_ZONED)
+// ---------------------------------------------------------------------------
+namespace {
+// Per-zone record form for zone shift zs from the sorted knot buckets f:
+// descriptors (first record << 5 | rank flag | s) and the record count.
+// Slot records take the largest s in [kZonedMinShift, min(kZonedMaxShift,
+// zs)] whose records hold at most kZonedSlots knots of the zone; a zone where
+// none does takes 64-bucket rank records.  false if zs is out of range or
+// needs > 64 zones.
+bool zone_plan(const std::vector<uint64_t>& f, uint64_t r, int zs, std::vector<uint32_t>& desc, uint64_t& nrec) {
+  if (zs < kZonedMinZoneShift || zs > 31) return false;
+  const uint64_t nz = (r >> zs) + 1;
+  if (nz > kZonedMaxZones) return false;
+  const int smax = std::min(kZonedMaxShift, zs);
+  // maxc[z][s - kZonedMinShift]: most knots in one 2^s-bucket record of zone z
+  constexpr int NS = kZonedMaxShift - kZonedMinShift + 1;
+  std::vector<std::array<uint32_t, NS>> maxc(nz);
+  for (auto& a : maxc) a.fill(0);
+  for (int si = 0; si + kZonedMinShift <= smax; ++si) {
+    const int sh = kZonedMinShift + si;
+    for (size_t i = 0; i < f.size();) {
+      const uint64_t key = f[i] >> sh;
+      size_t e = i;
+      while (e < f.size() && (f[e] >> sh) == key) ++e;
+      uint32_t& m = maxc[f[i] >> zs][si];
+      m = std::max<uint32_t>(m, (uint32_t)(e - i));
+      i = e;
+    }
+  }
+  desc.assign(nz, 0);
+  nrec = 0;
+  for (uint64_t z = 0; z < nz; ++z) {
+    const uint64_t zb = std::min<uint64_t>(1ull << zs, r + 1 - (z << zs));  // buckets of the zone
+    int s = -1;
+    for (int si = smax - kZonedMinShift; si >= 0; --si)
+      if (maxc[z][si] <= (uint32_t)kZonedSlots) {
+        s = kZonedMinShift + si;
+        break;
+      }
+    const bool rank = s < 0;
+    if (rank) s = 6;
+    if (nrec >= (1ull << 27)) return false;
+    desc[z] = (uint32_t)(nrec << 5) | (rank ? kZonedRankFlag : 0u) | (uint32_t)s;
+    nrec += (zb + (1ull << s) - 1) >> s;
+  }
+  return nrec < (1ull << 27);
+}
+
+int zoned_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
+                       uint64_t* f_scratch_dev, std::vector<uint64_t>& f, cudaStream_t s) {
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, s);
+  if (rc) return rc;
+  f.resize(n1);
+  FS_CUDA(cudaMemcpyAsync(f.data(), f_scratch_dev, n1 * 8, cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  (void)r;
+  return FS_OK;
+}
+}  // namespace
+
+uint64_t fs_zoned_bytes(uint64_t r, int32_t zs, uint64_t nrec) {
+  if (zs < kZonedMinZoneShift || zs > 31) return 0;
+  const uint64_t nz = (r >> zs) + 1;
+  if (nz > kZonedMaxZones) return 0;
+  return 4 * ((nz + 3) & ~3ull) + 16 * nrec;
+}
+
+int fs_plan_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                  uint64_t* f_scratch_dev, int32_t* zs_out, uint64_t* nrec_out, uint64_t* bytes_out,
+                  uint64_t* t0_out, uint64_t* nt_out, void* stream) {
+  if (!x_dev || !f_scratch_dev || n1 < 2 || !zs_out) return fail(FS_INVALID_ARG, "bad arguments");
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "zoned records need R < 2^32, N < 2^31");
+  // every knot costs at least 16/6 B of a slot record
+  if (16 * n1 / kZonedSlots > budget_bytes) return fail(FS_TOO_LARGE, "no zoned layout fits the budget");
+  std::vector<uint64_t> f;
+  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, r, f_scratch_dev, f, as_stream(stream));
+  if (rc) return rc;
+  // the fewest zones (32: one wavefront per warp's descriptor loads, else 64)
+  int zs32 = kZonedMinZoneShift;
+  while (zs32 < 31 && (r >> zs32) + 1 > 32) ++zs32;
+  int best = -1;
+  uint64_t best_nrec = 0, best_bytes = 0;
+  for (int zs : {zs32, zs32 - 1}) {
+    if (zs < kZonedMinZoneShift) continue;
+    std::vector<uint32_t> desc;
+    uint64_t nrec = 0;
+    if (!zone_plan(f, r, zs, desc, nrec)) continue;
+    const uint64_t bytes = fs_zoned_bytes(r, zs, nrec);
+    if (bytes + 128 > budget_bytes) continue;
+    best = zs;
+    best_nrec = nrec;
+    best_bytes = bytes;
+    break;
+  }
+  if (best < 0) return fail(FS_TOO_LARGE, "no zoned layout fits the budget");
+  // window of X: the densest nt consecutive knots (smallest bucket span)
+  const uint64_t es = dtype == FS_F32 ? 4 : 8;
+  const uint64_t room = budget_bytes - best_bytes - 128;
+  const uint64_t nt = std::min<uint64_t>(n1, room / es);
+  uint64_t t0 = 0;
+  if (nt > 0 && nt < n1) {
+    uint64_t span = ~0ull;
+    for (uint64_t a = 0; a + nt <= n1; ++a)
+      if (f[a + nt - 1] - f[a] < span) {
+        span = f[a + nt - 1] - f[a];
+        t0 = a;
+      }
+  }
+  *zs_out = best;
+  if (nrec_out) *nrec_out = best_nrec;
+  if (bytes_out) *bytes_out = best_bytes;
+  if (t0_out) *t0_out = t0;
+  if (nt_out) *nt_out = nt;
+  return FS_OK;
+}
+
+int fs_build_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t zs,
+                   uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "zoned records need R < 2^32, N < 2^31");
+  cudaStream_t s = as_stream(stream);
+  std::vector<uint64_t> f;
+  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, r, f_scratch_dev, f, s);
+  if (rc) return rc;
+  std::vector<uint32_t> desc;
+  uint64_t nrec = 0;
+  if (!zone_plan(f, r, zs, desc, nrec)) return fail(FS_INVALID_ARG, "zone shift out of range for this table");
+  const uint64_t nz = desc.size();
+  desc.resize((nz + 3) & ~3ull, 0u);
+  FS_CUDA(cudaMemcpyAsync(buf_dev, desc.data(), 4 * desc.size(), cudaMemcpyHostToDevice, s));
+  auto* R = reinterpret_cast<uint4*>(static_cast<char*>(buf_dev) + 4 * desc.size());
+  fill_zoned_kernel<<<grid_1d(nrec, 256), 256, 0, s>>>(f_scratch_dev, n1, zs, static_cast<const uint32_t*>(buf_dev),
+                                                       (uint32_t)nz, R, nrec);
+  FS_CUDA(cudaGetLastError());
+  FS_CUDA(cudaStreamSynchronize(s));  // desc must outlive the async upload
   return FS_OK;
 }
 

@@ -375,6 +375,30 @@ struct SparseProbe {
   }
 };
 
+// Rank of jl among the eight 12-bit offset fields of a 16-B record (g.y..g.w,
+// field k = 0x800 | offset at bit 12k, unused fields 0x7FF > any jl):
+// lt = #{offsets < jl}, knot = (field lt == jl).  96-bit SWAR: (0x800 |
+// offset) - jl keeps the field's bit 11 iff offset >= jl (no borrow leaves a
+// field); Y = jl in every 12-bit field.
+__device__ __forceinline__ void rec12_count(const uint4& g, uint32_t jl, uint32_t& lt, bool& knot) {
+  const uint32_t y0 = jl * 0x01001001u;
+  const uint32_t y1 = jl * 0x10010010u + (jl >> 8);
+  const uint32_t y2 = jl * 0x00100100u + (jl >> 4);
+  uint32_t d0, d1, d2;
+  asm("sub.cc.u32 %0, %3, %6;\n\tsubc.cc.u32 %1, %4, %7;\n\tsubc.u32 %2, %5, %8;"
+      : "=r"(d0), "=r"(d1), "=r"(d2)
+      : "r"(g.y), "r"(g.z), "r"(g.w), "r"(y0), "r"(y1), "r"(y2));
+  // guard bits at 11, 23, 35, 47, 59, 71, 83, 95: word0 bits 11, 23;
+  // word1 bits 3, 15, 27; word2 bits 7, 19, 31
+  const uint32_t ge = __popc(d0 & 0x00800800u) + __popc(d1 & 0x08008008u) + __popc(d2 & 0x80080080u);
+  lt = 8u - ge;
+  // field lt (bits 12 lt .. 12 lt + 11) through a funnel shift of its word pair
+  const uint32_t bit = 12u * lt, wi = bit >> 5, sh = bit & 31u;
+  const uint32_t a0 = wi == 0 ? g.y : (wi == 1 ? g.z : g.w);
+  const uint32_t a1 = wi == 0 ? g.z : g.w;
+  knot = lt < 8u && ((__funnelshift_r(a0, a1, sh) & 0x7FFu) == jl);
+}
+
 // Direct search (gap 1) over the group records of K (fill_sparse_rec_kernel),
 // staged in shared memory after X when X fits.  One LDS per query; SLOTS
 // selects the layout: 6 (16 B, 16-bit offsets), 2 (8 B, 16-bit offsets),
@@ -460,24 +484,8 @@ struct SparseRecProbe {
       const uint32_t fv = (uint32_t)(w64 >> (lt < 3u ? 25u + 13u * lt : 63u));  // field lt
       knot = lt < 3u && (fv & 0xFFFu) == jl;
     } else if constexpr (SLOTS == 8) {
-      // 96-bit SWAR: fields (0x800 | offset) - jl keep bit 11 iff offset >= jl
-      // (no borrow leaves a field); Y = jl in every 12-bit field
-      const uint32_t y0 = jl * 0x01001001u;
-      const uint32_t y1 = jl * 0x10010010u + (jl >> 8);
-      const uint32_t y2 = jl * 0x00100100u + (jl >> 4);
-      uint32_t d0, d1, d2;
-      asm("sub.cc.u32 %0, %3, %6;\n\tsubc.cc.u32 %1, %4, %7;\n\tsubc.u32 %2, %5, %8;"
-          : "=r"(d0), "=r"(d1), "=r"(d2)
-          : "r"(g.y), "r"(g.z), "r"(g.w), "r"(y0), "r"(y1), "r"(y2));
-      // guard bits at 11, 23, 35, 47, 59, 71, 83, 95: word0 bits 11, 23;
-      // word1 bits 3, 15, 27; word2 bits 7, 19, 31
-      ge = __popc(d0 & 0x00800800u) + __popc(d1 & 0x08008008u) + __popc(d2 & 0x80080080u);
-      lt = SLOTS - ge;
-      // field lt (bits 12 lt .. 12 lt + 11) through a funnel shift of its word pair
-      const uint32_t bit = 12u * lt, wi = bit >> 5, sh = bit & 31u;
-      const uint32_t a0 = wi == 0 ? g.y : (wi == 1 ? g.z : g.w);
-      const uint32_t a1 = wi == 0 ? g.z : g.w;
-      knot = lt < SLOTS && ((__funnelshift_r(a0, a1, sh) & 0x7FFu) == jl);
+      rec12_count(g, jl, lt, knot);
+      (void)ge;
     } else {
       uint32_t w;
       if constexpr (SLOTS == 6) {
@@ -615,6 +623,149 @@ struct HotRankProbe {
         T xv = z[g0 + q];
         if (knot) xv = tl < nt ? Xs[tl] : __ldg(X + t);
         o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
+      }
+    }
+  }
+};
+
+// Direct search (gap 1) over the zoned records of K (fill_zoned_kernel),
+// staged in shared memory after a window X[t0, t0 + nt) of the knots.  The
+// buckets are cut into nz = (R >> zs) + 1 zones of 2^zs; each zone takes the
+// 16-B record form its own knot density needs (fs_plan_zoned), so a table
+// whose density varies by orders of magnitude (cfg4's geometric knots) fits
+// in shared memory where one record shift for the whole table cannot:
+//   slot records  {base, six 16-bit offsets} per 2^s buckets, s <= 14,
+//                 never more than six knots (no overflow path);
+//   rank records  {base, 64-bit knot mask, 0} per 64 buckets.
+// Zone descriptor (u32, nz <= 64 of them at the table head, so a warp's
+// descriptor loads cost at most two wavefronts): first record << 5 |
+// rank << 4 | s.  K[j] = base + #{knots of the record below j} exactly, and
+// bucket j holds knot K[j] iff its offset / mask bit says so; X is read only
+// then, from the window or through L2.  Identical answers to
+// DirectProbe<GAP=1> (batch.py:315-317).
+template <typename T>
+struct ZonedProbe {
+  const T* X;
+  const unsigned char* xg;  // generic address of the X window
+  uint32_t xs, zd, rc;      // shared addresses: X window, zone descriptors, records
+  T h, x0;
+  uint32_t r, zs, zmask, t0, nt;
+  __device__ __forceinline__ ZonedProbe(const DevPlan<T>& p, unsigned char* smem) {
+    X = p.x;
+    asm volatile("mov.u32 %0, %1;" : "=r"(xs) : "r"((uint32_t)__cvta_generic_to_shared(smem)));
+    // the window's generic address held in a register (ptxas would otherwise
+    // rebuild it from the CTA's shared window in front of every load)
+    unsigned long long xgv;
+    asm volatile("cvta.shared.u64 %0, %1;" : "=l"(xgv) : "l"((unsigned long long)xs));
+    xg = reinterpret_cast<const unsigned char*>(xgv);
+    zd = xs + p.x_smem_bytes_aligned();
+    const uint32_t nz = (uint32_t)(p.r >> p.sparse_shift) + 1u;
+    rc = zd + 4u * ((nz + 3u) & ~3u);
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+    zs = (uint32_t)p.sparse_shift;
+    zmask = (1u << zs) - 1u;
+    t0 = p.hot_t0;
+    nt = p.hot_nt;
+  }
+  __device__ __forceinline__ uint32_t bucket(T z) const {
+    uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
+    return j < r ? j : r;
+  }
+  __device__ __forceinline__ uint32_t desc(uint32_t j) const {
+    uint32_t d;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(zd + 4u * (j >> zs)));
+    return d;
+  }
+  __device__ __forceinline__ uint4 rec(uint32_t j, uint32_t d) const {
+    uint4 g;
+    const uint32_t a = rc + 16u * ((d >> 5) + ((j & zmask) >> (d & 15u)));
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w) : "r"(a));
+    return g;
+  }
+  // Both record forms decoded branch-free and selected by the zone's rank
+  // flag: lanes of one warp fall in zones of either form (cfg4's query mix
+  // is half dense, half sparse), and a divergent branch would issue both
+  // decodes plus its reconvergence overhead anyway.
+  static __device__ __forceinline__ void resolve(const uint4& g, uint32_t d, uint32_t j, uint32_t& t, bool& knot) {
+    const uint32_t jl = j & ((1u << (d & 15u)) - 1u);
+    // rank view: 64-bit knot mask (jl < 64 in rank zones)
+    const unsigned long long m = ((unsigned long long)g.z << 32) | g.y;
+    const uint32_t jr = jl & 63u;
+    const uint32_t below = (uint32_t)__popcll(m & ((1ull << jr) - 1ull));
+    const uint32_t kr = (uint32_t)(m >> jr) & 1u;
+    // slot view: six 16-bit offsets (unused kRecSentinel > any jl, s <= 14):
+    // (w + hm) & H has bit 15 / 31 set iff the low / high offset >= jl
+    constexpr uint32_t H = 0x80008000u;
+    const uint32_t hm = H - jl * 0x10001u;
+    const uint32_t ge = __popc((g.y + hm) & H) + __popc((g.z + hm) & H) + __popc((g.w + hm) & H);
+    const uint32_t lt = 6u - ge;
+    uint32_t w;
+    asm("{\n\t.reg .pred p, q;\n\tsetp.lt.u32 p, %1, 2;\n\tsetp.lt.u32 q, %1, 4;\n\t"
+        "selp.b32 %0, %3, %4, q;\n\tselp.b32 %0, %2, %0, p;\n\t}"
+        : "=r"(w)
+        : "r"(lt), "r"(g.y), "r"(g.z), "r"(g.w));
+    const bool ks = lt < 6u && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
+    uint32_t cnt, kb;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\tselp.b32 %0, %2, %3, p;\n\tselp.b32 %1, %5, %6, p;\n\t}"
+        : "=r"(cnt), "=r"(kb)
+        : "r"(below), "r"(lt), "r"(d & 16u), "r"(kr), "r"((uint32_t)ks));
+    t = g.x + cnt;
+    knot = kb != 0;
+  }
+  // X[t] if `knot`, else z: one predicated generic load from the staged
+  // window or global memory (no branch between the two)
+  __device__ __forceinline__ T xsel(uint32_t t, bool knot, T z) const {
+    const uint32_t tl = t - t0;
+    const T* p = tl < nt ? reinterpret_cast<const T*>(xg) + tl : X + t;
+    T v = z;
+    if constexpr (sizeof(T) == 4)
+      asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.f32 %0, [%1];\n\t}" : "+f"(v) : "l"(p), "r"((uint32_t)knot));
+    else
+      asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.f64 %0, [%1];\n\t}" : "+d"(v) : "l"(p), "r"((uint32_t)knot));
+    return v;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    const uint32_t j = bucket(z);
+    const uint32_t d = desc(j);
+    uint32_t t;
+    bool knot;
+    resolve(rec(j, d), d, j, t, knot);
+    const T xv = xsel(t, knot, z);
+    return (int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z < xv));
+  }
+  // descriptors of a group, then its records, then the resolves: every load
+  // of a phase in flight before the first is consumed
+#ifndef FSG_ZONED_GROUP
+#define FSG_ZONED_GROUP 4
+#endif
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    constexpr int G = N < FSG_ZONED_GROUP ? N : FSG_ZONED_GROUP;
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += G) {
+      uint32_t j[G], d[G];
+      uint4 g[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        j[q] = bucket(z[g0 + q]);
+        d[q] = desc(j[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        g[q] = rec(j[q], d[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        uint32_t t;
+        bool knot;
+        resolve(g[q], d[q], j[q], t, knot);
+        const T xv = xsel(t, knot, z[g0 + q]);
+        o[g0 + q] = (R)((int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z[g0 + q] < xv)));
       }
     }
   }

@@ -18,6 +18,7 @@ def _fs():
     return fs
 
 
+
 def _edge_queries(xs, h, words):
     """Queries in the buckets around directory words `words` (32 buckets
     each): first and last bucket of each word, +-1 ulp around them."""

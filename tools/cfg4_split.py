@@ -1,5 +1,6 @@
-"""cfg4 diagnostics: rank-directory (L2) vs sparse+dense table on the uniform
-and the clustered halves of the query stream separately (tuning aid)."""
+"""cfg4 diagnostics: rank-directory (L2, with its hot window), sparse+dense
+table and zoned records on the uniform and the clustered halves of the query
+stream separately (tuning aid)."""
 
 import json
 import sys
@@ -27,10 +28,11 @@ for k, z in streams.items():
 out = torch.empty(m, dtype=torch.int32, device="cuda")
 st = fs.new_status()
 only = sys.argv[1:]  # optional: variant stream (profiling a single case)
-for variant in ("rank-l2", "sparse-dense"):
+for variant in ("rank-l2", "sparse-dense", "zoned"):
     if only and variant != only[0]:
         continue
-    batch.SPARSE_MAX_DENSE_KNOT_FRACTION = 0.25 if variant == "rank-l2" else 1.0
+    batch.SPARSE_MAX_DENSE_KNOT_FRACTION = 1.0 if variant == "sparse-dense" else 0.25
+    batch.ZONED = variant == "zoned"
     prep = fs.prepare("direct", p)
     for k, z in streams.items():
         if only and k != only[1]:
