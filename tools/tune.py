@@ -5,7 +5,8 @@ resident queries and prints one JSON line per variant.
     python tools/tune.py [--configs cfg3,cfg4] [--geometry] [--steps 10]
 
 Config specs: cfgN (BASELINE recipes), cfg5:<N+1>, cfg2:<seed>, cfg5u (the
-unfiltered cfg5 draw, bitset2 fall-back instance), big32:<N+1> (sorted f32
+unfiltered cfg5 draw, bitset2 fall-back instance), unif32:<size> / unif64:<size> (the throughput sweep's
+U[1,5]-gap partitions), big32:<N+1> (sorted f32
 U[0,1) knots).  Layout variants: direct-k (plain K), direct-rank (rank
 directory only), direct-hot / direct-hot:<KB> / direct-nohot (hot window on, of a given size, off), direct-zoned (zoned records ahead of the hot window), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
 records forced), bitset2-flat (no subtree records),
@@ -86,9 +87,16 @@ def main():
                 print(json.dumps({"config": spec, "algo": algo, "m": z.numel(), "gqs": round(z.numel() / t / 1e9, 2),
                                   "ok": ok, "placement": prep.placement()}), flush=True)
             continue
-        p = workloads.knots(name, **kw)
-        m = args.m or workloads.CONFIGS[name].m
-        z = workloads.queries_device(name, p, m, seed=1)
+        if name in ("unif32", "unif64"):  # the throughput sweep's partitions: gaps U[1, 5], seed 42
+            prec = "single" if name == "unif32" else "double"
+            p = fs.gen_uniform_gap_partition(int(arg), 1.0, 5.0, 42, prec)
+            m = args.m or (1 << 28)
+            zh = np.array(fs.gen_queries(p, 1 << 24, 43).values)
+            z = torch.from_numpy(zh).cuda().repeat(m >> 24)
+        else:
+            p = workloads.knots(name, **kw)
+            m = args.m or workloads.CONFIGS[name].m
+            z = workloads.queries_device(name, p, m, seed=1)
         out = torch.empty(m, dtype=torch.int32 if args.out_bytes == 4 else torch.int64, device="cuda")
         fb = fs.new_status()
         qbytes = z.element_size() + out.element_size()
