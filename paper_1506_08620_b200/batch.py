@@ -514,12 +514,12 @@ def _set_zoned(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:
     density varies by orders of magnitude (cfg4's geometric knots: one
     record shift for the whole table overflows at its dense end and exceeds
     shared memory at its sparse end) the whole directory then fits in shared
-    memory.  Used when the rank directory cannot be staged."""
+    memory.  Used when the rank directory cannot be staged, not even
+    without X."""
     dir_bytes = ((idx.r >> 5) + 1) * 8
-    x_bytes = len(p.values) * p.values.dtype.itemsize
     budget = _smem_budget() - 512
-    if idx.r >= (1 << 32) or len(p.values) >= (1 << 31) or dir_bytes + x_bytes <= budget:
-        return
+    if idx.r >= (1 << 32) or len(p.values) >= (1 << 31) or dir_bytes <= budget:
+        return  # the staged rank directory (X through L2 for knot buckets only) wins
     lib = _lib.load()
     dt = fs_dtype(p.precision)
     n1 = len(p.values)

@@ -252,9 +252,15 @@ Placement place(const fs_plan* p) {
                              ? fs_sparse_rec_bytes(p->sparse_format, p->n1, p->r, p->sparse_shift, p->sparse_ndense)
                              : fs_sparse_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense);
     const bool rank_fits = use_rank && align128(xb) + dir_b <= budget;
-    if (!rank_fits && cfb <= budget) {
+    // a sparse layout that cannot stage X beside it reads X through L2 like
+    // the rank directory does, with a dearer decode: the staged directory
+    // wins whenever it fits alone (gaps U[1,5], N+1 = 65535, R / N = 3:
+    // 555 vs 270 G queries/s f32, 405 vs 226 f64; profiles/r02/unif_layouts.txt)
+    const bool sparse_xs = align128(xb) + cfb <= budget;
+    const bool rank_alone_fits = use_rank && dir_b <= budget;
+    if (!rank_fits && cfb <= budget && (sparse_xs || !rank_alone_fits)) {
       pl.sparse = pl.ks = true;
-      pl.xs = align128(xb) + cfb <= budget;
+      pl.xs = sparse_xs;
       pl.x_bytes = pl.xs ? (uint32_t)xb : 0;
       pl.table_bytes = (uint32_t)cfb;
       if (pl.xs) {
