@@ -392,11 +392,16 @@ __device__ __forceinline__ void rec12_count(const uint4& g, uint32_t jl, uint32_
   // word1 bits 3, 15, 27; word2 bits 7, 19, 31
   const uint32_t ge = __popc(d0 & 0x00800800u) + __popc(d1 & 0x08008008u) + __popc(d2 & 0x80080080u);
   lt = 8u - ge;
-  // field lt (bits 12 lt .. 12 lt + 11) through a funnel shift of its word pair
-  const uint32_t bit = 12u * lt, wi = bit >> 5, sh = bit & 31u;
-  const uint32_t a0 = wi == 0 ? g.y : (wi == 1 ? g.z : g.w);
-  const uint32_t a1 = wi == 0 ? g.z : g.w;
-  knot = lt < 8u && ((__funnelshift_r(a0, a1, sh) & 0x7FFu) == jl);
+  // field lt (bits 12 lt .. 12 lt + 11) through a funnel shift of its word
+  // pair, chosen with predicated selects (ptxas otherwise branches on the
+  // word index: a reconvergence region per query)
+  const uint32_t bit = 12u * lt;
+  uint32_t a0, a1;
+  asm("{\n\t.reg .pred p, q;\n\tsetp.lt.u32 p, %2, 32;\n\tsetp.lt.u32 q, %2, 64;\n\t"
+      "selp.b32 %0, %4, %5, q;\n\tselp.b32 %0, %3, %0, p;\n\tselp.b32 %1, %4, %5, p;\n\t}"
+      : "=r"(a0), "=r"(a1)
+      : "r"(bit), "r"(g.y), "r"(g.z), "r"(g.w));
+  knot = lt < 8u && ((__funnelshift_r(a0, a1, bit & 31u) & 0x7FFu) == jl);
 }
 
 // Direct search (gap 1) over the group records of K (fill_sparse_rec_kernel),
