@@ -1526,8 +1526,15 @@ struct GateArrival {
   }
 };
 
-// Queries per staging slot of the pageable path (16 MB).
-uint64_t staged_chunk_elems(size_t es) { return ((16ull << 20) / es + 3) & ~3ull; }
+// Queries per staging slot of the pageable path (16 MB slots), and per chunk
+// of an m-query batch: an eighth of the batch between 2 and 16 MB, so the
+// host copies of one chunk overlap the DMA of the previous one even for
+// mid-size batches (16 MB of queries: 4.1 -> see profiles/r02/e2e_curve.jsonl).
+uint64_t staged_slot_elems(size_t es) { return ((16ull << 20) / es + 7) & ~7ull; }
+uint64_t staged_chunk_elems(size_t es, uint64_t m) {
+  const uint64_t lo = (2ull << 20) / es, hi = staged_slot_elems(es);
+  return (std::min(hi, std::max(lo, m / 8)) + 7) & ~7ull;  // 32-B aligned on device (8-query groups)
+}
 
 // How fs_search_host splits a batch: through the library's pinned staging
 // (pageable buffers of any real size) or straight from page-locked memory,
@@ -1543,7 +1550,7 @@ HostChunking host_chunking(const fs_plan* plan, const void* z_host, uint64_t m, 
   hc.staged = m * (uint64_t)out_bytes >= (4ull << 20) && !(flags & FS_HOST_NO_STAGING) &&
               !(is_pinned(z_host) && is_pinned(out_host));
   if (hc.staged) {
-    hc.chunk = staged_chunk_elems(es);
+    hc.chunk = staged_chunk_elems(es, m);
   } else {
     if (chunk_elems == 0) chunk_elems = (64ull << 20) / es;
     hc.chunk = (chunk_elems + 7) & ~7ull;  // keep every chunk 32-B aligned on device (8-query groups)
@@ -1561,8 +1568,8 @@ int search_host_staged(const fs_plan* plan, Placement pl, const void* z_host, ui
                        cudaStream_t cs, GateArrival& gate) {
   constexpr int kSlots = 3;
   const size_t es = plan->dtype == FS_F32 ? 4 : 8;
-  const uint64_t chunk = staged_chunk_elems(es);  // 16 MB of queries per slot
-  const size_t slot_bytes = chunk * std::max<size_t>(es, (size_t)ob);
+  const uint64_t chunk = staged_chunk_elems(es, m);
+  const size_t slot_bytes = staged_slot_elems(es) * std::max<size_t>(es, (size_t)ob);  // one cached slot size
   void* slot[kSlots] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev[kSlots] = {nullptr, nullptr, nullptr};
   int status = FS_OK;
