@@ -95,11 +95,24 @@ inline uint64_t b2_deep_total_bytes(int pbits, int top, int k) {
   for (int l = top; pbits - l >= kB2DeepMinLevels; l += std::min(k, pbits - l)) bytes += (1ull << l) * 32;
   return bytes;
 }
+// f64 bitset2 stages f32 shadow keys plus the exact f64 plane
+// (Bitset2Probe::kShadow) from this many levels: shallow trees, whose levels
+// are conflict-free or replicated anyway, lose to the extra conversion and
+// check (cfg5 N+1 = 33 528 -> 400, 1025 297 -> 269 Gq/s); deeper ones win on
+// the halved shared-memory wavefronts (cfg2 167 -> 207, N+1 = 32769 100 ->
+// 125; profiles/r02/bitset2_shadow.txt)
+#ifndef FSG_B2_SHADOW_MIN_BITS
+#define FSG_B2_SHADOW_MIN_BITS 13
+#endif
+inline bool b2_shadow(int pbits, size_t es) { return es == 8 && pbits >= FSG_B2_SHADOW_MIN_BITS; }
+// bytes per staged node: a shadow word plus the exact key, else the key
+inline size_t b2_node_bytes(int pbits, size_t es) { return b2_shadow(pbits, es) ? 12 : es; }
 inline int b2_top_bits(int pbits, size_t es) {
-  return std::min(bit_length(smem_budget() / es + 1) - 1, pbits);
+  return std::min(bit_length(smem_budget() / b2_node_bytes(pbits, es) + 1) - 1, pbits);
 }
 // levels [0, l1) plain, [l1, l2) 32 copies, [l2, l3) 16 copies, [l3, top) plain
-inline uint64_t b2_smem_bytes(int top, int l1, int l2, int l3, size_t es) {
+inline uint64_t b2_smem_bytes(int top, int l1, int l2, int l3, size_t es, bool shadow) {
+  if (shadow) return b2_shadow_bytes(top, l1, l2, l3) + ((1ull << top) - 1) * 8;
   return (((1ull << l1) - 1) + ((1ull << l2) - (1ull << l1)) * 32 + ((1ull << l3) - (1ull << l2)) * 16 +
           ((1ull << top) - (1ull << l3))) *
          es;
@@ -130,6 +143,7 @@ struct Placement {
   bool sparse = false;   // direct over the two-level sparse table in smem
   bool zoned = false;    // ... the zoned records (with a window of X)
   int merge = 0;         // status[0] = min(status[0], result) (chunked host path)
+  bool b2_shadow = false;  // bitset2 f64: f32 shadow keys + exact plane staged
 };
 
 int validate_plan(const fs_plan* p) {
@@ -361,6 +375,7 @@ Placement place(const fs_plan* p) {
       // as many levels as fit, then bank-private copies of the levels below
       // the conflict-free top six, as far as the remaining budget allows
       pl.top = true;
+      pl.b2_shadow = b2_shadow(p->pbits, es);
       const int tb = b2_top_bits(p->pbits, es);
       pl.top_bits = tb;
       pl.flags |= tb == p->pbits ? FS_PLACE_SMEM_X : FS_PLACE_SMEM_TOP;
@@ -368,7 +383,7 @@ Placement place(const fs_plan* p) {
       // (only when every level is in smem: with global levels below, the L1
       // the larger carve-out takes away costs more than the conflicts)
       while (kB2Replicate && tb == p->pbits && pl.b2_l2 < tb &&
-             b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2 + 1, pl.b2_l2 + 1, es) <= budget)
+             b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2 + 1, pl.b2_l2 + 1, es, pl.b2_shadow) <= budget)
         ++pl.b2_l2;
       // f64: the next levels in 16 copies where the rest of the budget allows
       // (a lane pair shares a copy: ~1.3 instead of ~3.5 wavefronts per level;
@@ -377,9 +392,9 @@ Placement place(const fs_plan* p) {
       // transitions than it saves (profiles/r01/tune_bitset2_half.txt)
       pl.b2_l3 = pl.b2_l2;
       while (FSG_B2_HALF && es == 8 && kB2Replicate && tb == p->pbits && pl.b2_l2 > pl.b2_l1 && pl.b2_l3 < tb &&
-             b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2, pl.b2_l3 + 1, es) <= budget)
+             b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2, pl.b2_l3 + 1, es, pl.b2_shadow) <= budget)
         ++pl.b2_l3;
-      pl.x_bytes = (uint32_t)b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2, pl.b2_l3, es);
+      pl.x_bytes = (uint32_t)b2_smem_bytes(tb, pl.b2_l1, pl.b2_l2, pl.b2_l3, es, pl.b2_shadow);
       pl.smem = pl.x_bytes;
       break;
     }
@@ -419,7 +434,7 @@ Placement place_for_batch(const fs_plan* p, uint64_t m) {
     const uint64_t query_bytes = m * (es + 4);
     if (query_bytes < (uint64_t)pl.smem * sm_count()) {
       pl.b2_l2 = pl.b2_l3 = pl.b2_l1;
-      pl.x_bytes = (uint32_t)b2_smem_bytes(pl.top_bits, pl.b2_l1, pl.b2_l2, pl.b2_l3, es);
+      pl.x_bytes = (uint32_t)b2_smem_bytes(pl.top_bits, pl.b2_l1, pl.b2_l2, pl.b2_l3, es, pl.b2_shadow);
       pl.smem = pl.x_bytes;
     }
     return pl;
@@ -567,8 +582,8 @@ struct BoundedFor<T, SparseProbe<T, true, DENSE>, OutT> {
 #ifndef FSG_B2_BOUNDED
 #define FSG_B2_BOUNDED 1
 #endif
-template <typename T, bool DEEP, typename OutT>
-struct BoundedFor<T, Bitset2Probe<T, true, DEEP>, OutT> {
+template <typename T, bool DEEP, bool SHADOW, typename OutT>
+struct BoundedFor<T, Bitset2Probe<T, true, DEEP, SHADOW>, OutT> {
   static constexpr bool value = FSG_B2_BOUNDED;
 };
 #ifndef FSG_ZONED_BOUNDED
@@ -812,6 +827,12 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       if (pl.ks) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
       return launch_probe<T, OutT, CacheProbe<T, uint32_t, false>>(d, pl, z, m, out, fb, base, st);
     case FS_ALGO_BITSET2:
+      if constexpr (sizeof(T) == 8) {
+        if (pl.top && pl.b2_shadow && d.b2_deep)
+          return launch_probe<T, OutT, Bitset2Probe<T, true, true, true>>(d, pl, z, m, out, fb, base, st);
+        if (pl.top && pl.b2_shadow)
+          return launch_probe<T, OutT, Bitset2Probe<T, true, false, true>>(d, pl, z, m, out, fb, base, st);
+      }
       if (pl.top && d.b2_deep) return launch_probe<T, OutT, Bitset2Probe<T, true, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.top) return launch_probe<T, OutT, Bitset2Probe<T, true>>(d, pl, z, m, out, fb, base, st);
       return launch_probe<T, OutT, Bitset2Probe<T, false>>(d, pl, z, m, out, fb, base, st);

@@ -842,14 +842,35 @@ struct CacheProbe<double, J, RS> {
 // regions are stacked in level order, which makes c1 / c2 level-independent):
 // one LDS, one compare, one select, one 3-input add per level.  Same
 // comparisons, same values as binsearch.py:72-86.
-template <typename T, bool TOP, bool DEEP = false>
+// Bytes of bitset2's staged f32 shadow region (levels [0, l1) plain, [l1, l2)
+// in 32 copies, [l2, l3) in 16, [l3, top) plain; 4-B words), 16-B aligned:
+// the f64 plane follows it.
+__host__ __device__ __forceinline__ uint32_t b2_shadow_bytes(int top, int l1, int l2, int l3) {
+  const uint32_t words = ((1u << l1) - 1) + ((1u << l2) - (1u << l1)) * 32 + ((1u << l3) - (1u << l2)) * 16 +
+                         ((1u << top) - (1u << l3));
+  return (4 * words + 15) & ~15u;
+}
+
+template <typename T, bool TOP, bool DEEP = false, bool SHADOW = false>
 struct Bitset2Probe {
-  const T* top;
+  // f64 partitions stage their top levels as f32 shadow keys (RN of each
+  // key, same region layout as f32: one bank per node instead of two) plus an
+  // exact f64 plane in plain level order.  RN is monotone, so z32 > k32
+  // implies z > k and z32 < k32 implies z < k: every left turn of the shadow
+  // walk is exact, and a right turn can only be wrong on a tie z32 == k32.
+  // The right-turn keys increase along the walk, so one exact check of the
+  // last one (the node at the final prefix, z >= X[prefix]) validates the
+  // whole walk; the rare failure re-descends exactly over the f64 plane.
+  static constexpr bool kShadow = sizeof(T) == 8 && SHADOW;
+  using K = std::conditional_t<kShadow, float, T>;  // staged key type
+  const K* top;
+  const double* plane;  // kShadow: exact keys of the staged levels, plain level order
   const T* xpad;
   const char* deep;  // subtree records of the global levels (fs_build_b2_deep) or NULL
   int pbits, top_bits, l1, l2, l3, deep_k;
   __device__ __forceinline__ Bitset2Probe(const DevPlan<T>& p, unsigned char* smem) {
-    top = reinterpret_cast<const T*>(smem);
+    top = reinterpret_cast<const K*>(smem);
+    plane = reinterpret_cast<const double*>(smem + b2_shadow_bytes(p.top_bits, p.b2_l1, p.b2_l2, p.b2_l3));
     xpad = static_cast<const T*>(p.table);
     pbits = p.pbits;
     top_bits = TOP ? p.top_bits : 0;
@@ -893,7 +914,7 @@ struct Bitset2Probe {
   }
   static __device__ __forceinline__ void prologue(const DevPlan<T>& p, unsigned char* smem) {
     if constexpr (TOP) {
-      T* dst = reinterpret_cast<T*>(smem);
+      K* dst = reinterpret_cast<K*>(smem);
       const T* src = static_cast<const T*>(p.table);
       const uint32_t n1w = (1u << p.b2_l1) - 1;                                   // P1 words
       const uint32_t nrw = ((1u << p.b2_l2) - (1u << p.b2_l1)) * 32u;            // R words
@@ -909,14 +930,23 @@ struct Bitset2Probe {
         const int l = 31 - __clz(node + 1);
         const uint32_t m = node + 1 - (1u << l);
         const uint64_t r = ((uint64_t)m << (p.pbits - l)) | (1ull << (p.pbits - 1 - l));
-        dst[w] = __ldg(src + r);
+        if constexpr (kShadow) dst[w] = __double2float_rn(__ldg(src + r));
+        else dst[w] = __ldg(src + r);
+      }
+      if constexpr (kShadow) {  // the exact plane: node n of level l at n, plain level order
+        double* pl = reinterpret_cast<double*>(smem + b2_shadow_bytes(p.top_bits, p.b2_l1, p.b2_l2, p.b2_l3));
+        for (uint32_t n = threadIdx.x; n < (1u << p.top_bits) - 1; n += blockDim.x) {
+          const int l = 31 - __clz(n + 1);
+          const uint32_t m = n + 1 - (1u << l);
+          pl[n] = __ldg(src + (((uint64_t)m << (p.pbits - l)) | (1ull << (p.pbits - 1 - l))));
+        }
       }
       __syncthreads();
     }
   }
-  static __device__ __forceinline__ T lds(uint32_t a) {
-    T v;
-    if constexpr (sizeof(T) == 4) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  static __device__ __forceinline__ K lds(uint32_t a) {
+    K v;
+    if constexpr (sizeof(K) == 4) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
     else asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
   }
@@ -932,13 +962,13 @@ struct Bitset2Probe {
   //   FORM 0: FSETP, SEL, IMAD            (ALU 2, FMA 1)
   //   FORM 1: FSETP, IMAD, predicated IMAD (ALU 1, FMA 2)
   template <int FORM>
-  static __device__ __forceinline__ uint32_t step(uint32_t a, T z, uint32_t c1, uint32_t c2, uint32_t two,
+  static __device__ __forceinline__ uint32_t step(uint32_t a, K z, uint32_t c1, uint32_t c2, uint32_t two,
                                                   uint32_t one) {
-    const T v = lds(a);
+    const K v = lds(a);
 #if FSG_B2_PIPE_MIX
     // f64 compares issue on the FP64 pipe, which leaves the ALU room: the
     // all-ALU form measures best there
-    if constexpr (sizeof(T) == 8) {
+    if constexpr (sizeof(K) == 8) {
       return a + a + (z >= v ? c2 : c1);
     } else {
       uint32_t r;
@@ -958,8 +988,8 @@ struct Bitset2Probe {
   // Levels [0, top_bits) for N queries in lockstep; returns, per query, the
   // bit prefix i (the index reached after top_bits levels, low bits clear).
   template <int N>
-  __device__ __forceinline__ void descend_top(const T (&z)[N], uint32_t (&i)[N]) const {
-    constexpr uint32_t sz = sizeof(T);
+  __device__ __forceinline__ void descend_top(const K (&z)[N], uint32_t (&i)[N]) const {
+    constexpr uint32_t sz = sizeof(K);
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(top);
     uint32_t two, one;  // opaque to ptxas: keeps the IMADs on the FMA pipe
     asm volatile("mov.u32 %0, 2;" : "=r"(two));
@@ -1039,7 +1069,28 @@ struct Bitset2Probe {
 #pragma unroll
     for (int q = 0; q < N; ++q) s[q] = 0;
     int lvl = top_bits;
-    if constexpr (TOP) {
+    if constexpr (TOP && kShadow) {
+      float zk[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) zk[q] = __double2float_rn(z[q]);
+      descend_top<N>(zk, s);
+      const int lo = pbits - top_bits;  // s: prefix << lo
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        // the last right turn's node: level pbits - 1 - ctz(s), prefix above it
+        bool ok = true;
+        if (s[q]) {
+          const int b = __ffs(s[q]) - 1;
+          const int l = pbits - 1 - b;
+          ok = z[q] >= plane[(1u << l) - 1 + (s[q] >> (b + 1))];
+        }
+        if (!ok) {  // a tie went right wrongly: redo the staged levels exactly
+          uint32_t i = 0;
+          for (int l = 0; l < top_bits; ++l) i = 2 * i + (z[q] >= plane[(1u << l) - 1 + i] ? 1u : 0u);
+          s[q] = i << lo;
+        }
+      }
+    } else if constexpr (TOP) {
       descend_top<N>(z, s);
     }
     if constexpr (DEEP) {

@@ -740,14 +740,15 @@ def test_launch_counts_match_the_kernels_launched(cuda):
             torch.cuda.synchronize()
         return sum(1 for e in prof.events() if "search_kernel" in e.name and e.device_type.name == "CUDA")
 
-    m = 3 * (16 << 20) // 4 + 12345  # four 16-MB staging slots / two 64-MB pinned chunks
+    m = 3 * (16 << 20) // 4 + 12345  # 50 MB of f32 queries
     z = orc.random_queries(p.values, m, seed=3)
     zt = torch.from_numpy(z).cuda()
     out_t = torch.empty(m, dtype=torch.int32, device=cuda)
     assert count(lambda: fs.batch_search(cfg, zt, out_t)) == prep.launches_per_batch(m) == 1
     out = np.empty(m, dtype=np.int32)
     n_pageable = prep.host_launches(z, out)
-    assert n_pageable == 4
+    chunk = (min(4 << 20, max((2 << 20) // 4, m // 8)) + 7) & ~7  # staged chunks: m/8 within 2..16 MB
+    assert n_pageable == -(-m // chunk) == 8
     assert count(lambda: fs.batch_search(cfg, z, out)) == n_pageable
     zp = torch.from_numpy(z).pin_memory()
     op = torch.empty(m, dtype=torch.int32).pin_memory()
