@@ -398,6 +398,14 @@ def per_config(steps: int, barrier, world: int, rank: int):
                "bytes_per_query": qb}
         flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=z.device) if qb * ml < L2_FLUSH_BYTES else None
         row["l2"] = "flushed before each launch" if flush is not None else "stream > L2, no flush"
+        if flush is not None and z.element_size() == 4:
+            # a stream this small is bound by its cold start, not by HBM bandwidth: time a
+            # copy of the same bytes (queries -> an int32 array) the same way as the floor
+            zi = z.view(torch.int32)
+            nc = steps * 10
+            t_copy = time_steps(lambda: out.copy_(zi), nc, 3, barrier, flush) / nc
+            row["copy_floor"] = {"us": 1e6 * t_copy, "what": "torch copy of the same stream into the int32 "
+                                 "output, L2 flushed before each copy (the small-transfer floor)"}
         for name in ("direct", "bitset2"):
             t_prep = time.perf_counter()
             prep = fs.prepare_with_fallback(p) if name == "direct" else fs.prepare("bitset2", p)
@@ -420,6 +428,8 @@ def per_config(steps: int, barrier, world: int, rank: int):
                 "verified": bad == 0,
                 "launches_per_step": prep.launches_per_batch(ml),
             }
+            if "copy_floor" in row:
+                ent["of_copy_floor"] = row["copy_floor"]["us"] / (1e6 * t)
             if name == "direct" and prep.algorithm.startswith("direct"):
                 ent["R"] = int(prep.structure.r)
                 ent["table_bytes"] = {"K": 4 * (int(prep.structure.r) + 1), "X": int(p.values.nbytes)}
