@@ -1267,14 +1267,14 @@ bool zone_plan(const std::vector<uint64_t>& f, uint64_t r, int zs, std::vector<u
   return nrec < (1ull << 27);
 }
 
-int zoned_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r,
-                       uint64_t* f_scratch_dev, std::vector<uint64_t>& f, cudaStream_t s) {
+// knot buckets f_i (sorted) computed on the device, read back for the planner
+int zoned_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t* f_scratch_dev,
+                       std::vector<uint64_t>& f, cudaStream_t s) {
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, s);
   if (rc) return rc;
   f.resize(n1);
   FS_CUDA(cudaMemcpyAsync(f.data(), f_scratch_dev, n1 * 8, cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
-  (void)r;
   return FS_OK;
 }
 }  // namespace
@@ -1295,7 +1295,7 @@ int fs_plan_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
   // every knot costs at least 16/6 B of a slot record
   if (16 * n1 / kZonedSlots > budget_bytes) return fail(FS_TOO_LARGE, "no zoned layout fits the budget");
   std::vector<uint64_t> f;
-  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, r, f_scratch_dev, f, as_stream(stream));
+  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, f, as_stream(stream));
   if (rc) return rc;
   // the fewest zones (32: one wavefront per warp's descriptor loads, else 64)
   int zs32 = kZonedMinZoneShift;
@@ -1343,7 +1343,7 @@ int fs_build_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "zoned records need R < 2^32, N < 2^31");
   cudaStream_t s = as_stream(stream);
   std::vector<uint64_t> f;
-  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, r, f_scratch_dev, f, s);
+  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, f, s);
   if (rc) return rc;
   std::vector<uint32_t> desc;
   uint64_t nrec = 0;
