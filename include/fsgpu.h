@@ -85,7 +85,7 @@ enum {
   FS_SPARSE_RECORDS8 = 2,  /* 8-B group records, two offsets (| F): fs_build_sparse_rec  */
   FS_SPARSE_RECORDS12 = 3, /* 16-B group records, eight 12-bit offsets (shift <= 10)      */
   FS_SPARSE_RECORDS8X3 = 4,/* 8-B group records, three 13-bit offsets (shift <= 11, N+1 <= 2^24) */
-  FS_SPARSE_ZONED = 5      /* zone descriptors | 16-B records, per-zone form: fs_build_zoned */
+  FS_SPARSE_ZONED = 5      /* zone descriptors | 8-B records, per-zone form: fs_build_zoned  */
 };
 
 /*
@@ -130,7 +130,7 @@ typedef struct fs_plan {
                           zoned: zone = 2^sparse_shift buckets (10..31)         */
   uint32_t sparse_ndense; /* two-level: dense (bitmask) super-buckets in `sparse`;
                              records: overflowing records (> 0: F follows);
-                             zoned: number of 16-B records                      */
+                             zoned: number of 8-B records                       */
   const void* b2_deep;  /* bitset2 only, optional: subtree records of the levels
                            below the shared-memory top (fs_build_b2_deep); one
                            32-B gather resolves b2_deep_k levels.  NULL = unused. */
@@ -290,11 +290,12 @@ int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64
 /*
  * Zoned records of the gap-1 table (FS_SPARSE_ZONED; a device layout of K,
  * no reference counterpart).  The buckets [0, R] are cut into nz = (R >>
- * zs) + 1 <= 64 zones of 2^zs buckets, and each zone takes the 16-B record
- * form its own knot density needs: slot records {K[j0], six 16-bit
- * offsets f_i - j0} per 2^s buckets (s = 7..min(14, zs), the largest whose
- * records hold at most six knots; unused offsets 0x7FFF), else rank records
- * {K[j0], 64-bit mask of the buckets holding a knot, 0} per 64 buckets.
+ * zs) + 1 <= 64 zones of 2^zs buckets (zs >= 11), and each zone takes the
+ * 8-B record form its own knot density needs: slot records (the
+ * FS_SPARSE_RECORDS8X3 word: K[j0] in bits 0..23, three fields 0x1000 |
+ * (f_i - j0) at bits 25 + 13k, unused 0x1FFF) per 2^s buckets (s = 6..11,
+ * the largest whose records hold at most three knots), else rank records
+ * {mask of the 32 buckets holding a knot, K[j0]}.  N+1 <= 2^24.
  * Buffer: nz u32 descriptors (first record << 5 | 16 if rank | s), padded to
  * a multiple of four, then the records.  The kernel resolves K[j] from one
  * descriptor and one record load, both in shared memory, and reads X only for

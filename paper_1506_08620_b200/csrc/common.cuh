@@ -38,16 +38,18 @@ constexpr int kRec12MaxShift = 10;
 // 0x1000 | offset at bits 25 + 13k (offsets < 2^11, unused 0x1FFF); shifts up
 // to 11.
 constexpr int kRec3MaxShift = 11;
-// Zoned records (FS_SPARSE_ZONED): at most this many zones, so a warp's
-// zone-descriptor loads touch at most two words per bank; slot records hold
-// up to kZonedSlots 16-bit offsets and use shifts kZonedMinShift..
-// kZonedMaxShift (below that a zone takes 64-bucket rank records, which cost
-// the same 16 B per 64 buckets and decode faster).
+// Zoned records (FS_SPARSE_ZONED, 8 B each): at most this many zones, so a
+// warp's zone-descriptor loads touch at most two words per bank; slot records
+// are the three-offset 8-B records (24-bit base, 13-bit fields) at shifts
+// kZonedMinShift..kZonedMaxShift; a zone no slot shift fits takes 32-bucket
+// rank records {mask, base} (the same 8 B per 32 buckets as a slot record at
+// shift 5, with a cheaper decode).
 constexpr uint32_t kZonedMaxZones = 64;
-constexpr int kZonedSlots = 6;
-constexpr int kZonedMinShift = 7;
-constexpr int kZonedMaxShift = 14;
-constexpr int kZonedMinZoneShift = 10;
+constexpr int kZonedSlots = 3;
+constexpr int kZonedMinShift = 6;
+constexpr int kZonedMaxShift = kRec3MaxShift;
+constexpr int kZonedMinZoneShift = kRec3MaxShift;
+constexpr int kZonedRankShift = 5;
 constexpr uint32_t kZonedRankFlag = 16u;
 
 // ---------------------------------------------------------------------------

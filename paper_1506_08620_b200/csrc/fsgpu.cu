@@ -170,7 +170,8 @@ int validate_plan(const fs_plan* p) {
                         p->sparse_format != FS_SPARSE_RECORDS8X3 && p->sparse_format != FS_SPARSE_ZONED))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
       if (p->sparse && p->sparse_format == FS_SPARSE_ZONED) {
-        if (fs_zoned_bytes(p->r, p->sparse_shift, p->sparse_ndense) == 0 || p->r >= (1ull << 32))
+        if (fs_zoned_bytes(p->r, p->sparse_shift, p->sparse_ndense) == 0 || p->r >= (1ull << 32) ||
+            p->n1 > (1ull << 24))
           return fail(FS_INVALID_ARG, "zoned table parameters out of range");
         if (p->hot_knot0 > p->n1 || p->hot_knots > p->n1 - p->hot_knot0)
           return fail(FS_INVALID_ARG, "knot window outside the knots");
@@ -1259,7 +1260,7 @@ bool zone_plan(const std::vector<uint64_t>& f, uint64_t r, int zs, std::vector<u
         break;
       }
     const bool rank = s < 0;
-    if (rank) s = 6;
+    if (rank) s = kZonedRankShift;
     if (nrec >= (1ull << 27)) return false;
     desc[z] = (uint32_t)(nrec << 5) | (rank ? kZonedRankFlag : 0u) | (uint32_t)s;
     nrec += (zb + (1ull << s) - 1) >> s;
@@ -1283,7 +1284,7 @@ uint64_t fs_zoned_bytes(uint64_t r, int32_t zs, uint64_t nrec) {
   if (zs < kZonedMinZoneShift || zs > 31) return 0;
   const uint64_t nz = (r >> zs) + 1;
   if (nz > kZonedMaxZones) return 0;
-  return 4 * ((nz + 3) & ~3ull) + 16 * nrec;
+  return 4 * ((nz + 3) & ~3ull) + 8 * nrec;
 }
 
 int fs_plan_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
@@ -1292,8 +1293,9 @@ int fs_plan_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
   if (!x_dev || !f_scratch_dev || n1 < 2 || !zs_out) return fail(FS_INVALID_ARG, "bad arguments");
   if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "zoned records need R < 2^32, N < 2^31");
-  // every knot costs at least 16/6 B of a slot record
-  if (16 * n1 / kZonedSlots > budget_bytes) return fail(FS_TOO_LARGE, "no zoned layout fits the budget");
+  if (n1 > (1ull << 24)) return fail(FS_TOO_LARGE, "zoned slot records need N+1 <= 2^24");
+  // every knot costs at least 8/3 B of a slot record
+  if (8 * n1 / kZonedSlots > budget_bytes) return fail(FS_TOO_LARGE, "no zoned layout fits the budget");
   std::vector<uint64_t> f;
   int rc = zoned_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, f, as_stream(stream));
   if (rc) return rc;
@@ -1351,7 +1353,8 @@ int fs_build_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint
   const uint64_t nz = desc.size();
   desc.resize((nz + 3) & ~3ull, 0u);
   FS_CUDA(cudaMemcpyAsync(buf_dev, desc.data(), 4 * desc.size(), cudaMemcpyHostToDevice, s));
-  auto* R = reinterpret_cast<uint4*>(static_cast<char*>(buf_dev) + 4 * desc.size());
+  if (n1 > (1ull << 24)) return fail(FS_TOO_LARGE, "zoned slot records need N+1 <= 2^24");
+  auto* R = reinterpret_cast<uint2*>(static_cast<char*>(buf_dev) + 4 * desc.size());
   fill_zoned_kernel<<<grid_1d(nrec, 256), 256, 0, s>>>(f_scratch_dev, n1, zs, static_cast<const uint32_t*>(buf_dev),
                                                        (uint32_t)nz, R, nrec);
   FS_CUDA(cudaGetLastError());

@@ -636,12 +636,12 @@ struct HotRankProbe {
 // Direct search (gap 1) over the zoned records of K (fill_zoned_kernel),
 // staged in shared memory after a window X[t0, t0 + nt) of the knots.  The
 // buckets are cut into nz = (R >> zs) + 1 zones of 2^zs; each zone takes the
-// 16-B record form its own knot density needs (fs_plan_zoned), so a table
+// 8-B record form its own knot density needs (fs_plan_zoned), so a table
 // whose density varies by orders of magnitude (cfg4's geometric knots) fits
 // in shared memory where one record shift for the whole table cannot:
-//   slot records  {base, six 16-bit offsets} per 2^s buckets, s <= 14,
-//                 never more than six knots (no overflow path);
-//   rank records  {base, 64-bit knot mask, 0} per 64 buckets.
+//   slot records  {24-bit base, three 13-bit offsets} per 2^s buckets,
+//                 s <= 11, never more than three knots (no overflow path);
+//   rank records  {32-bit knot mask, base} per 32 buckets.
 // Zone descriptor (u32, nz <= 64 of them at the table head, so a warp's
 // descriptor loads cost at most two wavefronts): first record << 5 |
 // rank << 4 | s.  K[j] = base + #{knots of the record below j} exactly, and
@@ -683,40 +683,38 @@ struct ZonedProbe {
     asm("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(zd + 4u * (j >> zs)));
     return d;
   }
-  __device__ __forceinline__ uint4 rec(uint32_t j, uint32_t d) const {
-    uint4 g;
-    const uint32_t a = rc + 16u * ((d >> 5) + ((j & zmask) >> (d & 15u)));
-    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w) : "r"(a));
+  __device__ __forceinline__ uint2 rec(uint32_t j, uint32_t d) const {
+    uint2 g;
+    const uint32_t a = rc + 8u * ((d >> 5) + ((j & zmask) >> (d & 15u)));
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(g.x), "=r"(g.y) : "r"(a));
     return g;
   }
   // Both record forms decoded branch-free and selected by the zone's rank
   // flag: lanes of one warp fall in zones of either form (cfg4's query mix
   // is half dense, half sparse), and a divergent branch would issue both
   // decodes plus its reconvergence overhead anyway.
-  static __device__ __forceinline__ void resolve(const uint4& g, uint32_t d, uint32_t j, uint32_t& t, bool& knot) {
+  static __device__ __forceinline__ void resolve(const uint2& g, uint32_t d, uint32_t j, uint32_t& t, bool& knot) {
     const uint32_t jl = j & ((1u << (d & 15u)) - 1u);
-    // rank view: 64-bit knot mask (jl < 64 in rank zones)
-    const unsigned long long m = ((unsigned long long)g.z << 32) | g.y;
-    const uint32_t jr = jl & 63u;
-    const uint32_t below = (uint32_t)__popcll(m & ((1ull << jr) - 1ull));
-    const uint32_t kr = (uint32_t)(m >> jr) & 1u;
-    // slot view: six 16-bit offsets (unused kRecSentinel > any jl, s <= 14):
-    // (w + hm) & H has bit 15 / 31 set iff the low / high offset >= jl
-    constexpr uint32_t H = 0x80008000u;
-    const uint32_t hm = H - jl * 0x10001u;
-    const uint32_t ge = __popc((g.y + hm) & H) + __popc((g.z + hm) & H) + __popc((g.w + hm) & H);
-    const uint32_t lt = 6u - ge;
-    uint32_t w;
-    asm("{\n\t.reg .pred p, q;\n\tsetp.lt.u32 p, %1, 2;\n\tsetp.lt.u32 q, %1, 4;\n\t"
-        "selp.b32 %0, %3, %4, q;\n\tselp.b32 %0, %2, %0, p;\n\t}"
-        : "=r"(w)
-        : "r"(lt), "r"(g.y), "r"(g.z), "r"(g.w));
-    const bool ks = lt < 6u && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
-    uint32_t cnt, kb;
+    // rank view: {mask, base} (jl < 32 in rank zones)
+    const uint32_t jr = jl & 31u;
+    const uint32_t tr = g.y + __popc(g.x & ((1u << jr) - 1u));
+    const uint32_t kr = (g.x >> jr) & 1u;
+    // slot view: 64-bit SWAR over the three fields 0x1000 | offset at bits
+    // 25 + 13k (guard bits 37, 50, 63 survive iff offset >= jl)
+    const uint32_t ylo = jl << 25, yhi = jl * 0x80040u + (jl >> 7);
+    uint32_t dlo, dhi;
+    asm("sub.cc.u32 %0, %2, %4;\n\tsubc.u32 %1, %3, %5;" : "=r"(dlo), "=r"(dhi) : "r"(g.x), "r"(g.y), "r"(ylo),
+        "r"(yhi));
+    (void)dlo;
+    const uint32_t lt = 3u - __popc(dhi & 0x80040020u);
+    const unsigned long long w64 = ((unsigned long long)g.y << 32) | g.x;
+    const uint32_t fv = (uint32_t)(w64 >> (lt < 3u ? 25u + 13u * lt : 63u));
+    const uint32_t ks = (lt < 3u && (fv & 0xFFFu) == jl) ? 1u : 0u;
+    const uint32_t ts = (g.x & 0xFFFFFFu) + lt;
+    uint32_t kb;
     asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\tselp.b32 %0, %2, %3, p;\n\tselp.b32 %1, %5, %6, p;\n\t}"
-        : "=r"(cnt), "=r"(kb)
-        : "r"(below), "r"(lt), "r"(d & 16u), "r"(kr), "r"((uint32_t)ks));
-    t = g.x + cnt;
+        : "=r"(t), "=r"(kb)
+        : "r"(tr), "r"(ts), "r"(d & kZonedRankFlag), "r"(kr), "r"(ks));
     knot = kb != 0;
   }
   // X[t] if `knot`, else z: one predicated generic load from the staged
@@ -751,7 +749,7 @@ struct ZonedProbe {
 #pragma unroll
     for (int g0 = 0; g0 < N; g0 += G) {
       uint32_t j[G], d[G];
-      uint4 g[G];
+      uint2 g[G];
 #pragma unroll
       for (int q = 0; q < G; ++q) {
         if (g0 + q >= N) break;

@@ -18,6 +18,18 @@ def _fs():
     return fs
 
 
+@pytest.fixture(autouse=True)
+def _no_zoned():
+    """These skewed tables take zoned records by default
+    (tests/test_gpu_zoned.py); the hot window is tested with zoning off."""
+    from paper_1506_08620_b200 import batch
+
+    keep = batch.ZONED
+    batch.ZONED = False
+    yield
+    batch.ZONED = keep
+
+
 
 def _edge_queries(xs, h, words):
     """Queries in the buckets around directory words `words` (32 buckets

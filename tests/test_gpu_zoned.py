@@ -14,7 +14,7 @@ from oracle import fs_oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-MIN_SHIFT, MAX_SHIFT, SLOTS, SENTINEL, RANK_FLAG = 7, 14, 6, 0x7FFF, 16
+MIN_SHIFT, MAX_SHIFT, SLOTS, RANK_SHIFT, RANK_FLAG = 6, 11, 3, 5, 16
 
 
 def _fs():
@@ -23,22 +23,11 @@ def _fs():
     return fs
 
 
-@pytest.fixture(autouse=True)
-def _zoned_first():
-    """cfg4 takes its hot window by default (measured faster on its query
-    mix); these tests put zoned records ahead of it."""
-    from paper_1506_08620_b200 import batch
-
-    keep = batch.ZONED
-    batch.ZONED = "first"
-    yield
-    batch.ZONED = keep
-
-
 def expected_zoned(xs, h, r, zs):
-    """(desc uint32[nz], records uint32[nrec, 4]) as fs_build_zoned lays them
-    out: per zone the largest shift 7..min(14, zs) whose records hold <= 6
-    knots (slot records), else 64-bucket rank records."""
+    """(desc uint32[nz], records uint32[nrec, 2]) as fs_build_zoned lays them
+    out: per zone the largest shift 6..min(11, zs) whose records hold <= 3
+    knots (slot records: base | fields 0x1000 | offset at bits 25 + 13k,
+    unused 0x1FFF), else 32-bucket rank records {mask, base}."""
     f = orc.knot_buckets(xs, h).astype(np.int64)
     nz = (r >> zs) + 1
     desc, recs = [], []
@@ -54,7 +43,7 @@ def expected_zoned(xs, h, r, zs):
                 break
         rank = s < 0
         if rank:
-            s = 6
+            s = RANK_SHIFT
         n = (zb + (1 << s) - 1) >> s
         desc.append((nrec << 5) | (RANK_FLAG if rank else 0) | s)
         j0 = zlo + (np.arange(n, dtype=np.int64) << s)
@@ -63,12 +52,13 @@ def expected_zoned(xs, h, r, zs):
         for g in range(n):
             inr = [int(v) for v in f[lo[g]:hi[g]] - j0[g]]
             if rank:
-                m = sum(1 << o for o in inr)
-                recs.append([int(lo[g]), m & 0xFFFFFFFF, m >> 32, 0])
+                recs.append([sum(1 << o for o in inr), int(lo[g])])
             else:
                 assert len(inr) <= SLOTS
-                offs = inr + [SENTINEL] * (SLOTS - len(inr))
-                recs.append([int(lo[g])] + [offs[2 * w] | (offs[2 * w + 1] << 16) for w in range(3)])
+                w = int(lo[g])
+                for k, o in enumerate(inr + [0xFFF] * (SLOTS - len(inr))):
+                    w |= (0x1000 | o) << (25 + 13 * k)
+                recs.append([w & 0xFFFFFFFF, w >> 32])
         nrec += n
     return np.array(desc, dtype=np.uint32), np.array(recs, dtype=np.uint64).astype(np.uint32)
 
@@ -149,8 +139,8 @@ def _geometric(n, ratio, dtype):
 
 
 def test_zoned_chosen_for_cfg4(cuda):
-    """cfg4 (geometric knots, R = 7.0 M, directory 1.75 MB), zoned records
-    ahead of the hot window: the planner stages zoned records (rank records at the dense start, slot records of
+    """cfg4 (geometric knots, R = 7.0 M, directory 1.75 MB): the planner
+    stages zoned records (rank records at the dense start, slot records of
     growing shift behind) plus the densest knots; buffer bit-exact, answers
     equal the oracle for both halves of the query mix, zone and record edges,
     knots and window edges, int32 and int64 outputs."""
@@ -199,7 +189,7 @@ def test_zoned_every_window_and_zone_shift(cuda, dtype):
     p = fs.validate_partition(xs)
     prep = fs.prepare("direct", p)
     idx = prep.structure
-    zs32 = 10
+    zs32 = 11
     while (idx.r >> zs32) + 1 > 32:
         zs32 += 1
     f = orc.knot_buckets(xs, idx.h).astype(np.int64)
@@ -211,6 +201,8 @@ def test_zoned_every_window_and_zone_shift(cuda, dtype):
     n1 = len(xs)
     budget = batch._smem_budget() - 512
     for zs in (zs32, zs32 - 1):
+        if zs < 11:
+            continue
         for t0, nt in ((0, 0), (0, 4000), (7000, 2500), (n1 - 1000, 1000)):
             buf, desc, rec = with_zoned(fs, p, prep, zs, t0, nt)
             if 4 * len(desc) + rec.nbytes + 128 + nt * xs.itemsize > budget:
@@ -261,39 +253,25 @@ def test_zoned_out_of_domain_and_last_bucket(cuda):
 def test_zoned_not_used_when_directory_fits(cuda):
     """Tables whose rank directory (+ X) fits in shared memory, or that a
     sparse layout serves, keep those layouts (cfg3, cfg5 N+1 = 1025); a table
-    no zoning fits keeps the L2 directory (cfg5 N+1 = 2^20 + 1); by default
-    cfg4 keeps its hot window."""
+    no zoning fits keeps the L2 directory (cfg5 N+1 = 2^20 + 1); with zoning
+    off, cfg4 takes its hot window."""
     fs = _fs()
     from paper_1506_08620_b200 import batch, workloads
 
     for name, kw in (("cfg3", {}), ("cfg5", {"n1": 1025}), ("cfg5", {"n1": 1_048_577})):
         prep = fs.prepare("direct", workloads.knots(name, **kw))
         assert prep.placement()["sparse_format"] != "zoned", (name, kw)
-    batch.ZONED = True
-    pl = fs.prepare("direct", workloads.knots("cfg4")).placement()
+    keep = batch.ZONED
+    batch.ZONED = False
+    try:
+        pl = fs.prepare("direct", workloads.knots("cfg4")).placement()
+    finally:
+        batch.ZONED = keep
     assert pl["smem_hot"] and pl["sparse_format"] != "zoned", pl
 
 
-def test_zoned_when_no_hot_window(cuda):
-    """A skewed table without a hot window (cfg4 with hot_window=False) takes
-    zoned records by default; answers equal the oracle."""
-    fs = _fs()
-    from paper_1506_08620_b200 import batch
-
-    from paper_1506_08620_b200 import workloads
-
-    batch.ZONED = True
-    p = workloads.knots("cfg4")
-    xs = p.values
-    prep = fs.prepare("direct", p, hot_window=False)
-    assert prep.placement()["sparse_format"] == "zoned", prep.placement()
-    _check_buffer(prep, p)
-    z = np.concatenate([orc.random_queries(xs, 300_000, seed=12), orc.boundary_probes(xs)])
-    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
-
-
 def test_zoned_abi_validation(cuda):
-    """validate_plan: zone shifts giving > 64 zones or < 2^10 buckets, and a
+    """validate_plan: zone shifts giving > 64 zones or < 2^11 buckets, and a
     knot window outside X, are rejected; fs_zoned_bytes reports 0 for them."""
     fs = _fs()
     from paper_1506_08620_b200 import _lib, workloads
@@ -304,10 +282,10 @@ def test_zoned_abi_validation(cuda):
     plan = prep.plan
     lib = _lib.load()
     r = prep.structure.r
-    assert lib.fs_zoned_bytes(r, 9, 100) == 0
+    assert lib.fs_zoned_bytes(r, 10, 100) == 0
     assert lib.fs_zoned_bytes(r, 12, 100) == 0  # 1711 zones
-    assert lib.fs_zoned_bytes(r, plan.sparse_shift, 100) == 4 * (((r >> plan.sparse_shift) + 4) // 4 * 4) + 1600
-    for field, value in (("sparse_shift", 9), ("sparse_shift", 12), ("hot_knots", len(p.values) + 1)):
+    assert lib.fs_zoned_bytes(r, plan.sparse_shift, 100) == 4 * (((r >> plan.sparse_shift) + 4) // 4 * 4) + 800
+    for field, value in (("sparse_shift", 10), ("sparse_shift", 12), ("hot_knots", len(p.values) + 1)):
         keep = getattr(plan, field)
         setattr(plan, field, value)
         with pytest.raises(ValueError):

@@ -8,7 +8,7 @@ Config specs: cfgN (BASELINE recipes), cfg5:<N+1>, cfg2:<seed>, cfg5u (the
 unfiltered cfg5 draw, bitset2 fall-back instance), unif32:<size> / unif64:<size> (the throughput sweep's
 U[1,5]-gap partitions), big32:<N+1> (sorted f32
 U[0,1) knots).  Layout variants: direct-k (plain K), direct-rank (rank
-directory only), direct-hot / direct-hot:<KB> / direct-nohot (hot window on, of a given size, off), direct-zoned (zoned records ahead of the hot window), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
+directory only), direct-hot / direct-hot:<KB> / direct-nohot (hot window on, of a given size, off), direct-nozoned (zoned records off), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
 records forced), bitset2-flat (no subtree records),
 direct-gap2-k (gap 2 over plain K), fallback (prepare_with_fallback), gap:<q>
 (direct with gap q over its count directory).
@@ -109,7 +109,7 @@ def main():
         for algo in args.algos.split(","):
             try:
                 base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct", "direct-nohot": "direct",
-                        "direct-zoned": "direct",
+                        "direct-nozoned": "direct",
                         "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
                 if algo.startswith("direct-hot:"):  # hot window of the given size in KB
                     base = "direct"
@@ -142,10 +142,10 @@ def main():
                     prep = fs.prepare("direct", p, hot_window=True)
                 if algo == "direct-nohot":
                     prep = fs.prepare("direct", p, hot_window=False)
-                if algo == "direct-zoned":  # zoned records ahead of the hot window
+                if algo == "direct-nozoned":  # no zoned records: the hot window / L2 directory
                     from paper_1506_08620_b200 import batch as _b
 
-                    _b.ZONED = "first"
+                    _b.ZONED = False
                     try:
                         prep = fs.prepare("direct", p)
                     finally:
