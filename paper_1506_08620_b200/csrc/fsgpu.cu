@@ -514,6 +514,13 @@ template <>
 struct UnrollVW8For<HotRankProbe<float>> {
   static constexpr int value = FSG_UNROLL_VW8_RANK;
 };
+#ifndef FSG_UNROLL_VW8_ZONED
+#define FSG_UNROLL_VW8_ZONED 1  // one 8-query group per thread (2: cfg4 465 -> 448 Gq/s)
+#endif
+template <>
+struct UnrollVW8For<ZonedProbe<float>> {
+  static constexpr int value = FSG_UNROLL_VW8_ZONED;
+};
 template <bool TOP, bool DEEP>
 struct UnrollVW8For<Bitset2Probe<float, TOP, DEEP>> {
   static constexpr int value = 2;

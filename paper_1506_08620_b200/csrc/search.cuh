@@ -741,7 +741,7 @@ struct ZonedProbe {
   // descriptors of a group, then its records, then the resolves: every load
   // of a phase in flight before the first is consumed
 #ifndef FSG_ZONED_GROUP
-#define FSG_ZONED_GROUP 4
+#define FSG_ZONED_GROUP 2  // cfg4: 1 452, 2 465, 3 457, 4 450, 8 436 Gq/s
 #endif
   template <int N, typename R>
   __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
