@@ -9,6 +9,7 @@ for label in cfg1 cfg2_s0 cfg2_s1 cfg2_s2 cfg3 cfg4 cfg5_33 cfg5_1025 cfg5_32769
     f=gpurun_out/traffic/${label}_${algo}.csv
     timeout 600 ncu --metrics $M --clock-control none -k regex:search_kernel --launch-skip 3 --launch-count 1 --csv \
       --log-file $f python tools/traffic_capture.py run $label $algo > gpurun_out/traffic/${label}_${algo}.log 2>&1
+    # the JSONs are written by `collect` (run it here too, or from the merged CSVs on the host)
     python tools/traffic_capture.py collect $label $algo $f > /dev/null || echo "collect failed: $label $algo"
   done
 done
