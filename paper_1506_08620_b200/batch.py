@@ -505,9 +505,9 @@ def _set_hot_window(plan, p: SortedPartition, idx: DirectIndex, rank) -> None:
 
 def _set_zoned(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:
     """Zoned records of K (fs_build_zoned): the buckets cut into at most 64
-    zones, each zone in the 16-B record form its knot density needs (slot
-    records of 2^7..2^14 buckets holding at most six 16-bit knot offsets, or
-    64-bucket rank records), plus a window of the densest knots.  For tables whose
+    zones, each zone in the 8-B record form its knot density needs (slot
+    records of 2^6..2^11 buckets holding at most three 13-bit knot offsets,
+    or 32-bucket rank words), plus a window of the densest knots.  For tables whose
     density varies by orders of magnitude (cfg4's geometric knots: one
     record shift for the whole table overflows at its dense end and exceeds
     shared memory at its sparse end) the whole directory then fits in shared

@@ -1234,7 +1234,7 @@ namespace {
 // descriptors (first record << 5 | rank flag | s) and the record count.
 // Slot records take the largest s in [kZonedMinShift, min(kZonedMaxShift,
 // zs)] whose records hold at most kZonedSlots knots of the zone; a zone where
-// none does takes 64-bucket rank records.  false if zs is out of range or
+// none does takes 32-bucket rank words.  false if zs is out of range or
 // needs > 64 zones.
 bool zone_plan(const std::vector<uint64_t>& f, uint64_t r, int zs, std::vector<uint32_t>& desc, uint64_t& nrec) {
   if (zs < kZonedMinZoneShift || zs > 31) return false;
