@@ -837,3 +837,22 @@ def test_sharded_batch_search_spans_on_one_device(cuda):
     with pytest.raises(fs.OutOfDomain) as ei:
         fsdist.sharded_batch_search(prep, zt[a:b], out[a:b], a)
     assert ei.value.position == 777_777
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+def test_staged_rank_directory_beats_unstaged_sparse(cuda, precision):
+    """Uniform gaps U[1, 5] at N+1 = 65535 (R / N = 3): X cannot be staged
+    beside any sparse layout, so the rank directory (49 KB) is staged alone
+    and X read through L2 for the buckets holding a knot (place();
+    profiles/r02/unif_layouts.txt).  Answers equal the oracle at every knot,
+    its neighbours and random queries."""
+    fs = _fs()
+    p = fs.gen_uniform_gap_partition(65535, 1.0, 5.0, 42, precision)
+    prep = fs.prepare("direct", p)
+    pl = prep.placement()
+    assert pl["smem_table"] and not pl["smem_x"] and not pl["smem_sparse"], pl
+    xs = p.values
+    z = np.concatenate([orc.random_queries(xs, 300_000, seed=6), orc.boundary_probes(xs),
+                        xs[:-1], np.nextafter(xs[1:], -np.inf)]).astype(xs.dtype)
+    z = z[(z >= xs[0]) & (z < xs[-1])]
+    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
