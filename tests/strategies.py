@@ -51,8 +51,9 @@ def partitions(draw, max_size=96):
 def big_partitions(draw):
     """Large strictly increasing knot arrays (2^12 .. 2^20 + 1 knots) that
     reach the big-table device paths: subtree records below the smem top
-    (bitset2), the sparse two-level table and the L2 rank directory
-    (direct), bank-replicated levels with large batches."""
+    and f32 shadow keys (bitset2), the sparse two-level table, group and
+    zoned records, the hot window and the L2 rank directory (direct),
+    bank-replicated levels with large batches."""
     dtype = draw(st.sampled_from([np.float32, np.float64]))
     n1 = draw(st.sampled_from([(1 << 12) + 1, 5000, (1 << 15) + 1, 70_000, (1 << 17) + 3, 300_000, (1 << 20) + 1]))
     seed = draw(st.integers(min_value=0, max_value=2**32 - 1))

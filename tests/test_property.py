@@ -145,3 +145,14 @@ def test_gpu_big_tables_equal_oracle(cuda, xs):
                                    prep.plan.sparse_shift, prep.plan.sparse_ndense)
     finally:
         batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, batch.SPARSE_RECORDS8_MAX_PAST_PPM = keep
+    # zoned records and the hot window are alternatives for skewed tables: when
+    # the planner took one, the other (zoning off) must answer the same
+    if fs.prepare("direct", p).placement()["sparse_format"] == "zoned":
+        keep_z = batch.ZONED
+        batch.ZONED = False
+        try:
+            prep = fs.prepare("direct", p)
+        finally:
+            batch.ZONED = keep_z
+        assert prep.placement()["sparse_format"] != "zoned"
+        assert np.array_equal(fs.run_batch(prep, z), want), ("zoning off", len(xs), prep.placement())
