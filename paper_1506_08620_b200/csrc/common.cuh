@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace fsg {
@@ -51,6 +52,33 @@ constexpr int kZonedMaxShift = kRec3MaxShift;
 constexpr int kZonedMinZoneShift = kRec3MaxShift;
 constexpr int kZonedRankShift = 5;
 constexpr uint32_t kZonedRankFlag = 16u;
+
+// Bounds-checked builds (FSG_BOUNDS_CHECK=1, tools/bounds_check.sh): every
+// table gather of the search probes checks its index against the table's
+// extent, and every shared-memory gather its offset against the CTA's dynamic
+// shared memory, and traps on a violation.  compute-sanitizer is closed on
+// this GPU pool; the GPU test suite runs against this build instead.
+#ifndef FSG_BOUNDS_CHECK
+#define FSG_BOUNDS_CHECK 0
+#endif
+#if FSG_BOUNDS_CHECK
+#define FSG_BOUND(c)                                                                   \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("fsg bounds check failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);         \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define FSG_BOUND(c) \
+  do {               \
+  } while (0)
+#endif
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+  uint32_t v;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
 
 // ---------------------------------------------------------------------------
 // Exact arithmetic in the partition's precision

@@ -91,7 +91,9 @@ struct DirectProbe {
   T h, x0;
   J r;
   int q;
+  uint64_t n1;  // knots (bounds checks)
   __device__ __forceinline__ DirectProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = p.n1;
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
     K = KS ? reinterpret_cast<const uint32_t*>(smem + p.x_smem_bytes_aligned()) : static_cast<const uint32_t*>(p.table);
     h = p.h;
@@ -103,6 +105,7 @@ struct DirectProbe {
     J j = trunc_to<J>(mul_rn(sub_rn(z, x0), h));
     j = j < r ? j : r;
     const uint32_t t = tload<KS>(K, j);
+    FSG_BOUND((uint64_t)j <= (uint64_t)r && (uint64_t)t < n1 + (uint64_t)q);  // X holds q - 1 left pads
     if constexpr (GAP == 1) {
       return (int64_t)t - (z < tload<XS>(X, t) ? 1 : 0);
     } else if constexpr (GAP == 2) {
@@ -132,7 +135,9 @@ struct RankProbe {
   const uint2* D;
   T h, x0;
   J r;
+  uint64_t n1;
   __device__ __forceinline__ RankProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = p.n1;
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
     D = DS ? reinterpret_cast<const uint2*>(smem + p.x_smem_bytes_aligned()) : p.rank;
     h = p.h;
@@ -146,6 +151,7 @@ struct RankProbe {
     const uint32_t b = (uint32_t)j & 31u;
     const uint32_t t = d.y + __popc(d.x & ((1u << b) - 1u));
     const bool knot = (d.x >> b) & 1u;
+    FSG_BOUND((uint64_t)j <= (uint64_t)r && (!knot || t < n1));
     // lanes whose bucket holds no knot read X[0] (a broadcast), never a
     // conflicting bank, and their answer is t - 1 regardless
     const T xv = tload<XS>(X, knot ? t : 0u);
@@ -168,6 +174,7 @@ struct RankProbe {
         J j = trunc_to<J>(mul_rn(sub_rn(z[g0 + q], x0), h));
         j = j < r ? j : r;
         b[q] = (uint32_t)j & 31u;
+        FSG_BOUND((uint64_t)j <= (uint64_t)r);
         d[q] = tload<DS>(D, (uint64_t)(j >> 5));
       }
 #pragma unroll
@@ -175,6 +182,7 @@ struct RankProbe {
         if (g0 + q >= N) break;
         const uint32_t t = d[q].y + __popc(d[q].x & ((1u << b[q]) - 1u));
         const bool knot = (d[q].x >> b[q]) & 1u;
+        FSG_BOUND(!knot || t < n1);
         T xv = z[g0 + q];
         if (knot) xv = tload<XS>(X, t);
         o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
@@ -196,7 +204,9 @@ struct Rank2Probe {
   const uint4* D;
   T h, x0;
   uint32_t r;
+  uint64_t n1;
   __device__ __forceinline__ Rank2Probe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = p.n1;
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
     D = DS ? reinterpret_cast<const uint4*>(smem + p.x_smem_bytes_aligned()) : reinterpret_cast<const uint4*>(p.rank);
     h = p.h;
@@ -208,6 +218,7 @@ struct Rank2Probe {
     const uint32_t t = d.z + __popc(d.x & le) + __popc(d.y & le) - 1u;
     const uint32_t c = ((d.x >> b) & 1u) + ((d.y >> b) & 1u);
     uint32_t miss = 0;
+    FSG_BOUND(c == 0 || (t < n1 && t + 1 >= c));
     if (c >= 1) miss += z < tload<XS>(X, t) ? 1u : 0u;
     if (c == 2) miss += z < tload<XS>(X, t - 1) ? 1u : 0u;
     return (int64_t)t - (int64_t)miss;
@@ -257,7 +268,9 @@ struct CountDirProbe {
   const uint2* D;
   T h, x0;
   uint32_t r;
+  uint64_t n1;
   __device__ __forceinline__ CountDirProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = p.n1;
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
     D = DS ? reinterpret_cast<const uint2*>(smem + p.x_smem_bytes_aligned()) : p.rank;
     h = p.h;
@@ -281,6 +294,7 @@ struct CountDirProbe {
     sums(d.x, b, s, c);
     const uint32_t t = d.y + s - 1u;
     uint32_t miss = 0;
+    FSG_BOUND(c == 0 || (t < n1 && t + 1 >= c));
     for (uint32_t k = 0; k < c; ++k) miss += z < tload<XS>(X, t - k) ? 1u : 0u;
     return (int64_t)t - (int64_t)miss;
   }
@@ -329,7 +343,9 @@ struct SparseProbe {
   const uint16_t* Dp;  //                     per-word knot prefix counts
   T h, x0;
   uint32_t r, s, mask, wshift;
+  uint64_t n1;
   __device__ __forceinline__ SparseProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = p.n1;
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
     unsigned char* cf = smem + p.x_smem_bytes_aligned();
     const uint64_t nc = ((uint64_t)p.r >> p.sparse_shift) + 2;
@@ -349,6 +365,7 @@ struct SparseProbe {
     uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
     j = j < r ? j : r;
     const uint32_t J = j >> s, jl = j & mask;
+    FSG_BOUND(J <= (r >> s));
     const uint32_t c = C[J];
     uint32_t t;
     bool knot;
@@ -369,6 +386,7 @@ struct SparseProbe {
       t = lo;
       knot = lo < end && F[lo] == jl;
     }
+    FSG_BOUND(!knot || t < n1);
     T xv = z;
     if (knot) xv = tload<XS>(X, t);
     return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
@@ -423,7 +441,9 @@ struct SparseRecProbe {
   const uint16_t* F;
   T h, x0;
   uint32_t r, s, mask;
+  uint64_t n1;
   __device__ __forceinline__ SparseRecProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = p.n1;
     X = XS ? reinterpret_cast<const T*>(smem) : p.x;
     // held in a register (volatile mov): ptxas would otherwise rebuild the
     // shared-window address (S2R + 3 ALU) in front of every X load
@@ -505,10 +525,12 @@ struct SparseRecProbe {
       knot = lt < SLOTS && ((w >> ((lt & 1u) << 4)) & 0xFFFFu) == jl;
     }
     t = base_of(g) + lt;
+    FSG_BOUND((j >> s) <= (r >> s) && (!knot || t < n1));
     if constexpr (OVF) {
       if (overflows(g) && lt == SLOTS) {  // past the last recorded knot of an overflowing super-bucket
         uint32_t lo = t, hi = base_of(G[(j >> s) + 1]);
         const uint32_t end = hi;
+        FSG_BOUND(t <= end && end <= n1);
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
           if (F[mid] < jl) lo = mid + 1;
@@ -575,7 +597,9 @@ struct HotRankProbe {
   const uint2* Ds;
   T h, x0;
   uint32_t r, w0, nw, t0, nt;
+  uint64_t n1;
   __device__ __forceinline__ HotRankProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = p.n1;
     X = p.x;
     D = p.rank;
     Xs = reinterpret_cast<const T*>(smem);
@@ -597,6 +621,7 @@ struct HotRankProbe {
     const uint32_t t = d.y + __popc(d.x & ((1u << b) - 1u));
     const bool knot = (d.x >> b) & 1u;
     const uint32_t tl = t - t0;
+    FSG_BOUND((j >> 5) <= (r >> 5) && (!knot || t < n1));
     T xv = z;  // any value: unused unless `knot`
     if (knot) xv = tl < nt ? Xs[tl] : __ldg(X + t);
     return (int64_t)t - ((!knot || z < xv) ? 1 : 0);
@@ -625,6 +650,7 @@ struct HotRankProbe {
         const uint32_t t = d[q].y + __popc(d[q].x & ((1u << b[q]) - 1u));
         const bool knot = (d[q].x >> b[q]) & 1u;
         const uint32_t tl = t - t0;
+        FSG_BOUND(!knot || t < n1);
         T xv = z[g0 + q];
         if (knot) xv = tl < nt ? Xs[tl] : __ldg(X + t);
         o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
@@ -655,7 +681,10 @@ struct ZonedProbe {
   uint32_t xs, zd, rc;      // shared addresses: X window, zone descriptors, records
   T h, x0;
   uint32_t r, zs, zmask, t0, nt;
+  uint64_t n1, nrec;
   __device__ __forceinline__ ZonedProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = p.n1;
+    nrec = p.sparse_ndense;
     X = p.x;
     asm volatile("mov.u32 %0, %1;" : "=r"(xs) : "r"((uint32_t)__cvta_generic_to_shared(smem)));
     // the window's generic address held in a register (ptxas would otherwise
@@ -680,12 +709,14 @@ struct ZonedProbe {
   }
   __device__ __forceinline__ uint32_t desc(uint32_t j) const {
     uint32_t d;
+    FSG_BOUND((j >> zs) <= (r >> zs) && zd + 4u * (j >> zs) - xs < dyn_smem_bytes());
     asm("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(zd + 4u * (j >> zs)));
     return d;
   }
   __device__ __forceinline__ uint2 rec(uint32_t j, uint32_t d) const {
     uint2 g;
     const uint32_t a = rc + 8u * ((d >> 5) + ((j & zmask) >> (d & 15u)));
+    FSG_BOUND((d >> 5) + ((j & zmask) >> (d & 15u)) < nrec && a + 8u - xs <= dyn_smem_bytes());
     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(g.x), "=r"(g.y) : "r"(a));
     return g;
   }
@@ -721,6 +752,7 @@ struct ZonedProbe {
   // window or global memory (no branch between the two)
   __device__ __forceinline__ T xsel(uint32_t t, bool knot, T z) const {
     const uint32_t tl = t - t0;
+    FSG_BOUND(!knot || t < n1);
     const T* p = tl < nt ? reinterpret_cast<const T*>(xg) + tl : X + t;
     T v = z;
     if constexpr (sizeof(T) == 4)
@@ -1058,7 +1090,10 @@ struct Bitset2Probe {
       }
     }
 #pragma unroll
-    for (int q = 0; q < N; ++q) i[q] = ((a[q] - b2) / sz + s0 - ((1u << top_bits) - 1)) << (pbits - top_bits);
+    for (int q = 0; q < N; ++q) {
+      i[q] = ((a[q] - b2) / sz + s0 - ((1u << top_bits) - 1)) << (pbits - top_bits);
+      FSG_BOUND((i[q] >> (pbits - top_bits)) < (1u << top_bits));
+    }
   }
   // N queries descend in lockstep: N independent smem/L2 loads per level.
   template <int N, typename R>
@@ -1080,6 +1115,7 @@ struct Bitset2Probe {
         if (s[q]) {
           const int b = __ffs(s[q]) - 1;
           const int l = pbits - 1 - b;
+          FSG_BOUND(l < top_bits && (s[q] >> (b + 1)) < (1u << l));
           ok = z[q] >= plane[(1u << l) - 1 + (s[q] >> (b + 1))];
         }
         if (!ok) {  // a tie went right wrongly: redo the staged levels exactly
@@ -1103,7 +1139,10 @@ struct Bitset2Probe {
             Rec r[G];
 #pragma unroll
             for (int q = 0; q < G; ++q)
-              if (g0 + q < N) r[q] = ld_rec(deep + off + (uint64_t)(s[g0 + q] >> sh) * 32);
+              if (g0 + q < N) {
+                FSG_BOUND((s[g0 + q] >> sh) < (1u << lvl));
+                r[q] = ld_rec(deep + off + (uint64_t)(s[g0 + q] >> sh) * 32);
+              }
 #pragma unroll
             for (int q = 0; q < G; ++q)
               if (g0 + q < N) s[g0 + q] |= walk_rec(r[q], z[g0 + q], kc) << (sh - kc);
@@ -1118,6 +1157,7 @@ struct Bitset2Probe {
 #pragma unroll
       for (int q = 0; q < N; ++q) {
         const uint32_t r = s[q] | bit;
+        FSG_BOUND(r < (1u << pbits));
         if (z[q] >= __ldg(xpad + r)) s[q] = r;
       }
     }
