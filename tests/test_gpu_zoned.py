@@ -298,6 +298,11 @@ def test_zoned_abi_validation(cuda):
     rc = lib.fs_plan_zoned(_lib.FS_F32, p.device_values().data_ptr(), len(p.values), float(prep.structure.h), r,
                            1000, f.data_ptr(), ctypes.byref(zs), *[ctypes.byref(o) for o in outs], None)
     assert rc == _lib.FS_TOO_LARGE
+    buf = _device_f(4096)
+    for bad_zs in (5, 12, 40):  # below the minimum zone, > 64 zones, beyond 31
+        rc = lib.fs_build_zoned(_lib.FS_F32, p.device_values().data_ptr(), len(p.values), float(prep.structure.h), r,
+                                bad_zs, f.data_ptr(), buf.data_ptr(), None)
+        assert rc == _lib.FS_INVALID_ARG, bad_zs
 
 
 def _device_f(n):
