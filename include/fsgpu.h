@@ -296,7 +296,8 @@ int fs_build_sparse_rec(int32_t format, int32_t dtype, const void* x_dev, uint64
  * (f_i - j0) at bits 25 + 13k, unused 0x1FFF) per 2^s buckets (s = 6..11,
  * the largest whose records hold at most three knots), else rank records
  * {mask of the 32 buckets holding a knot, K[j0]}.  N+1 <= 2^24.
- * Buffer: nz u32 descriptors (first record << 5 | 16 if rank | s), padded to
+ * Buffer: nz u32 descriptors ((first record - (z << (zs - s))) << 5, as a
+ * signed 27-bit value | 16 if rank | s), padded to
  * a multiple of four, then the records.  The kernel resolves K[j] from one
  * descriptor and one record load, both in shared memory, and reads X only for
  * a bucket holding a knot -- from a staged window X[t0, t0 + nt) or L2.

@@ -326,7 +326,8 @@ __global__ void fill_sparse_rec_kernel(const uint64_t* __restrict__ f, uint64_t 
 }
 
 // Zoned records of the gap-1 table (fs_build_zoned): one thread per 8-B
-// record.  zdesc[z] = first record << 5 | rank flag | s for zone z (buckets
+// record.  zdesc[z] = (first record - (z << (zs - s))) << 5 | rank flag | s
+// for zone z (buckets
 // [z 2^zs, (z+1) 2^zs)); record g of zone z covers buckets j0 .. j0 + 2^s - 1,
 // j0 = z 2^zs + (g - first) 2^s, and base = lower_bound(f, j0) = K[j0].  Slot
 // records pack base (bits 0..23) and the offsets f_i - j0 of the (at most
@@ -337,12 +338,17 @@ __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, i
                                   const uint32_t* __restrict__ zdesc, uint32_t nz, uint2* __restrict__ R,
                                   uint64_t nrec) {
   for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nrec; g += (uint64_t)gridDim.x * blockDim.x) {
+    // zone z's first record = ((int)desc >> 5) + (z << (zs - s))
+    auto first = [&](uint32_t k) {
+      const uint32_t dk = __ldg(zdesc + k);
+      return (uint64_t)((int64_t)((int32_t)dk >> 5) + ((int64_t)k << (zs - (int)(dk & 15u))));
+    };
     uint32_t z = 0;
     for (uint32_t k = 1; k < nz; ++k)
-      if ((uint64_t)(__ldg(zdesc + k) >> 5) <= g) z = k;
+      if (first(k) <= g) z = k;
     const uint32_t d = __ldg(zdesc + z);
     const int s = (int)(d & 15u);
-    const uint64_t j0 = ((uint64_t)z << zs) + ((g - (d >> 5)) << s);
+    const uint64_t j0 = ((uint64_t)z << zs) + ((g - first(z)) << s);
     const uint64_t j1 = j0 + (1ull << s);
     const uint64_t lo = bound_search<false>(f, 0, n1, j0);
     if (d & kZonedRankFlag) {

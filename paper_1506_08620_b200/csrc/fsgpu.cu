@@ -1269,7 +1269,10 @@ bool zone_plan(const std::vector<uint64_t>& f, uint64_t r, int zs, std::vector<u
     const bool rank = s < 0;
     if (rank) s = kZonedRankShift;
     if (nrec >= (1ull << 27)) return false;
-    desc[z] = (uint32_t)(nrec << 5) | (rank ? kZonedRankFlag : 0u) | (uint32_t)s;
+    // first record relative to the zone's start in records (may be negative):
+    // the probe's record index is then (int)d >> 5 plus j >> s, no zone mask
+    const int64_t rel = (int64_t)nrec - (int64_t)(z << (zs - s));
+    desc[z] = ((uint32_t)rel << 5) | (rank ? kZonedRankFlag : 0u) | (uint32_t)s;
     nrec += (zb + (1ull << s) - 1) >> s;
   }
   return nrec < (1ull << 27);

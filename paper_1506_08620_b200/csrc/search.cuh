@@ -669,8 +669,9 @@ struct HotRankProbe {
 //                 s <= 11, never more than three knots (no overflow path);
 //   rank records  {32-bit knot mask, base} per 32 buckets.
 // Zone descriptor (u32, nz <= 64 of them at the table head, so a warp's
-// descriptor loads cost at most two wavefronts): first record << 5 |
-// rank << 4 | s.  K[j] = base + #{knots of the record below j} exactly, and
+// descriptor loads cost at most two wavefronts): (first record - (z <<
+// (zs - s))) << 5 | rank << 4 | s, so record index = ((int)d >> 5) + (j >> s).
+// K[j] = base + #{knots of the record below j} exactly, and
 // bucket j holds knot K[j] iff its offset / mask bit says so; X is read only
 // then, from the window or through L2.  Identical answers to
 // DirectProbe<GAP=1> (batch.py:315-317).
@@ -715,8 +716,9 @@ struct ZonedProbe {
   }
   __device__ __forceinline__ uint2 rec(uint32_t j, uint32_t d) const {
     uint2 g;
-    const uint32_t a = rc + 8u * ((d >> 5) + ((j & zmask) >> (d & 15u)));
-    FSG_BOUND((d >> 5) + ((j & zmask) >> (d & 15u)) < nrec && a + 8u - xs <= dyn_smem_bytes());
+    const uint32_t idx = (uint32_t)((int32_t)d >> 5) + (j >> (d & 15u));  // descriptors are zone-relative
+    const uint32_t a = rc + 8u * idx;
+    FSG_BOUND(idx < nrec && a + 8u - xs <= dyn_smem_bytes());
     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(g.x), "=r"(g.y) : "r"(a));
     return g;
   }
@@ -725,11 +727,16 @@ struct ZonedProbe {
   // is half dense, half sparse), and a divergent branch would issue both
   // decodes plus its reconvergence overhead anyway.
   static __device__ __forceinline__ void resolve(const uint2& g, uint32_t d, uint32_t j, uint32_t& t, bool& knot) {
-    const uint32_t jl = j & ((1u << (d & 15u)) - 1u);
-    // rank view: {mask, base} (jl < 32 in rank zones)
-    const uint32_t jr = jl & 31u;
-    const uint32_t tr = g.y + __popc(g.x & ((1u << jr) - 1u));
-    const uint32_t kr = (g.x >> jr) & 1u;
+    uint32_t smask;  // the low s bits (bmsk: one instruction)
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(smask) : "r"(d & 15u));
+    const uint32_t jl = j & smask;
+    // rank view: {mask, base} (jl < 32 in rank zones; in slot zones the view
+    // is discarded, and PTX clamps the counts >= 32, so no mask of jl)
+    uint32_t below, kr;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(jl));
+    asm("shr.b32 %0, %1, %2;" : "=r"(kr) : "r"(g.x), "r"(jl));
+    const uint32_t tr = g.y + __popc(g.x & below);
+    kr &= 1u;
     // slot view: 64-bit SWAR over the three fields 0x1000 | offset at bits
     // 25 + 13k (guard bits 37, 50, 63 survive iff offset >= jl)
     const uint32_t ylo = jl << 25, yhi = jl * 0x80040u + (jl >> 7);

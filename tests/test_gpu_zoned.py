@@ -45,7 +45,8 @@ def expected_zoned(xs, h, r, zs):
         if rank:
             s = RANK_SHIFT
         n = (zb + (1 << s) - 1) >> s
-        desc.append((nrec << 5) | (RANK_FLAG if rank else 0) | s)
+        rel = nrec - (z << (zs - s))  # zone-relative first record (signed 27 bits)
+        desc.append(((rel << 5) & 0xFFFFFFFF) | (RANK_FLAG if rank else 0) | s)
         j0 = zlo + (np.arange(n, dtype=np.int64) << s)
         lo = np.searchsorted(f, j0, side="left")
         hi = np.searchsorted(f, j0 + (1 << s), side="left")
