@@ -571,15 +571,33 @@ struct SparseRecProbe {
         j[q] = bucket(z[g0 + q]);
         g[q] = G[j[q] >> s];
       }
+      if constexpr (XS) {
 #pragma unroll
-      for (int q = 0; q < GR; ++q) {
-        if (g0 + q >= N) break;
-        uint32_t t;
-        bool knot;
-        resolve(g[q], j[q], t, knot);
-        T xv = z[g0 + q];
-        if (knot) xv = xat<sizeof(R) == 4>(t);
-        o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
+        for (int q = 0; q < GR; ++q) {
+          if (g0 + q >= N) break;
+          uint32_t t;
+          bool knot;
+          resolve(g[q], j[q], t, knot);
+          T xv = z[g0 + q];
+          if (knot) xv = xat<sizeof(R) == 4>(t);
+          o[g0 + q] = (R)((int64_t)t - ((!knot || z[g0 + q] < xv) ? 1 : 0));
+        }
+      } else {  // X through L2: every X gather of the group in flight before the first is used
+        uint32_t t[GR];
+        bool knot[GR];
+        T xv[GR];
+#pragma unroll
+        for (int q = 0; q < GR; ++q) {
+          if (g0 + q >= N) break;
+          resolve(g[q], j[q], t[q], knot[q]);
+          xv[q] = z[g0 + q];
+          if (knot[q]) xv[q] = xat(t[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < GR; ++q) {
+          if (g0 + q >= N) break;
+          o[g0 + q] = (R)((int64_t)t[q] - ((!knot[q] || z[g0 + q] < xv[q]) ? 1 : 0));
+        }
       }
     }
   }
