@@ -105,6 +105,8 @@ def run_throughput(sizes, precision, algorithms, queries, seed, reps, *, min_tim
     unknown = [a for a in algorithms if a not in batch.ALGORITHMS]
     if unknown:
         raise ValueError(f"unknown algorithm(s) {unknown}; pick from {batch.ALGORITHMS}")
+    if reps < 1 or queries < 1 or min_time < 0:
+        raise ValueError("repetitions and queries must be >= 1, min_time >= 0")
     rows, skipped = [], []
     for size in sizes:
         p = gen_uniform_gap_partition(size, gap_lo, gap_hi, seed, precision)

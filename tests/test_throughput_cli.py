@@ -19,7 +19,8 @@ def _run(*args):
 
 
 def test_usage_errors_exit_1():
-    for bad in (["--sizes", "a,b"], ["--precision", "half"], ["--format", "xml"], ["--out-bytes", "2"]):
+    for bad in (["--sizes", "a,b"], ["--precision", "half"], ["--format", "xml"], ["--out-bytes", "2"],
+                ["--reps", "0"], ["--queries", "0"], ["--algos", "direct,nope"]):
         r = _run(*bad)
         assert r.returncode == 1, (bad, r.stderr)
         assert "usage" in r.stderr
@@ -65,3 +66,16 @@ def test_infeasible_only_exit_2(cuda):
              "--gap-hi", "1", "--queries", "1024", "--reps", "1")
     assert r.returncode == 2, r.stderr
     assert r.stderr.count("skipped direct") == 2 and "Overflow" in r.stderr
+
+
+@pytest.mark.gpu
+def test_infeasible_recorded_not_fatal(cuda):
+    """A sweep where the direct index is infeasible for one size keeps the
+    other sizes and algorithms (the reference's harness behaviour)."""
+    from paper_1506_08620_b200 import throughput
+
+    rows, skipped = throughput.run_throughput([255, 1_000_000], "double", ["direct", "bitset2"], 1 << 16, 42, 1,
+                                              min_time=0.0, gap_lo=1e-9, gap_hi=1.0)
+    assert ("direct", 1_000_000) in {(a, s) for a, s, _ in skipped}
+    got = {(r["algorithm"], r["size"]) for r in rows}
+    assert ("bitset2", 1_000_000) in got and ("direct", 255) in got and ("bitset2", 255) in got
