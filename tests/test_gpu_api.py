@@ -416,7 +416,7 @@ def test_gap2_rank_directory(cuda, name, kw):
 
 
 def test_concurrent_big_tables_prepare_then_search(cuda):
-    """Soak: four threads on one stream each repeatedly build a large index
+    """Soak: five threads on one stream each repeatedly build a large index
     (sparse table, rank directory, subtree records, gap-2 directory) and
     search immediately through the device, pageable and pinned paths, while
     the others' builds are still queued -- the pattern behind the upload
@@ -429,7 +429,8 @@ def test_concurrent_big_tables_prepare_then_search(cuda):
     from paper_1506_08620_b200 import workloads
 
     specs = [("cfg5", {"n1": 32_769}, "direct"), ("cfg5", {"n1": 1025}, "direct"),
-             ("cfg4", {}, "direct-gap2"), ("cfg5", {"n1": 1_048_577, "filtered": False}, "bitset2")]
+             ("cfg4", {}, "direct-gap2"), ("cfg5", {"n1": 1_048_577, "filtered": False}, "bitset2"),
+             ("cfg4", {}, "direct")]  # zoned records
     errors = []
 
     def work(k):
