@@ -75,10 +75,23 @@ def lib_sha16() -> str | None:
     return hashlib.sha256(lib.read_bytes()).hexdigest()[:16] if lib.exists() else None
 
 
+def src_sha16() -> str | None:
+    """Source hash the LOADED library was built from (fs_version's last field;
+    nvcc output is not byte-reproducible, so builds are identified by this)."""
+    try:
+        from paper_1506_08620_b200 import _lib
+
+        v = _lib.load().fs_version().decode().split()
+        return v[-1] if len(v) >= 2 and v[-2] == "src" else None
+    except Exception:
+        return None
+
+
 def ncu_traffic(name: str) -> dict | None:
     """DRAM bytes per launch (and L2 sectors per query) of a config's search
     kernel from the committed ncu capture profiles/traffic/<name>.json, with
-    whether that capture was taken of this very build (lib_sha16)."""
+    whether that capture was taken of a build of these very sources
+    (src_sha16: the hash the loaded library embeds)."""
     p = ROOT / "profiles" / "traffic" / f"{name}.json"
     if not p.exists():
         return None
@@ -87,7 +100,7 @@ def ncu_traffic(name: str) -> dict | None:
     except Exception:
         return None
     d["profile"] = str(p.relative_to(ROOT))
-    d["same_build"] = d.get("lib_sha16") == lib_sha16()
+    d["same_build"] = d.get("src_sha16") is not None and d.get("src_sha16") == src_sha16()
     return d
 
 
@@ -629,7 +642,7 @@ def main():
                 "l2": "inputs 4 GiB + outputs 4 GiB >> 126 MB L2; no flush needed",
                 "parallelism": f"query shards x{world} of one global stream, X/J replicated (built locally)",
                 "verified": verified,
-                "lib_sha16": lib_sha16(),
+                "lib_sha16": lib_sha16(), "src_sha16": src_sha16(),
             },
             "kernel_only": {
                 "value": m / kstep,
@@ -644,7 +657,7 @@ def main():
                 "frac": achieved / pk["hbm_gbs"],
                 "traffic": (traffic or {}).get("dram_bytes_per_launch") if world == 1 else None,
                 "traffic_source": None if not traffic else {
-                    k: traffic.get(k) for k in ("profile", "kernel", "lib_sha16", "same_build", "queries")},
+                    k: traffic.get(k) for k in ("profile", "kernel", "src_sha16", "same_build", "queries")},
                 "peak_source": pk["source"],
                 "frac_of_spec": achieved / SPEC_HBM_GBS,  # the ~8 TB/s nominal peak the north star cites
                 "algorithmic_bytes_per_query": BYTES_PER_QUERY,

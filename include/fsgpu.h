@@ -142,7 +142,8 @@ typedef struct fs_plan {
                            (fs_build_sparse_rec)                                  */
 } fs_plan;
 
-/* Library identification. */
+/* Library identification: "fsgpu <version> (sm_100a) src <16 hex>", the last
+   field hashing the sources and nvcc flags the library was built from. */
 const char* fs_version(void);
 /* Message for the last FS_CUDA_ERROR / FS_INVALID_ARG on this thread. */
 const char* fs_last_error(void);

@@ -923,7 +923,10 @@ int certify_impl(const T* x, uint64_t n1, int qbits, int q, CertStatus* st, T* h
 // ===========================================================================
 extern "C" {
 
-const char* fs_version(void) { return "fsgpu 0.1.0 (sm_100a)"; }
+#ifndef FSG_SRC_SHA16
+#define FSG_SRC_SHA16 "unknown"
+#endif
+const char* fs_version(void) { return "fsgpu 0.1.0 (sm_100a) src " FSG_SRC_SHA16; }
 
 const char* fs_last_error(void) { return g_last_error.c_str(); }
 

@@ -40,6 +40,13 @@ def test_version_and_workspace():
     assert lib.fs_workspace_bytes() >= 64
 
 
+def test_library_built_from_these_sources():
+    # fs_version() embeds the hash of the sources + nvcc flags it was built from
+    import __graft_entry__ as g
+
+    assert _lib.load().fs_version().decode().split()[-2:] == ["src", g.source_sha16()]
+
+
 def test_library_is_sm100a_code():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out

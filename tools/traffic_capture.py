@@ -9,8 +9,9 @@
 knots, the same seeded global query stream, direct through
 prepare_with_fallback, or bitset2) and launches the search 4 times; ncu
 captures the 4th (--launch-skip 3 --launch-count 1).  The JSON records the
-library build (lib_sha16) so bench.py can say whether the capture is of the
-build it runs.
+library build (src_sha16, the source hash fs_version() embeds; lib_sha16 of
+the binary for information) so bench.py can say whether the capture is of a
+build of the sources it runs.
 """
 
 import csv
@@ -85,6 +86,7 @@ def collect(label, algo, csv_path):
         "l2_sectors_per_query": v["lts__t_sectors_srcunit_tex_op_read.sum"] / m,
         "l1tex_pct": v["l1tex__throughput.avg.pct_of_peak_sustained_active"],
         "lib_sha16": hashlib.sha256(lib.read_bytes()).hexdigest()[:16],
+        "src_sha16": bench.src_sha16(),
         "how": "ncu --metrics " + ",".join(METRICS) + " --clock-control none (cold caches, serialised), "
                "4th launch of tools/traffic_capture.py run",
     }
