@@ -62,6 +62,8 @@ def _num(text):
 
 
 def collect(label, algo, csv_path):
+    import bench
+
     _, _, _, m = _row(label)
     rows = [r for r in csv.reader(open(csv_path)) if r]
     hdr = next(i for i, r in enumerate(rows) if "Metric Name" in r)
