@@ -85,7 +85,8 @@ enum {
   FS_SPARSE_RECORDS8 = 2,  /* 8-B group records, two offsets (| F): fs_build_sparse_rec  */
   FS_SPARSE_RECORDS12 = 3, /* 16-B group records, eight 12-bit offsets (shift <= 10)      */
   FS_SPARSE_RECORDS8X3 = 4,/* 8-B group records, three 13-bit offsets (shift <= 11, N+1 <= 2^24) */
-  FS_SPARSE_ZONED = 5      /* zone descriptors | 8-B records, per-zone form: fs_build_zoned  */
+  FS_SPARSE_ZONED = 5,     /* zone descriptors | 8-B records, per-zone form: fs_build_zoned  */
+  FS_SPARSE_ZONED_RANK = 6 /* zone descriptors | 8-B striped rank words: fs_build_zoned_rank */
 };
 
 /*
@@ -317,6 +318,39 @@ int fs_plan_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
                   uint64_t* t0_out, uint64_t* nt_out, void* stream);
 int fs_build_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t zs,
                    uint64_t* f_scratch_dev, void* buf_dev, void* stream);
+
+/*
+ * Striped rank words of the gap-1 table (FS_SPARSE_ZONED_RANK; a device
+ * layout of K, no reference counterpart).  The same zones as above, every
+ * zone in 8-B rank words {mask, K[j0]} whose 32 mask bits each stand for a
+ * stripe of 2^k buckets (a word covers 2^(k+5) buckets from j0), k per zone
+ * (0..10) and never so large that a stripe holds two knots.  For bucket j
+ * of the query z, b = (j >> k) & 31 and t = K[j0] + popc(mask below bit b):
+ * the knots of earlier stripes lie below z and those of later stripes above
+ * it (the bucket function of direct.py:194-197 is monotone), so the answer of
+ * batch.py:315-317 is t - 1 when bit b is clear and t - (z < X[t]) when it is
+ * set -- X is read whenever the query's stripe holds a knot, from the staged
+ * window X[t0, t0 + nt) or L2.  The decode is a mask and a popcount; tables
+ * with smoothly varying gaps (cfg4's geometric knots) fit in shared memory
+ * with stripes of a few buckets.
+ * Buffer: nz u32 descriptors ((first word - (z << (zs - k - 5))) << 5, as a
+ * signed 27-bit value | 16 | k), padded to a multiple of four, then the words.
+ *   fs_plan_zoned_rank: zs, words, table bytes and the window of X for
+ *     budget_bytes (an eighth of it is kept for the window; the stripes are
+ *     refined, densest zone first, while the words fit the rest), plus the
+ *     share of the buckets lying in knot-holding stripes in parts per million
+ *     (uniform queries that read X).  FS_TOO_LARGE if nothing fits.  SYNC.
+ *   fs_build_zoned_rank: fill the buffer for (zs, nrec) as planned;
+ *     FS_INVALID_ARG if no plan of that zone shift has nrec words.  SYNC.
+ * Set fs_plan.sparse to the buffer, sparse_format = FS_SPARSE_ZONED_RANK,
+ * sparse_shift = zs, sparse_ndense = nrec, hot_knot0 = t0, hot_knots = nt
+ * (hot_words = 0).  Bytes: fs_zoned_bytes.  f_scratch_dev: n1 uint64.
+ */
+int fs_plan_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                       uint64_t* f_scratch_dev, int32_t* zs_out, uint64_t* nrec_out, uint64_t* bytes_out,
+                       uint64_t* t0_out, uint64_t* nt_out, uint64_t* xread_ppm_out, void* stream);
+int fs_build_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t zs,
+                        uint64_t nrec, uint64_t* f_scratch_dev, void* buf_dev, void* stream);
 
 /*
  * Hot window of a rank directory for shared-memory staging: among all

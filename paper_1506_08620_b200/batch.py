@@ -308,7 +308,7 @@ class PreparedKernel:
             "smem_sparse": bool(f & _lib.PLACE_SMEM_SPARSE),
             "sparse_format": {_lib.SPARSE_RECORDS: "records", _lib.SPARSE_RECORDS8: "records8",
                               _lib.SPARSE_RECORDS12: "records12", _lib.SPARSE_RECORDS8X3: "records8x3",
-                              _lib.SPARSE_ZONED: "zoned"}.get(
+                              _lib.SPARSE_ZONED: "zoned", _lib.SPARSE_ZONED_RANK: "zoned-rank"}.get(
                 self.plan.sparse_format, "two-level") if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
         }
@@ -474,6 +474,12 @@ HOT_WINDOW_MIN_DENSITY_RATIO = 4.0
 #: -- 449 vs 242 on its uniform half, 438 vs 510 on its clustered half
 #: (profiles/r02/zoned_cfg4.txt)
 ZONED = True
+#: striped rank words (fs_build_zoned_rank: every zone in {mask, base} words
+#: whose bits stand for 2^k-bucket stripes) are tried before the mixed
+#: slot/rank records, and used when at most this share (ppm) of the buckets
+#: lies in knot-holding stripes -- the uniform queries that read X.  False /
+#: 0 skips them.
+ZONED_RANK_MAX_XREAD_PPM = 150_000
 
 
 def _smem_budget() -> int:
@@ -523,6 +529,26 @@ def _set_zoned(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:
     x = p.device_values()
     f = _device.empty(n1, np.uint64)
     zs, nrec, nbytes, t0, nt = ctypes.c_int32(-1), *(ctypes.c_uint64(0) for _ in range(4))
+    if ZONED_RANK_MAX_XREAD_PPM:
+        ppm = ctypes.c_uint64(0)
+        rc = lib.fs_plan_zoned_rank(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, f.data_ptr(), ctypes.byref(zs),
+                                    ctypes.byref(nrec), ctypes.byref(nbytes), ctypes.byref(t0), ctypes.byref(nt),
+                                    ctypes.byref(ppm), _device.stream_ptr())
+        if rc != _lib.FS_TOO_LARGE:
+            _lib.check(rc, what="fs_plan_zoned_rank")
+        if rc == _lib.FS_OK and ppm.value <= ZONED_RANK_MAX_XREAD_PPM:
+            buf = _device.empty(int(nbytes.value), np.uint8)
+            rc = lib.fs_build_zoned_rank(dt, x.data_ptr(), n1, float(idx.h), idx.r, zs.value, nrec.value,
+                                         f.data_ptr(), buf.data_ptr(), _device.stream_ptr())
+            _lib.check(rc, what="fs_build_zoned_rank")
+            plan.sparse = buf.data_ptr()
+            plan.sparse_format = _lib.SPARSE_ZONED_RANK
+            plan.sparse_shift = zs.value
+            plan.sparse_ndense = nrec.value
+            plan.hot_word0, plan.hot_words = 0, 0
+            plan.hot_knot0, plan.hot_knots = t0.value, nt.value
+            keep.append(buf)
+            return
     rc = lib.fs_plan_zoned(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, f.data_ptr(), ctypes.byref(zs),
                            ctypes.byref(nrec), ctypes.byref(nbytes), ctypes.byref(t0), ctypes.byref(nt),
                            _device.stream_ptr())

@@ -333,7 +333,11 @@ __global__ void fill_sparse_rec_kernel(const uint64_t* __restrict__ f, uint64_t 
 // records pack base (bits 0..23) and the offsets f_i - j0 of the (at most
 // three, by the planner's choice of s) knots in range as 0x1000 | offset at
 // bits 25 + 13k, unused 0x1FFF; rank records are {mask of the 32 buckets
-// holding a knot, base}.
+// holding a knot, base}.  STRIPED (fs_build_zoned_rank): every zone in rank
+// records whose descriptor holds the stripe shift k instead of s; a record
+// covers 2^(k+5) buckets and mask bit b is set iff a knot falls in buckets
+// [j0 + b 2^k, j0 + (b+1) 2^k) (at most one does, by the planner's k).
+template <bool STRIPED>
 __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, int zs,
                                   const uint32_t* __restrict__ zdesc, uint32_t nz, uint2* __restrict__ R,
                                   uint64_t nrec) {
@@ -341,13 +345,14 @@ __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, i
     // zone z's first record = ((int)desc >> 5) + (z << (zs - s))
     auto first = [&](uint32_t k) {
       const uint32_t dk = __ldg(zdesc + k);
-      return (uint64_t)((int64_t)((int32_t)dk >> 5) + ((int64_t)k << (zs - (int)(dk & 15u))));
+      return (uint64_t)((int64_t)((int32_t)dk >> 5) + ((int64_t)k << (zs - (int)(dk & 15u) - (STRIPED ? kZonedRankShift : 0))));
     };
     uint32_t z = 0;
     for (uint32_t k = 1; k < nz; ++k)
       if (first(k) <= g) z = k;
     const uint32_t d = __ldg(zdesc + z);
-    const int s = (int)(d & 15u);
+    const int kst = STRIPED ? (int)(d & 15u) : 0;  // stripe shift
+    const int s = (int)(d & 15u) + (STRIPED ? kZonedRankShift : 0);
     const uint64_t j0 = ((uint64_t)z << zs) + ((g - first(z)) << s);
     const uint64_t j1 = j0 + (1ull << s);
     const uint64_t lo = bound_search<false>(f, 0, n1, j0);
@@ -356,7 +361,7 @@ __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, i
       for (uint64_t k = lo; k < n1; ++k) {
         const uint64_t fi = __ldg(f + k);
         if (fi >= j1) break;
-        m |= 1u << (fi - j0);
+        m |= 1u << ((fi - j0) >> kst);
       }
       R[g] = make_uint2(m, (uint32_t)lo);
     } else {

@@ -52,6 +52,7 @@ constexpr int kZonedMaxShift = kRec3MaxShift;
 constexpr int kZonedMinZoneShift = kRec3MaxShift;
 constexpr int kZonedRankShift = 5;
 constexpr uint32_t kZonedRankFlag = 16u;
+constexpr int kZonedMaxStripe = 10;  // striped rank words: a mask bit per 2^k buckets, k <= 10
 
 // Bounds-checked builds (FSG_BOUNDS_CHECK=1, tools/bounds_check.sh): every
 // table gather of the search probes checks its index against the table's

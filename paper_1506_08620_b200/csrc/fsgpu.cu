@@ -146,6 +146,8 @@ struct Placement {
   bool b2_shadow = false;  // bitset2 f64: f32 shadow keys + exact plane staged
 };
 
+inline bool is_zoned(int32_t format) { return format == FS_SPARSE_ZONED || format == FS_SPARSE_ZONED_RANK; }
+
 int validate_plan(const fs_plan* p) {
   if (!p) return fail(FS_INVALID_ARG, "plan is NULL");
   if (p->dtype != FS_F32 && p->dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
@@ -167,18 +169,19 @@ int validate_plan(const fs_plan* p) {
         return fail(FS_INVALID_ARG, "hot window outside the rank directory / knots");
       if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS &&
                         p->sparse_format != FS_SPARSE_RECORDS8 && p->sparse_format != FS_SPARSE_RECORDS12 &&
-                        p->sparse_format != FS_SPARSE_RECORDS8X3 && p->sparse_format != FS_SPARSE_ZONED))
+                        p->sparse_format != FS_SPARSE_RECORDS8X3 && p->sparse_format != FS_SPARSE_ZONED &&
+                        p->sparse_format != FS_SPARSE_ZONED_RANK))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
-      if (p->sparse && p->sparse_format == FS_SPARSE_ZONED) {
+      if (p->sparse && is_zoned(p->sparse_format)) {
         if (fs_zoned_bytes(p->r, p->sparse_shift, p->sparse_ndense) == 0 || p->r >= (1ull << 32) ||
-            p->n1 > (1ull << 24))
+            (p->sparse_format == FS_SPARSE_ZONED && p->n1 > (1ull << 24)))
           return fail(FS_INVALID_ARG, "zoned table parameters out of range");
         if (p->hot_knot0 > p->n1 || p->hot_knots > p->n1 - p->hot_knot0)
           return fail(FS_INVALID_ARG, "knot window outside the knots");
       }
       if (p->sparse && p->sparse_format == FS_SPARSE_RECORDS8X3 && p->n1 > (1ull << 24))
         return fail(FS_INVALID_ARG, "3-offset records need N+1 <= 2^24");
-      if (p->sparse && p->sparse_format != FS_SPARSE_ZONED && (p->sparse_shift < 5 ||
+      if (p->sparse && !is_zoned(p->sparse_format) && (p->sparse_shift < 5 ||
                         p->sparse_shift > (p->sparse_format == FS_SPARSE_TWO_LEVEL    ? 16
                                            : p->sparse_format == FS_SPARSE_RECORDS12 ? kRec12MaxShift
                                            : p->sparse_format == FS_SPARSE_RECORDS8X3 ? kRec3MaxShift
@@ -232,7 +235,7 @@ Placement place(const fs_plan* p) {
   const bool use_dir = use_rank || use_rank2 || use_count;
   // zoned records + a window of X (prepare sets them only when the rank
   // directory cannot be staged)
-  if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->sparse_format == FS_SPARSE_ZONED && p->q == 1 &&
+  if (p->algorithm == FS_ALGO_DIRECT && p->sparse && is_zoned(p->sparse_format) && p->q == 1 &&
       !force_global && p->r < (1ull << 32)) {
     const uint64_t tb = fs_zoned_bytes(p->r, p->sparse_shift, p->sparse_ndense);
     const uint64_t xb = p->hot_knots * es;
@@ -259,7 +262,7 @@ Placement place(const fs_plan* p) {
     }
   }
   // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
-  if (p->algorithm == FS_ALGO_DIRECT && p->sparse && p->sparse_format != FS_SPARSE_ZONED && p->q == 1 &&
+  if (p->algorithm == FS_ALGO_DIRECT && p->sparse && !is_zoned(p->sparse_format) && p->q == 1 &&
       !force_global && p->r < (1ull << 32) && p->sparse_shift >= 5 && p->sparse_shift <= 16) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
@@ -517,8 +520,8 @@ struct UnrollVW8For<HotRankProbe<float>> {
 #ifndef FSG_UNROLL_VW8_ZONED
 #define FSG_UNROLL_VW8_ZONED 1  // one 8-query group per thread (2: cfg4 465 -> 448 Gq/s)
 #endif
-template <>
-struct UnrollVW8For<ZonedProbe<float>> {
+template <bool STRIPED>
+struct UnrollVW8For<ZonedProbe<float, STRIPED>> {
   static constexpr int value = FSG_UNROLL_VW8_ZONED;
 };
 template <bool TOP, bool DEEP>
@@ -597,8 +600,8 @@ struct BoundedFor<T, Bitset2Probe<T, true, DEEP, SHADOW>, OutT> {
 #ifndef FSG_ZONED_BOUNDED
 #define FSG_ZONED_BOUNDED 1
 #endif
-template <typename T, typename OutT>
-struct BoundedFor<T, ZonedProbe<T>, OutT> {
+template <typename T, bool STRIPED, typename OutT>
+struct BoundedFor<T, ZonedProbe<T, STRIPED>, OutT> {
   static constexpr bool value = FSG_ZONED_BOUNDED;
 };
 template <typename T, int SLOTS, bool XS, bool OVF, typename OutT>
@@ -790,6 +793,8 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
     case FS_ALGO_DIRECT:
       if (pl.records) return launch_probe<T, OutT, CacheProbe<T, uint32_t, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.hot) return launch_probe<T, OutT, HotRankProbe<T>>(d, pl, z, m, out, fb, base, st);
+      if (pl.zoned && p->sparse_format == FS_SPARSE_ZONED_RANK)
+        return launch_probe<T, OutT, ZonedProbe<T, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.zoned) return launch_probe<T, OutT, ZonedProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS)
         return dispatch_records<T, OutT, 6>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
@@ -1281,6 +1286,75 @@ bool zone_plan(const std::vector<uint64_t>& f, uint64_t r, int zs, std::vector<u
   return nrec < (1ull << 27);
 }
 
+
+// Striped rank words (FS_SPARSE_ZONED_RANK): per zone the stripe shift k (a
+// mask bit per 2^k buckets, a word per 2^(k+5)).  kmax(zone) is the largest
+// k <= min(kZonedMaxStripe, zs - 5) whose stripes hold at most one knot each:
+// consecutive knot buckets a < b of a zone share a 2^k stripe iff k exceeds
+// the highest bit in which they differ.  Starting from kmax everywhere (the
+// smallest table), stripes are then refined while the table stays within
+// `table_budget` bytes: each step halves the stripes of the zone that has the
+// most buckets inside knot-holding stripes (cnt << k: the uniform queries that
+// must read X), if that still fits, else the next such zone.  Deterministic
+// in (f, r, zs, table_budget); re-running it with the budget set to its own
+// result's size reproduces the plan (fs_build_zoned_rank does).
+bool zone_plan_rank(const std::vector<uint64_t>& f, uint64_t r, int zs, uint64_t table_budget,
+                    std::vector<uint32_t>& desc, uint64_t& nrec, uint64_t* xread_buckets) {
+  if (zs < kZonedMinZoneShift || zs > 31) return false;
+  const uint64_t nz = (r >> zs) + 1;
+  if (nz > kZonedMaxZones) return false;
+  const int kcap = std::min(kZonedMaxStripe, zs - kZonedRankShift);
+  std::vector<int> k(nz, kcap);
+  std::vector<uint64_t> cnt(nz, 0), zb(nz);
+  for (uint64_t z = 0; z < nz; ++z) zb[z] = std::min<uint64_t>(1ull << zs, r + 1 - (z << zs));
+  for (size_t i = 0; i < f.size(); ++i) {
+    const uint64_t z = f[i] >> zs;
+    if (z >= nz) return false;
+    ++cnt[z];
+    if (i + 1 < f.size() && (f[i + 1] >> zs) == z) {
+      if (f[i + 1] <= f[i]) return false;  // not a gap-1 table
+      const int hb = 63 - __builtin_clzll(f[i] ^ f[i + 1]);
+      k[z] = std::min(k[z], hb);
+    }
+  }
+  auto words = [&](uint64_t z, int kz) { return (zb[z] + (1ull << (kz + kZonedRankShift)) - 1) >> (kz + kZonedRankShift); };
+  uint64_t total = 0;
+  for (uint64_t z = 0; z < nz; ++z) total += words(z, k[z]);
+  const uint64_t head = 4 * ((nz + 3) & ~3ull);
+  if (head + 8 * total > table_budget || total >= (1ull << 27)) return false;
+  for (;;) {
+    // zones by descending cnt << k (ties: lower zone first)
+    int64_t pick = -1;
+    std::vector<uint64_t> order;
+    for (uint64_t z = 0; z < nz; ++z)
+      if (k[z] > 0 && cnt[z] > 0) order.push_back(z);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint64_t a, uint64_t b) { return (cnt[a] << k[a]) > (cnt[b] << k[b]); });
+    for (uint64_t z : order) {
+      const uint64_t t2 = total - words(z, k[z]) + words(z, k[z] - 1);
+      if (head + 8 * t2 <= table_budget && t2 < (1ull << 27)) {
+        pick = (int64_t)z;
+        total = t2;
+        break;
+      }
+    }
+    if (pick < 0) break;
+    --k[pick];
+  }
+  desc.assign(nz, 0);
+  nrec = 0;
+  uint64_t xr = 0;
+  for (uint64_t z = 0; z < nz; ++z) {
+    const int s = k[z] + kZonedRankShift;
+    const int64_t rel = (int64_t)nrec - (int64_t)(z << (zs - s));
+    desc[z] = ((uint32_t)rel << 5) | kZonedRankFlag | (uint32_t)k[z];
+    nrec += words(z, k[z]);
+    xr += std::min<uint64_t>(cnt[z] << k[z], zb[z]);
+  }
+  if (xread_buckets) *xread_buckets = xr;
+  return true;
+}
+
 // knot buckets f_i (sorted) computed on the device, read back for the planner
 int zoned_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t* f_scratch_dev,
                        std::vector<uint64_t>& f, cudaStream_t s) {
@@ -1368,8 +1442,90 @@ int fs_build_zoned(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint
   FS_CUDA(cudaMemcpyAsync(buf_dev, desc.data(), 4 * desc.size(), cudaMemcpyHostToDevice, s));
   if (n1 > (1ull << 24)) return fail(FS_TOO_LARGE, "zoned slot records need N+1 <= 2^24");
   auto* R = reinterpret_cast<uint2*>(static_cast<char*>(buf_dev) + 4 * desc.size());
-  fill_zoned_kernel<<<grid_1d(nrec, 256), 256, 0, s>>>(f_scratch_dev, n1, zs, static_cast<const uint32_t*>(buf_dev),
-                                                       (uint32_t)nz, R, nrec);
+  fill_zoned_kernel<false><<<grid_1d(nrec, 256), 256, 0, s>>>(f_scratch_dev, n1, zs, static_cast<const uint32_t*>(buf_dev),
+                                                              (uint32_t)nz, R, nrec);
+  FS_CUDA(cudaGetLastError());
+  FS_CUDA(cudaStreamSynchronize(s));  // desc must outlive the async upload
+  return FS_OK;
+}
+
+int fs_plan_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                       uint64_t* f_scratch_dev, int32_t* zs_out, uint64_t* nrec_out, uint64_t* bytes_out,
+                       uint64_t* t0_out, uint64_t* nt_out, uint64_t* xread_ppm_out, void* stream) {
+  if (!x_dev || !f_scratch_dev || n1 < 2 || !zs_out) return fail(FS_INVALID_ARG, "bad arguments");
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "zoned records need R < 2^32, N < 2^31");
+  // every knot needs its own mask bit
+  if (n1 / 4 > budget_bytes) return fail(FS_TOO_LARGE, "no striped layout fits the budget");
+  std::vector<uint64_t> f;
+  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, f, as_stream(stream));
+  if (rc) return rc;
+  const uint64_t es = dtype == FS_F32 ? 4 : 8;
+  // an eighth of the budget is kept for the window of X (the densest knots);
+  // what the words leave unused goes to the window too
+  const uint64_t win = std::min<uint64_t>(align128(n1 * es), (budget_bytes / 8) & ~127ull);
+  if (budget_bytes < win + 256) return fail(FS_TOO_LARGE, "no striped layout fits the budget");
+  const uint64_t table_budget = budget_bytes - win - 128;
+  int zs32 = kZonedMinZoneShift;
+  while (zs32 < 31 && (r >> zs32) + 1 > 32) ++zs32;
+  int best = -1;
+  uint64_t best_nrec = 0, best_bytes = 0, best_xr = ~0ull;
+  // both zone counts (32: one wavefront per warp's descriptor loads; 64:
+  // finer stripes): the one whose uniform queries read X least
+  for (int zs : {zs32, zs32 - 1}) {
+    if (zs < kZonedMinZoneShift) continue;
+    std::vector<uint32_t> desc;
+    uint64_t nrec = 0, xr = 0;
+    if (!zone_plan_rank(f, r, zs, table_budget, desc, nrec, &xr)) continue;
+    if (best < 0 || xr + (r + 1) / 64 < best_xr) {  // 64 zones must save >= 1.6% of X reads
+      best = zs;
+      best_nrec = nrec;
+      best_bytes = fs_zoned_bytes(r, zs, nrec);
+      best_xr = xr;
+    }
+  }
+  if (best < 0) return fail(FS_TOO_LARGE, "no striped layout fits the budget");
+  const uint64_t room = budget_bytes - best_bytes - 128;
+  const uint64_t nt = std::min<uint64_t>(n1, room / es);
+  uint64_t t0 = 0;
+  if (nt > 0 && nt < n1) {
+    uint64_t span = ~0ull;
+    for (uint64_t a = 0; a + nt <= n1; ++a)
+      if (f[a + nt - 1] - f[a] < span) {
+        span = f[a + nt - 1] - f[a];
+        t0 = a;
+      }
+  }
+  *zs_out = best;
+  if (nrec_out) *nrec_out = best_nrec;
+  if (bytes_out) *bytes_out = best_bytes;
+  if (t0_out) *t0_out = t0;
+  if (nt_out) *nt_out = nt;
+  if (xread_ppm_out) *xread_ppm_out = (uint64_t)((long double)best_xr * 1e6L / (long double)(r + 1));
+  return FS_OK;
+}
+
+int fs_build_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t zs,
+                        uint64_t nrec, uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "zoned records need R < 2^32, N < 2^31");
+  const uint64_t bytes = fs_zoned_bytes(r, zs, nrec);
+  if (!bytes) return fail(FS_INVALID_ARG, "zone shift out of range for this table");
+  cudaStream_t s = as_stream(stream);
+  std::vector<uint64_t> f;
+  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, f, s);
+  if (rc) return rc;
+  std::vector<uint32_t> desc;
+  uint64_t got = 0;
+  if (!zone_plan_rank(f, r, zs, bytes, desc, got, nullptr) || got != nrec)
+    return fail(FS_INVALID_ARG, "no striped plan of this zone shift has that many words");
+  const uint64_t nz = desc.size();
+  desc.resize((nz + 3) & ~3ull, 0u);
+  FS_CUDA(cudaMemcpyAsync(buf_dev, desc.data(), 4 * desc.size(), cudaMemcpyHostToDevice, s));
+  auto* R = reinterpret_cast<uint2*>(static_cast<char*>(buf_dev) + 4 * desc.size());
+  fill_zoned_kernel<true><<<grid_1d(nrec, 256), 256, 0, s>>>(f_scratch_dev, n1, zs, static_cast<const uint32_t*>(buf_dev),
+                                                             (uint32_t)nz, R, nrec);
   FS_CUDA(cudaGetLastError());
   FS_CUDA(cudaStreamSynchronize(s));  // desc must outlive the async upload
   return FS_OK;

@@ -693,7 +693,19 @@ struct HotRankProbe {
 // bucket j holds knot K[j] iff its offset / mask bit says so; X is read only
 // then, from the window or through L2.  Identical answers to
 // DirectProbe<GAP=1> (batch.py:315-317).
-template <typename T>
+//
+// STRIPED (FS_SPARSE_ZONED_RANK, fs_build_zoned_rank): every zone in rank
+// words whose 32 mask bits each stand for a stripe of 2^k buckets, k per zone
+// (descriptor: zone-relative first record << 5 | rank flag | k; a word covers
+// 2^(k+5) buckets).  The planner picks k so that no stripe holds two knots.
+// With b = (j >> k) & 31: t = base + popc(mask below b) counts the knots in
+// earlier stripes, whose buckets are below j, so X_i < z for all of them
+// (the bucket function is monotone); knots in later stripes lie above z; and
+// if stripe b holds a knot it is X[t], compared directly: the answer is
+// t - (z < X[t]), else t - 1.  The same answers with a ~10-instruction decode
+// (the slot form's SWAR count and field select are gone); the price is an X
+// read whenever the query's stripe -- not its exact bucket -- holds a knot.
+template <typename T, bool STRIPED = false>
 struct ZonedProbe {
   const T* X;
   const unsigned char* xg;  // generic address of the X window
@@ -734,7 +746,8 @@ struct ZonedProbe {
   }
   __device__ __forceinline__ uint2 rec(uint32_t j, uint32_t d) const {
     uint2 g;
-    const uint32_t idx = (uint32_t)((int32_t)d >> 5) + (j >> (d & 15u));  // descriptors are zone-relative
+    // descriptors are zone-relative
+    const uint32_t idx = (uint32_t)((int32_t)d >> 5) + (STRIPED ? (j >> (d & 15u)) >> 5 : j >> (d & 15u));
     const uint32_t a = rc + 8u * idx;
     FSG_BOUND(idx < nrec && a + 8u - xs <= dyn_smem_bytes());
     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(g.x), "=r"(g.y) : "r"(a));
@@ -745,6 +758,14 @@ struct ZonedProbe {
   // is half dense, half sparse), and a divergent branch would issue both
   // decodes plus its reconvergence overhead anyway.
   static __device__ __forceinline__ void resolve(const uint2& g, uint32_t d, uint32_t j, uint32_t& t, bool& knot) {
+    if constexpr (STRIPED) {
+      const uint32_t b = (j >> (d & 15u)) & 31u;
+      uint32_t below;
+      asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(b));
+      t = g.y + __popc(g.x & below);
+      knot = (g.x >> b) & 1u;
+      return;
+    }
     uint32_t smask;  // the low s bits (bmsk: one instruction)
     asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(smask) : "r"(d & 15u));
     const uint32_t jl = j & smask;

@@ -17,6 +17,18 @@ pytestmark = pytest.mark.gpu
 MIN_SHIFT, MAX_SHIFT, SLOTS, RANK_SHIFT, RANK_FLAG = 6, 11, 3, 5, 16
 
 
+@pytest.fixture(autouse=True)
+def mixed_records_only():
+    """These tests cover the mixed slot/rank records; the striped rank words
+    that prepare() tries first (tests/test_gpu_zoned_rank.py) are switched off."""
+    from paper_1506_08620_b200 import batch
+
+    keep = batch.ZONED_RANK_MAX_XREAD_PPM
+    batch.ZONED_RANK_MAX_XREAD_PPM = 0
+    yield
+    batch.ZONED_RANK_MAX_XREAD_PPM = keep
+
+
 def _fs():
     import paper_1506_08620_b200 as fs
 

@@ -1,5 +1,5 @@
 """cfg4 diagnostics: rank-directory (L2, with its hot window), sparse+dense
-table and zoned records on the uniform and the clustered halves of the query
+table, zoned records (mixed slot/rank) and striped rank words on the uniform and the clustered halves of the query
 stream separately (tuning aid)."""
 
 import json
@@ -28,11 +28,12 @@ for k, z in streams.items():
 out = torch.empty(m, dtype=torch.int32, device="cuda")
 st = fs.new_status()
 only = sys.argv[1:]  # optional: variant stream (profiling a single case)
-for variant in ("rank-l2", "sparse-dense", "zoned"):
+for variant in ("rank-l2", "sparse-dense", "zoned", "zoned-rank"):
     if only and variant != only[0]:
         continue
     batch.SPARSE_MAX_DENSE_KNOT_FRACTION = 1.0 if variant == "sparse-dense" else 0.25
-    batch.ZONED = variant == "zoned"
+    batch.ZONED = variant.startswith("zoned")
+    batch.ZONED_RANK_MAX_XREAD_PPM = 150_000 if variant == "zoned-rank" else 0  # striped rank words / mixed records
     prep = fs.prepare("direct", p)
     for k, z in streams.items():
         if only and k != only[1]:
