@@ -428,7 +428,7 @@ def per_config(steps: int, barrier, world: int, rank: int):
             t = time_steps(lambda: prep.launch(z, out, fb), n, 3, barrier, flush) / n
             ok = fs.first_bad_of(fb) is None and verify_bracket(p, z, out)
             tt = torch.tensor([t, 0.0 if ok else 1.0], dtype=torch.float64, device=z.device)
-            if world > 1:
+            if dist.is_initialized():
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t, bad = tt.tolist()
             ent = {
@@ -481,6 +481,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=CPU_SAMPLE, help="reference arm: queries per step")
     ap.add_argument("--ref-min-time", type=float, default=0.0, help="reference arm: minimum seconds sampled")
     ap.add_argument("--plan-only", action="store_true", help="print the sharding plan (CPU, no GPU work)")
+    ap.add_argument("--dist-single", action="store_true",
+                    help="run the N>1 plumbing (NCCL group, barriers, reductions, weak leg) with one rank (tests)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -493,7 +495,8 @@ def main():
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    use_dist = world > 1 or args.dist_single
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
         def barrier():
@@ -532,7 +535,7 @@ def main():
     del z
     # weak scaling (round-1 line): every rank its own full 2^30 stream
     t_weak = None
-    if world > 1:
+    if use_dist:
         torch.cuda.empty_cache()
         zw = workloads.queries_device("cfg3", p, m, seed=1 + rank)
         ow = torch.empty(m, dtype=torch.int32, device=zw.device)
@@ -593,7 +596,7 @@ def main():
 
     times = torch.tensor([t_step, t_kern, t_bs, t_weak or 0.0, t_e2e, t_e2e_ov, t_e2e_pg], dtype=torch.float64,
                          device="cuda")
-    if world > 1:
+    if use_dist:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
         v = torch.tensor([1 if (verified and e2e_ok) else 0], device="cuda")
         dist.all_reduce(v, op=dist.ReduceOp.MIN)
@@ -704,7 +707,7 @@ def main():
             "gpu_launches": args.steps * prep.launches_per_batch(ml),
             "clocks": clocks,
         }
-        if world > 1:
+        if use_dist:
             line["weak"] = {"value": world * m / (t_weak / args.steps), "queries_per_gpu": m,
                             "ms_per_step": 1e3 * t_weak / args.steps,
                             "what": "every rank its own 2^30-query stream (weak scaling), kernel launches"}
@@ -725,7 +728,7 @@ def main():
             }
             line["config"]["cpu_sample_matches_gpu"] = bool(np.array_equal(outc, o_cpu))
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0
