@@ -476,7 +476,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--m", type=int, default=M_GLOBAL, help="global queries (sharded over the ranks)")
+    ap.add_argument("--m", "--queries", dest="m", type=int, default=M_GLOBAL, help="global queries (sharded over the ranks)")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config sweep (cfg1..cfg5)")
     ap.add_argument("--ref-sample", type=int, default=CPU_SAMPLE, help="reference arm: queries per step")
     ap.add_argument("--ref-min-time", type=float, default=0.0, help="reference arm: minimum seconds sampled")

@@ -705,7 +705,17 @@ struct HotRankProbe {
 // t - (z < X[t]), else t - 1.  The same answers with a ~10-instruction decode
 // (the slot form's SWAR count and field select are gone); the price is an X
 // read whenever the query's stripe -- not its exact bucket -- holds a knot.
-template <typename T, bool STRIPED = false>
+//
+// STRIPED == 2 (FS_SPARSE_ZONED_COUNT, fs_build_zoned_count): striped count
+// words.  A word holds 16 stripes with a 2-bit knot count each (the planner's
+// k keeps every stripe at three knots or fewer), so tables of uniformly drawn
+// knots, whose closest pairs rule out one-knot stripes of any useful width,
+// fit in shared memory too.  With b = (j >> k) & 15 and m = mask below bit
+// 2b: t = base + popc(m) + popc(m & 0xAAAAAAAA) counts the knots of earlier
+// stripes (all below z), c = (mask >> 2b) & 3 is the count of the query's
+// own stripe, whose knots X[t .. t+c-1] are compared directly (predicated
+// loads; the second and third are rare): the answer is t - 1 + #{X[t+e] <= z}.
+template <typename T, int STRIPED = 0>
 struct ZonedProbe {
   const T* X;
   const unsigned char* xg;  // generic address of the X window
@@ -747,7 +757,9 @@ struct ZonedProbe {
   __device__ __forceinline__ uint2 rec(uint32_t j, uint32_t d) const {
     uint2 g;
     // descriptors are zone-relative
-    const uint32_t idx = (uint32_t)((int32_t)d >> 5) + (STRIPED ? (j >> (d & 15u)) >> 5 : j >> (d & 15u));
+    const uint32_t idx = (uint32_t)((int32_t)d >> 5) + (STRIPED == 2   ? (j >> (d & 15u)) >> kZonedCountShift
+                                                         : STRIPED == 1 ? (j >> (d & 15u)) >> kZonedRankShift
+                                                                        : j >> (d & 15u));
     const uint32_t a = rc + 8u * idx;
     FSG_BOUND(idx < nrec && a + 8u - xs <= dyn_smem_bytes());
     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(g.x), "=r"(g.y) : "r"(a));
@@ -758,7 +770,8 @@ struct ZonedProbe {
   // is half dense, half sparse), and a divergent branch would issue both
   // decodes plus its reconvergence overhead anyway.
   static __device__ __forceinline__ void resolve(const uint2& g, uint32_t d, uint32_t j, uint32_t& t, bool& knot) {
-    if constexpr (STRIPED) {
+    static_assert(STRIPED != 2, "count words resolve through resolve_count");
+    if constexpr (STRIPED == 1) {
       const uint32_t b = (j >> (d & 15u)) & 31u;
       uint32_t below;
       asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(b));
@@ -807,14 +820,52 @@ struct ZonedProbe {
       asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.f64 %0, [%1];\n\t}" : "+d"(v) : "l"(p), "r"((uint32_t)knot));
     return v;
   }
+  // count words: knots of earlier stripes -> t, knots of the query's stripe -> c
+  static __device__ __forceinline__ void resolve_count(const uint2& g, uint32_t d, uint32_t j, uint32_t& t, uint32_t& c) {
+    const uint32_t b2 = ((j >> (d & 15u)) & 15u) * 2u;
+    uint32_t below;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(b2));
+    const uint32_t m = g.x & below;
+    t = g.y + __popc(m) + __popc(m & 0xAAAAAAAAu);
+    c = (g.x >> b2) & 3u;
+  }
+  // t - 1 + #{e < c : X[t + e] <= z}: up to three predicated loads from the
+  // staged window (when all three slots lie inside it) or global memory; a
+  // slot not loaded keeps +inf and counts nothing
+  __device__ __forceinline__ int64_t finish_count(uint32_t t, uint32_t c, T z) const {
+    const uint32_t tl = t - t0;
+    FSG_BOUND(c == 0 || t + c <= n1);
+    const T* p = (tl < nt && tl + (kZonedCountMaxKnots - 1) < nt) ? reinterpret_cast<const T*>(xg) + tl : X + t;
+    T a, b, e;
+    if constexpr (sizeof(T) == 4) {
+      a = b = e = __int_as_float(0x7f800000);
+      asm("{\n\t.reg .pred p1, p2, p3;\n\tsetp.ne.u32 p1, %4, 0;\n\tsetp.gt.u32 p2, %4, 1;\n\tsetp.gt.u32 p3, %4, 2;\n\t"
+          "@p1 ld.f32 %0, [%3];\n\t@p2 ld.f32 %1, [%3+4];\n\t@p3 ld.f32 %2, [%3+8];\n\t}"
+          : "+f"(a), "+f"(b), "+f"(e)
+          : "l"(p), "r"(c));
+    } else {
+      a = b = e = __longlong_as_double(0x7ff0000000000000ll);
+      asm("{\n\t.reg .pred p1, p2, p3;\n\tsetp.ne.u32 p1, %4, 0;\n\tsetp.gt.u32 p2, %4, 1;\n\tsetp.gt.u32 p3, %4, 2;\n\t"
+          "@p1 ld.f64 %0, [%3];\n\t@p2 ld.f64 %1, [%3+8];\n\t@p3 ld.f64 %2, [%3+16];\n\t}"
+          : "+d"(a), "+d"(b), "+d"(e)
+          : "l"(p), "r"(c));
+    }
+    return (int64_t)t - 1 + (int64_t)((uint32_t)(z >= a) + (uint32_t)(z >= b) + (uint32_t)(z >= e));
+  }
   __device__ __forceinline__ int64_t operator()(T z) const {
     const uint32_t j = bucket(z);
     const uint32_t d = desc(j);
     uint32_t t;
-    bool knot;
-    resolve(rec(j, d), d, j, t, knot);
-    const T xv = xsel(t, knot, z);
-    return (int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z < xv));
+    if constexpr (STRIPED == 2) {
+      uint32_t c;
+      resolve_count(rec(j, d), d, j, t, c);
+      return finish_count(t, c, z);
+    } else {
+      bool knot;
+      resolve(rec(j, d), d, j, t, knot);
+      const T xv = xsel(t, knot, z);
+      return (int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z < xv));
+    }
   }
   // descriptors of a group, then its records, then the resolves: every load
   // of a phase in flight before the first is consumed
@@ -843,10 +894,16 @@ struct ZonedProbe {
       for (int q = 0; q < G; ++q) {
         if (g0 + q >= N) break;
         uint32_t t;
-        bool knot;
-        resolve(g[q], d[q], j[q], t, knot);
-        const T xv = xsel(t, knot, z[g0 + q]);
-        o[g0 + q] = (R)((int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z[g0 + q] < xv)));
+        if constexpr (STRIPED == 2) {
+          uint32_t c;
+          resolve_count(g[q], d[q], j[q], t, c);
+          o[g0 + q] = (R)finish_count(t, c, z[g0 + q]);
+        } else {
+          bool knot;
+          resolve(g[q], d[q], j[q], t, knot);
+          const T xv = xsel(t, knot, z[g0 + q]);
+          o[g0 + q] = (R)((int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z[g0 + q] < xv)));
+        }
       }
     }
   }

@@ -105,7 +105,7 @@ def test_bench_under_torchrun_one_rank(cuda):
     carries the contract's keys and the verified flag."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "1", "--steps", "3", "--warmup",
-           "3", "--m", str(1 << 24), "--no-cpu-baseline", "--dist-single"]
+           "3", "--queries", str(1 << 24), "--no-cpu-baseline", "--dist-single"]
     done = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT))
     assert done.returncode == 0, done.stderr[-3000:]
     lines = [ln for ln in done.stdout.splitlines() if ln.startswith("{")]
