@@ -86,7 +86,8 @@ enum {
   FS_SPARSE_RECORDS12 = 3, /* 16-B group records, eight 12-bit offsets (shift <= 10)      */
   FS_SPARSE_RECORDS8X3 = 4,/* 8-B group records, three 13-bit offsets (shift <= 11, N+1 <= 2^24) */
   FS_SPARSE_ZONED = 5,     /* zone descriptors | 8-B records, per-zone form: fs_build_zoned  */
-  FS_SPARSE_ZONED_RANK = 6 /* zone descriptors | 8-B striped rank words: fs_build_zoned_rank */
+  FS_SPARSE_ZONED_RANK = 6,/* zone descriptors | 8-B striped rank words: fs_build_zoned_rank */
+  FS_SPARSE_COUNT = 7      /* 8-B count words, one stripe shift for the table: fs_build_count_words */
 };
 
 /*
@@ -351,6 +352,40 @@ int fs_plan_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, 
                        uint64_t* t0_out, uint64_t* nt_out, uint64_t* xread_ppm_out, void* stream);
 int fs_build_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t zs,
                         uint64_t nrec, uint64_t* f_scratch_dev, void* buf_dev, void* stream);
+
+/*
+ * Count words of the gap-1 table (FS_SPARSE_COUNT; a device layout of K, no
+ * reference counterpart) for tables of few knots and many buckets (R >> N:
+ * uniformly drawn knots, cfg2 and cfg5).  One stripe shift k for the whole
+ * table; 8-B word g = {mask, base} covers buckets [g 2^(k+4), (g+1) 2^(k+4))
+ * in 16 stripes of 2^k; bits 2b, 2b+1 of the mask hold the number of knots in
+ * stripe b (saturated at 3), base = K[g 2^(k+4)] with bit 31 set when a
+ * stripe of the word holds four or more knots.  For bucket j of the query z,
+ * b = (j >> k) & 15 and m = mask below bit 2b: t = base + popc(m) + popc(m &
+ * 0xAAAAAAAA) knots lie in earlier stripes, all below z (the bucket function
+ * of direct.py:194-197 is monotone), knots of later stripes lie above z, and
+ * the c = (mask >> 2b) & 3 knots of the query's own stripe are compared
+ * directly: the answer of batch.py:315-317 is t - 1 + #{e : X[t+e] <= z}, one
+ * predicated compare when c <= 1, a forward scan of X from t (from base for a
+ * flagged word) when c >= 2.  Exact for every k; k only sets how many queries
+ * take the scan.  Buffer: (R >> (k + 4)) + 1 words (fs_count_words_bytes).
+ *   fs_plan_count_words: the finest k whose words fit budget_bytes beside all
+ *     of X (when X takes at most half the budget: *with_x_out = 1) or alone
+ *     (0: X is read through L2), the share of buckets in knot-holding stripes
+ *     (queries that read X) and in stripes of two or more knots or flagged
+ *     words (queries that scan), both in parts per million.  FS_TOO_LARGE if
+ *     nothing fits or there are more knots than stripes.  SYNC.
+ *   fs_build_count_words: fill the words for that k.  Async.
+ * Set fs_plan.sparse to the buffer, sparse_format = FS_SPARSE_COUNT,
+ * sparse_shift = k, sparse_ndense = 0.  The search stages X beside the words
+ * when both fit.  f_scratch_dev: n1 uint64.
+ */
+uint64_t fs_count_words_bytes(uint64_t r, int32_t k);
+int fs_plan_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                        uint64_t* f_scratch_dev, int32_t* k_out, uint64_t* bytes_out, int32_t* with_x_out,
+                        uint64_t* xread_ppm_out, uint64_t* rare_ppm_out, void* stream);
+int fs_build_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t k,
+                         uint64_t* f_scratch_dev, void* buf_dev, void* stream);
 
 /*
  * Hot window of a rank directory for shared-memory staging: among all

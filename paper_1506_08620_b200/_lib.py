@@ -62,6 +62,7 @@ SPARSE_RECORDS12 = 3
 SPARSE_RECORDS8X3 = 4
 SPARSE_ZONED = 5
 SPARSE_ZONED_RANK = 6
+SPARSE_COUNT = 7
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (
@@ -84,6 +85,9 @@ EXPORTED = (
     "fs_build_zoned",
     "fs_plan_zoned_rank",
     "fs_build_zoned_rank",
+    "fs_count_words_bytes",
+    "fs_plan_count_words",
+    "fs_build_count_words",
     "fs_build_fused",
     "fs_build_padded",
     "fs_build_rank2",
@@ -196,6 +200,13 @@ def _declare(lib):
                                        _p_u64, _p_u64, _p_u64, _vp]
     lib.fs_build_zoned_rank.restype = ctypes.c_int
     lib.fs_build_zoned_rank.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _u64, _vp, _vp, _vp]
+    lib.fs_count_words_bytes.restype = ctypes.c_uint64
+    lib.fs_count_words_bytes.argtypes = [_u64, _i32]
+    lib.fs_plan_count_words.restype = ctypes.c_int
+    lib.fs_plan_count_words.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _u64, _vp, _p_i32, _p_u64, _p_i32,
+                                        _p_u64, _p_u64, _vp]
+    lib.fs_build_count_words.restype = ctypes.c_int
+    lib.fs_build_count_words.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp]
     lib.fs_build_hot_window.restype = ctypes.c_int
     lib.fs_build_hot_window.argtypes = [_i32, _vp, _u64, _u64, _vp, _p_u64, _p_u64, _p_u64, _p_u64, _p_u64, _vp]
     lib.fs_build_fused.restype = ctypes.c_int

@@ -308,7 +308,8 @@ class PreparedKernel:
             "smem_sparse": bool(f & _lib.PLACE_SMEM_SPARSE),
             "sparse_format": {_lib.SPARSE_RECORDS: "records", _lib.SPARSE_RECORDS8: "records8",
                               _lib.SPARSE_RECORDS12: "records12", _lib.SPARSE_RECORDS8X3: "records8x3",
-                              _lib.SPARSE_ZONED: "zoned", _lib.SPARSE_ZONED_RANK: "zoned-rank"}.get(
+                              _lib.SPARSE_ZONED: "zoned", _lib.SPARSE_ZONED_RANK: "zoned-rank",
+                              _lib.SPARSE_COUNT: "count-words"}.get(
                 self.plan.sparse_format, "two-level") if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
         }
@@ -458,7 +459,15 @@ SPARSE_RECORDS_MIN_LOAD = 0.2
 SPARSE_RECORDS8_MAX_PAST_PPM = 5_000
 #: sparse layouts allowed; a tuning run or test may narrow it to one
 #: (a leading records format also skips the load rule)
-SPARSE_FORMATS = ("two-level", "records8", "records8x3", "records", "records12")
+SPARSE_FORMATS = ("count-words", "two-level", "records8", "records8x3", "records", "records12")
+#: count words (fs_build_count_words) are tried first and used when at most
+#: this share (ppm) of the buckets lies in stripes of two or more knots --
+#: the uniform queries that take the probe's scan path; 0 skips them
+COUNT_WORDS_MAX_RARE_PPM = 10_000
+#: ... and, when X cannot be staged beside the words, at most this share
+#: (ppm) lies in knot-holding stripes -- the queries that read X through L2
+#: (cfg5 N+1 = 32769: 9% of them, 363 G queries/s against 430 on group records)
+COUNT_WORDS_MAX_L2_XREAD_PPM = 20_000
 
 #: hot-window staging budget: small enough that the L2-gather kernel keeps
 #: full occupancy (3-4 CTAs per SM) for the queries outside the window
@@ -658,6 +667,42 @@ def _plan_two_level(p: SortedPartition, idx: DirectIndex, f, budget: int):
     return None
 
 
+def _set_count_words(plan, p: SortedPartition, idx: DirectIndex, keep: list, f, budget: int) -> bool:
+    """Count words of K (fs_build_count_words): 8-B words of sixteen 2^k-bucket
+    stripes with a 2-bit knot count each, one k for the table; a popcount
+    decode, one X compare when the query's stripe holds a knot, a short scan
+    when it holds several.  Used when the rank directory and X cannot be
+    staged together and at most COUNT_WORDS_MAX_RARE_PPM of the buckets lie in
+    stripes of two or more knots.  ``f``: n1 uint64 scratch."""
+    n1 = len(p.values)
+    x_bytes = (n1 * p.values.dtype.itemsize + 127) // 128 * 128
+    if x_bytes + ((idx.r >> 5) + 1) * 8 <= budget:
+        return False  # the staged rank directory + X: one knot per mask bit, no scan path
+    lib = _lib.load()
+    dt = fs_dtype(p.precision)
+    x = p.device_values()
+    k, with_x = ctypes.c_int32(-1), ctypes.c_int32(0)
+    nbytes, xread, rare = (ctypes.c_uint64(0) for _ in range(3))
+    rc = lib.fs_plan_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, f.data_ptr(), ctypes.byref(k),
+                                 ctypes.byref(nbytes), ctypes.byref(with_x), ctypes.byref(xread), ctypes.byref(rare),
+                                 _device.stream_ptr())
+    if rc == _lib.FS_TOO_LARGE:
+        return False
+    _lib.check(rc, what="fs_plan_count_words")
+    if rare.value > COUNT_WORDS_MAX_RARE_PPM or (not with_x.value and xread.value > COUNT_WORDS_MAX_L2_XREAD_PPM):
+        return False
+    buf = _device.empty(int(nbytes.value), np.uint8)
+    rc = lib.fs_build_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, k.value, f.data_ptr(), buf.data_ptr(),
+                                  _device.stream_ptr())
+    _lib.check(rc, what="fs_build_count_words")
+    plan.sparse = buf.data_ptr()
+    plan.sparse_format = _lib.SPARSE_COUNT
+    plan.sparse_shift = k.value
+    plan.sparse_ndense = 0
+    keep.append(buf)
+    return True
+
+
 def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:
     """For R >> N, a sparse encoding of K fits in shared memory where the
     rank directory does not; the kernel picks it over L2 gathers when the
@@ -678,6 +723,9 @@ def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) ->
     # 16-bit ones); then 8-B and 16-B records with X read through L2 (fine
     # for uniform queries, but streams with many exact-knot queries, like
     # cfg2's 1%, lose: 433 -> 423).
+    if "count-words" in SPARSE_FORMATS and COUNT_WORDS_MAX_RARE_PPM and _set_count_words(plan, p, idx, keep, f, budget):
+        return
+
     def records(name, wx):
         return name in SPARSE_FORMATS and _set_sparse_records(plan, p, idx, keep, f, budget, name, wx)
 

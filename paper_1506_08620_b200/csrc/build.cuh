@@ -337,27 +337,22 @@ __global__ void fill_sparse_rec_kernel(const uint64_t* __restrict__ f, uint64_t 
 // records whose descriptor holds the stripe shift k instead of s; a record
 // covers 2^(k+5) buckets and mask bit b is set iff a knot falls in buckets
 // [j0 + b 2^k, j0 + (b+1) 2^k) (at most one does, by the planner's k).
-// MODE 2 (fs_build_zoned_count): striped count words -- a record covers
-// 2^(k+4) buckets in 16 stripes, and bits 2b, 2b+1 of the mask hold the
-// number of knots (0..3, by the planner's k) in stripe b.
-template <int MODE>
+template <bool STRIPED>
 __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, int zs,
                                   const uint32_t* __restrict__ zdesc, uint32_t nz, uint2* __restrict__ R,
                                   uint64_t nrec) {
-  // buckets per record beyond the descriptor's shift: 2^5 / 2^4 stripes
-  constexpr int kWordShift = MODE == 1 ? kZonedRankShift : MODE == 2 ? kZonedCountShift : 0;
   for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nrec; g += (uint64_t)gridDim.x * blockDim.x) {
     // zone z's first record = ((int)desc >> 5) + (z << (zs - s))
     auto first = [&](uint32_t k) {
       const uint32_t dk = __ldg(zdesc + k);
-      return (uint64_t)((int64_t)((int32_t)dk >> 5) + ((int64_t)k << (zs - (int)(dk & 15u) - kWordShift)));
+      return (uint64_t)((int64_t)((int32_t)dk >> 5) + ((int64_t)k << (zs - (int)(dk & 15u) - (STRIPED ? kZonedRankShift : 0))));
     };
     uint32_t z = 0;
     for (uint32_t k = 1; k < nz; ++k)
       if (first(k) <= g) z = k;
     const uint32_t d = __ldg(zdesc + z);
-    const int kst = MODE ? (int)(d & 15u) : 0;  // stripe shift
-    const int s = (int)(d & 15u) + kWordShift;
+    const int kst = STRIPED ? (int)(d & 15u) : 0;  // stripe shift
+    const int s = (int)(d & 15u) + (STRIPED ? kZonedRankShift : 0);
     const uint64_t j0 = ((uint64_t)z << zs) + ((g - first(z)) << s);
     const uint64_t j1 = j0 + (1ull << s);
     const uint64_t lo = bound_search<false>(f, 0, n1, j0);
@@ -366,10 +361,7 @@ __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, i
       for (uint64_t k = lo; k < n1; ++k) {
         const uint64_t fi = __ldg(f + k);
         if (fi >= j1) break;
-        if constexpr (MODE == 2)
-          m += 1u << (2 * (uint32_t)((fi - j0) >> kst));  // a 2-bit count per stripe (never past 3)
-        else
-          m |= 1u << ((fi - j0) >> kst);
+        m |= 1u << ((fi - j0) >> kst);
       }
       R[g] = make_uint2(m, (uint32_t)lo);
     } else {
@@ -383,6 +375,30 @@ __global__ void fill_zoned_kernel(const uint64_t* __restrict__ f, uint64_t n1, i
       for (; k < kZonedSlots; ++k) w |= 0x1FFFull << (25 + 13 * k);
       R[g] = make_uint2((uint32_t)w, (uint32_t)(w >> 32));
     }
+  }
+}
+
+// Count words of the gap-1 table (fs_build_count_words): one thread per 8-B
+// word.  Word g covers buckets j0 .. j0 + 2^(k+4) - 1, j0 = g 2^(k+4), in 16
+// stripes of 2^k; bits 2b, 2b+1 of the mask hold the number of knots in
+// stripe b, saturated at 3; base = lower_bound(f, j0) = K[j0], with bit 31
+// set when a stripe of the word holds four or more knots (its counts are
+// then no longer exact and the probe scans the word's knots instead).
+__global__ void fill_count_words_kernel(const uint64_t* __restrict__ f, uint64_t n1, int k, uint2* __restrict__ W,
+                                        uint64_t nwords) {
+  const int s = k + kCountWordShift;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nwords; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j0 = g << s, j1 = j0 + (1ull << s);
+    const uint64_t lo = bound_search<false>(f, 0, n1, j0);
+    uint32_t m = 0, flag = 0;
+    for (uint64_t i = lo; i < n1; ++i) {
+      const uint64_t fi = __ldg(f + i);
+      if (fi >= j1) break;
+      const uint32_t sh = 2u * (uint32_t)((fi - j0) >> k);
+      if (((m >> sh) & 3u) == 3u) flag = kCountFlag;  // a fourth knot in this stripe
+      else m += 1u << sh;
+    }
+    W[g] = make_uint2(m, (uint32_t)lo | flag);
   }
 }
 

@@ -53,11 +53,12 @@ constexpr int kZonedMinZoneShift = kRec3MaxShift;
 constexpr int kZonedRankShift = 5;
 constexpr uint32_t kZonedRankFlag = 16u;
 constexpr int kZonedMaxStripe = 10;  // striped rank words: a mask bit per 2^k buckets, k <= 10
-// striped count words (FS_SPARSE_ZONED_COUNT): 16 stripes of 2^k buckets per
-// word, a 2-bit knot count each (at most three knots per stripe), k <= 15
-constexpr int kZonedCountShift = 4;
-constexpr int kZonedMaxCountStripe = 15;
-constexpr int kZonedCountMaxKnots = 3;
+// Count words (FS_SPARSE_COUNT): one stripe shift k for the whole table, 16
+// stripes of 2^k buckets per 8-B word {2-bit knot counts, first knot index},
+// bit 31 of the index flags a word with a stripe of four or more knots
+constexpr int kCountWordShift = 4;
+constexpr int kCountMaxShift = 27;
+constexpr uint32_t kCountFlag = 0x80000000u;
 
 // Bounds-checked builds (FSG_BOUNDS_CHECK=1, tools/bounds_check.sh): every
 // table gather of the search probes checks its index against the table's

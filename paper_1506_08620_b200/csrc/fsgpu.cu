@@ -170,8 +170,11 @@ int validate_plan(const fs_plan* p) {
       if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS &&
                         p->sparse_format != FS_SPARSE_RECORDS8 && p->sparse_format != FS_SPARSE_RECORDS12 &&
                         p->sparse_format != FS_SPARSE_RECORDS8X3 && p->sparse_format != FS_SPARSE_ZONED &&
-                        p->sparse_format != FS_SPARSE_ZONED_RANK))
+                        p->sparse_format != FS_SPARSE_ZONED_RANK && p->sparse_format != FS_SPARSE_COUNT))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
+      if (p->sparse && p->sparse_format == FS_SPARSE_COUNT &&
+          (fs_count_words_bytes(p->r, p->sparse_shift) == 0 || p->n1 - 1 >= (1ull << 31)))
+        return fail(FS_INVALID_ARG, "count-word parameters out of range");
       if (p->sparse && is_zoned(p->sparse_format)) {
         if (fs_zoned_bytes(p->r, p->sparse_shift, p->sparse_ndense) == 0 || p->r >= (1ull << 32) ||
             (p->sparse_format == FS_SPARSE_ZONED && p->n1 > (1ull << 24)))
@@ -181,7 +184,7 @@ int validate_plan(const fs_plan* p) {
       }
       if (p->sparse && p->sparse_format == FS_SPARSE_RECORDS8X3 && p->n1 > (1ull << 24))
         return fail(FS_INVALID_ARG, "3-offset records need N+1 <= 2^24");
-      if (p->sparse && !is_zoned(p->sparse_format) && (p->sparse_shift < 5 ||
+      if (p->sparse && !is_zoned(p->sparse_format) && p->sparse_format != FS_SPARSE_COUNT && (p->sparse_shift < 5 ||
                         p->sparse_shift > (p->sparse_format == FS_SPARSE_TWO_LEVEL    ? 16
                                            : p->sparse_format == FS_SPARSE_RECORDS12 ? kRec12MaxShift
                                            : p->sparse_format == FS_SPARSE_RECORDS8X3 ? kRec3MaxShift
@@ -263,10 +266,12 @@ Placement place(const fs_plan* p) {
   }
   // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
   if (p->algorithm == FS_ALGO_DIRECT && p->sparse && !is_zoned(p->sparse_format) && p->q == 1 &&
-      !force_global && p->r < (1ull << 32) && p->sparse_shift >= 5 && p->sparse_shift <= 16) {
+      !force_global && p->r < (1ull << 32) &&
+      (p->sparse_format == FS_SPARSE_COUNT || (p->sparse_shift >= 5 && p->sparse_shift <= 16))) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
-    const uint64_t cfb = p->sparse_format != FS_SPARSE_TWO_LEVEL
+    const uint64_t cfb = p->sparse_format == FS_SPARSE_COUNT ? fs_count_words_bytes(p->r, p->sparse_shift)
+                         : p->sparse_format != FS_SPARSE_TWO_LEVEL
                              ? fs_sparse_rec_bytes(p->sparse_format, p->n1, p->r, p->sparse_shift, p->sparse_ndense)
                              : fs_sparse_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense);
     const bool rank_fits = use_rank && align128(xb) + dir_b <= budget;
@@ -550,6 +555,16 @@ template <int SLOTS, bool XS, bool OVF>
 struct UnrollFor<double, SparseRecProbe<double, SLOTS, XS, OVF>> {
   static constexpr int value = FSG_UNROLL_F64_REC;
 };
+// count words: three 4-query groups per thread, the word loads of a whole
+// group in flight (cfg2 486 -> 514, cfg5 N+1 = 1025 515 -> 550 Gq/s over two
+// groups of two loads; four groups 453; profiles/r02/count_words.txt)
+#ifndef FSG_UNROLL_F64_COUNT
+#define FSG_UNROLL_F64_COUNT 3
+#endif
+template <bool XS>
+struct UnrollFor<double, CountWordProbe<double, XS>> {
+  static constexpr int value = FSG_UNROLL_F64_COUNT;
+};
 // The light three-offset probe takes a third group with int32 outputs (cfg2
 // 459 -> 470 Gq/s; int64 outputs 370 -> 355 and the other probes lose with
 // it: profiles/r01/tune_sparse_records.txt).
@@ -603,6 +618,13 @@ struct BoundedFor<T, Bitset2Probe<T, true, DEEP, SHADOW>, OutT> {
 template <typename T, bool STRIPED, typename OutT>
 struct BoundedFor<T, ZonedProbe<T, STRIPED>, OutT> {
   static constexpr bool value = FSG_ZONED_BOUNDED;
+};
+#ifndef FSG_COUNT_BOUNDED
+#define FSG_COUNT_BOUNDED 1
+#endif
+template <typename T, bool XS, typename OutT>
+struct BoundedFor<T, CountWordProbe<T, XS>, OutT> {
+  static constexpr bool value = FSG_COUNT_BOUNDED;
 };
 template <typename T, int SLOTS, bool XS, bool OVF, typename OutT>
 struct BoundedFor<T, SparseRecProbe<T, SLOTS, XS, OVF>, OutT> {
@@ -796,6 +818,10 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       if (pl.zoned && p->sparse_format == FS_SPARSE_ZONED_RANK)
         return launch_probe<T, OutT, ZonedProbe<T, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.zoned) return launch_probe<T, OutT, ZonedProbe<T>>(d, pl, z, m, out, fb, base, st);
+      if (pl.sparse && p->sparse_format == FS_SPARSE_COUNT) {
+        if (pl.xs) return launch_probe<T, OutT, CountWordProbe<T, true>>(d, pl, z, m, out, fb, base, st);
+        return launch_probe<T, OutT, CountWordProbe<T, false>>(d, pl, z, m, out, fb, base, st);
+      }
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS)
         return dispatch_records<T, OutT, 6>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS8X3)
@@ -1366,6 +1392,67 @@ int zoned_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, 
   return FS_OK;
 }
 }  // namespace
+
+uint64_t fs_count_words_bytes(uint64_t r, int32_t k) {
+  if (k < 0 || k > kCountMaxShift || r >= (1ull << 32)) return 0;
+  return 8 * ((r >> (k + kCountWordShift)) + 1);
+}
+
+int fs_plan_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
+                        uint64_t* f_scratch_dev, int32_t* k_out, uint64_t* bytes_out, int32_t* with_x_out,
+                        uint64_t* xread_ppm_out, uint64_t* rare_ppm_out, void* stream) {
+  if (!x_dev || !f_scratch_dev || n1 < 2 || !k_out) return fail(FS_INVALID_ARG, "bad arguments");
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "count words need R < 2^32, N < 2^31");
+  const uint64_t es = dtype == FS_F32 ? 4 : 8;
+  // all of X beside the words when it takes at most half the budget, else none of it
+  const uint64_t xb = align128(n1 * es) <= budget_bytes / 2 ? align128(n1 * es) : 0;
+  if (budget_bytes < xb + 128 + 8) return fail(FS_TOO_LARGE, "no count-word layout fits the budget");
+  const uint64_t table_budget = budget_bytes - xb - 128;
+  int k = 0;
+  while (k <= kCountMaxShift && fs_count_words_bytes(r, k) > table_budget) ++k;
+  if (k > kCountMaxShift) return fail(FS_TOO_LARGE, "no count-word layout fits the budget");
+  // more knots than stripes: nearly every query would scan (the planner's caller would refuse it anyway)
+  if (n1 > ((r >> k) + 1)) return fail(FS_TOO_LARGE, "count words: more knots than stripes");
+  std::vector<uint64_t> f;
+  int rc = zoned_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, f, as_stream(stream));
+  if (rc) return rc;
+  // buckets whose queries read X (stripes holding a knot) and whose queries
+  // scan (stripes holding two or more; every stripe of a flagged word)
+  uint64_t xread = 0, rare = 0;
+  const uint64_t sw = 1ull << k, ww = 1ull << (k + kCountWordShift);
+  for (size_t i = 0; i < f.size();) {
+    size_t e = i + 1;
+    while (e < f.size() && (f[e] >> k) == (f[i] >> k)) ++e;
+    const uint64_t width = std::min<uint64_t>(sw, r + 1 - ((f[i] >> k) << k));
+    xread += width;
+    if (e - i >= 2) rare += width;
+    if (e - i >= 4) rare += std::min<uint64_t>(ww, r + 1 - ((f[i] >> (k + kCountWordShift)) << (k + kCountWordShift)));
+    i = e;
+  }
+  *k_out = k;
+  if (bytes_out) *bytes_out = fs_count_words_bytes(r, k);
+  if (with_x_out) *with_x_out = xb != 0;
+  if (xread_ppm_out) *xread_ppm_out = (uint64_t)((long double)xread * 1e6L / (long double)(r + 1));
+  if (rare_ppm_out) *rare_ppm_out = (uint64_t)((long double)std::min<uint64_t>(rare, r + 1) * 1e6L / (long double)(r + 1));
+  return FS_OK;
+}
+
+int fs_build_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t k,
+                         uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "count words need R < 2^32, N < 2^31");
+  const uint64_t bytes = fs_count_words_bytes(r, k);
+  if (!bytes) return fail(FS_INVALID_ARG, "stripe shift out of range");
+  cudaStream_t s = as_stream(stream);
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, s);
+  if (rc) return rc;
+  const uint64_t nwords = bytes / 8;
+  fill_count_words_kernel<<<grid_1d(nwords, 256), 256, 0, s>>>(f_scratch_dev, n1, k, static_cast<uint2*>(buf_dev), nwords);
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
 
 uint64_t fs_zoned_bytes(uint64_t r, int32_t zs, uint64_t nrec) {
   if (zs < kZonedMinZoneShift || zs > 31) return 0;

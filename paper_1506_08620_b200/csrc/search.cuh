@@ -603,6 +603,118 @@ struct SparseRecProbe {
   }
 };
 
+// Direct search (gap 1) over the count words of K (fill_count_words_kernel),
+// staged in shared memory after X when X fits.  A word {mask, base} covers 16
+// stripes of 2^k buckets (one k for the table) with a 2-bit knot count each.
+// For bucket j: b = (j >> k) & 15, m = mask below bit 2b, and
+//   t = base + popc(m) + popc(m & 0xAAAAAAAA)
+// knots lie in earlier stripes -- all below z, the bucket function being
+// monotone (direct.py:194-197) -- while knots of later stripes lie above it, so
+// only the c = (mask >> 2b) & 3 knots X[t .. t+c-1] of the query's own stripe
+// need comparing: the answer of batch.py:315-317 is t - 1 + #{X[t+e] <= z}.
+// Common path (c <= 1): one predicated X load and one compare, as the rank
+// directory does.  Rare path (c >= 2, or a flagged word whose counts
+// saturated): a forward scan X[s], X[s+1], ... <= z from s = t (s = base for
+// a flagged word), which stops at the first knot above z -- exact for any
+// number of knots in a stripe, so correctness never depends on k; the
+// planner picks the finest k that fits and reports how many queries go the
+// rare way (uniformly drawn knots: ~lambda^2 / 2 of them at lambda knots per
+// stripe).  A popcount decode instead of the group records' SWAR counts.
+template <typename T, bool XS>
+struct CountWordProbe {
+  const T* X;
+  uint32_t xs, ws;  // shared addresses of X (XS) and of the words
+  T h, x0;
+  uint32_t r, k, n1;
+  __device__ __forceinline__ CountWordProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = (uint32_t)p.n1;
+    X = p.x;
+    // held in registers (volatile mov): ptxas would otherwise rebuild the
+    // shared-window addresses in front of every load
+    asm volatile("mov.u32 %0, %1;" : "=r"(xs) : "r"((uint32_t)__cvta_generic_to_shared(smem)));
+    asm volatile("mov.u32 %0, %1;" : "=r"(ws) : "r"(xs + p.x_smem_bytes_aligned()));
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+    k = (uint32_t)p.sparse_shift;
+  }
+  __device__ __forceinline__ uint32_t bucket(T z) const {
+    uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
+    return j < r ? j : r;
+  }
+  __device__ __forceinline__ uint2 word(uint32_t j) const {
+    uint2 g;
+    const uint32_t a = ws + 8u * ((j >> k) >> kCountWordShift);
+    FSG_BOUND(a + 8u - xs <= dyn_smem_bytes());
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(g.x), "=r"(g.y) : "r"(a));
+    return g;
+  }
+  __device__ __forceinline__ T xat(uint32_t t) const {
+    FSG_BOUND(t < n1);
+    if constexpr (XS) {
+      T v;
+      if constexpr (sizeof(T) == 4) asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xs + 4u * t));
+      else asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(xs + 8u * t));
+      return v;
+    } else {
+      return __ldg(X + t);
+    }
+  }
+  // knots in earlier stripes -> t, knots in the query's stripe -> c
+  __device__ __forceinline__ void resolve(const uint2& g, uint32_t j, uint32_t& t, uint32_t& c) const {
+    const uint32_t b2 = ((j >> k) & 15u) * 2u;
+    uint32_t below;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(b2));
+    const uint32_t m = g.x & below;
+    t = g.y + __popc(m) + __popc(m & 0xAAAAAAAAu);  // the flag bit rides along; flagged words go the rare way
+    c = (g.x >> b2) & 3u;
+  }
+  __device__ __forceinline__ int64_t finish(const uint2& g, uint32_t t, uint32_t c, T z) const {
+    T xv = z;
+    if (c != 0 && (int32_t)g.y >= 0) xv = xat(t);
+    uint32_t res = t - ((c == 0 || z < xv) ? 1u : 0u);
+    if (c > 1u || (int32_t)g.y < 0) {  // rare: scan the stripe's (a flagged word's) knots
+      uint32_t e = (int32_t)g.y < 0 ? (g.y & ~kCountFlag) : t;
+      while (e < n1 && xat(e) <= z) ++e;
+      res = e - 1u;
+    }
+    return (int64_t)(int32_t)res;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    const uint32_t j = bucket(z);
+    const uint2 g = word(j);
+    uint32_t t, c;
+    resolve(g, j, t, c);
+    return finish(g, t, c, z);
+  }
+  // every word load of a group issued before the first is resolved
+#ifndef FSG_COUNT_GROUP
+#define FSG_COUNT_GROUP 4  // 1: 464, 2: 486, 4: 493 Gq/s on cfg2 (unroll 2)
+#endif
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    constexpr int G = N < FSG_COUNT_GROUP ? N : FSG_COUNT_GROUP;
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += G) {
+      uint2 g[G];
+      uint32_t j[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        j[q] = bucket(z[g0 + q]);
+        g[q] = word(j[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        uint32_t t, c;
+        resolve(g[q], j[q], t, c);
+        o[g0 + q] = (R)finish(g[q], t, c, z[g0 + q]);
+      }
+    }
+  }
+};
+
 // RankProbe with a shared-memory hot window: directory words [w0, w0 + nw)
 // and knots X[t0 .. t0 + nt) are staged (X window at smem offset 0, the
 // directory window after it); lanes outside the window gather through L2.
@@ -705,17 +817,7 @@ struct HotRankProbe {
 // t - (z < X[t]), else t - 1.  The same answers with a ~10-instruction decode
 // (the slot form's SWAR count and field select are gone); the price is an X
 // read whenever the query's stripe -- not its exact bucket -- holds a knot.
-//
-// STRIPED == 2 (FS_SPARSE_ZONED_COUNT, fs_build_zoned_count): striped count
-// words.  A word holds 16 stripes with a 2-bit knot count each (the planner's
-// k keeps every stripe at three knots or fewer), so tables of uniformly drawn
-// knots, whose closest pairs rule out one-knot stripes of any useful width,
-// fit in shared memory too.  With b = (j >> k) & 15 and m = mask below bit
-// 2b: t = base + popc(m) + popc(m & 0xAAAAAAAA) counts the knots of earlier
-// stripes (all below z), c = (mask >> 2b) & 3 is the count of the query's
-// own stripe, whose knots X[t .. t+c-1] are compared directly (predicated
-// loads; the second and third are rare): the answer is t - 1 + #{X[t+e] <= z}.
-template <typename T, int STRIPED = 0>
+template <typename T, bool STRIPED = false>
 struct ZonedProbe {
   const T* X;
   const unsigned char* xg;  // generic address of the X window
@@ -757,9 +859,7 @@ struct ZonedProbe {
   __device__ __forceinline__ uint2 rec(uint32_t j, uint32_t d) const {
     uint2 g;
     // descriptors are zone-relative
-    const uint32_t idx = (uint32_t)((int32_t)d >> 5) + (STRIPED == 2   ? (j >> (d & 15u)) >> kZonedCountShift
-                                                         : STRIPED == 1 ? (j >> (d & 15u)) >> kZonedRankShift
-                                                                        : j >> (d & 15u));
+    const uint32_t idx = (uint32_t)((int32_t)d >> 5) + (STRIPED ? (j >> (d & 15u)) >> 5 : j >> (d & 15u));
     const uint32_t a = rc + 8u * idx;
     FSG_BOUND(idx < nrec && a + 8u - xs <= dyn_smem_bytes());
     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(g.x), "=r"(g.y) : "r"(a));
@@ -770,8 +870,7 @@ struct ZonedProbe {
   // is half dense, half sparse), and a divergent branch would issue both
   // decodes plus its reconvergence overhead anyway.
   static __device__ __forceinline__ void resolve(const uint2& g, uint32_t d, uint32_t j, uint32_t& t, bool& knot) {
-    static_assert(STRIPED != 2, "count words resolve through resolve_count");
-    if constexpr (STRIPED == 1) {
+    if constexpr (STRIPED) {
       const uint32_t b = (j >> (d & 15u)) & 31u;
       uint32_t below;
       asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(b));
@@ -820,52 +919,14 @@ struct ZonedProbe {
       asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.f64 %0, [%1];\n\t}" : "+d"(v) : "l"(p), "r"((uint32_t)knot));
     return v;
   }
-  // count words: knots of earlier stripes -> t, knots of the query's stripe -> c
-  static __device__ __forceinline__ void resolve_count(const uint2& g, uint32_t d, uint32_t j, uint32_t& t, uint32_t& c) {
-    const uint32_t b2 = ((j >> (d & 15u)) & 15u) * 2u;
-    uint32_t below;
-    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(b2));
-    const uint32_t m = g.x & below;
-    t = g.y + __popc(m) + __popc(m & 0xAAAAAAAAu);
-    c = (g.x >> b2) & 3u;
-  }
-  // t - 1 + #{e < c : X[t + e] <= z}: up to three predicated loads from the
-  // staged window (when all three slots lie inside it) or global memory; a
-  // slot not loaded keeps +inf and counts nothing
-  __device__ __forceinline__ int64_t finish_count(uint32_t t, uint32_t c, T z) const {
-    const uint32_t tl = t - t0;
-    FSG_BOUND(c == 0 || t + c <= n1);
-    const T* p = (tl < nt && tl + (kZonedCountMaxKnots - 1) < nt) ? reinterpret_cast<const T*>(xg) + tl : X + t;
-    T a, b, e;
-    if constexpr (sizeof(T) == 4) {
-      a = b = e = __int_as_float(0x7f800000);
-      asm("{\n\t.reg .pred p1, p2, p3;\n\tsetp.ne.u32 p1, %4, 0;\n\tsetp.gt.u32 p2, %4, 1;\n\tsetp.gt.u32 p3, %4, 2;\n\t"
-          "@p1 ld.f32 %0, [%3];\n\t@p2 ld.f32 %1, [%3+4];\n\t@p3 ld.f32 %2, [%3+8];\n\t}"
-          : "+f"(a), "+f"(b), "+f"(e)
-          : "l"(p), "r"(c));
-    } else {
-      a = b = e = __longlong_as_double(0x7ff0000000000000ll);
-      asm("{\n\t.reg .pred p1, p2, p3;\n\tsetp.ne.u32 p1, %4, 0;\n\tsetp.gt.u32 p2, %4, 1;\n\tsetp.gt.u32 p3, %4, 2;\n\t"
-          "@p1 ld.f64 %0, [%3];\n\t@p2 ld.f64 %1, [%3+8];\n\t@p3 ld.f64 %2, [%3+16];\n\t}"
-          : "+d"(a), "+d"(b), "+d"(e)
-          : "l"(p), "r"(c));
-    }
-    return (int64_t)t - 1 + (int64_t)((uint32_t)(z >= a) + (uint32_t)(z >= b) + (uint32_t)(z >= e));
-  }
   __device__ __forceinline__ int64_t operator()(T z) const {
     const uint32_t j = bucket(z);
     const uint32_t d = desc(j);
     uint32_t t;
-    if constexpr (STRIPED == 2) {
-      uint32_t c;
-      resolve_count(rec(j, d), d, j, t, c);
-      return finish_count(t, c, z);
-    } else {
-      bool knot;
-      resolve(rec(j, d), d, j, t, knot);
-      const T xv = xsel(t, knot, z);
-      return (int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z < xv));
-    }
+    bool knot;
+    resolve(rec(j, d), d, j, t, knot);
+    const T xv = xsel(t, knot, z);
+    return (int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z < xv));
   }
   // descriptors of a group, then its records, then the resolves: every load
   // of a phase in flight before the first is consumed
@@ -894,16 +955,10 @@ struct ZonedProbe {
       for (int q = 0; q < G; ++q) {
         if (g0 + q >= N) break;
         uint32_t t;
-        if constexpr (STRIPED == 2) {
-          uint32_t c;
-          resolve_count(g[q], d[q], j[q], t, c);
-          o[g0 + q] = (R)finish_count(t, c, z[g0 + q]);
-        } else {
-          bool knot;
-          resolve(g[q], d[q], j[q], t, knot);
-          const T xv = xsel(t, knot, z[g0 + q]);
-          o[g0 + q] = (R)((int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z[g0 + q] < xv)));
-        }
+        bool knot;
+        resolve(g[q], d[q], j[q], t, knot);
+        const T xv = xsel(t, knot, z[g0 + q]);
+        o[g0 + q] = (R)((int64_t)t - (int64_t)((uint32_t)!knot | (uint32_t)(z[g0 + q] < xv)));
       }
     }
   }

@@ -8,7 +8,7 @@ Config specs: cfgN (BASELINE recipes), cfg5:<N+1>, cfg2:<seed>, cfg5u (the
 unfiltered cfg5 draw, bitset2 fall-back instance), unif32:<size> / unif64:<size> (the throughput sweep's
 U[1,5]-gap partitions), big32:<N+1> (sorted f32
 U[0,1) knots).  Layout variants: direct-k (plain K), direct-rank (rank
-directory only), direct-hot / direct-hot:<KB> / direct-nohot (hot window on, of a given size, off), direct-nozoned (zoned records off), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
+directory only), direct-hot / direct-hot:<KB> / direct-nohot (hot window on, of a given size, off), direct-nozoned (zoned records off), direct-count / direct-nocount (count words forced / excluded), direct-sparse2 / direct-rec / direct-rec8 (two-level sparse table / 16-B / 8-B group
 records forced), bitset2-flat (no subtree records),
 direct-gap2-k (gap 2 over plain K), fallback (prepare_with_fallback), gap:<q>
 (direct with gap q over its count directory).
@@ -109,7 +109,7 @@ def main():
         for algo in args.algos.split(","):
             try:
                 base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct", "direct-nohot": "direct",
-                        "direct-nozoned": "direct",
+                        "direct-nozoned": "direct", "direct-count": "direct", "direct-nocount": "direct",
                         "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
                 if algo.startswith("direct-hot:"):  # hot window of the given size in KB
                     base = "direct"
@@ -142,6 +142,19 @@ def main():
                     prep = fs.prepare("direct", p, hot_window=True)
                 if algo == "direct-nohot":
                     prep = fs.prepare("direct", p, hot_window=False)
+                if algo in ("direct-count", "direct-nocount"):  # count words forced / excluded
+                    from paper_1506_08620_b200 import batch as _b
+
+                    keep_c = (_b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM)
+                    if algo == "direct-count":
+                        _b.SPARSE_FORMATS = ("count-words",)
+                        _b.COUNT_WORDS_MAX_RARE_PPM = _b.COUNT_WORDS_MAX_L2_XREAD_PPM = 10**6
+                    else:
+                        _b.SPARSE_FORMATS = tuple(n for n in keep_c[0] if n != "count-words")
+                    try:
+                        prep = fs.prepare("direct", p)
+                    finally:
+                        _b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM = keep_c
                 if algo == "direct-nozoned":  # no zoned records: the hot window / L2 directory
                     from paper_1506_08620_b200 import batch as _b
 
