@@ -368,24 +368,30 @@ int fs_build_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h,
  * directly: the answer of batch.py:315-317 is t - 1 + #{e : X[t+e] <= z}, one
  * predicated compare when c <= 1, a forward scan of X from t (from base for a
  * flagged word) when c >= 2.  Exact for every k; k only sets how many queries
- * take the scan.  Buffer: (R >> (k + 4)) + 1 words (fs_count_words_bytes).
- *   fs_plan_count_words: the finest k whose words fit budget_bytes beside all
- *     of X (when X takes at most half the budget: *with_x_out = 1) or alone
- *     (0: X is read through L2), the share of buckets in knot-holding stripes
- *     (queries that read X) and in stripes of two or more knots or flagged
- *     words (queries that scan), both in parts per million.  FS_TOO_LARGE if
- *     nothing fits or there are more knots than stripes.  SYNC.
- *   fs_build_count_words: fill the words for that k.  Async.
+ * take the scan.  When X is too large to stage, one byte per knot can be
+ * (k <= 8): O[i] = f_i mod 2^k, knot i's bucket inside its stripe; a knot in a
+ * lower bucket than the query's lies below z and one in a higher bucket above
+ * it, so X is read (through L2) only for a knot in the query's own bucket.
+ * Buffer: (R >> (k + 4)) + 1 words, then, if built with offsets, N+1 offset
+ * bytes padded to 16 (fs_count_words_bytes(r, k, noff = N+1 or 0)).
+ *   fs_plan_count_words: the finest k whose words fit budget_bytes in the
+ *     given mode -- 1: beside all of X; 2: beside the knot offsets (k <= 8
+ *     must fit); 0: alone, every knot read through L2 -- plus the share of
+ *     buckets in knot-holding stripes (queries that read X or an offset) and
+ *     in stripes of two or more knots or flagged words (queries that scan),
+ *     in parts per million.  FS_TOO_LARGE if nothing fits or there are more
+ *     knots than stripes.  SYNC.
+ *   fs_build_count_words: fill the words (and the offsets) for that k.  Async.
  * Set fs_plan.sparse to the buffer, sparse_format = FS_SPARSE_COUNT,
- * sparse_shift = k, sparse_ndense = 0.  The search stages X beside the words
- * when both fit.  f_scratch_dev: n1 uint64.
+ * sparse_shift = k, sparse_ndense = N+1 if built with offsets, else 0.  The
+ * search stages X beside plain words when both fit.  f_scratch_dev: n1 uint64.
  */
-uint64_t fs_count_words_bytes(uint64_t r, int32_t k);
+uint64_t fs_count_words_bytes(uint64_t r, int32_t k, uint64_t noff);
 int fs_plan_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
-                        uint64_t* f_scratch_dev, int32_t* k_out, uint64_t* bytes_out, int32_t* with_x_out,
+                        int32_t mode, uint64_t* f_scratch_dev, int32_t* k_out, uint64_t* bytes_out,
                         uint64_t* xread_ppm_out, uint64_t* rare_ppm_out, void* stream);
 int fs_build_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t k,
-                         uint64_t* f_scratch_dev, void* buf_dev, void* stream);
+                         int32_t with_offsets, uint64_t* f_scratch_dev, void* buf_dev, void* stream);
 
 /*
  * Hot window of a rank directory for shared-memory staging: among all

@@ -201,12 +201,12 @@ def _declare(lib):
     lib.fs_build_zoned_rank.restype = ctypes.c_int
     lib.fs_build_zoned_rank.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _u64, _vp, _vp, _vp]
     lib.fs_count_words_bytes.restype = ctypes.c_uint64
-    lib.fs_count_words_bytes.argtypes = [_u64, _i32]
+    lib.fs_count_words_bytes.argtypes = [_u64, _i32, _u64]
     lib.fs_plan_count_words.restype = ctypes.c_int
-    lib.fs_plan_count_words.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _u64, _vp, _p_i32, _p_u64, _p_i32,
+    lib.fs_plan_count_words.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _u64, _i32, _vp, _p_i32, _p_u64,
                                         _p_u64, _p_u64, _vp]
     lib.fs_build_count_words.restype = ctypes.c_int
-    lib.fs_build_count_words.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _vp, _vp, _vp]
+    lib.fs_build_count_words.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _i32, _vp, _vp, _vp]
     lib.fs_build_hot_window.restype = ctypes.c_int
     lib.fs_build_hot_window.argtypes = [_i32, _vp, _u64, _u64, _vp, _p_u64, _p_u64, _p_u64, _p_u64, _p_u64, _vp]
     lib.fs_build_fused.restype = ctypes.c_int

@@ -460,14 +460,34 @@ SPARSE_RECORDS8_MAX_PAST_PPM = 5_000
 #: sparse layouts allowed; a tuning run or test may narrow it to one
 #: (a leading records format also skips the load rule)
 SPARSE_FORMATS = ("count-words", "two-level", "records8", "records8x3", "records", "records12")
-#: count words (fs_build_count_words) are tried first and used when at most
-#: this share (ppm) of the buckets lies in stripes of two or more knots --
-#: the uniform queries that take the probe's scan path; 0 skips them
+#: Count words (fs_build_count_words), by what is staged beside them:
+#: * all of X (tried before the group records): used when at most
+#:   COUNT_WORDS_MAX_XREAD_PPM of the buckets lie in knot-holding stripes
+#:   (cfg2 at 5%: 516 vs 496 / 436 G queries/s on group records; cfg5 N+1 =
+#:   8193 at 5%: 545 vs 465; N+1 = 16385 at 21%: 455 vs 506, records stay);
+#: * a byte per knot, X being too large to stage (tried after the 8-B group
+#:   records, before the 16-B ones): used when at most
+#:   COUNT_WORDS_MAX_RARE_PPM lie in stripes of two or more knots -- the
+#:   queries that take the probe's scan path (cfg5 N+1 = 32769 at 0.4%: 452
+#:   vs 430); or nothing, when at most COUNT_WORDS_MAX_L2_XREAD_PPM lie in
+#:   knot-holding stripes (every knot is then read through L2);
+#: * when no group record layout fits either, they replace the two-level
+#:   table up to COUNT_WORDS_LATE_MAX_RARE_PPM (cfg5 N+1 = 49153 / 65537: 413
+#:   / 378 vs 308 / 300), with all of shared memory.
+#: profiles/r02/count_words.txt.  COUNT_WORDS_MAX_RARE_PPM = 0 skips them.
+COUNT_WORDS_MAX_XREAD_PPM = 80_000
 COUNT_WORDS_MAX_RARE_PPM = 10_000
-#: ... and, when X cannot be staged beside the words, at most this share
-#: (ppm) lies in knot-holding stripes -- the queries that read X through L2
-#: (cfg5 N+1 = 32769: 9% of them, 363 G queries/s against 430 on group records)
 COUNT_WORDS_MAX_L2_XREAD_PPM = 20_000
+COUNT_WORDS_LATE_MAX_RARE_PPM = 50_000
+#: shared memory the count words and what is staged beside them may take
+#: before the late stage: past the 196 KB carve-out step the streaming loads
+#: are left 28 KB of L1 to be in flight through, and this probe is bound by
+#: their latency (cfg5 N+1 = 8193: 545 G queries/s at 142 KB with stripes
+#: twice as wide, 454 at 218 KB)
+COUNT_WORDS_BUDGET_BYTES = 195 * 1024
+#: count words with a byte per knot (its bucket inside its stripe) staged
+#: instead of an X that does not fit; False keeps the group records there
+COUNT_WORDS_OFFSETS = True
 
 #: hot-window staging budget: small enough that the L2-gather kernel keeps
 #: full occupancy (3-4 CTAs per SM) for the queries outside the window
@@ -491,11 +511,16 @@ ZONED = True
 ZONED_RANK_MAX_XREAD_PPM = 150_000
 
 
+#: planner override of the shared-memory budget in bytes (tuning: tools/tune.py --smem-kb); None = the device's
+SMEM_BUDGET_OVERRIDE = None
+
+
 def _smem_budget() -> int:
     import torch
 
     props = torch.cuda.get_device_properties(torch.cuda.current_device())
-    return int(getattr(props, "shared_memory_per_block_optin", 227 * 1024)) - 1024
+    full = int(getattr(props, "shared_memory_per_block_optin", 227 * 1024)) - 1024
+    return min(full, SMEM_BUDGET_OVERRIDE) if SMEM_BUDGET_OVERRIDE else full
 
 
 def _set_hot_window(plan, p: SortedPartition, idx: DirectIndex, rank) -> None:
@@ -667,13 +692,17 @@ def _plan_two_level(p: SortedPartition, idx: DirectIndex, f, budget: int):
     return None
 
 
-def _set_count_words(plan, p: SortedPartition, idx: DirectIndex, keep: list, f, budget: int) -> bool:
+def _set_count_words(plan, p: SortedPartition, idx: DirectIndex, keep: list, f, budget: int, modes=(1,),
+                     late: bool = False) -> bool:
     """Count words of K (fs_build_count_words): 8-B words of sixteen 2^k-bucket
     stripes with a 2-bit knot count each, one k for the table; a popcount
-    decode, one X compare when the query's stripe holds a knot, a short scan
-    when it holds several.  Used when the rank directory and X cannot be
-    staged together and at most COUNT_WORDS_MAX_RARE_PPM of the buckets lie in
-    stripes of two or more knots.  ``f``: n1 uint64 scratch."""
+    decode, one compare when the query's stripe holds a knot, a short scan
+    when it holds several.  Staged beside all of X (mode 1), beside a byte
+    per knot -- its bucket inside its stripe, so that X is read through L2
+    only for a knot in the query's own bucket (mode 2) -- or alone (mode 0).
+    Used when the rank directory and X cannot be staged together and the
+    table's statistics pass the COUNT_WORDS_* bounds; ``late`` = nothing but
+    the two-level table is left to try.  ``f``: n1 uint64 scratch."""
     n1 = len(p.values)
     x_bytes = (n1 * p.values.dtype.itemsize + 127) // 128 * 128
     if x_bytes + ((idx.r >> 5) + 1) * 8 <= budget:
@@ -681,24 +710,36 @@ def _set_count_words(plan, p: SortedPartition, idx: DirectIndex, keep: list, f, 
     lib = _lib.load()
     dt = fs_dtype(p.precision)
     x = p.device_values()
-    k, with_x = ctypes.c_int32(-1), ctypes.c_int32(0)
+    k = ctypes.c_int32(-1)
     nbytes, xread, rare = (ctypes.c_uint64(0) for _ in range(3))
-    rc = lib.fs_plan_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, f.data_ptr(), ctypes.byref(k),
-                                 ctypes.byref(nbytes), ctypes.byref(with_x), ctypes.byref(xread), ctypes.byref(rare),
-                                 _device.stream_ptr())
-    if rc == _lib.FS_TOO_LARGE:
-        return False
-    _lib.check(rc, what="fs_plan_count_words")
-    if rare.value > COUNT_WORDS_MAX_RARE_PPM or (not with_x.value and xread.value > COUNT_WORDS_MAX_L2_XREAD_PPM):
+    if not late:
+        budget = min(budget, COUNT_WORDS_BUDGET_BYTES)
+    for mode in modes:
+        if mode == 2 and not COUNT_WORDS_OFFSETS:
+            continue
+        rc = lib.fs_plan_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, mode, f.data_ptr(),
+                                     ctypes.byref(k), ctypes.byref(nbytes), ctypes.byref(xread), ctypes.byref(rare),
+                                     _device.stream_ptr())
+        if rc == _lib.FS_TOO_LARGE:
+            continue
+        _lib.check(rc, what="fs_plan_count_words")
+        if late:
+            ok = rare.value <= COUNT_WORDS_LATE_MAX_RARE_PPM
+        else:
+            ok = rare.value <= COUNT_WORDS_MAX_RARE_PPM and xread.value <= {
+                1: COUNT_WORDS_MAX_XREAD_PPM, 2: 10**6, 0: COUNT_WORDS_MAX_L2_XREAD_PPM}[mode]
+        if ok:
+            break
+    else:
         return False
     buf = _device.empty(int(nbytes.value), np.uint8)
-    rc = lib.fs_build_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, k.value, f.data_ptr(), buf.data_ptr(),
-                                  _device.stream_ptr())
+    rc = lib.fs_build_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, k.value, int(mode == 2),
+                                  f.data_ptr(), buf.data_ptr(), _device.stream_ptr())
     _lib.check(rc, what="fs_build_count_words")
     plan.sparse = buf.data_ptr()
     plan.sparse_format = _lib.SPARSE_COUNT
     plan.sparse_shift = k.value
-    plan.sparse_ndense = 0
+    plan.sparse_ndense = n1 if mode == 2 else 0
     keep.append(buf)
     return True
 
@@ -723,7 +764,8 @@ def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) ->
     # 16-bit ones); then 8-B and 16-B records with X read through L2 (fine
     # for uniform queries, but streams with many exact-knot queries, like
     # cfg2's 1%, lose: 433 -> 423).
-    if "count-words" in SPARSE_FORMATS and COUNT_WORDS_MAX_RARE_PPM and _set_count_words(plan, p, idx, keep, f, budget):
+    count_words = "count-words" in SPARSE_FORMATS and COUNT_WORDS_MAX_RARE_PPM
+    if count_words and _set_count_words(plan, p, idx, keep, f, budget, (1,)):
         return
 
     def records(name, wx):
@@ -746,8 +788,14 @@ def _set_sparse_table(plan, p: SortedPartition, idx: DirectIndex, keep: list) ->
     two = _plan_two_level(p, idx, f, budget) if "two-level" in SPARSE_FORMATS else None
     load = n1 / ((idx.r >> two[0]) + 1) if two else None
     if load is None or load >= SPARSE_RECORDS_MIN_LOAD:
-        if wide_records(1) or records("records8", (0,)) or records("records8x3", (0,)) or wide_records(0):
+        if wide_records(1) or records("records8", (0,)) or records("records8x3", (0,)):
             return
+        if count_words and _set_count_words(plan, p, idx, keep, f, budget, (2, 0)):
+            return
+        if wide_records(0):
+            return
+    if count_words and _set_count_words(plan, p, idx, keep, f, budget, (1, 2), late=True):
+        return
     if two is None:
         return
     shift, ndense, nbytes = two

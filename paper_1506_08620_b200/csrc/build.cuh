@@ -402,6 +402,14 @@ __global__ void fill_count_words_kernel(const uint64_t* __restrict__ f, uint64_t
   }
 }
 
+// Knot offsets beside the count words (fs_build_count_words with offsets):
+// O[i] = f_i mod 2^k, knot i's bucket inside its stripe (k <= 8: one byte).
+__global__ void fill_count_offsets_kernel(const uint64_t* __restrict__ f, uint64_t n1, int k, uint8_t* __restrict__ O,
+                                          uint64_t npad) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += (uint64_t)gridDim.x * blockDim.x)
+    O[i] = i < n1 ? (uint8_t)(__ldg(f + i) & ((1ull << k) - 1)) : (uint8_t)0;
+}
+
 // Dense super-buckets of the sparse table (more than kDenseOcc knots): one
 // CTA per dense slot builds the 2^s-bit knot mask of super-bucket
 // J = dense_j[slot] in W = 2^(s-5) words plus per-word knot prefix counts,

@@ -59,6 +59,7 @@ constexpr int kZonedMaxStripe = 10;  // striped rank words: a mask bit per 2^k b
 constexpr int kCountWordShift = 4;
 constexpr int kCountMaxShift = 27;
 constexpr uint32_t kCountFlag = 0x80000000u;
+constexpr int kCountMaxOffsetShift = 8;  // knot offsets beside the words are bytes: stripes of at most 2^8 buckets
 
 // Bounds-checked builds (FSG_BOUNDS_CHECK=1, tools/bounds_check.sh): every
 // table gather of the search probes checks its index against the table's

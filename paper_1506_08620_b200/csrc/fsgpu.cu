@@ -173,7 +173,8 @@ int validate_plan(const fs_plan* p) {
                         p->sparse_format != FS_SPARSE_ZONED_RANK && p->sparse_format != FS_SPARSE_COUNT))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
       if (p->sparse && p->sparse_format == FS_SPARSE_COUNT &&
-          (fs_count_words_bytes(p->r, p->sparse_shift) == 0 || p->n1 - 1 >= (1ull << 31)))
+          (fs_count_words_bytes(p->r, p->sparse_shift, p->sparse_ndense) == 0 || p->n1 - 1 >= (1ull << 31) ||
+           (p->sparse_ndense != 0 && p->sparse_ndense != p->n1)))
         return fail(FS_INVALID_ARG, "count-word parameters out of range");
       if (p->sparse && is_zoned(p->sparse_format)) {
         if (fs_zoned_bytes(p->r, p->sparse_shift, p->sparse_ndense) == 0 || p->r >= (1ull << 32) ||
@@ -270,7 +271,8 @@ Placement place(const fs_plan* p) {
       (p->sparse_format == FS_SPARSE_COUNT || (p->sparse_shift >= 5 && p->sparse_shift <= 16))) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
-    const uint64_t cfb = p->sparse_format == FS_SPARSE_COUNT ? fs_count_words_bytes(p->r, p->sparse_shift)
+    const uint64_t cfb = p->sparse_format == FS_SPARSE_COUNT
+                             ? fs_count_words_bytes(p->r, p->sparse_shift, p->sparse_ndense)
                          : p->sparse_format != FS_SPARSE_TWO_LEVEL
                              ? fs_sparse_rec_bytes(p->sparse_format, p->n1, p->r, p->sparse_shift, p->sparse_ndense)
                              : fs_sparse_bytes(p->n1, p->r, p->sparse_shift, p->sparse_ndense);
@@ -279,7 +281,8 @@ Placement place(const fs_plan* p) {
     // the rank directory does, with a dearer decode: the staged directory
     // wins whenever it fits alone (gaps U[1,5], N+1 = 65535, R / N = 3:
     // 555 vs 270 G queries/s f32, 405 vs 226 f64; profiles/r02/unif_layouts.txt)
-    const bool sparse_xs = align128(xb) + cfb <= budget;
+    // (count words built with knot offsets are the layout for an X that is not staged)
+    const bool sparse_xs = align128(xb) + cfb <= budget && !(p->sparse_format == FS_SPARSE_COUNT && p->sparse_ndense);
     const bool rank_alone_fits = use_rank && dir_b <= budget;
     if (!rank_fits && cfb <= budget && (sparse_xs || !rank_alone_fits)) {
       pl.sparse = pl.ks = true;
@@ -561,8 +564,8 @@ struct UnrollFor<double, SparseRecProbe<double, SLOTS, XS, OVF>> {
 #ifndef FSG_UNROLL_F64_COUNT
 #define FSG_UNROLL_F64_COUNT 3
 #endif
-template <bool XS>
-struct UnrollFor<double, CountWordProbe<double, XS>> {
+template <int XM>
+struct UnrollFor<double, CountWordProbe<double, XM>> {
   static constexpr int value = FSG_UNROLL_F64_COUNT;
 };
 // The light three-offset probe takes a third group with int32 outputs (cfg2
@@ -622,8 +625,8 @@ struct BoundedFor<T, ZonedProbe<T, STRIPED>, OutT> {
 #ifndef FSG_COUNT_BOUNDED
 #define FSG_COUNT_BOUNDED 1
 #endif
-template <typename T, bool XS, typename OutT>
-struct BoundedFor<T, CountWordProbe<T, XS>, OutT> {
+template <typename T, int XM, typename OutT>
+struct BoundedFor<T, CountWordProbe<T, XM>, OutT> {
   static constexpr bool value = FSG_COUNT_BOUNDED;
 };
 template <typename T, int SLOTS, bool XS, bool OVF, typename OutT>
@@ -819,8 +822,9 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
         return launch_probe<T, OutT, ZonedProbe<T, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.zoned) return launch_probe<T, OutT, ZonedProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_COUNT) {
-        if (pl.xs) return launch_probe<T, OutT, CountWordProbe<T, true>>(d, pl, z, m, out, fb, base, st);
-        return launch_probe<T, OutT, CountWordProbe<T, false>>(d, pl, z, m, out, fb, base, st);
+        if (pl.xs) return launch_probe<T, OutT, CountWordProbe<T, 1>>(d, pl, z, m, out, fb, base, st);
+        if (p->sparse_ndense) return launch_probe<T, OutT, CountWordProbe<T, 2>>(d, pl, z, m, out, fb, base, st);
+        return launch_probe<T, OutT, CountWordProbe<T, 0>>(d, pl, z, m, out, fb, base, st);
       }
       if (pl.sparse && p->sparse_format == FS_SPARSE_RECORDS)
         return dispatch_records<T, OutT, 6>(d, pl, p->sparse_ndense != 0, z, m, out, fb, base, st);
@@ -1393,32 +1397,35 @@ int zoned_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, 
 }
 }  // namespace
 
-uint64_t fs_count_words_bytes(uint64_t r, int32_t k) {
-  if (k < 0 || k > kCountMaxShift || r >= (1ull << 32)) return 0;
-  return 8 * ((r >> (k + kCountWordShift)) + 1);
+uint64_t fs_count_words_bytes(uint64_t r, int32_t k, uint64_t noff) {
+  if (k < 0 || k > kCountMaxShift || r >= (1ull << 32) || (noff && k > kCountMaxOffsetShift)) return 0;
+  return 8 * ((r >> (k + kCountWordShift)) + 1) + ((noff + 15) & ~15ull);
 }
 
 int fs_plan_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t budget_bytes,
-                        uint64_t* f_scratch_dev, int32_t* k_out, uint64_t* bytes_out, int32_t* with_x_out,
+                        int32_t mode, uint64_t* f_scratch_dev, int32_t* k_out, uint64_t* bytes_out,
                         uint64_t* xread_ppm_out, uint64_t* rare_ppm_out, void* stream) {
   if (!x_dev || !f_scratch_dev || n1 < 2 || !k_out) return fail(FS_INVALID_ARG, "bad arguments");
   if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  if (mode < 0 || mode > 2) return fail(FS_INVALID_ARG, "mode: 0 words alone, 1 beside X, 2 beside knot offsets");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "count words need R < 2^32, N < 2^31");
   const uint64_t es = dtype == FS_F32 ? 4 : 8;
-  // all of X beside the words when it takes at most half the budget, else none of it
-  const uint64_t xb = align128(n1 * es) <= budget_bytes / 2 ? align128(n1 * es) : 0;
-  if (budget_bytes < xb + 128 + 8) return fail(FS_TOO_LARGE, "no count-word layout fits the budget");
-  const uint64_t table_budget = budget_bytes - xb - 128;
+  // what is staged beside the words: nothing, all of X, or a byte per knot
+  const uint64_t beside = mode == 1 ? align128(n1 * es) : mode == 2 ? ((n1 + 15) & ~15ull) : 0;
+  if (budget_bytes < beside + 128 + 8) return fail(FS_TOO_LARGE, "no count-word layout fits the budget");
+  const uint64_t table_budget = budget_bytes - beside - 128;
   int k = 0;
-  while (k <= kCountMaxShift && fs_count_words_bytes(r, k) > table_budget) ++k;
+  while (k <= kCountMaxShift && fs_count_words_bytes(r, k, 0) > table_budget) ++k;
+  if (mode == 2 && k > kCountMaxOffsetShift)
+    return fail(FS_TOO_LARGE, "knot offsets are bytes: no stripe shift <= 8 fits the budget");
   if (k > kCountMaxShift) return fail(FS_TOO_LARGE, "no count-word layout fits the budget");
   // more knots than stripes: nearly every query would scan (the planner's caller would refuse it anyway)
   if (n1 > ((r >> k) + 1)) return fail(FS_TOO_LARGE, "count words: more knots than stripes");
   std::vector<uint64_t> f;
   int rc = zoned_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, f, as_stream(stream));
   if (rc) return rc;
-  // buckets whose queries read X (stripes holding a knot) and whose queries
-  // scan (stripes holding two or more; every stripe of a flagged word)
+  // buckets whose queries read X or a knot offset (stripes holding a knot) and
+  // whose queries scan (stripes holding two or more; every stripe of a flagged word)
   uint64_t xread = 0, rare = 0;
   const uint64_t sw = 1ull << k, ww = 1ull << (k + kCountWordShift);
   for (size_t i = 0; i < f.size();) {
@@ -1431,26 +1438,31 @@ int fs_plan_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h,
     i = e;
   }
   *k_out = k;
-  if (bytes_out) *bytes_out = fs_count_words_bytes(r, k);
-  if (with_x_out) *with_x_out = xb != 0;
+  if (bytes_out) *bytes_out = fs_count_words_bytes(r, k, mode == 2 ? n1 : 0);
   if (xread_ppm_out) *xread_ppm_out = (uint64_t)((long double)xread * 1e6L / (long double)(r + 1));
   if (rare_ppm_out) *rare_ppm_out = (uint64_t)((long double)std::min<uint64_t>(rare, r + 1) * 1e6L / (long double)(r + 1));
   return FS_OK;
 }
 
 int fs_build_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t k,
-                         uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
+                         int32_t with_offsets, uint64_t* f_scratch_dev, void* buf_dev, void* stream) {
   if (!x_dev || !f_scratch_dev || !buf_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
   if (dtype != FS_F32 && dtype != FS_F64) return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
   if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "count words need R < 2^32, N < 2^31");
-  const uint64_t bytes = fs_count_words_bytes(r, k);
+  const uint64_t bytes = fs_count_words_bytes(r, k, with_offsets ? n1 : 0);
   if (!bytes) return fail(FS_INVALID_ARG, "stripe shift out of range");
   cudaStream_t s = as_stream(stream);
   int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, s);
   if (rc) return rc;
-  const uint64_t nwords = bytes / 8;
+  const uint64_t nwords = fs_count_words_bytes(r, k, 0) / 8;
   fill_count_words_kernel<<<grid_1d(nwords, 256), 256, 0, s>>>(f_scratch_dev, n1, k, static_cast<uint2*>(buf_dev), nwords);
   FS_CUDA(cudaGetLastError());
+  if (with_offsets) {
+    const uint64_t npad = (n1 + 15) & ~15ull;
+    fill_count_offsets_kernel<<<grid_1d(npad, 256), 256, 0, s>>>(f_scratch_dev, n1, k,
+                                                                static_cast<uint8_t*>(buf_dev) + 8 * nwords, npad);
+    FS_CUDA(cudaGetLastError());
+  }
   return FS_OK;
 }
 

@@ -620,12 +620,19 @@ struct SparseRecProbe {
 // planner picks the finest k that fits and reports how many queries go the
 // rare way (uniformly drawn knots: ~lambda^2 / 2 of them at lambda knots per
 // stripe).  A popcount decode instead of the group records' SWAR counts.
-template <typename T, bool XS>
+//
+// XM = where the stripe's knot is compared: 1 = X staged in shared memory;
+// 0 = X read through L2; 2 = X too large to stage but one byte per knot is:
+// O[i] = knot i's bucket inside its stripe (k <= 8), staged after the words.
+// A knot in a lower bucket than the query's lies below z and one in a higher
+// bucket above it (monotone buckets again), so X itself is read -- through
+// L2 -- only when both share a bucket (2^-k of the stripe's queries).
+template <typename T, int XM>
 struct CountWordProbe {
   const T* X;
-  uint32_t xs, ws;  // shared addresses of X (XS) and of the words
+  uint32_t xs, ws, os;  // shared addresses of X (XM 1), the words, the offsets (XM 2)
   T h, x0;
-  uint32_t r, k, n1;
+  uint32_t r, k, n1, smask;
   __device__ __forceinline__ CountWordProbe(const DevPlan<T>& p, unsigned char* smem) {
     n1 = (uint32_t)p.n1;
     X = p.x;
@@ -637,6 +644,8 @@ struct CountWordProbe {
     x0 = p.x0;
     r = (uint32_t)p.r;
     k = (uint32_t)p.sparse_shift;
+    smask = (1u << k) - 1u;
+    os = ws + 8u * ((r >> (k + kCountWordShift)) + 1u);
   }
   __device__ __forceinline__ uint32_t bucket(T z) const {
     uint32_t j = trunc_to<uint32_t>(mul_rn(sub_rn(z, x0), h));
@@ -651,7 +660,7 @@ struct CountWordProbe {
   }
   __device__ __forceinline__ T xat(uint32_t t) const {
     FSG_BOUND(t < n1);
-    if constexpr (XS) {
+    if constexpr (XM == 1) {
       T v;
       if constexpr (sizeof(T) == 4) asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xs + 4u * t));
       else asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(xs + 8u * t));
@@ -659,6 +668,12 @@ struct CountWordProbe {
     } else {
       return __ldg(X + t);
     }
+  }
+  __device__ __forceinline__ uint32_t oat(uint32_t t) const {
+    uint32_t o;
+    FSG_BOUND(t < n1 && os + t + 1u - xs <= dyn_smem_bytes());
+    asm("ld.shared.u8 %0, [%1];" : "=r"(o) : "r"(os + t));
+    return o;
   }
   // knots in earlier stripes -> t, knots in the query's stripe -> c
   __device__ __forceinline__ void resolve(const uint2& g, uint32_t j, uint32_t& t, uint32_t& c) const {
@@ -669,14 +684,56 @@ struct CountWordProbe {
     t = g.y + __popc(m) + __popc(m & 0xAAAAAAAAu);  // the flag bit rides along; flagged words go the rare way
     c = (g.x >> b2) & 3u;
   }
-  __device__ __forceinline__ int64_t finish(const uint2& g, uint32_t t, uint32_t c, T z) const {
-    T xv = z;
-    if (c != 0 && (int32_t)g.y >= 0) xv = xat(t);
-    uint32_t res = t - ((c == 0 || z < xv) ? 1u : 0u);
-    if (c > 1u || (int32_t)g.y < 0) {  // rare: scan the stripe's (a flagged word's) knots
-      uint32_t e = (int32_t)g.y < 0 ? (g.y & ~kCountFlag) : t;
-      while (e < n1 && xat(e) <= z) ++e;
-      res = e - 1u;
+  __device__ __forceinline__ int64_t finish(const uint2& g, uint32_t j, uint32_t t, uint32_t c, T z) const {
+    const bool flagged = (int32_t)g.y < 0;
+    uint32_t res;
+    bool rare = c > 1u || flagged;
+    // the stripe's first knot (its offset byte / X[t]) through a predicated
+    // load: a branch here would put a reconvergence region, and an exposed
+    // load latency, around every query of the group
+    const uint32_t take = (c != 0u && !flagged) ? 1u : 0u;
+    FSG_BOUND(!take || t < n1);
+    if constexpr (XM == 2) {
+      const uint32_t jo = j & smask;
+      uint32_t o = jo + 1u;  // no knot: neither below nor beside the query
+      asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u8 %0, [%1];\n\t}" : "+r"(o) : "r"(os + t), "r"(take));
+      res = t - (o < jo ? 0u : 1u);
+      rare = rare || o == jo;
+    } else {
+      T xv = z;
+      if constexpr (XM == 1) {
+        if constexpr (sizeof(T) == 4)
+          asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.f32 %0, [%1];\n\t}" : "+f"(xv) : "r"(xs + 4u * t), "r"(take));
+        else
+          asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.f64 %0, [%1];\n\t}" : "+d"(xv) : "r"(xs + 8u * t), "r"(take));
+      } else {
+        if constexpr (sizeof(T) == 4)
+          asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.nc.f32 %0, [%1];\n\t}" : "+f"(xv) : "l"(X + t), "r"(take));
+        else
+          asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.nc.f64 %0, [%1];\n\t}" : "+d"(xv) : "l"(X + t), "r"(take));
+      }
+      res = t - ((take == 0u || z < xv) ? 1u : 0u);
+    }
+    if (rare) {
+      if (XM == 2 && !flagged) {
+        // the stripe's knots by their buckets; X decides only a shared bucket
+        // (a gap-1 table holds one knot per bucket: nothing after it counts)
+        const uint32_t jo = j & smask;
+        res = t - 1u;
+        for (uint32_t e = 0; e < c; ++e) {
+          const uint32_t o = oat(t + e);
+          if (o < jo) {
+            ++res;
+          } else {
+            if (o == jo && xat(t + e) <= z) ++res;
+            break;
+          }
+        }
+      } else {  // scan the stripe's (a flagged word's) knots
+        uint32_t e = flagged ? (g.y & ~kCountFlag) : t;
+        while (e < n1 && xat(e) <= z) ++e;
+        res = e - 1u;
+      }
     }
     return (int64_t)(int32_t)res;
   }
@@ -685,7 +742,7 @@ struct CountWordProbe {
     const uint2 g = word(j);
     uint32_t t, c;
     resolve(g, j, t, c);
-    return finish(g, t, c, z);
+    return finish(g, j, t, c, z);
   }
   // every word load of a group issued before the first is resolved
 #ifndef FSG_COUNT_GROUP
@@ -709,7 +766,7 @@ struct CountWordProbe {
         if (g0 + q >= N) break;
         uint32_t t, c;
         resolve(g[q], j[q], t, c);
-        o[g0 + q] = (R)finish(g[q], t, c, z[g0 + q]);
+        o[g0 + q] = (R)finish(g[q], j[q], t, c, z[g0 + q]);
       }
     }
   }

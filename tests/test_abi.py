@@ -105,7 +105,8 @@ def test_argument_validation_without_gpu():
         assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
         assert b"count-word" in lib.fs_last_error()
     cb = lib.fs_count_words_bytes
-    assert cb(1000, 0) == 8 * 63 and cb(1000, 6) == 8 and cb(1000, 27) == 8 and cb(1000, 28) == 0 and cb(1 << 32, 3) == 0
+    assert cb(1000, 0, 0) == 8 * 63 and cb(1000, 6, 0) == 8 and cb(1000, 27, 0) == 8 and cb(1000, 28, 0) == 0
+    assert cb(1 << 32, 3, 0) == 0 and cb(1000, 6, 4) == 8 + 16 and cb(1000, 9, 4) == 0  # offsets: bytes, k <= 8
     rb = lib.fs_sparse_rec_bytes
     assert rb(_lib.SPARSE_RECORDS, 4, 1000, 15, 0) == 0 and rb(_lib.SPARSE_RECORDS, 4, 1000, 5, 0) == 16 * 33
     assert rb(_lib.SPARSE_RECORDS8, 4, 1000, 5, 0) == (8 * 33 + 15) // 16 * 16

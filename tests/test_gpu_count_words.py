@@ -4,7 +4,7 @@ statistics and the device buffer against a numpy construction from the
 oracle's knot buckets (bit for bit), and every answer against the oracle
 (batch.py:315-317 semantics) on tables of uniformly drawn knots (cfg2, cfg5),
 stripes holding one, two, three and more knots (flagged words), every knot
-and its neighbours, word / stripe edges, X staged and read through L2, f32
+and its neighbours, word / stripe edges, X staged, read through L2 and replaced by staged knot offsets, f32
 and f64 with int32 and int64 outputs, the last bucket R and out-of-domain
 lanes."""
 
@@ -17,7 +17,7 @@ from oracle import fs_oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-WORD_SHIFT, MAX_SHIFT, FLAG = 4, 27, 0x80000000
+WORD_SHIFT, MAX_SHIFT, MAX_OFFSET_SHIFT, FLAG = 4, 27, 8, 0x80000000
 
 
 def _fs():
@@ -26,21 +26,20 @@ def _fs():
     return fs
 
 
-def words_bytes(r, k):
-    return 8 * ((r >> (k + WORD_SHIFT)) + 1)
+def words_bytes(r, k, noff=0):
+    return 8 * ((r >> (k + WORD_SHIFT)) + 1) + (noff + 15) // 16 * 16
 
 
-def expected_plan(f, r, n1, es, budget):
-    """(k, with_x, xread_ppm, rare_ppm) as fs_plan_count_words picks them, or None."""
-    xb = (n1 * es + 127) // 128 * 128
-    xb = xb if xb <= budget // 2 else 0
-    if budget < xb + 128 + 8:
+def expected_plan(f, r, n1, es, budget, mode):
+    """(k, xread_ppm, rare_ppm) as fs_plan_count_words picks them for ``mode`` (1: beside
+    all of X; 2: beside a byte per knot, k <= 8; 0: words alone), or None."""
+    beside = {0: 0, 1: (n1 * es + 127) // 128 * 128, 2: (n1 + 15) // 16 * 16}[mode]
+    if budget < beside + 128 + 8:
         return None
-    tb = budget - xb - 128
     k = 0
-    while k <= MAX_SHIFT and words_bytes(r, k) > tb:
+    while k <= MAX_SHIFT and words_bytes(r, k) > budget - beside - 128:
         k += 1
-    if k > MAX_SHIFT or n1 > (r >> k) + 1:
+    if k > MAX_SHIFT or (mode == 2 and k > MAX_OFFSET_SHIFT) or n1 > (r >> k) + 1:
         return None
     stripe, cnt = np.unique(f >> k, return_counts=True)
     width = np.minimum(1 << k, r + 1 - (stripe << k))
@@ -49,12 +48,12 @@ def expected_plan(f, r, n1, es, budget):
     ws = k + WORD_SHIFT
     rare += int(np.minimum(1 << ws, r + 1 - ((stripe[cnt >= 4] >> WORD_SHIFT) << ws)).sum())
     rare = min(rare, r + 1)
-    return k, int(xb != 0), xread * 10**6 // (r + 1), rare * 10**6 // (r + 1)
+    return k, xread * 10**6 // (r + 1), rare * 10**6 // (r + 1)
 
 
 def _same_plan(got, exp):
-    """k and the X rule exactly; the ppm statistics to one part (the library rounds in long double)."""
-    return tuple(got[:2]) == tuple(exp[:2]) and all(abs(int(a) - int(b)) <= 1 for a, b in zip(got[2:], exp[2:]))
+    """k exactly; the ppm statistics to one part (the library rounds in long double)."""
+    return got[0] == exp[0] and all(abs(int(a) - int(b)) <= 1 for a, b in zip(got[1:], exp[1:]))
 
 
 def expected_words(f, r, k):
@@ -78,9 +77,10 @@ def expected_words(f, r, k):
     return out.astype(np.uint32), top, flagged
 
 
-def with_count_words(fs, p, prep, budget, k=None):
-    """Plan (or take ``k``) and build count words on prep's table and set them
-    on its plan.  Returns (buffer, k, with_x, xread_ppm, rare_ppm) or None."""
+def with_count_words(fs, p, prep, budget, k=None, offsets=False, mode=None):
+    """Plan for ``mode`` (or take ``k`` and ``offsets``) and build count words on
+    prep's table and set them on its plan.  Returns (buffer, k, xread_ppm,
+    rare_ppm) or None."""
     from paper_1506_08620_b200 import _device, _lib
 
     idx = prep.structure
@@ -88,20 +88,21 @@ def with_count_words(fs, p, prep, budget, k=None):
     dt = _lib.FS_F32 if p.precision == "single" else _lib.FS_F64
     n1 = len(p.values)
     f_dev = _device.empty(n1, np.uint64)
-    kk, wx = ctypes.c_int32(-1), ctypes.c_int32(0)
+    kk = ctypes.c_int32(-1)
     nbytes, xread, rare = (ctypes.c_uint64(0) for _ in range(3))
     x = p.device_values()
     if k is None:
-        rc = lib.fs_plan_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, f_dev.data_ptr(),
-                                     ctypes.byref(kk), ctypes.byref(nbytes), ctypes.byref(wx), ctypes.byref(xread),
-                                     ctypes.byref(rare), _device.stream_ptr())
+        rc = lib.fs_plan_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, budget, mode, f_dev.data_ptr(),
+                                     ctypes.byref(kk), ctypes.byref(nbytes), ctypes.byref(xread), ctypes.byref(rare),
+                                     _device.stream_ptr())
         if rc == _lib.FS_TOO_LARGE:
             return None
         _lib.check(rc)
-        k = kk.value
-        assert nbytes.value == lib.fs_count_words_bytes(idx.r, k) == words_bytes(idx.r, k)
-    buf = _device.empty(words_bytes(idx.r, k), np.uint8)
-    _lib.check(lib.fs_build_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, k, f_dev.data_ptr(),
+        k, offsets = kk.value, mode == 2
+        assert nbytes.value == lib.fs_count_words_bytes(idx.r, k, n1 if offsets else 0)
+        assert nbytes.value == words_bytes(idx.r, k, n1 if offsets else 0)
+    buf = _device.empty(words_bytes(idx.r, k, n1 if offsets else 0), np.uint8)
+    _lib.check(lib.fs_build_count_words(dt, x.data_ptr(), n1, float(idx.h), idx.r, k, int(offsets), f_dev.data_ptr(),
                                         buf.data_ptr(), _device.stream_ptr()))
     plan = prep.plan
     plan.records = None
@@ -109,9 +110,22 @@ def with_count_words(fs, p, prep, budget, k=None):
     plan.sparse = buf.data_ptr()
     plan.sparse_format = _lib.SPARSE_COUNT
     plan.sparse_shift = k
-    plan.sparse_ndense = 0
+    plan.sparse_ndense = n1 if offsets else 0
     plan.hot_word0 = plan.hot_words = plan.hot_knot0 = plan.hot_knots = 0
-    return buf, k, wx.value, xread.value, rare.value
+    return buf, k, xread.value, rare.value
+
+
+def _check_buffer(buf, f, r, k, offsets):
+    """Words (and offset bytes) bit for bit; returns (largest stripe count, flagged words)."""
+    want_words, top, flagged = expected_words(f, r, k)
+    got = buf.cpu().numpy()
+    assert np.array_equal(got[: want_words.nbytes].view(np.uint32).reshape(-1, 2), want_words), k
+    if offsets:
+        assert np.array_equal(got[want_words.nbytes: want_words.nbytes + len(f)], (f & ((1 << k) - 1)).astype(np.uint8)), k
+        assert len(got) == want_words.nbytes + (len(f) + 15) // 16 * 16 and not got[want_words.nbytes + len(f):].any()
+    else:
+        assert len(got) == want_words.nbytes
+    return top, flagged
 
 
 def _buffer_of(prep, ptr):
@@ -156,12 +170,12 @@ def test_count_words_chosen_for_cfg2(cuda, label):
     xs = p.values
     idx = prep.structure
     f = orc.knot_buckets(xs, idx.h).astype(np.int64)
-    budget = batch._smem_budget() - 512
-    k, with_x, xread, rare = expected_plan(f, idx.r, len(xs), xs.itemsize, budget)
-    assert (prep.plan.sparse_shift, with_x) == (k, 1) and rare <= batch.COUNT_WORDS_MAX_RARE_PPM
-    want_words, top, flagged = expected_words(f, idx.r, k)
-    got = _buffer_of(prep, prep.plan.sparse).cpu().numpy().view(np.uint32).reshape(-1, 2)
-    assert np.array_equal(got, want_words)
+    budget = min(batch._smem_budget() - 512, batch.COUNT_WORDS_BUDGET_BYTES)
+    k, xread, rare = expected_plan(f, idx.r, len(xs), xs.itemsize, budget, 1)
+    assert (prep.plan.sparse_shift, prep.plan.sparse_ndense) == (k, 0)
+    assert rare <= batch.COUNT_WORDS_MAX_RARE_PPM and xread <= batch.COUNT_WORDS_MAX_XREAD_PPM
+    assert pl["smem_bytes"] <= 196 * 1024  # under the carve-out step that leaves L1 only 28 KB
+    top, flagged = _check_buffer(_buffer_of(prep, prep.plan.sparse), f, idx.r, k, False)
     assert top >= 2  # uniform draws: some stripes hold two knots (seed 2: one holds four, a flagged word)
     z = np.concatenate([
         workloads.queries_host("cfg2", p, 300_000, seed=5), _all_knots(xs), _edge_queries(xs, idx.h, idx.r, k),
@@ -175,32 +189,58 @@ def test_count_words_chosen_for_cfg2(cuda, label):
     assert np.array_equal(out32, want)
 
 
-def test_count_words_rule_keeps_records_without_x(cuda):
-    """cfg5 N+1 = 32769: X (256 KB) cannot be staged and 9% of the buckets lie
-    in knot-holding stripes, so the planner keeps the group records; forced,
-    the count words (every knot read through L2) give the same answers."""
+@pytest.mark.parametrize("size", [32769, 65537])
+def test_count_words_with_offsets_for_cfg5(cuda, size):
+    """cfg5 N+1 = 32769 (and 65537, where no group record layout fits and the
+    count words replace the two-level table): X cannot be staged, a byte per knot can:
+    prepare() stages count words (k = 5) and the knots' in-stripe buckets, and
+    reads X through L2 only for a knot in the query's own bucket.  Plan, words
+    and offsets bit-exact; answers equal the oracle at every knot and its
+    neighbours, layout and bucket edges and uniform queries.  With the
+    offsets switched off the planner keeps the group records (9% of the
+    buckets lie in knot-holding stripes: too many L2 reads); forced, the
+    plain words give the same answers."""
     fs = _fs()
     from paper_1506_08620_b200 import batch, workloads
 
-    p = workloads.knots("cfg5", n1=32769)
-    prep = fs.prepare("direct", p)
-    assert prep.placement()["sparse_format"].startswith("records")
+    p = workloads.knots("cfg5", n1=size)
     xs = p.values
+    prep = fs.prepare("direct", p)
+    pl = prep.placement()
+    assert pl["smem_sparse"] and pl["sparse_format"] == "count-words" and not pl["smem_x"], pl
     idx = prep.structure
     f = orc.knot_buckets(xs, idx.h).astype(np.int64)
-    got = with_count_words(fs, p, prep, batch._smem_budget() - 512)
-    assert got is not None
-    buf, k, with_x, xread, rare = got
-    assert _same_plan((k, with_x, xread, rare), expected_plan(f, idx.r, len(xs), xs.itemsize, batch._smem_budget() - 512))
-    assert with_x == 0 and xread > batch.COUNT_WORDS_MAX_L2_XREAD_PPM
-    pl = prep.placement()
-    assert pl["sparse_format"] == "count-words" and not pl["smem_x"], pl
-    want_words, top, _ = expected_words(f, idx.r, k)
-    assert np.array_equal(buf.cpu().numpy().view(np.uint32).reshape(-1, 2), want_words) and top >= 2
+    # 32769: tried before the 16-B group records, within the carve-out budget; 65537: the late
+    # stage (nothing but the two-level table left), with all of shared memory
+    budget = batch._smem_budget() - 512
+    if size == 32769:
+        budget = min(budget, batch.COUNT_WORDS_BUDGET_BYTES)
+    assert expected_plan(f, idx.r, len(xs), xs.itemsize, budget, 1) is None  # X does not fit beside any words
+    k, xread, rare = expected_plan(f, idx.r, len(xs), xs.itemsize, budget, 2)
+    assert (prep.plan.sparse_shift, prep.plan.sparse_ndense) == (k, len(xs)) and k <= MAX_OFFSET_SHIFT
+    top, _ = _check_buffer(_buffer_of(prep, prep.plan.sparse), f, idx.r, k, True)
+    assert top >= 2
     z = np.concatenate([workloads.queries_host("cfg5", p, 300_000, seed=5), _all_knots(xs),
-                        _edge_queries(xs, idx.h, idx.r, k)]).astype(xs.dtype)
+                        _edge_queries(xs, idx.h, idx.r, k), orc.boundary_probes(xs),
+                        orc.bucket_edge_probes(xs, idx.h, idx.r, 100_000, seed=4)]).astype(xs.dtype)
     z = z[(z >= xs[0]) & (z < xs[-1])]
-    assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(xs, z))
+    want = orc.rank_oracle(xs, z)
+    assert np.array_equal(fs.run_batch(prep, z), want)
+    out32 = np.empty(len(z), dtype=np.int32)
+    fs.batch_search(fs.LaneConfig(1, "direct", prep), z, out32)
+    assert np.array_equal(out32, want)
+    saved = batch.COUNT_WORDS_OFFSETS
+    try:
+        batch.COUNT_WORDS_OFFSETS = False
+        prep = fs.prepare("direct", p)
+    finally:
+        batch.COUNT_WORDS_OFFSETS = saved
+    assert prep.placement()["sparse_format"] != "count-words"  # group records (32769) / the two-level table
+    buf, k0, *_ = with_count_words(fs, p, prep, 0, k=5)
+    pl = prep.placement()
+    assert pl["sparse_format"] == "count-words" and not pl["smem_x"] and prep.plan.sparse_ndense == 0, pl
+    _check_buffer(buf, f, idx.r, 5, False)
+    assert np.array_equal(fs.run_batch(prep, z), want)
 
 
 def _clumped(n, dtype, seed, clump=(0, 3)):
@@ -236,26 +276,27 @@ def test_count_words_every_shift(cuda, dtype, clump):
     for k in range(0, kmax + 1):
         if words_bytes(idx.r, k) + len(xs) * xs.itemsize + 256 > 220_000:
             continue
-        buf, *_ = with_count_words(fs, p, prep, 0, k=k)
-        pl = prep.placement()
-        assert pl["sparse_format"] == "count-words" and pl["smem_x"], (k, pl)
-        want_words, top, flagged = expected_words(f, idx.r, k)
-        assert np.array_equal(buf.cpu().numpy().view(np.uint32).reshape(-1, 2), want_words), k
-        seen_top, seen_flagged = max(seen_top, top), max(seen_flagged, flagged)
         z = np.concatenate([base, _edge_queries(xs, idx.h, idx.r, k)]).astype(dtype)
         z = z[(z >= xs[0]) & (z < xs[-1])]
         want = orc.rank_oracle(xs, z)
-        assert np.array_equal(fs.run_batch(prep, z), want), k
-        out32 = np.empty(len(z), dtype=np.int32)
-        fs.batch_search(fs.LaneConfig(1, "direct", prep), z, out32)
-        assert np.array_equal(out32, want), k
+        for offsets in (False, True) if k <= MAX_OFFSET_SHIFT else (False,):
+            buf, *_ = with_count_words(fs, p, prep, 0, k=k, offsets=offsets)
+            pl = prep.placement()
+            # plain words sit beside X; words built with offsets are the layout without it
+            assert pl["sparse_format"] == "count-words" and pl["smem_x"] == (not offsets), (k, offsets, pl)
+            top, flagged = _check_buffer(buf, f, idx.r, k, offsets)
+            seen_top, seen_flagged = max(seen_top, top), max(seen_flagged, flagged)
+            assert np.array_equal(fs.run_batch(prep, z), want), (k, offsets)
+            out32 = np.empty(len(z), dtype=np.int32)
+            fs.batch_search(fs.LaneConfig(1, "direct", prep), z, out32)
+            assert np.array_equal(out32, want), (k, offsets)
     assert seen_top >= 4 and seen_flagged > 0  # coarse stripes saturate: the flagged-word scan ran
 
 
 def test_count_words_planner_budgets(cuda):
-    """fs_plan_count_words over budgets: k, the X rule (all of X when it takes
-    at most half the budget, else none) and both statistics equal the numpy
-    plan; FS_TOO_LARGE when nothing fits; answers equal the oracle either way."""
+    """fs_plan_count_words over budgets and modes (words alone, beside all of
+    X, beside the knot offsets with k <= 8): k and both statistics equal the
+    numpy plan; FS_TOO_LARGE when nothing fits; answers equal the oracle either way."""
     fs = _fs()
     xs = _clumped(4000, np.float64, seed=3)
     p = fs.validate_partition(xs, "double")
@@ -265,17 +306,20 @@ def test_count_words_planner_budgets(cuda):
     f = orc.knot_buckets(xs, idx.h).astype(np.int64)
     z = np.concatenate([_all_knots(xs), orc.random_queries(xs, 50_000, seed=1)])
     want = orc.rank_oracle(xs, z)
-    staged = set()
-    for budget in (100, 3000, 20_000, 50_000, 70_000, 150_000, 225_000):
-        exp = expected_plan(f, idx.r, len(xs), xs.itemsize, budget)
-        got = with_count_words(fs, p, prep, budget)
-        if exp is None:
-            assert got is None, budget
-            continue
-        assert got is not None and _same_plan(got[1:], exp), (budget, got[1:], exp)
-        staged.add(exp[1])
-        assert np.array_equal(fs.run_batch(prep, z), want), budget
-    assert staged == {0, 1}
+    fitted = set()
+    for budget in (100, 3000, 6000, 20_000, 50_000, 70_000, 150_000, 225_000):
+        for mode in (0, 1, 2):
+            exp = expected_plan(f, idx.r, len(xs), xs.itemsize, budget, mode)
+            got = with_count_words(fs, p, prep, budget, mode=mode)
+            if exp is None:
+                assert got is None, (budget, mode)
+                continue
+            assert got is not None and _same_plan(got[1:], exp), (budget, mode, got[1:], exp)
+            fitted.add(mode)
+            pl = prep.placement()
+            assert pl["sparse_format"] == "count-words" and pl["smem_x"] == (mode != 2), (budget, mode, pl)
+            assert np.array_equal(fs.run_batch(prep, z), want), (budget, mode)
+    assert fitted == {0, 1, 2}  # words alone (placement adds X when it fits), beside X, beside the knot offsets
 
 
 def test_count_words_out_of_domain_and_last_bucket(cuda):
@@ -288,8 +332,8 @@ def test_count_words_out_of_domain_and_last_bucket(cuda):
     xs = p.values
     prep = fs.prepare("direct", p)
     idx = prep.structure
-    for k in (2, 9):
-        with_count_words(fs, p, prep, 0, k=k)
+    for k, offsets in ((2, False), (9, False), (3, True), (8, True)):
+        with_count_words(fs, p, prep, 0, k=k, offsets=offsets)
         assert prep.placement()["sparse_format"] == "count-words"
         tail = np.concatenate([xs[-8:-1], np.nextafter(xs[-8:], -np.inf), orc.random_queries(xs, 5000, seed=3)])
         tail = tail[(tail >= xs[0]) & (tail < xs[-1])]
@@ -344,32 +388,36 @@ def test_count_words_abi_validation(cuda):
     n1 = len(p.values)
     x = p.device_values()
     f_dev = _device.empty(n1, np.uint64)
-    k, wx = ctypes.c_int32(-1), ctypes.c_int32(0)
+    k = ctypes.c_int32(-1)
     outs = [ctypes.c_uint64(0) for _ in range(3)]
     st = _device.stream_ptr()
 
-    def plan(dt, xp, budget, fp=f_dev.data_ptr()):
-        return lib.fs_plan_count_words(dt, xp, n1, float(idx.h), idx.r, budget, fp, ctypes.byref(k),
-                                       ctypes.byref(outs[0]), ctypes.byref(wx), ctypes.byref(outs[1]),
-                                       ctypes.byref(outs[2]), st)
+    def plan(dt, xp, budget, fp=f_dev.data_ptr(), mode=1):
+        return lib.fs_plan_count_words(dt, xp, n1, float(idx.h), idx.r, budget, mode, fp, ctypes.byref(k),
+                                       ctypes.byref(outs[0]), ctypes.byref(outs[1]), ctypes.byref(outs[2]), st)
 
     assert plan(_lib.FS_F32, None, 100_000) == _lib.FS_INVALID_ARG
     assert plan(_lib.FS_F32, x.data_ptr(), 100_000, None) == _lib.FS_INVALID_ARG
     assert plan(7, x.data_ptr(), 100_000) == _lib.FS_INVALID_ARG
+    assert plan(_lib.FS_F32, x.data_ptr(), 100_000, mode=3) == _lib.FS_INVALID_ARG
     assert plan(_lib.FS_F32, x.data_ptr(), 100) == _lib.FS_TOO_LARGE
+    assert plan(_lib.FS_F32, x.data_ptr(), 4000, mode=2) == _lib.FS_TOO_LARGE  # offsets need k <= 8
     assert plan(_lib.FS_F32, x.data_ptr(), 100_000) == _lib.FS_OK
-    assert lib.fs_count_words_bytes(idx.r, -1) == 0 and lib.fs_count_words_bytes(idx.r, MAX_SHIFT + 1) == 0
-    assert lib.fs_count_words_bytes(1 << 32, 3) == 0
+    assert lib.fs_count_words_bytes(idx.r, -1, 0) == 0 and lib.fs_count_words_bytes(idx.r, MAX_SHIFT + 1, 0) == 0
+    assert lib.fs_count_words_bytes(1 << 32, 3, 0) == 0 and lib.fs_count_words_bytes(idx.r, MAX_OFFSET_SHIFT + 1, n1) == 0
     buf = _device.empty(words_bytes(idx.r, k.value), np.uint8)
-    for bad_k in (-1, MAX_SHIFT + 1):
-        assert lib.fs_build_count_words(_lib.FS_F32, x.data_ptr(), n1, float(idx.h), idx.r, bad_k, f_dev.data_ptr(),
-                                        buf.data_ptr(), st) == _lib.FS_INVALID_ARG
-    assert lib.fs_build_count_words(_lib.FS_F32, x.data_ptr(), n1, float(idx.h), idx.r, k.value, f_dev.data_ptr(),
+    for bad_k, off in ((-1, 0), (MAX_SHIFT + 1, 0), (MAX_OFFSET_SHIFT + 1, 1)):
+        assert lib.fs_build_count_words(_lib.FS_F32, x.data_ptr(), n1, float(idx.h), idx.r, bad_k, off,
+                                        f_dev.data_ptr(), buf.data_ptr(), st) == _lib.FS_INVALID_ARG
+    assert lib.fs_build_count_words(_lib.FS_F32, x.data_ptr(), n1, float(idx.h), idx.r, k.value, 0, f_dev.data_ptr(),
                                     None, st) == _lib.FS_INVALID_ARG
-    with_count_words(fs, p, prep, 100_000)
+    with_count_words(fs, p, prep, 100_000, mode=1)
     z = orc.random_queries(p.values, 1000, seed=1)
     assert np.array_equal(fs.run_batch(prep, z), orc.rank_oracle(p.values, z))
     for bad_k in (-1, MAX_SHIFT + 1):
         prep.plan.sparse_shift = bad_k
         with pytest.raises(ValueError):
             fs.run_batch(prep, z)
+    prep.plan.sparse_shift, prep.plan.sparse_ndense = 3, n1 - 1  # offsets come for every knot or none
+    with pytest.raises(ValueError):
+        fs.run_batch(prep, z)

@@ -129,12 +129,13 @@ def test_gpu_big_tables_equal_oracle(cuda, xs):
     from paper_1506_08620_b200 import batch
 
     keep = batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, batch.SPARSE_RECORDS8_MAX_PAST_PPM
-    keep_cw = batch.COUNT_WORDS_MAX_RARE_PPM, batch.COUNT_WORDS_MAX_L2_XREAD_PPM
+    keep_cw = batch.COUNT_WORDS_MAX_RARE_PPM, batch.COUNT_WORDS_MAX_L2_XREAD_PPM, batch.COUNT_WORDS_MAX_XREAD_PPM
     try:
         for fmt in (("count-words",), ("records",), ("records8",), ("records12",), ("records8x3",), ("two-level",)):
             batch.SPARSE_FORMATS = fmt
             batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM = batch.SPARSE_RECORDS8_MAX_PAST_PPM = 10**6
             batch.COUNT_WORDS_MAX_RARE_PPM = batch.COUNT_WORDS_MAX_L2_XREAD_PPM = 10**6  # past the scan-path bound too
+            batch.COUNT_WORDS_MAX_XREAD_PPM = 10**6
             try:
                 prep = fs.prepare("direct", p)
             except fs.InfeasibleError:
@@ -147,7 +148,7 @@ def test_gpu_big_tables_equal_oracle(cuda, xs):
                                    prep.plan.sparse_shift, prep.plan.sparse_ndense)
     finally:
         batch.SPARSE_FORMATS, batch.SPARSE_RECORDS_MAX_PAST_SIXTH_PPM, batch.SPARSE_RECORDS8_MAX_PAST_PPM = keep
-        batch.COUNT_WORDS_MAX_RARE_PPM, batch.COUNT_WORDS_MAX_L2_XREAD_PPM = keep_cw
+        batch.COUNT_WORDS_MAX_RARE_PPM, batch.COUNT_WORDS_MAX_L2_XREAD_PPM, batch.COUNT_WORDS_MAX_XREAD_PPM = keep_cw
     # zoned records and the hot window are alternatives for skewed tables: when
     # the planner took one, the other (zoning off) must answer the same
     if fs.prepare("direct", p).placement()["sparse_format"] == "zoned":

@@ -61,7 +61,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--m", type=int, default=0)
     ap.add_argument("--out-bytes", type=int, default=4)
+    ap.add_argument("--smem-kb", type=int, default=0, help="cap the planners' shared-memory budget (KB)")
     args = ap.parse_args()
+    if args.smem_kb:
+        from paper_1506_08620_b200 import batch as _bb
+
+        _bb.SMEM_BUDGET_OVERRIDE = args.smem_kb * 1024
     torch.cuda.set_device(0)
     for spec in args.configs.split(","):
         name, _, arg = spec.partition(":")
@@ -111,7 +116,7 @@ def main():
                 base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct", "direct-nohot": "direct",
                         "direct-nozoned": "direct", "direct-count": "direct", "direct-nocount": "direct",
                         "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
-                if algo.startswith("direct-hot:"):  # hot window of the given size in KB
+                if algo.startswith("direct-hot:") or algo.startswith("direct-count:"):
                     base = "direct"
                 if algo in ("direct-sparse2", "direct-rec", "direct-rec8", "direct-rec12", "direct-rec8x3"):
                     from paper_1506_08620_b200 import batch as _b
@@ -142,19 +147,36 @@ def main():
                     prep = fs.prepare("direct", p, hot_window=True)
                 if algo == "direct-nohot":
                     prep = fs.prepare("direct", p, hot_window=False)
+                if algo.startswith("direct-count:"):  # count words forced within a shared-memory budget (KB)
+                    from paper_1506_08620_b200 import batch as _b
+
+                    keep_c = (_b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM,
+                              _b.COUNT_WORDS_MAX_XREAD_PPM, _b.COUNT_WORDS_BUDGET_BYTES)
+                    _b.SPARSE_FORMATS = ("count-words",)
+                    _b.COUNT_WORDS_MAX_RARE_PPM = _b.COUNT_WORDS_MAX_L2_XREAD_PPM = 10**6
+                    _b.COUNT_WORDS_MAX_XREAD_PPM = 10**6
+                    _b.COUNT_WORDS_BUDGET_BYTES = int(algo.split(":")[1]) * 1024
+                    try:
+                        prep = fs.prepare("direct", p)
+                    finally:
+                        (_b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM,
+                         _b.COUNT_WORDS_MAX_XREAD_PPM, _b.COUNT_WORDS_BUDGET_BYTES) = keep_c
                 if algo in ("direct-count", "direct-nocount"):  # count words forced / excluded
                     from paper_1506_08620_b200 import batch as _b
 
-                    keep_c = (_b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM)
+                    keep_c = (_b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM,
+                              _b.COUNT_WORDS_MAX_XREAD_PPM)
                     if algo == "direct-count":
                         _b.SPARSE_FORMATS = ("count-words",)
                         _b.COUNT_WORDS_MAX_RARE_PPM = _b.COUNT_WORDS_MAX_L2_XREAD_PPM = 10**6
+                        _b.COUNT_WORDS_MAX_XREAD_PPM = 10**6
                     else:
                         _b.SPARSE_FORMATS = tuple(n for n in keep_c[0] if n != "count-words")
                     try:
                         prep = fs.prepare("direct", p)
                     finally:
-                        _b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM = keep_c
+                        (_b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM,
+                         _b.COUNT_WORDS_MAX_XREAD_PPM) = keep_c
                 if algo == "direct-nozoned":  # no zoned records: the hot window / L2 directory
                     from paper_1506_08620_b200 import batch as _b
 
