@@ -422,25 +422,36 @@ def prepare(algorithm: str, p: SortedPartition, qbits: int = 32, *, hot_window: 
         plan.rank = d.data_ptr()
         keep.append(d)
     if plan.algorithm == _lib.ALGO_CODES["direct"] and structure.q == 1:
-        if (structure.r + 1) * rec_bytes <= SMEM_RECORDS_MAX:
-            rec = _device.empty((structure.r + 1) * rec_bytes, np.uint8)
-            rc = _lib.load().fs_build_fused(fs_dtype(p.precision), p.device_values().data_ptr(), len(p.values),
-                                            structure.k_dev.data_ptr(), structure.r, rec.data_ptr(),
-                                            _device.stream_ptr())
-            _lib.check(rc, what="fs_build_fused")
-            plan.records = rec.data_ptr()
-            keep.append(rec)
-        rank = build_rank_directory(p, structure)
-        plan.rank = rank.data_ptr()
-        keep.append(rank)
-        if not plan.records:
-            _set_sparse_table(plan, p, structure, keep)
-        if ZONED and not plan.records and not plan.sparse:
-            _set_zoned(plan, p, structure, keep)
-        if hot_window and not plan.sparse:
-            _set_hot_window(plan, p, structure, rank)
+        set_direct_layouts(plan, p, structure, keep, hot_window)
     scalar, lanes = _make_callables(plan, p)
     return PreparedKernel(algorithm, p, structure, scalar, lanes, plan=plan, buffers=tuple(keep))
+
+
+def set_direct_layouts(plan, p: SortedPartition, structure: DirectIndex, keep: list, hot_window: bool = True) -> None:
+    """The device layouts of a gap-1 table K that the direct kernel can search
+    instead of K itself, all with identical answers: fused records when they
+    fit in shared memory, the rank directory, and -- when the directory (plus
+    X) cannot be staged -- count words / group records / the two-level table
+    for R >> N, zoned tables for skewed ones, else a hot window of the
+    directory.  Shared by prepare() and persist.prepare_loaded()."""
+    rec_bytes = 8 if p.precision == "single" else 16
+    if (structure.r + 1) * rec_bytes <= SMEM_RECORDS_MAX:
+        rec = _device.empty((structure.r + 1) * rec_bytes, np.uint8)
+        rc = _lib.load().fs_build_fused(fs_dtype(p.precision), p.device_values().data_ptr(), len(p.values),
+                                        structure.k_dev.data_ptr(), structure.r, rec.data_ptr(),
+                                        _device.stream_ptr())
+        _lib.check(rc, what="fs_build_fused")
+        plan.records = rec.data_ptr()
+        keep.append(rec)
+    rank = build_rank_directory(p, structure)
+    plan.rank = rank.data_ptr()
+    keep.append(rank)
+    if not plan.records:
+        _set_sparse_table(plan, p, structure, keep)
+    if ZONED and not plan.records and not plan.sparse:
+        _set_zoned(plan, p, structure, keep)
+    if hot_window and not plan.sparse:
+        _set_hot_window(plan, p, structure, rank)
 
 
 #: the sparse two-level table is used when its dense (bitmask) super-buckets

@@ -107,13 +107,14 @@ LOADED_ALGORITHM = {1: "direct", 2: "direct-gap2"}
 
 def prepare_loaded(idx: DirectIndex, p, algorithm: str | None = None):
     """A PreparedKernel over a loaded index and its partition (the search
-    kernels of batch.prepare, without rebuilding the table).  The kernel
+    kernels and shared-memory layouts of batch.prepare, without rebuilding
+    the table).  The kernel
     follows the index's gap q: "direct" for q = 1, "direct-gap2" for q = 2,
     "direct-generic" otherwise (the reference's direct_search_generic,
     direct.py:294-300); an explicit ``algorithm`` that does not match q
     raises ValueError, since a gap-1 probe over a gap-q table (or the
     reverse) returns wrong answers."""
-    from .batch import PreparedKernel, _make_callables, _plan_for, build_rank_directory
+    from .batch import PreparedKernel, _make_callables, _plan_for, set_direct_layouts
 
     want = LOADED_ALGORITHM.get(idx.q, "direct-generic")
     if algorithm is None:
@@ -128,8 +129,6 @@ def prepare_loaded(idx: DirectIndex, p, algorithm: str | None = None):
         return prepare_direct_gap(p, idx.q, idx.qbits, idx=idx)  # over its count directory
     plan, keep = _plan_for(algorithm, idx, p)
     if algorithm == "direct":
-        rank = build_rank_directory(p, idx)
-        plan.rank = rank.data_ptr()
-        keep.append(rank)
+        set_direct_layouts(plan, p, idx, keep)  # the same layouts prepare() builds over a fresh table
     scalar, lanes = _make_callables(plan, p)
     return PreparedKernel(algorithm, p, idx, scalar, lanes, plan=plan, buffers=tuple(keep))

@@ -92,6 +92,32 @@ def test_gpu_round_trip_search_identical(cuda, tmp_path):
 
 
 @pytest.mark.gpu
+def test_gpu_loaded_index_gets_prepares_layouts(cuda, tmp_path):
+    """A loaded gap-1 index is searched through the same shared-memory layouts
+    prepare() builds over a fresh table (persist.prepare_loaded calls
+    batch.set_direct_layouts): cfg3's fused records, cfg5 N+1 = 1025's count
+    words beside X (K: 33 MB on disk) and cfg4's striped rank words, with
+    identical placements and the oracle's answers."""
+    import paper_1506_08620_b200 as fs
+    from paper_1506_08620_b200 import workloads
+
+    for name, kw in (("cfg3", {}), ("cfg5", {"n1": 1025}), ("cfg4", {})):
+        p = workloads.knots(name, **kw)
+        fresh = fs.prepare("direct", p)
+        path = tmp_path / f"{name}.idx"
+        persist.save_index(fresh.structure, path)
+        loaded = persist.prepare_loaded(persist.load_index(path), p)
+        path.unlink()
+        assert loaded.placement() == fresh.placement(), name
+        assert loaded.placement()["smem_table"] or loaded.placement()["smem_sparse"], name
+        z = np.concatenate([workloads.queries_host(name, p, 200_000, seed=3), orc.boundary_probes(p.values)])
+        z = z[(z >= p.values[0]) & (z < p.values[-1])].astype(p.values.dtype)
+        want = orc.rank_oracle(p.values, z)
+        assert np.array_equal(fs.run_batch(loaded, z), want), name
+        assert np.array_equal(fs.run_batch(fresh, z), want), name
+
+
+@pytest.mark.gpu
 def test_gpu_corrupt_payload_detected(cuda, tmp_path):
     raw = bytearray((IDX / "s100_double.idx").read_bytes())
     raw[60] ^= 0xFF
