@@ -378,8 +378,9 @@ int fs_build_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h,
  *     given mode -- 1: beside all of X; 2: beside the knot offsets (k <= 8
  *     must fit); 0: alone, every knot read through L2 -- plus the share of
  *     buckets in knot-holding stripes (queries that read X or an offset) and
- *     in stripes of two or more knots or flagged words (queries that scan),
- *     in parts per million.  FS_TOO_LARGE if nothing fits or there are more
+ *     in stripes of two or more knots or flagged words -- in mode 2 also the
+ *     buckets that hold a lone knot themselves -- (queries that scan), in
+ *     parts per million.  FS_TOO_LARGE if nothing fits or there are more
  *     knots than stripes.  SYNC.
  *   fs_build_count_words: fill the words (and the offsets) for that k.  Async.
  * Set fs_plan.sparse to the buffer, sparse_format = FS_SPARSE_COUNT,

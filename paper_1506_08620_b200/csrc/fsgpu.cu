@@ -1434,6 +1434,7 @@ int fs_plan_count_words(int32_t dtype, const void* x_dev, uint64_t n1, double h,
     const uint64_t width = std::min<uint64_t>(sw, r + 1 - ((f[i] >> k) << k));
     xread += width;
     if (e - i >= 2) rare += width;
+    else if (mode == 2) rare += 1;  // beside offsets, the knot's own bucket is decided by X on the scan path
     if (e - i >= 4) rare += std::min<uint64_t>(ww, r + 1 - ((f[i] >> (k + kCountWordShift)) << (k + kCountWordShift)));
     i = e;
   }

@@ -45,6 +45,8 @@ def expected_plan(f, r, n1, es, budget, mode):
     width = np.minimum(1 << k, r + 1 - (stripe << k))
     xread = int(width.sum())
     rare = int(width[cnt >= 2].sum())
+    if mode == 2:
+        rare += int((cnt == 1).sum())  # a lone knot's own bucket: X decides it on the scan path
     ws = k + WORD_SHIFT
     rare += int(np.minimum(1 << ws, r + 1 - ((stripe[cnt >= 4] >> WORD_SHIFT) << ws)).sum())
     rare = min(rare, r + 1)
