@@ -87,7 +87,8 @@ enum {
   FS_SPARSE_RECORDS8X3 = 4,/* 8-B group records, three 13-bit offsets (shift <= 11, N+1 <= 2^24) */
   FS_SPARSE_ZONED = 5,     /* zone descriptors | 8-B records, per-zone form: fs_build_zoned  */
   FS_SPARSE_ZONED_RANK = 6,/* zone descriptors | 8-B striped rank words: fs_build_zoned_rank */
-  FS_SPARSE_COUNT = 7      /* 8-B count words, one stripe shift for the table: fs_build_count_words */
+  FS_SPARSE_COUNT = 7,     /* 8-B count words, one stripe shift for the table: fs_build_count_words */
+  FS_SPARSE_KNOT_BYTES = 8 /* a byte per knot beside the rank directory (fs_plan.rank): fs_build_knot_bytes */
 };
 
 /*
@@ -352,6 +353,22 @@ int fs_plan_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, 
                        uint64_t* t0_out, uint64_t* nt_out, uint64_t* xread_ppm_out, void* stream);
 int fs_build_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, int32_t zs,
                         uint64_t nrec, uint64_t* f_scratch_dev, void* buf_dev, void* stream);
+
+/*
+ * Knot bytes (FS_SPARSE_KNOT_BYTES; no reference counterpart) for tables whose
+ * rank directory fits in shared memory but whose X does not (the paper's
+ * uniform-gap arrays at 65,535 knots): B[i] = floor(256 frac(p_i)), p_i =
+ * RN(h RN(X_i - X0)) the product whose floor is knot i's bucket
+ * (direct.py:194-197).  The search stages the directory and B; for a query
+ * whose bucket holds knot t it compares the same byte of its own product with
+ * B[t] -- RN is monotone, so a smaller byte means z < X[t] and a larger one z >
+ * X[t] -- and reads X[t] (through L2) only on a tie.  Same answers as the rank
+ * directory (batch.py:315-317).  Buffer: N+1 bytes padded to 16.  Async.
+ * Set fs_plan.sparse to the buffer (fs_plan.rank to the directory),
+ * sparse_format = FS_SPARSE_KNOT_BYTES, sparse_ndense = N+1, sparse_shift = 0.
+ * Used when directory + bytes fit shared memory and directory + X do not.
+ */
+int fs_build_knot_bytes(int32_t dtype, const void* x_dev, uint64_t n1, double h, void* buf_dev, void* stream);
 
 /*
  * Count words of the gap-1 table (FS_SPARSE_COUNT; a device layout of K, no

@@ -309,7 +309,7 @@ class PreparedKernel:
             "sparse_format": {_lib.SPARSE_RECORDS: "records", _lib.SPARSE_RECORDS8: "records8",
                               _lib.SPARSE_RECORDS12: "records12", _lib.SPARSE_RECORDS8X3: "records8x3",
                               _lib.SPARSE_ZONED: "zoned", _lib.SPARSE_ZONED_RANK: "zoned-rank",
-                              _lib.SPARSE_COUNT: "count-words"}.get(
+                              _lib.SPARSE_COUNT: "count-words", _lib.SPARSE_KNOT_BYTES: "knot-bytes"}.get(
                 self.plan.sparse_format, "two-level") if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
         }
@@ -446,6 +446,8 @@ def set_direct_layouts(plan, p: SortedPartition, structure: DirectIndex, keep: l
     rank = build_rank_directory(p, structure)
     plan.rank = rank.data_ptr()
     keep.append(rank)
+    if not plan.records and _set_knot_bytes(plan, p, structure, keep):
+        return
     if not plan.records:
         _set_sparse_table(plan, p, structure, keep)
     if ZONED and not plan.records and not plan.sparse:
@@ -701,6 +703,36 @@ def _plan_two_level(p: SortedPartition, idx: DirectIndex, f, budget: int):
         if rc != _lib.FS_TOO_LARGE:
             _lib.check(rc, what="fs_plan_sparse")
     return None
+
+
+#: a byte per knot staged beside the rank directory when X does not fit there
+#: (fs_build_knot_bytes); False keeps the directory alone, X through L2
+KNOT_BYTES = True
+
+
+def _set_knot_bytes(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> bool:
+    """Tables whose rank directory fits in shared memory but whose X does not:
+    stage a byte per knot -- where inside its bucket the knot falls, to 1/256,
+    from the same rounded product the bucket index comes from -- and read X
+    through L2 only when the query's byte ties with the knot's."""
+    n1 = len(p.values)
+    budget = _smem_budget() - 512
+    dir_bytes = ((idx.r >> 5) + 1) * 8
+    x_bytes = (n1 * p.values.dtype.itemsize + 127) // 128 * 128
+    nbytes = (n1 + 15) // 16 * 16
+    if (not KNOT_BYTES or idx.r >= (1 << 32) or n1 >= (1 << 31) or x_bytes + dir_bytes <= budget
+            or (nbytes + 127) // 128 * 128 + dir_bytes > budget):
+        return False
+    buf = _device.empty(nbytes, np.uint8)
+    rc = _lib.load().fs_build_knot_bytes(fs_dtype(p.precision), p.device_values().data_ptr(), n1, float(idx.h),
+                                         buf.data_ptr(), _device.stream_ptr())
+    _lib.check(rc, what="fs_build_knot_bytes")
+    plan.sparse = buf.data_ptr()
+    plan.sparse_format = _lib.SPARSE_KNOT_BYTES
+    plan.sparse_shift = 0
+    plan.sparse_ndense = n1
+    keep.append(buf)
+    return True
 
 
 def _set_count_words(plan, p: SortedPartition, idx: DirectIndex, keep: list, f, budget: int, modes=(1,),

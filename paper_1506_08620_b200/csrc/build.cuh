@@ -152,6 +152,26 @@ __global__ void knot_buckets_kernel(const T* __restrict__ x, uint64_t n1, T h, u
   }
 }
 
+// Knot bytes beside the rank directory (fs_build_knot_bytes): B[i] = floor(256
+// frac(p_i)) for p_i = RN(h RN(X_i - X0)), the product whose floor is knot
+// i's bucket (direct.py:194-197) -- where inside its bucket the knot falls, to
+// 1/256.  RN is monotone, so for a query z with product p: p < p_i implies
+// z < X_i and p > p_i implies z > X_i; comparing (bucket, byte) pairs decides
+// all but ties, which read X.
+template <typename T>
+__global__ void fill_knot_bytes_kernel(const T* __restrict__ x, uint64_t n1, T h, uint8_t* __restrict__ B,
+                                       uint64_t npad) {
+  const T x0 = x[0];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t q = 0;
+    if (i < n1) {
+      const T p = mul_rn(h, sub_rn(__ldg(x + i), x0));
+      q = trunc_to<uint32_t>(mul_rn(sub_rn(p, floor(p)), (T)256));
+    }
+    B[i] = (uint8_t)q;
+  }
+}
+
 // First index in [lo, hi) with f[i] >= key (UPPER=false) or f[i] > key (UPPER=true).
 template <bool UPPER>
 __device__ __forceinline__ uint64_t bound_search(const uint64_t* __restrict__ f, uint64_t lo, uint64_t hi,

@@ -170,8 +170,12 @@ int validate_plan(const fs_plan* p) {
       if (p->sparse && (p->sparse_format != FS_SPARSE_TWO_LEVEL && p->sparse_format != FS_SPARSE_RECORDS &&
                         p->sparse_format != FS_SPARSE_RECORDS8 && p->sparse_format != FS_SPARSE_RECORDS12 &&
                         p->sparse_format != FS_SPARSE_RECORDS8X3 && p->sparse_format != FS_SPARSE_ZONED &&
-                        p->sparse_format != FS_SPARSE_ZONED_RANK && p->sparse_format != FS_SPARSE_COUNT))
+                        p->sparse_format != FS_SPARSE_ZONED_RANK && p->sparse_format != FS_SPARSE_COUNT &&
+                        p->sparse_format != FS_SPARSE_KNOT_BYTES))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
+      if (p->sparse && p->sparse_format == FS_SPARSE_KNOT_BYTES &&
+          (!p->rank || p->q != 1 || p->sparse_ndense != p->n1 || p->r >= (1ull << 32) || p->n1 - 1 >= (1ull << 31)))
+        return fail(FS_INVALID_ARG, "knot bytes go with the gap-1 rank directory, one per knot");
       if (p->sparse && p->sparse_format == FS_SPARSE_COUNT &&
           (fs_count_words_bytes(p->r, p->sparse_shift, p->sparse_ndense) == 0 || p->n1 - 1 >= (1ull << 31) ||
            (p->sparse_ndense != 0 && p->sparse_ndense != p->n1)))
@@ -185,7 +189,8 @@ int validate_plan(const fs_plan* p) {
       }
       if (p->sparse && p->sparse_format == FS_SPARSE_RECORDS8X3 && p->n1 > (1ull << 24))
         return fail(FS_INVALID_ARG, "3-offset records need N+1 <= 2^24");
-      if (p->sparse && !is_zoned(p->sparse_format) && p->sparse_format != FS_SPARSE_COUNT && (p->sparse_shift < 5 ||
+      if (p->sparse && !is_zoned(p->sparse_format) && p->sparse_format != FS_SPARSE_COUNT &&
+          p->sparse_format != FS_SPARSE_KNOT_BYTES && (p->sparse_shift < 5 ||
                         p->sparse_shift > (p->sparse_format == FS_SPARSE_TWO_LEVEL    ? 16
                                            : p->sparse_format == FS_SPARSE_RECORDS12 ? kRec12MaxShift
                                            : p->sparse_format == FS_SPARSE_RECORDS8X3 ? kRec3MaxShift
@@ -237,6 +242,24 @@ Placement place(const fs_plan* p) {
   // gap q >= 3 over its count directory (8-B words of 16 / 8 buckets, fs_build_countdir)
   const bool use_count = p->algorithm == FS_ALGO_DIRECT_GENERIC && p->rank != nullptr && p->q >= 2 && p->q <= 15;
   const bool use_dir = use_rank || use_rank2 || use_count;
+  // the rank directory and a byte per knot, when X does not fit beside the directory
+  if (use_rank && p->sparse && p->sparse_format == FS_SPARSE_KNOT_BYTES && !force_global && p->r < (1ull << 32)) {
+    const uint64_t db = ((p->r >> 5) + 1) * 8, bb = (p->n1 + 15) & ~15ull;
+    if (align128(bb) + db <= budget && align128(p->n1 * es) + db > budget) {
+      // the bytes take the X segment's place (at offset 0), the directory follows
+      pl.sparse = pl.ks = pl.xs = true;
+      pl.x_bytes = (uint32_t)bb;
+      pl.table_bytes = (uint32_t)db;
+      pl.seg0_src = p->sparse;
+      pl.seg0_bytes = (uint32_t)bb;
+      pl.seg1_src = p->rank;
+      pl.seg1_bytes = (uint32_t)db;
+      pl.nseg = 2;
+      pl.smem = align128(bb) + db;
+      pl.flags |= FS_PLACE_SMEM_K | FS_PLACE_SMEM_SPARSE;
+      return pl;
+    }
+  }
   // zoned records + a window of X (prepare sets them only when the rank
   // directory cannot be staged)
   if (p->algorithm == FS_ALGO_DIRECT && p->sparse && is_zoned(p->sparse_format) && p->q == 1 &&
@@ -267,7 +290,7 @@ Placement place(const fs_plan* p) {
   }
   // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
   if (p->algorithm == FS_ALGO_DIRECT && p->sparse && !is_zoned(p->sparse_format) && p->q == 1 &&
-      !force_global && p->r < (1ull << 32) &&
+      p->sparse_format != FS_SPARSE_KNOT_BYTES && !force_global && p->r < (1ull << 32) &&
       (p->sparse_format == FS_SPARSE_COUNT || (p->sparse_shift >= 5 && p->sparse_shift <= 16))) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
@@ -622,6 +645,31 @@ template <typename T, bool STRIPED, typename OutT>
 struct BoundedFor<T, ZonedProbe<T, STRIPED>, OutT> {
   static constexpr bool value = FSG_ZONED_BOUNDED;
 };
+// knot bytes beside the directory: 1024-thread CTAs, two 8-query groups per
+// thread for f32, two queries per load phase (uniform-gap N+1 = 65535: f32 625
+// -> 680, f64 467 -> 493 Gq/s over the unbounded / one-group / four-query
+// build; profiles/r02/knot_bytes.txt)
+#ifndef FSG_RANKBYTES_BOUNDED
+#define FSG_RANKBYTES_BOUNDED 1
+#endif
+template <typename T, typename OutT>
+struct BoundedFor<T, RankBytesProbe<T>, OutT> {
+  static constexpr bool value = FSG_RANKBYTES_BOUNDED;
+};
+#ifndef FSG_UNROLL_VW8_RANKBYTES
+#define FSG_UNROLL_VW8_RANKBYTES 2
+#endif
+template <>
+struct UnrollVW8For<RankBytesProbe<float>> {
+  static constexpr int value = FSG_UNROLL_VW8_RANKBYTES;
+};
+#ifndef FSG_UNROLL_F64_RANKBYTES
+#define FSG_UNROLL_F64_RANKBYTES FSG_UNROLL_F64
+#endif
+template <>
+struct UnrollFor<double, RankBytesProbe<double>> {
+  static constexpr int value = FSG_UNROLL_F64_RANKBYTES;
+};
 #ifndef FSG_COUNT_BOUNDED
 #define FSG_COUNT_BOUNDED 1
 #endif
@@ -821,6 +869,8 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
       if (pl.zoned && p->sparse_format == FS_SPARSE_ZONED_RANK)
         return launch_probe<T, OutT, ZonedProbe<T, true>>(d, pl, z, m, out, fb, base, st);
       if (pl.zoned) return launch_probe<T, OutT, ZonedProbe<T>>(d, pl, z, m, out, fb, base, st);
+      if (pl.sparse && p->sparse_format == FS_SPARSE_KNOT_BYTES)
+        return launch_probe<T, OutT, RankBytesProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (pl.sparse && p->sparse_format == FS_SPARSE_COUNT) {
         if (pl.xs) return launch_probe<T, OutT, CountWordProbe<T, 1>>(d, pl, z, m, out, fb, base, st);
         if (p->sparse_ndense) return launch_probe<T, OutT, CountWordProbe<T, 2>>(d, pl, z, m, out, fb, base, st);
@@ -1396,6 +1446,23 @@ int zoned_knot_buckets(int32_t dtype, const void* x_dev, uint64_t n1, double h, 
   return FS_OK;
 }
 }  // namespace
+
+int fs_build_knot_bytes(int32_t dtype, const void* x_dev, uint64_t n1, double h, void* buf_dev, void* stream) {
+  if (!x_dev || !buf_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  cudaStream_t s = as_stream(stream);
+  const uint64_t npad = (n1 + 15) & ~15ull;
+  const int g = grid_1d(npad, 256);
+  if (dtype == FS_F32)
+    fill_knot_bytes_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(x_dev), n1, (float)h,
+                                                   static_cast<uint8_t*>(buf_dev), npad);
+  else if (dtype == FS_F64)
+    fill_knot_bytes_kernel<double><<<g, 256, 0, s>>>(static_cast<const double*>(x_dev), n1, h,
+                                                    static_cast<uint8_t*>(buf_dev), npad);
+  else
+    return fail(FS_INVALID_ARG, "dtype must be FS_F32 or FS_F64");
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
 
 uint64_t fs_count_words_bytes(uint64_t r, int32_t k, uint64_t noff) {
   if (k < 0 || k > kCountMaxShift || r >= (1ull << 32) || (noff && k > kCountMaxOffsetShift)) return 0;

@@ -192,6 +192,85 @@ struct RankProbe {
 #endif
 };
 
+// RankProbe for tables whose directory fits in shared memory but whose X does
+// not: the directory and one byte per knot (fill_knot_bytes_kernel: where
+// inside its bucket the knot falls, to 1/256, from the same rounded product p
+// whose floor is the bucket) are staged.  For a query in a bucket holding knot
+// t, the byte of its own product against the knot's decides z < X[t] (RN is
+// monotone: p_z < p_t implies z < X[t], p_z > p_t implies z > X[t]); only a tie
+// (1/256 of those queries) reads X[t] through L2.  Same answers as RankProbe.
+template <typename T>
+struct RankBytesProbe {
+  const T* X;
+  uint32_t ds, bs;  // shared addresses of the directory and the knot bytes
+  T h, x0;
+  uint32_t r, n1;
+  __device__ __forceinline__ RankBytesProbe(const DevPlan<T>& p, unsigned char* smem) {
+    n1 = (uint32_t)p.n1;
+    X = p.x;
+    // staged as [knot bytes | directory]
+    asm volatile("mov.u32 %0, %1;" : "=r"(bs) : "r"((uint32_t)__cvta_generic_to_shared(smem)));
+    asm volatile("mov.u32 %0, %1;" : "=r"(ds) : "r"(bs + p.x_smem_bytes_aligned()));
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+  }
+  // bucket j (clamped to R) and the query's byte inside it
+  __device__ __forceinline__ void locate(T z, uint32_t& j, uint32_t& qz) const {
+    const T p = mul_rn(sub_rn(z, x0), h);
+    const T fl = floor(p);
+    j = trunc_to<uint32_t>(fl);
+    j = j < r ? j : r;
+    qz = trunc_to<uint32_t>(mul_rn(sub_rn(p, fl), (T)256));
+  }
+  __device__ __forceinline__ uint2 word(uint32_t j) const {
+    uint2 d;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d.x), "=r"(d.y) : "r"(ds + 8u * (j >> 5)));
+    return d;
+  }
+  __device__ __forceinline__ int64_t finish(const uint2& d, uint32_t j, uint32_t qz, T z) const {
+    const uint32_t b = j & 31u;
+    uint32_t below;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(b));
+    const uint32_t t = d.y + __popc(d.x & below);
+    const uint32_t knot = (d.x >> b) & 1u;
+    FSG_BOUND(!knot || t < n1);
+    uint32_t o = 256u;  // no knot in the bucket: every query byte is below it
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u8 %0, [%1];\n\t}" : "+r"(o) : "r"(bs + t), "r"(knot));
+    uint32_t res = t - (qz < o ? 1u : 0u);
+    if (qz == o) res = t - (z < __ldg(X + t) ? 1u : 0u);  // a tie in the byte (knot is set: o < 256)
+    return (int64_t)(int32_t)res;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    uint32_t j, qz;
+    locate(z, j, qz);
+    return finish(word(j), j, qz, z);
+  }
+#ifndef FSG_RANKBYTES_GROUP
+#define FSG_RANKBYTES_GROUP 2
+#endif
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    constexpr int G = N < FSG_RANKBYTES_GROUP ? N : FSG_RANKBYTES_GROUP;
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += G) {
+      uint2 d[G];
+      uint32_t j[G], qz[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        locate(z[g0 + q], j[q], qz[q]);
+        d[q] = word(j[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        o[g0 + q] = (R)finish(d[q], j[q], qz[q], z[g0 + q]);
+      }
+    }
+  }
+};
+
 // Direct search (gap 2) over the rank directory of its table (fill_rank2_
 // kernel): t = K2[j] recovered exactly; a bucket holding no knot needs no X
 // read (its last knot lies in an earlier bucket, so X[t] < z by the

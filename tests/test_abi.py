@@ -95,9 +95,13 @@ def test_argument_validation_without_gpu():
         plan.sparse_shift, plan.sparse_ndense = shift, novf
         assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
         assert b"sparse" in lib.fs_last_error()
-    plan.sparse_format, plan.sparse_shift, plan.sparse_ndense = 8, 8, 0
+    plan.sparse_format, plan.sparse_shift, plan.sparse_ndense = 9, 8, 0
     assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
     assert b"sparse" in lib.fs_last_error()
+    # knot bytes: one per knot, beside the gap-1 rank directory
+    plan.sparse_format, plan.sparse_shift, plan.sparse_ndense = _lib.SPARSE_KNOT_BYTES, 0, 3  # n1 = 4
+    assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
+    assert b"knot bytes" in lib.fs_last_error()
     # count words: one stripe shift 0..27 for the table
     plan.sparse_format = _lib.SPARSE_COUNT
     for shift in (-1, 28):

@@ -841,13 +841,18 @@ def test_sharded_batch_search_spans_on_one_device(cuda):
 
 
 @pytest.mark.parametrize("precision", ["single", "double"])
-def test_staged_rank_directory_beats_unstaged_sparse(cuda, precision):
+def test_staged_rank_directory_beats_unstaged_sparse(cuda, precision, monkeypatch):
     """Uniform gaps U[1, 5] at N+1 = 65535 (R / N = 3): X cannot be staged
     beside any sparse layout, so the rank directory (49 KB) is staged alone
     and X read through L2 for the buckets holding a knot (place();
     profiles/r02/unif_layouts.txt).  Answers equal the oracle at every knot,
     its neighbours and random queries."""
     fs = _fs()
+    from paper_1506_08620_b200 import batch
+
+    # (round 2: a byte per knot is staged beside this directory by default, tests/test_gpu_knot_bytes.py;
+    # the placement rule under test is the one without it)
+    monkeypatch.setattr(batch, "KNOT_BYTES", False)
     p = fs.gen_uniform_gap_partition(65535, 1.0, 5.0, 42, precision)
     prep = fs.prepare("direct", p)
     pl = prep.placement()

@@ -115,6 +115,7 @@ def main():
             try:
                 base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct", "direct-nohot": "direct",
                         "direct-nozoned": "direct", "direct-count": "direct", "direct-nocount": "direct",
+                        "direct-nobytes": "direct",
                         "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
                 if algo.startswith("direct-hot:") or algo.startswith("direct-count:"):
                     base = "direct"
@@ -177,6 +178,14 @@ def main():
                     finally:
                         (_b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM,
                          _b.COUNT_WORDS_MAX_XREAD_PPM) = keep_c
+                if algo == "direct-nobytes":  # the staged directory alone, X through L2 (no knot bytes)
+                    from paper_1506_08620_b200 import batch as _b
+
+                    _b.KNOT_BYTES = False
+                    try:
+                        prep = fs.prepare("direct", p)
+                    finally:
+                        _b.KNOT_BYTES = True
                 if algo == "direct-nozoned":  # no zoned records: the hot window / L2 directory
                     from paper_1506_08620_b200 import batch as _b
 
