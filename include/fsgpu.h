@@ -88,7 +88,8 @@ enum {
   FS_SPARSE_ZONED = 5,     /* zone descriptors | 8-B records, per-zone form: fs_build_zoned  */
   FS_SPARSE_ZONED_RANK = 6,/* zone descriptors | 8-B striped rank words: fs_build_zoned_rank */
   FS_SPARSE_COUNT = 7,     /* 8-B count words, one stripe shift for the table: fs_build_count_words */
-  FS_SPARSE_KNOT_BYTES = 8 /* a byte per knot beside the rank directory (fs_plan.rank): fs_build_knot_bytes */
+  FS_SPARSE_KNOT_BYTES = 8,/* a byte per knot beside the rank directory (fs_plan.rank): fs_build_knot_bytes */
+  FS_SPARSE_RANK_ROWS = 9  /* 16-B rank rows {mask, base, eight knot bytes} read through L2: fs_build_rank_rows */
 };
 
 /*
@@ -369,6 +370,22 @@ int fs_build_zoned_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h,
  * Used when directory + bytes fit shared memory and directory + X do not.
  */
 int fs_build_knot_bytes(int32_t dtype, const void* x_dev, uint64_t n1, double h, void* buf_dev, void* stream);
+
+/*
+ * Rank rows (FS_SPARSE_RANK_ROWS; no reference counterpart) for tables whose
+ * rank directory is read through L2 (nothing fits in shared memory): row w =
+ * {mask of the buckets 32w .. 32w+31 holding a knot, K[32w], the knot bytes
+ * (fs_build_knot_bytes) of the row's first eight knots}, 16 B.  One gather
+ * -- one 32-B sector, as for the 8-B directory word -- brings the word and
+ * the bytes; X[t] is gathered only on a tie of the query's byte with its
+ * knot's, or for a row's ninth and later knots.  Same answers as the rank
+ * directory (batch.py:315-317).  rows_dev: ((R >> 5) + 1) * 16 bytes;
+ * f_scratch_dev: n1 uint64; bytes_scratch_dev: n1 bytes padded to 16.  Async.
+ * Set fs_plan.sparse to the rows, sparse_format = FS_SPARSE_RANK_ROWS
+ * (sparse_shift = sparse_ndense = 0); used only when nothing is staged.
+ */
+int fs_build_rank_rows(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t* f_scratch_dev,
+                       void* bytes_scratch_dev, void* rows_dev, void* stream);
 
 /*
  * Count words of the gap-1 table (FS_SPARSE_COUNT; a device layout of K, no

@@ -64,6 +64,7 @@ SPARSE_ZONED = 5
 SPARSE_ZONED_RANK = 6
 SPARSE_COUNT = 7
 SPARSE_KNOT_BYTES = 8
+SPARSE_RANK_ROWS = 9
 
 # Every symbol include/fsgpu.h declares (checked by the CPU test suite).
 EXPORTED = (
@@ -87,6 +88,7 @@ EXPORTED = (
     "fs_plan_zoned_rank",
     "fs_build_zoned_rank",
     "fs_build_knot_bytes",
+    "fs_build_rank_rows",
     "fs_count_words_bytes",
     "fs_plan_count_words",
     "fs_build_count_words",
@@ -204,6 +206,8 @@ def _declare(lib):
     lib.fs_build_zoned_rank.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _i32, _u64, _vp, _vp, _vp]
     lib.fs_build_knot_bytes.restype = ctypes.c_int
     lib.fs_build_knot_bytes.argtypes = [_i32, _vp, _u64, ctypes.c_double, _vp, _vp]
+    lib.fs_build_rank_rows.restype = ctypes.c_int
+    lib.fs_build_rank_rows.argtypes = [_i32, _vp, _u64, ctypes.c_double, _u64, _vp, _vp, _vp, _vp]
     lib.fs_count_words_bytes.restype = ctypes.c_uint64
     lib.fs_count_words_bytes.argtypes = [_u64, _i32, _u64]
     lib.fs_plan_count_words.restype = ctypes.c_int

@@ -309,7 +309,7 @@ class PreparedKernel:
             "sparse_format": {_lib.SPARSE_RECORDS: "records", _lib.SPARSE_RECORDS8: "records8",
                               _lib.SPARSE_RECORDS12: "records12", _lib.SPARSE_RECORDS8X3: "records8x3",
                               _lib.SPARSE_ZONED: "zoned", _lib.SPARSE_ZONED_RANK: "zoned-rank",
-                              _lib.SPARSE_COUNT: "count-words", _lib.SPARSE_KNOT_BYTES: "knot-bytes"}.get(
+                              _lib.SPARSE_COUNT: "count-words", _lib.SPARSE_KNOT_BYTES: "knot-bytes", _lib.SPARSE_RANK_ROWS: "rank-rows"}.get(
                 self.plan.sparse_format, "two-level") if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
         }
@@ -454,6 +454,8 @@ def set_direct_layouts(plan, p: SortedPartition, structure: DirectIndex, keep: l
         _set_zoned(plan, p, structure, keep)
     if hot_window and not plan.sparse:
         _set_hot_window(plan, p, structure, rank)
+    if not plan.records and not plan.sparse and not plan.hot_words:
+        _set_rank_rows(plan, p, structure, keep)
 
 
 #: the sparse two-level table is used when its dense (bitmask) super-buckets
@@ -703,6 +705,36 @@ def _plan_two_level(p: SortedPartition, idx: DirectIndex, f, budget: int):
         if rc != _lib.FS_TOO_LARGE:
             _lib.check(rc, what="fs_plan_sparse")
     return None
+
+
+#: 16-B rank rows (fs_build_rank_rows: the directory word and the knot bytes of
+#: its first eight knots in one gather) for tables searched through L2, when at
+#: least this share of the buckets holds a knot (the queries that would gather
+#: X as well); 0 keeps the 8-B directory
+RANK_ROWS_MIN_KNOT_SHARE = 0.03
+
+
+def _set_rank_rows(plan, p: SortedPartition, idx: DirectIndex, keep: list) -> None:
+    """Tables whose directory and X both stay in L2 (neither fits in shared
+    memory): widen the directory word to a 16-B row carrying its knots' bytes."""
+    n1 = len(p.values)
+    budget = _smem_budget() - 512
+    dir_bytes = ((idx.r >> 5) + 1) * 8
+    x_bytes = n1 * p.values.dtype.itemsize
+    if (not RANK_ROWS_MIN_KNOT_SHARE or idx.r >= (1 << 32) or n1 >= (1 << 31) or dir_bytes <= budget
+            or x_bytes <= budget or n1 < RANK_ROWS_MIN_KNOT_SHARE * (idx.r + 1)):
+        return
+    f = _device.empty(n1, np.uint64)
+    scratch = _device.empty((n1 + 15) // 16 * 16, np.uint8)
+    rows = _device.empty(2 * dir_bytes, np.uint8)
+    rc = _lib.load().fs_build_rank_rows(fs_dtype(p.precision), p.device_values().data_ptr(), n1, float(idx.h), idx.r,
+                                        f.data_ptr(), scratch.data_ptr(), rows.data_ptr(), _device.stream_ptr())
+    _lib.check(rc, what="fs_build_rank_rows")
+    plan.sparse = rows.data_ptr()
+    plan.sparse_format = _lib.SPARSE_RANK_ROWS
+    plan.sparse_shift = 0
+    plan.sparse_ndense = 0
+    keep.append(rows)
 
 
 #: a byte per knot staged beside the rank directory when X does not fit there

@@ -230,6 +230,29 @@ __global__ void fill_rank_kernel(const uint64_t* __restrict__ f, uint64_t n1, ui
   }
 }
 
+// Rank rows (fs_build_rank_rows): the rank directory word of 32 buckets {mask,
+// base} widened to 16 B with the knot bytes (fill_knot_bytes_kernel) of the
+// row's first eight knots, B[base .. base+7] (zero past the last knot).
+__global__ void fill_rank_rows_kernel(const uint64_t* __restrict__ f, const uint8_t* __restrict__ B, uint64_t n1,
+                                      uint64_t r, uint4* __restrict__ rows) {
+  const uint64_t words = (r >> 5) + 1;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j0 = w << 5;
+    const uint64_t base = bound_search<false>(f, 0, n1, j0);
+    uint32_t mask = 0, lo = 0, hi = 0, cnt = 0;
+    for (uint64_t i = base; i < n1; ++i) {
+      const uint64_t fi = __ldg(f + i);
+      if (fi >= j0 + 32) break;
+      mask |= 1u << (uint32_t)(fi - j0);
+      const uint32_t b = __ldg(B + i);
+      if (cnt < 4) lo |= b << (8 * cnt);
+      else if (cnt < 8) hi |= b << (8 * (cnt - 4));
+      ++cnt;
+    }
+    rows[w] = make_uint4(mask, (uint32_t)base, lo, hi);
+  }
+}
+
 // Rank directory of the gap-2 table (fs_build_rank2).  A gap-2 certificate
 // allows at most two knots per bucket (f_{i+2} > f_i), so word w holds
 // m1 = buckets with >= 1 knot, m2 = buckets with 2 knots and base =

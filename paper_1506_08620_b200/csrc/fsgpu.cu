@@ -171,8 +171,11 @@ int validate_plan(const fs_plan* p) {
                         p->sparse_format != FS_SPARSE_RECORDS8 && p->sparse_format != FS_SPARSE_RECORDS12 &&
                         p->sparse_format != FS_SPARSE_RECORDS8X3 && p->sparse_format != FS_SPARSE_ZONED &&
                         p->sparse_format != FS_SPARSE_ZONED_RANK && p->sparse_format != FS_SPARSE_COUNT &&
-                        p->sparse_format != FS_SPARSE_KNOT_BYTES))
+                        p->sparse_format != FS_SPARSE_KNOT_BYTES && p->sparse_format != FS_SPARSE_RANK_ROWS))
         return fail(FS_INVALID_ARG, "unknown sparse table format");
+      if (p->sparse && p->sparse_format == FS_SPARSE_RANK_ROWS &&
+          (p->q != 1 || p->r >= (1ull << 32) || p->n1 - 1 >= (1ull << 31)))
+        return fail(FS_INVALID_ARG, "rank rows serve the gap-1 table with R < 2^32, N < 2^31");
       if (p->sparse && p->sparse_format == FS_SPARSE_KNOT_BYTES &&
           (!p->rank || p->q != 1 || p->sparse_ndense != p->n1 || p->r >= (1ull << 32) || p->n1 - 1 >= (1ull << 31)))
         return fail(FS_INVALID_ARG, "knot bytes go with the gap-1 rank directory, one per knot");
@@ -190,7 +193,8 @@ int validate_plan(const fs_plan* p) {
       if (p->sparse && p->sparse_format == FS_SPARSE_RECORDS8X3 && p->n1 > (1ull << 24))
         return fail(FS_INVALID_ARG, "3-offset records need N+1 <= 2^24");
       if (p->sparse && !is_zoned(p->sparse_format) && p->sparse_format != FS_SPARSE_COUNT &&
-          p->sparse_format != FS_SPARSE_KNOT_BYTES && (p->sparse_shift < 5 ||
+          p->sparse_format != FS_SPARSE_KNOT_BYTES && p->sparse_format != FS_SPARSE_RANK_ROWS &&
+          (p->sparse_shift < 5 ||
                         p->sparse_shift > (p->sparse_format == FS_SPARSE_TWO_LEVEL    ? 16
                                            : p->sparse_format == FS_SPARSE_RECORDS12 ? kRec12MaxShift
                                            : p->sparse_format == FS_SPARSE_RECORDS8X3 ? kRec3MaxShift
@@ -290,7 +294,8 @@ Placement place(const fs_plan* p) {
   }
   // rank directory (+ X) too big for smem: the two-level sparse table, if it fits
   if (p->algorithm == FS_ALGO_DIRECT && p->sparse && !is_zoned(p->sparse_format) && p->q == 1 &&
-      p->sparse_format != FS_SPARSE_KNOT_BYTES && !force_global && p->r < (1ull << 32) &&
+      p->sparse_format != FS_SPARSE_KNOT_BYTES && p->sparse_format != FS_SPARSE_RANK_ROWS && !force_global &&
+      p->r < (1ull << 32) &&
       (p->sparse_format == FS_SPARSE_COUNT || (p->sparse_shift >= 5 && p->sparse_shift <= 16))) {
     const uint64_t xb = p->n1 * es;
     const uint64_t dir_b = ((p->r >> 5) + 1) * 8;
@@ -548,6 +553,10 @@ template <>
 struct UnrollVW8For<HotRankProbe<float>> {
   static constexpr int value = FSG_UNROLL_VW8_RANK;
 };
+template <>
+struct UnrollVW8For<RankRowsProbe<float>> {
+  static constexpr int value = FSG_UNROLL_VW8_RANK;
+};
 #ifndef FSG_UNROLL_VW8_ZONED
 #define FSG_UNROLL_VW8_ZONED 1  // one 8-query group per thread (2: cfg4 465 -> 448 Gq/s)
 #endif
@@ -788,6 +797,7 @@ DevPlan<T> make_devplan(const fs_plan* p, const Placement& pl) {
   d.x = static_cast<const T*>(p->x);
   d.table = p->table;
   d.rank = static_cast<const uint2*>(p->rank);
+  d.rows = p->sparse && p->sparse_format == FS_SPARSE_RANK_ROWS ? p->sparse : nullptr;
   d.n1 = p->n1;
   d.r = p->r;
   d.h = (T)p->h;
@@ -892,6 +902,9 @@ int dispatch(const fs_plan* p, const Placement& pl, const T* z, uint64_t m, OutT
         if (pl.xs) return launch_probe<T, OutT, SparseProbe<T, true, false>>(d, pl, z, m, out, fb, base, st);
         return launch_probe<T, OutT, SparseProbe<T, false, false>>(d, pl, z, m, out, fb, base, st);
       }
+      // nothing staged and 16-B rank rows built: one gather brings the directory word and its knots' bytes
+      if (d.rows && !wide && pl.smem == 0)
+        return launch_probe<T, OutT, RankRowsProbe<T>>(d, pl, z, m, out, fb, base, st);
       if (p->rank && p->q == 1) {
         if (wide) return launch_probe<T, OutT, RankProbe<T, uint64_t, false, false>>(d, pl, z, m, out, fb, base, st);
         if (pl.xs && pl.ks) return launch_probe<T, OutT, RankProbe<T, uint32_t, true, true>>(d, pl, z, m, out, fb, base, st);
@@ -1089,6 +1102,22 @@ int fs_build_rank(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint6
   cudaStream_t s = as_stream(stream);
   const uint64_t words = (r >> 5) + 1;
   fill_rank_kernel<<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, n1, r, static_cast<uint2*>(dir_dev));
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_build_rank_rows(int32_t dtype, const void* x_dev, uint64_t n1, double h, uint64_t r, uint64_t* f_scratch_dev,
+                       void* bytes_scratch_dev, void* rows_dev, void* stream) {
+  if (!x_dev || !f_scratch_dev || !bytes_scratch_dev || !rows_dev || n1 < 2) return fail(FS_INVALID_ARG, "bad arguments");
+  if (n1 - 1 >= (1ull << 31) || r >= (1ull << 32)) return fail(FS_TOO_LARGE, "rank rows need R < 2^32, N < 2^31");
+  int rc = fs_knot_buckets(dtype, x_dev, n1, h, f_scratch_dev, stream);
+  if (rc) return rc;
+  rc = fs_build_knot_bytes(dtype, x_dev, n1, h, bytes_scratch_dev, stream);
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  const uint64_t words = (r >> 5) + 1;
+  fill_rank_rows_kernel<<<grid_1d(words, 256), 256, 0, s>>>(f_scratch_dev, static_cast<const uint8_t*>(bytes_scratch_dev),
+                                                          n1, r, static_cast<uint4*>(rows_dev));
   FS_CUDA(cudaGetLastError());
   return FS_OK;
 }

@@ -50,6 +50,7 @@ struct DevPlan {
   const T* x;            // knots
   const void* table;     // K / records / padded / tree
   const uint2* rank;     // rank directory of K (direct, gap 1) or NULL
+  const void* rows;      // 16-B rank rows (FS_SPARSE_RANK_ROWS) or NULL
   uint64_t n1;           // N+1
   uint64_t r;            // R (direct family)
   T h, x0, xn;           // scale, domain
@@ -261,6 +262,82 @@ struct RankBytesProbe {
         if (g0 + q >= N) break;
         locate(z[g0 + q], j[q], qz[q]);
         d[q] = word(j[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        o[g0 + q] = (R)finish(d[q], j[q], qz[q], z[g0 + q]);
+      }
+    }
+  }
+};
+
+// RankProbe through L2 over 16-B rank rows (fill_rank_rows_kernel): the
+// directory word of the query's 32 buckets and the knot bytes of the row's
+// first eight knots arrive in one gather (one 32-B sector either way), so the
+// second gather -- X[t], for every query whose bucket holds a knot -- is left
+// to ties of the bytes and to a row's ninth and later knots.  For tables whose
+// directory does not fit in shared memory (cfg5 N+1 = 2^20 + 1: 1.1 -> 1.0
+// gathers per query).  Same answers as RankProbe.
+template <typename T>
+struct RankRowsProbe {
+  const T* X;
+  const uint4* D;
+  T h, x0;
+  uint32_t r, n1;
+  __device__ __forceinline__ RankRowsProbe(const DevPlan<T>& p, unsigned char*) {
+    n1 = (uint32_t)p.n1;
+    X = p.x;
+    D = static_cast<const uint4*>(p.rows);
+    h = p.h;
+    x0 = p.x0;
+    r = (uint32_t)p.r;
+  }
+  __device__ __forceinline__ void locate(T z, uint32_t& j, uint32_t& qz) const {
+    const T p = mul_rn(sub_rn(z, x0), h);
+    const T fl = floor(p);
+    j = trunc_to<uint32_t>(fl);
+    j = j < r ? j : r;
+    qz = trunc_to<uint32_t>(mul_rn(sub_rn(p, fl), (T)256));
+  }
+  __device__ __forceinline__ int64_t finish(const uint4& d, uint32_t j, uint32_t qz, T z) const {
+    const uint32_t b = j & 31u;
+    uint32_t below;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(b));
+    const uint32_t tl = __popc(d.x & below);
+    const uint32_t t = d.y + tl;
+    const bool knot = (d.x >> b) & 1u;
+    FSG_BOUND(!knot || t < n1);
+    // the knot's byte (its place inside its bucket): byte tl of the row's eight;
+    // no knot: above every query byte; a ninth or later knot: a forced tie
+    uint32_t o = __byte_perm(d.z, d.w, tl & 7u) & 255u;
+    o = tl < 8u ? o : qz;
+    o = knot ? o : 256u;
+    uint32_t res = t - (qz < o ? 1u : 0u);
+    if (qz == o) res = t - (z < __ldg(X + t) ? 1u : 0u);  // a tie (knot is set: o < 256)
+    return (int64_t)(int32_t)res;
+  }
+  __device__ __forceinline__ int64_t operator()(T z) const {
+    uint32_t j, qz;
+    locate(z, j, qz);
+    return finish(__ldg(D + (j >> 5)), j, qz, z);
+  }
+#ifndef FSG_RANKROWS_GROUP
+#define FSG_RANKROWS_GROUP 4
+#endif
+  template <int N, typename R>
+  __device__ __forceinline__ void batch(const T (&z)[N], R (&o)[N]) const {
+    constexpr int G = N < FSG_RANKROWS_GROUP ? N : FSG_RANKROWS_GROUP;
+#pragma unroll
+    for (int g0 = 0; g0 < N; g0 += G) {
+      uint4 d[G];
+      uint32_t j[G], qz[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (g0 + q >= N) break;
+        locate(z[g0 + q], j[q], qz[q]);
+        FSG_BOUND(j[q] <= r);
+        d[q] = __ldg(D + (j[q] >> 5));
       }
 #pragma unroll
       for (int q = 0; q < G; ++q) {

@@ -95,7 +95,7 @@ def test_argument_validation_without_gpu():
         plan.sparse_shift, plan.sparse_ndense = shift, novf
         assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
         assert b"sparse" in lib.fs_last_error()
-    plan.sparse_format, plan.sparse_shift, plan.sparse_ndense = 9, 8, 0
+    plan.sparse_format, plan.sparse_shift, plan.sparse_ndense = 10, 8, 0
     assert lib.fs_search_device(ctypes.byref(plan), None, 0, None, 4, 1, None) == _lib.FS_INVALID_ARG
     assert b"sparse" in lib.fs_last_error()
     # knot bytes: one per knot, beside the gap-1 rank directory

@@ -115,7 +115,7 @@ def main():
             try:
                 base = {"direct-k": "direct", "direct-rank": "direct", "direct-hot": "direct", "direct-nohot": "direct",
                         "direct-nozoned": "direct", "direct-count": "direct", "direct-nocount": "direct",
-                        "direct-nobytes": "direct",
+                        "direct-nobytes": "direct", "direct-norows": "direct",
                         "bitset2-flat": "bitset2", "direct-gap2-k": "direct-gap2"}.get(algo, algo)
                 if algo.startswith("direct-hot:") or algo.startswith("direct-count:"):
                     base = "direct"
@@ -178,6 +178,15 @@ def main():
                     finally:
                         (_b.SPARSE_FORMATS, _b.COUNT_WORDS_MAX_RARE_PPM, _b.COUNT_WORDS_MAX_L2_XREAD_PPM,
                          _b.COUNT_WORDS_MAX_XREAD_PPM) = keep_c
+                if algo == "direct-norows":  # the 8-B rank directory through L2 (no 16-B rank rows)
+                    from paper_1506_08620_b200 import batch as _b
+
+                    keep_rr = _b.RANK_ROWS_MIN_KNOT_SHARE
+                    _b.RANK_ROWS_MIN_KNOT_SHARE = 0
+                    try:
+                        prep = fs.prepare("direct", p)
+                    finally:
+                        _b.RANK_ROWS_MIN_KNOT_SHARE = keep_rr
                 if algo == "direct-nobytes":  # the staged directory alone, X through L2 (no knot bytes)
                     from paper_1506_08620_b200 import batch as _b
 
