@@ -312,6 +312,10 @@ class PreparedKernel:
                               _lib.SPARSE_COUNT: "count-words", _lib.SPARSE_KNOT_BYTES: "knot-bytes", _lib.SPARSE_RANK_ROWS: "rank-rows"}.get(
                 self.plan.sparse_format, "two-level") if f & _lib.PLACE_SMEM_SPARSE else None,
             "smem_bytes": int(smem.value),
+            # what a search that stages nothing gathers through L2 besides X
+            "l2_directory": (None if smem.value else
+                             "rank-rows" if self.plan.sparse and self.plan.sparse_format == _lib.SPARSE_RANK_ROWS else
+                             "rank" if self.plan.rank else None),
         }
 
     def launches_per_batch(self, m: int) -> int:

@@ -82,7 +82,7 @@ def test_rank_rows_for_l2_tables(cuda, name):
     idx = prep.structure
     assert prep.plan.sparse_format == _lib.SPARSE_RANK_ROWS and prep.plan.sparse
     pl = prep.placement()
-    assert pl["smem_bytes"] == 0 and not pl["smem_sparse"] and not pl["smem_hot"], pl
+    assert pl["smem_bytes"] == 0 and not pl["smem_sparse"] and not pl["smem_hot"] and pl["l2_directory"] == "rank-rows", pl
     want_rows, per_row = expected_rows(xs, idx.h, idx.r)
     got = _buffer_of(prep, prep.plan.sparse).cpu().numpy().view(np.uint32).reshape(-1, 4)
     assert np.array_equal(got, want_rows)
@@ -121,7 +121,7 @@ def test_rank_rows_rule_switch_and_out_of_domain(cuda):
         plain = fs.prepare("direct", p)
     finally:
         batch.RANK_ROWS_MIN_KNOT_SHARE = saved
-    assert not plain.plan.sparse and plain.placement()["smem_bytes"] == 0
+    assert not plain.plan.sparse and plain.placement()["smem_bytes"] == 0 and plain.placement()["l2_directory"] == "rank"
     assert np.array_equal(fs.run_batch(plain, z), want)
     tail = np.concatenate([xs[-8:-1], np.nextafter(xs[-8:], -np.inf)])
     tail = tail[(tail >= xs[0]) & (tail < xs[-1])]
